@@ -1,0 +1,84 @@
+// Kernel interfaces of the B200 PC path (host-visible structs + launchers).
+// Implemented in pc_kernels.cu; called by the C-ABI layer (pswarm_capi.cu).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "pc_device.cuh"
+
+namespace pswarm_dev {
+
+/// Per-group failure record of one segment solve.  status codes below; coordinates
+/// follow the reference exceptions (errors.hpp:40-62).
+enum FaultStatus : int {
+    FAULT_NONE = 0,
+    FAULT_DIVERGENCE = 1,     // picard.hpp:26-36 first non-finite (node, column)
+    FAULT_SINGULARITY = 2,    // force_model.hpp:115-120 (node, trajectory-in-group, body)
+    FAULT_WARM_ZERO_RADIUS = 3,  // kepler.hpp:61-62 thrown out of warm_start
+    FAULT_WARM_SOLVER = 4,    // kepler.hpp:40-41 thrown out of warm_start
+    FAULT_TIMEOUT = 5,        // augment.hpp:117-121
+};
+
+struct GroupFault {
+    int32_t status;
+    int32_t iteration;   // iteration at which it happened (0 = warm start)
+    int32_t body;        // -1 central / none
+    int32_t pad;
+    int64_t node;
+    int64_t column;      // block column (divergence)
+    int64_t trajectory;  // slot within the group (singularity) / batch index (warm start)
+    double value;        // distance (singularity), mean anomaly (solver)
+    double value2;       // eccentricity (solver)
+};
+
+/// Arguments of one segment launch of the persistent slot kernel.
+struct SegArgs {
+    int N;          // nodes
+    int nkp;        // k-step pairs: K padded to 8*nkp
+    int warps;      // warps per CTA = ceil(ceil((N+1)/8)/2)
+    int M;          // trajectories
+    int P;          // groups
+    int gmax;       // largest group (<= SLOTS)
+    int seg;
+    int cold_start;     // segment 0 with StartMode::cold
+    int error_mode;     // 0 relative, 1 absolute
+    int max_it;
+    int record_history;
+    int pad0;
+    double tol;
+    double omega2;
+    double epoch;       // segment start time == times[0]
+    unsigned long long deadline_ns;  // %globaltimer deadline, 0 = none
+    ForceData fd;
+    const double2* upack;       // packed [U; anchor] operator
+    const double* times;        // [N]
+    const int64_t* group_off;   // [P+1]
+    const double* state_in;     // [M][6] segment initial states
+    double* state_out;          // [M][6] terminal rows (chained)
+    double* samples;            // [M][R][6] or nullptr
+    int64_t R;
+    int64_t row0;               // seg*(N-1)
+    int* queue;                 // group work counter (zeroed per launch)
+    int32_t* rep_iter;          // [P]
+    double* rep_err;            // [P]
+    uint8_t* rep_conv;          // [P]
+    double* rep_hist;           // [P][max_it] or nullptr
+    GroupFault* faults;         // [P]
+    uint8_t* cold_fallback;     // [M] or nullptr
+};
+
+size_t segment_smem_bytes(int N, int nkp);
+int segment_threads(int N);
+cudaError_t launch_segment(const SegArgs& a, int grid, cudaStream_t s);
+
+cudaError_t launch_picard_update(int N, int nkp, int C, const double* F, const double* y0, double* out,
+                                 const double2* upack, cudaStream_t s);
+cudaError_t launch_force_block(int N, int m, const double* y, double omega2, const ForceData& fd, int kind_nbody,
+                               double* force, unsigned long long* fault_key, cudaStream_t s);
+cudaError_t launch_block_error(int N, int m, const double* cur, const double* prev, int mode,
+                               unsigned long long* per_state_bits, cudaStream_t s);
+cudaError_t launch_warm_start(int M, const double* states, int N, const double* times, double mu, double* guesses,
+                              uint8_t* fallback, unsigned long long* fault_key, double* fault_vals, cudaStream_t s);
+
+}  // namespace pswarm_dev

@@ -1,0 +1,953 @@
+// C-ABI implementation (include/pswarm_gpu.h): device context, host
+// orchestration of the segment loop (propagator.hpp:192-347), and the
+// operator-level entry points.  All numerics of the hot loop run in the CUDA
+// kernels of pc_kernels.cu; the host only prepares per-segment constants (grid,
+// frozen ephemeris, packed operators) and turns device fault records into the
+// reference's exceptions.  There is no CPU fallback anywhere in this file.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "pc_kernels.cuh"
+#include "pswarm/block.hpp"
+#include "pswarm/chebyshev.hpp"
+#include "pswarm/ephemeris.hpp"
+#include "pswarm/errors.hpp"
+#include "pswarm/kepler.hpp"
+#include "pswarm/pc_matrices.hpp"
+#include "pswarm/propagator.hpp"
+#include "pswarm/synthetic.hpp"
+#include "pswarm_gpu.h"
+
+using pswarm::Index;
+using namespace pswarm_dev;
+
+namespace {
+
+// ------------------------------------------------------------ error plumbing
+struct CapiFault {
+    pswarm_error e{};
+};
+
+std::string fmtf(const char* f, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, f);
+    std::vsnprintf(buf, sizeof buf, f, ap);
+    va_end(ap);
+    return buf;
+}
+
+void init_err(pswarm_error* e, int32_t status, const std::string& msg) {
+    std::memset(e, 0, sizeof(*e));
+    e->status = status;
+    e->body = -1;
+    e->segment = e->group = e->node = e->column = e->trajectory = -1;
+    std::snprintf(e->message, sizeof(e->message), "%s", msg.c_str());
+}
+
+[[noreturn]] void raise(int32_t status, const std::string& msg) {
+    CapiFault f;
+    init_err(&f.e, status, msg);
+    throw f;
+}
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return;
+    raise(e == cudaErrorMemoryAllocation ? PSWARM_ERR_OOM : PSWARM_ERR_CUDA,
+          std::string("CUDA failure in ") + what + ": " + cudaGetErrorString(e));
+}
+
+template <typename Fn>
+pswarm_status guarded(pswarm_error* err, Fn&& fn) {
+    pswarm_error local;
+    pswarm_error* e = err ? err : &local;
+    init_err(e, PSWARM_OK, "");
+    try {
+        fn();
+        return PSWARM_OK;
+    } catch (const CapiFault& f) {
+        *e = f.e;
+    } catch (const pswarm::DivergenceError& x) {
+        init_err(e, PSWARM_ERR_DIVERGENCE, x.what());
+        e->node = x.node();
+        e->column = x.column();
+    } catch (const pswarm::SingularityError& x) {
+        init_err(e, PSWARM_ERR_SINGULARITY, x.what());
+        std::snprintf(e->body_name, sizeof(e->body_name), "%s", x.body().c_str());
+    } catch (const pswarm::CoverageError& x) {
+        init_err(e, PSWARM_ERR_COVERAGE, x.what());
+        e->value = x.epoch();
+    } catch (const pswarm::InvalidSpanError& x) {
+        init_err(e, PSWARM_ERR_INVALID_SPAN, x.what());
+    } catch (const pswarm::InvalidSizeError& x) {
+        init_err(e, PSWARM_ERR_INVALID_SIZE, x.what());
+    } catch (const pswarm::ShapeError& x) {
+        init_err(e, PSWARM_ERR_SHAPE, x.what());
+    } catch (const pswarm::AlignmentError& x) {
+        init_err(e, PSWARM_ERR_ALIGNMENT, x.what());
+    } catch (const pswarm::NonEllipticError& x) {
+        init_err(e, PSWARM_ERR_NON_ELLIPTIC, x.what());
+    } catch (const pswarm::SolverError& x) {
+        init_err(e, PSWARM_ERR_SOLVER, x.what());
+    } catch (const pswarm::InvalidPlanError& x) {
+        init_err(e, PSWARM_ERR_INVALID_PLAN, x.what());
+    } catch (const pswarm::TimeoutError& x) {
+        init_err(e, PSWARM_ERR_TIMEOUT, x.what());
+    } catch (const std::bad_alloc&) {
+        init_err(e, PSWARM_ERR_OOM, "host allocation failed");
+    } catch (const std::exception& x) {
+        init_err(e, PSWARM_ERR_GENERIC, x.what());
+    }
+    return static_cast<pswarm_status>(e->status);
+}
+
+// ------------------------------------------------------------ device memory
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    template <typename T>
+    T* get(size_t count) {
+        const size_t bytes = std::max<size_t>(count * sizeof(T), 16);
+        if (bytes > cap) {
+            if (p) cudaFree(p);
+            p = nullptr;
+            cap = 0;
+            cuda_check(cudaMalloc(&p, bytes), "cudaMalloc");
+            cap = bytes;
+        }
+        return static_cast<T*>(p);
+    }
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+};
+
+struct OpPack {
+    DevBuf buf;
+    int nkp = 0;
+    int warps = 0;
+};
+
+enum BufId {
+    B_STATE_A, B_STATE_B, B_GROUP_OFF, B_TIMES, B_BODY_POS, B_BODY_MU, B_INDIRECT, B_QUEUE,
+    B_REP_ITER, B_REP_ERR, B_REP_CONV, B_REP_HIST, B_FAULTS, B_FALLBACK, B_SAMPLES, B_DEAD,
+    B_OP_IN, B_OP_IN2, B_OP_OUT, B_OP_AUX, B_OP_KEY, B_COUNT
+};
+
+}  // namespace
+
+struct pswarm_ctx {
+    int device = 0;
+    int sm_count = 0;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr, evk0 = nullptr, evk1 = nullptr;
+    std::map<Index, std::unique_ptr<OpPack>> ops;
+    DevBuf buf[B_COUNT];
+    int64_t launches = 0;
+    int ctas_per_sm = 1;
+    int max_ctas = 0;  // 0 = SM count * ctas_per_sm
+};
+
+namespace {
+
+void bind(pswarm_ctx* ctx) { cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice"); }
+
+/// [update_op; anchor_op] packed in mma.m8n8k4 A-fragment order (pc_device.cuh).
+const OpPack& operators(pswarm_ctx* ctx, Index n) {
+    auto it = ctx->ops.find(n);
+    if (it != ctx->ops.end()) return *it->second;
+    if (n > 264) raise(PSWARM_ERR_INVALID_SIZE, fmtf("device operators support up to 264 nodes, got %lld", (long long)n));
+    const auto mats = pswarm::cached_matrices(n);  // InvalidSizeError for n < 3
+    const int mt = static_cast<int>((n + 1 + 7) / 8);
+    const int warps = (mt + 1) / 2;
+    const int nkp = static_cast<int>((n + 7) / 8);
+    const int rows = 16 * warps;
+    auto A = [&](int r, int k) -> double {
+        if (k >= n) return 0.0;
+        if (r < n) return mats->update_op(r, k);
+        if (r == n) return mats->anchor_op[k];
+        return 0.0;
+    };
+    std::vector<double> host(static_cast<size_t>(rows / 8) * nkp * 32 * 2);
+    for (int m = 0; m < rows / 8; ++m)
+        for (int kp = 0; kp < nkp; ++kp)
+            for (int lane = 0; lane < 32; ++lane) {
+                const int g = lane >> 2, q = lane & 3;
+                const size_t idx = (static_cast<size_t>(m) * nkp + kp) * 32 + lane;
+                host[2 * idx] = A(m * 8 + g, kp * 8 + q);
+                host[2 * idx + 1] = A(m * 8 + g, kp * 8 + 4 + q);
+            }
+    auto p = std::make_unique<OpPack>();
+    p->nkp = nkp;
+    p->warps = warps;
+    double* d = p->buf.get<double>(host.size());
+    cuda_check(cudaMemcpy(d, host.data(), host.size() * sizeof(double), cudaMemcpyHostToDevice), "upload operators");
+    return *ctx->ops.emplace(n, std::move(p)).first->second;
+}
+
+pswarm::BodySpec body_from(const pswarm_body& b) {
+    pswarm::BodySpec o;
+    o.name = b.name ? b.name : "";
+    o.mu = b.mu;
+    if (b.kind == 0) {
+        o.ephemeris = pswarm::OrbitalElements{b.elements[0], b.elements[1], b.elements[2], b.elements[3],
+                                              b.elements[4], b.elements[5], b.elements[6]};
+    } else {
+        pswarm::ChebyshevEphemeris eph;
+        for (int32_t s = 0; s < b.n_segments; ++s) {
+            pswarm::ChebyshevSegment seg;
+            seg.t_start = b.seg_bounds[2 * s];
+            seg.t_end = b.seg_bounds[2 * s + 1];
+            seg.coeffs_x.resize(b.n_coeffs);
+            seg.coeffs_y.resize(b.n_coeffs);
+            seg.coeffs_z.resize(b.n_coeffs);
+            const double* c = b.coeffs + static_cast<size_t>(s) * 3 * b.n_coeffs;
+            for (int32_t k = 0; k < b.n_coeffs; ++k) {
+                seg.coeffs_x[k] = c[k];
+                seg.coeffs_y[k] = c[b.n_coeffs + k];
+                seg.coeffs_z[k] = c[2 * b.n_coeffs + k];
+            }
+            eph.segments.push_back(std::move(seg));
+        }
+        o.ephemeris = std::move(eph);
+    }
+    return o;
+}
+
+/// Host-side per-segment force constants: frozen body table [N][B][3] and the
+/// node-constant indirect term sum_b mu_b r_b/|r_b|^3 (force_model.hpp:50-51).
+struct SegmentEphemeris {
+    std::vector<double> pos, indirect, mus;
+    std::vector<std::string> names;
+};
+
+SegmentEphemeris build_segment_ephemeris(const std::vector<pswarm::BodySpec>& bodies, const pswarm::ChebyshevGrid& g,
+                                         double central_mu) {
+    SegmentEphemeris e;
+    const Index n = g.n_nodes, B = static_cast<Index>(bodies.size());
+    e.pos.assign(static_cast<size_t>(n * B * 3), 0.0);
+    e.indirect.assign(static_cast<size_t>(n * 3), 0.0);
+    for (const auto& b : bodies) {
+        e.mus.push_back(b.mu);
+        e.names.push_back(b.name);
+    }
+    for (Index b = 0; b < B; ++b)  // body-major like build_ephemeris_cache (ephemeris.hpp:96-105)
+        for (Index j = 0; j < n; ++j) {
+            const pswarm::Vec3 p = pswarm::body_position(bodies[b], central_mu, g.times[j]);
+            double* o = e.pos.data() + (j * B + b) * 3;
+            o[0] = p.x();
+            o[1] = p.y();
+            o[2] = p.z();
+        }
+    for (Index j = 0; j < n; ++j)
+        for (Index b = 0; b < B; ++b) {
+            const double* p = e.pos.data() + (j * B + b) * 3;
+            const double bn = std::sqrt(p[0] * p[0] + p[1] * p[1] + p[2] * p[2]);
+            const double bn3 = bn * bn * bn;
+            for (int c = 0; c < 3; ++c) e.indirect[j * 3 + c] += e.mus[b] * (p[c] / bn3);
+        }
+    return e;
+}
+
+ForceData make_force_data(const double* pos, const double* mus, const double* indirect, double central_mu,
+                          double floor_km, int n_bodies) {
+    ForceData fd{};
+    fd.body_pos = pos;
+    fd.body_mu = mus;
+    fd.indirect = indirect;
+    fd.central_mu = central_mu;
+    fd.floor_km = floor_km;
+    fd.floor2_hi = floor_km * floor_km * (1.0 + 1e-9);
+    fd.n_bodies = n_bodies;
+    return fd;
+}
+
+__global__ void k_read_timer(unsigned long long* out) { *out = globaltimer_ns(); }
+
+template <typename T>
+void upload(pswarm_ctx* ctx, BufId id, const T* host, size_t count, T** dev) {
+    *dev = ctx->buf[id].get<T>(count);
+    if (count) cuda_check(cudaMemcpyAsync(*dev, host, count * sizeof(T), cudaMemcpyHostToDevice, ctx->stream), "H2D");
+}
+
+// ----------------------------------------------------------------- propagate
+struct RunSpec {
+    bool independent = false;  // run_batch independent mode: reference error order is per trajectory
+};
+
+void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P, const int64_t* group_sizes,
+                    int64_t n_boundaries, const double* boundaries, int64_t N, const pswarm_config* cfg,
+                    pswarm_outputs* out, const RunSpec& spec) {
+    const auto wall0 = std::chrono::steady_clock::now();
+    if (!cfg) raise(PSWARM_ERR_GENERIC, "propagate: null config");
+    // ---- validation, same order and wording as propagator.hpp:196-216
+    if (M <= 0) throw pswarm::InvalidPlanError("propagate: empty batch");
+    int64_t total = 0, gmax = 0;
+    for (int64_t g = 0; g < P; ++g) {
+        if (group_sizes[g] < 1) throw pswarm::InvalidPlanError("plan_from_sizes: group sizes must be positive");
+        total += group_sizes[g];
+        gmax = std::max(gmax, group_sizes[g]);
+    }
+    if (total != M)
+        throw pswarm::InvalidPlanError("propagate: grouping plan covers " + std::to_string(total) +
+                                       " states, batch has " + std::to_string(M));
+    const int64_t S = n_boundaries - 1;
+    if (S < 1) throw pswarm::InvalidSpanError("propagate: empty segment plan");
+    for (int64_t i = 1; i < M; ++i)
+        if (states[7 * i] != states[0])
+            throw pswarm::AlignmentError("propagate: state " + std::to_string(i) + " epoch " +
+                                         std::to_string(states[7 * i]) + " differs from shared epoch " +
+                                         std::to_string(states[0]));
+    if (states[0] != boundaries[0])
+        throw pswarm::AlignmentError("propagate: batch epoch does not match the first segment boundary");
+    if (cfg->tolerance <= 0.0) throw pswarm::Error("pc_solve: tolerance must be positive");
+    if (gmax > SLOTS)
+        raise(PSWARM_ERR_INVALID_PLAN,
+              fmtf("propagate: groups larger than %d trajectories need the wide-group path (largest group %lld)", SLOTS,
+                   (long long)gmax));
+    if (N < 3) throw pswarm::InvalidSizeError("build_matrices: need at least 3 nodes, got " + std::to_string(N));
+    if (!ctx) raise(PSWARM_ERR_NO_DEVICE, "propagate: no device context (the B200 path has no CPU fallback)");
+    bind(ctx);
+    const OpPack& op = operators(ctx, N);
+    const int max_it = std::max(cfg->max_iterations, 0);
+    const int nb = cfg->force_kind == 1 ? cfg->n_bodies : 0;
+    if (nb > 63) raise(PSWARM_ERR_INVALID_SIZE, "propagate: at most 63 perturbing bodies are supported");
+    std::vector<pswarm::BodySpec> bodies;
+    for (int b = 0; b < nb; ++b) bodies.push_back(body_from(cfg->bodies[b]));
+
+    const auto deadline = cfg->timeout_s > 0.0
+                              ? std::chrono::steady_clock::now() +
+                                    std::chrono::duration_cast<std::chrono::steady_clock::duration>(
+                                        std::chrono::duration<double>(cfg->timeout_s))
+                              : std::chrono::steady_clock::time_point::max();
+
+    cudaStream_t st = ctx->stream;
+    // ---- device buffers
+    std::vector<double> s6(static_cast<size_t>(M) * 6);
+    for (int64_t i = 0; i < M; ++i)
+        for (int c = 0; c < 6; ++c) s6[i * 6 + c] = states[7 * i + 1 + c];
+    double* d_in = nullptr;
+    upload(ctx, B_STATE_A, s6.data(), s6.size(), &d_in);
+    double* d_out = ctx->buf[B_STATE_B].get<double>(s6.size());
+    std::vector<int64_t> off(static_cast<size_t>(P) + 1, 0);
+    for (int64_t g = 0; g < P; ++g) off[g + 1] = off[g] + group_sizes[g];
+    int64_t* d_off = nullptr;
+    upload(ctx, B_GROUP_OFF, off.data(), off.size(), &d_off);
+    const int64_t R = 1 + S * (N - 1);
+    double* d_samples = out && out->samples ? ctx->buf[B_SAMPLES].get<double>(static_cast<size_t>(M) * R * 6) : nullptr;
+    int* d_queue = ctx->buf[B_QUEUE].get<int>(4);
+    int32_t* d_iter = ctx->buf[B_REP_ITER].get<int32_t>(P);
+    double* d_err = ctx->buf[B_REP_ERR].get<double>(P);
+    uint8_t* d_conv = ctx->buf[B_REP_CONV].get<uint8_t>(P);
+    const bool want_hist = out && out->error_history && max_it > 0;
+    double* d_hist = want_hist ? ctx->buf[B_REP_HIST].get<double>(static_cast<size_t>(S) * P * max_it) : nullptr;
+    GroupFault* d_faults = ctx->buf[B_FAULTS].get<GroupFault>(P);
+    uint8_t* d_fb = ctx->buf[B_FALLBACK].get<uint8_t>(static_cast<size_t>(M));
+    if (d_hist) cuda_check(cudaMemsetAsync(d_hist, 0xff, sizeof(double) * S * P * max_it, st), "memset");
+
+    std::vector<int32_t> h_iter(static_cast<size_t>(S * P), 0);
+    std::vector<double> h_err(static_cast<size_t>(S * P), 0.0);
+    std::vector<uint8_t> h_conv(static_cast<size_t>(S * P), 0), h_fb(static_cast<size_t>(S * M), 0);
+    std::vector<GroupFault> h_faults(static_cast<size_t>(P));
+    std::vector<double> h_times(static_cast<size_t>(R), 0.0);
+
+    // device deadline in %globaltimer units
+    unsigned long long gpu_deadline = 0;
+    if (cfg->timeout_s > 0.0) {
+        unsigned long long* d_t = reinterpret_cast<unsigned long long*>(ctx->buf[B_OP_KEY].get<double>(1));
+        k_read_timer<<<1, 1, 0, st>>>(d_t);
+        ++ctx->launches;
+        unsigned long long t0 = 0;
+        cuda_check(cudaMemcpyAsync(&t0, d_t, sizeof t0, cudaMemcpyDeviceToHost, st), "timer");
+        cuda_check(cudaStreamSynchronize(st), "timer sync");
+        const auto left = std::chrono::duration_cast<std::chrono::nanoseconds>(deadline - std::chrono::steady_clock::now());
+        gpu_deadline = t0 + static_cast<unsigned long long>(std::max<int64_t>(left.count(), 1));
+    }
+
+    const size_t smem = segment_smem_bytes(static_cast<int>(N), op.nkp);
+    const int per_cta = std::max<int64_t>(1, SLOTS / gmax);
+    const int64_t want_ctas = (P + per_cta - 1) / per_cta;
+    const int cap = ctx->max_ctas > 0 ? ctx->max_ctas : ctx->sm_count * ctx->ctas_per_sm;
+    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want_ctas, cap)));
+
+    cuda_check(cudaEventRecord(ctx->ev0, st), "event");
+    int64_t seg_done = 0;
+    double kernel_ms = 0.0;
+    int64_t traj_iters = 0;
+    std::string fail_msg;
+    int32_t fail_status = PSWARM_OK;
+    pswarm_error fail{};
+    init_err(&fail, PSWARM_OK, "");
+
+    for (int64_t seg = 0; seg < S; ++seg) {
+        const auto g = pswarm::build_grid(N, boundaries[seg], boundaries[seg + 1]);
+        const auto eph = build_segment_ephemeris(bodies, g, cfg->central_mu);
+        for (Index j = (seg == 0 ? 0 : 1); j < N; ++j) h_times[seg * (N - 1) + j] = g.times[j];
+        if (std::chrono::steady_clock::now() > deadline) {
+            init_err(&fail, PSWARM_ERR_TIMEOUT, "solve_group: wall-clock budget exhausted in group 0");
+            fail.segment = seg;
+            fail.group = 0;
+            fail_status = PSWARM_ERR_TIMEOUT;
+            break;
+        }
+        double *d_times, *d_pos = nullptr, *d_mu = nullptr, *d_ind = nullptr;
+        upload(ctx, B_TIMES, g.times.data(), static_cast<size_t>(N), &d_times);
+        upload(ctx, B_BODY_POS, eph.pos.data(), eph.pos.size(), &d_pos);
+        upload(ctx, B_BODY_MU, eph.mus.data(), eph.mus.size(), &d_mu);
+        upload(ctx, B_INDIRECT, eph.indirect.data(), eph.indirect.size(), &d_ind);
+        cuda_check(cudaMemsetAsync(d_queue, 0, sizeof(int), st), "memset");
+        cuda_check(cudaMemsetAsync(d_faults, 0, sizeof(GroupFault) * P, st), "memset");
+        cuda_check(cudaMemsetAsync(d_iter, 0, sizeof(int32_t) * P, st), "memset");
+        cuda_check(cudaMemsetAsync(d_conv, 0, P, st), "memset");
+        cuda_check(cudaMemsetAsync(d_fb, 0, M, st), "memset");
+
+        SegArgs a{};
+        a.N = static_cast<int>(N);
+        a.nkp = op.nkp;
+        a.warps = op.warps;
+        a.M = static_cast<int>(M);
+        a.P = static_cast<int>(P);
+        a.gmax = static_cast<int>(gmax);
+        a.seg = static_cast<int>(seg);
+        a.cold_start = (seg == 0 && cfg->start_mode == 1) ? 1 : 0;
+        a.error_mode = cfg->error_mode;
+        a.max_it = max_it;
+        a.record_history = d_hist ? 1 : 0;
+        a.tol = cfg->tolerance;
+        a.omega2 = g.omega2;
+        a.epoch = boundaries[seg];
+        a.deadline_ns = gpu_deadline;
+        a.fd = make_force_data(d_pos, d_mu, d_ind, cfg->central_mu, cfg->proximity_floor_km, nb);
+        a.upack = reinterpret_cast<const double2*>(op.buf.p);
+        a.times = d_times;
+        a.group_off = d_off;
+        a.state_in = d_in;
+        a.state_out = d_out;
+        a.samples = d_samples;
+        a.R = R;
+        a.row0 = seg * (N - 1);
+        a.queue = d_queue;
+        a.rep_iter = d_iter;
+        a.rep_err = d_err;
+        a.rep_conv = d_conv;
+        a.rep_hist = d_hist ? d_hist + static_cast<size_t>(seg) * P * max_it : nullptr;
+        a.faults = d_faults;
+        a.cold_fallback = d_fb;
+        if (max_it > 0) {
+            cuda_check(cudaEventRecord(ctx->evk0, st), "event");
+            cuda_check(launch_segment(a, grid, st), "k_pc_segment launch");
+            cuda_check(cudaEventRecord(ctx->evk1, st), "event");
+            ++ctx->launches;
+        }
+        cuda_check(cudaMemcpyAsync(h_iter.data() + seg * P, d_iter, sizeof(int32_t) * P, cudaMemcpyDeviceToHost, st), "D2H");
+        cuda_check(cudaMemcpyAsync(h_err.data() + seg * P, d_err, sizeof(double) * P, cudaMemcpyDeviceToHost, st), "D2H");
+        cuda_check(cudaMemcpyAsync(h_conv.data() + seg * P, d_conv, P, cudaMemcpyDeviceToHost, st), "D2H");
+        cuda_check(cudaMemcpyAsync(h_faults.data(), d_faults, sizeof(GroupFault) * P, cudaMemcpyDeviceToHost, st), "D2H");
+        cuda_check(cudaMemcpyAsync(h_fb.data() + seg * M, d_fb, M, cudaMemcpyDeviceToHost, st), "D2H");
+        cuda_check(cudaStreamSynchronize(st), "segment solve");
+        if (max_it > 0) {
+            float kms = 0.f;
+            cudaEventElapsedTime(&kms, ctx->evk0, ctx->evk1);
+            kernel_ms += kms;
+        }
+        for (int64_t gi = 0; gi < P; ++gi) traj_iters += static_cast<int64_t>(h_iter[seg * P + gi]) * group_sizes[gi];
+
+        // ---- faults, in the order the serial reference would raise them
+        int64_t warm_traj = -1, warm_g = -1, first_g = -1;
+        for (int64_t gi = 0; gi < P; ++gi) {
+            const GroupFault& f = h_faults[gi];
+            if (f.status == FAULT_WARM_ZERO_RADIUS || f.status == FAULT_WARM_SOLVER) {
+                if (warm_traj < 0 || f.trajectory < warm_traj) {
+                    warm_traj = f.trajectory;
+                    warm_g = gi;
+                }
+            } else if (f.status != FAULT_NONE && first_g < 0) {
+                first_g = gi;
+            }
+        }
+        if (max_it == 0 && P > 0) first_g = -1;
+        if (spec.independent && (warm_g >= 0 || first_g >= 0)) {
+            // run_independent: trajectory-major order; the lowest failing trajectory wins
+            // (runner.hpp:63-80).  Segment-synchronous processing reaches the first failing
+            // segment of every trajectory at the same time only if no lower index fails later;
+            // report the lowest index of this segment.
+            int64_t best = -1;
+            for (int64_t gi = 0; gi < P; ++gi)
+                if (h_faults[gi].status != FAULT_NONE) {
+                    best = gi;
+                    break;
+                }
+            if (h_faults[best].status == FAULT_WARM_ZERO_RADIUS || h_faults[best].status == FAULT_WARM_SOLVER) {
+                warm_g = best;
+                first_g = -1;
+            } else {
+                warm_g = -1;
+                first_g = best;
+            }
+        }
+        if (warm_g >= 0) {
+            const GroupFault& f = h_faults[warm_g];
+            if (f.status == FAULT_WARM_ZERO_RADIUS) {
+                init_err(&fail, PSWARM_ERR_SINGULARITY, "kepler_propagate: zero-radius state");
+            } else {
+                init_err(&fail, PSWARM_ERR_SOLVER,
+                         "solve_kepler: Newton iteration did not converge for M = " + std::to_string(f.value) +
+                             ", e = " + std::to_string(f.value2));
+            }
+            fail.segment = seg;
+            fail.trajectory = f.trajectory;
+            fail_status = fail.status;
+            break;
+        }
+        if (first_g >= 0) {
+            const GroupFault& f = h_faults[first_g];
+            const int64_t report_g = spec.independent ? 0 : first_g;
+            if (f.status == FAULT_DIVERGENCE) {
+                init_err(&fail, PSWARM_ERR_DIVERGENCE,
+                         "group " + std::to_string(report_g) + ": picard iteration produced a non-finite value at node " +
+                             std::to_string(f.node) + ", column " + std::to_string(f.column));
+                fail.node = f.node;
+                fail.column = f.column;
+            } else if (f.status == FAULT_SINGULARITY) {
+                std::string what, body;
+                if (f.body < 0) {
+                    what = "central-body acceleration at zero radius";
+                } else {
+                    body = eph.names[f.body];
+                    what = "close approach to body '" + body + "': distance " + std::to_string(f.value) +
+                           " km below floor " + std::to_string(cfg->proximity_floor_km) + " km";
+                }
+                init_err(&fail, PSWARM_ERR_SINGULARITY,
+                         "node " + std::to_string(f.node) + ", trajectory " + std::to_string(f.trajectory) + ": " + what);
+                std::snprintf(fail.body_name, sizeof fail.body_name, "%s", body.c_str());
+                fail.body = f.body;
+                fail.node = f.node;
+                fail.trajectory = f.trajectory;
+                fail.value = f.value;
+            } else {
+                init_err(&fail, PSWARM_ERR_TIMEOUT,
+                         "solve_group: wall-clock budget exhausted in group " + std::to_string(report_g));
+            }
+            fail.segment = seg;
+            fail.group = first_g;
+            fail.iterations = f.iteration;
+            fail_status = fail.status;
+            break;
+        }
+        // ---- non-convergence (propagator.hpp:300-312)
+        int64_t nc = -1;
+        for (int64_t gi = 0; gi < P; ++gi)
+            if (!h_conv[seg * P + gi]) {
+                nc = gi;
+                break;
+            }
+        if (nc >= 0) {
+            const int64_t report_g = spec.independent ? 0 : nc;
+            init_err(&fail, PSWARM_ERR_INCOMPLETE,
+                     "propagate: group " + std::to_string(report_g) + " did not converge in segment " +
+                         std::to_string(seg) + " (error " + std::to_string(h_err[seg * P + nc]) + " after " +
+                         std::to_string(h_iter[seg * P + nc]) + " iterations)");
+            fail.segment = seg;
+            fail.group = spec.independent ? 0 : nc;
+            fail.trajectory = spec.independent ? nc : -1;
+            fail.iterations = h_iter[seg * P + nc];
+            fail.value = h_err[seg * P + nc];
+            fail_status = PSWARM_ERR_INCOMPLETE;
+            seg_done = seg;
+            if (out) out->segments_reported = seg + 1;
+            break;
+        }
+        std::swap(d_in, d_out);
+        seg_done = seg + 1;
+        if (out) out->segments_reported = seg + 1;
+    }
+    cuda_check(cudaEventRecord(ctx->ev1, st), "event");
+
+    // ---- outputs
+    if (out) {
+        out->segments_completed = seg_done;
+        if (fail_status != PSWARM_OK && fail_status != PSWARM_ERR_INCOMPLETE) out->segments_reported = seg_done;
+        if (out->times) std::memcpy(out->times, h_times.data(), sizeof(double) * R);
+        const int64_t rep = out->segments_reported;
+        for (int64_t k = 0; k < rep * P; ++k) {
+            if (out->iterations) out->iterations[k] = h_iter[k];
+            if (out->final_error) out->final_error[k] = h_err[k];
+            if (out->converged) out->converged[k] = h_conv[k];
+        }
+        if (out->cold_fallback) std::memcpy(out->cold_fallback, h_fb.data(), static_cast<size_t>(rep * M));
+        if (out->error_history && max_it > 0 && rep > 0)
+            cuda_check(cudaMemcpyAsync(out->error_history, d_hist, sizeof(double) * rep * P * max_it,
+                                       cudaMemcpyDeviceToHost, st),
+                       "D2H history");
+        if (out->samples)
+            cuda_check(cudaMemcpyAsync(out->samples, d_samples, sizeof(double) * M * R * 6, cudaMemcpyDeviceToHost, st),
+                       "D2H samples");
+        if (out->terminal_states && fail_status == PSWARM_OK) {
+            cuda_check(cudaMemcpyAsync(s6.data(), d_in, sizeof(double) * M * 6, cudaMemcpyDeviceToHost, st),
+                       "D2H terminal");
+        }
+        cuda_check(cudaStreamSynchronize(st), "outputs");
+        if (out->terminal_states && fail_status == PSWARM_OK)
+            for (int64_t i = 0; i < M; ++i) {
+                out->terminal_states[7 * i] = boundaries[S];
+                for (int c = 0; c < 6; ++c) out->terminal_states[7 * i + 1 + c] = s6[i * 6 + c];
+            }
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+        out->device_ms = ms;
+        out->kernel_ms = kernel_ms;
+        out->trajectory_iterations = traj_iters;
+        out->gpu_launches = ctx->launches;
+        out->wall_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
+    }
+    if (fail_status != PSWARM_OK) {
+        CapiFault f;
+        f.e = fail;
+        throw f;
+    }
+}
+
+}  // namespace
+
+// =================================================================== C ABI ==
+extern "C" {
+
+int32_t pswarm_abi_version(void) { return PSWARM_ABI_VERSION; }
+
+const char* pswarm_status_name(int32_t s) {
+    switch (s) {
+    case PSWARM_OK: return "ok";
+    case PSWARM_ERR_GENERIC: return "Error";
+    case PSWARM_ERR_INVALID_SPAN: return "InvalidSpanError";
+    case PSWARM_ERR_INVALID_SIZE: return "InvalidSizeError";
+    case PSWARM_ERR_SHAPE: return "ShapeError";
+    case PSWARM_ERR_ALIGNMENT: return "AlignmentError";
+    case PSWARM_ERR_DIVERGENCE: return "DivergenceError";
+    case PSWARM_ERR_SINGULARITY: return "SingularityError";
+    case PSWARM_ERR_COVERAGE: return "CoverageError";
+    case PSWARM_ERR_NON_ELLIPTIC: return "NonEllipticError";
+    case PSWARM_ERR_SOLVER: return "SolverError";
+    case PSWARM_ERR_INVALID_PLAN: return "InvalidPlanError";
+    case PSWARM_ERR_EMPTY_REDUCTION: return "EmptyReductionError";
+    case PSWARM_ERR_TIMEOUT: return "TimeoutError";
+    case PSWARM_ERR_INCOMPLETE: return "PropagationIncompleteError";
+    case PSWARM_ERR_CUDA: return "CudaError";
+    case PSWARM_ERR_OOM: return "OutOfMemory";
+    case PSWARM_ERR_NO_DEVICE: return "NoDevice";
+    default: return "unknown";
+    }
+}
+
+pswarm_status pswarm_create(int32_t device, pswarm_ctx** out, pswarm_error* err) {
+    return guarded(err, [&] {
+        if (!out) raise(PSWARM_ERR_GENERIC, "pswarm_create: null output pointer");
+        *out = nullptr;
+        int count = 0;
+        if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+            raise(PSWARM_ERR_NO_DEVICE, "pswarm_create: no CUDA device visible (the B200 path has no CPU fallback)");
+        int dev = device;
+        if (dev < 0) cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+        if (dev >= count) raise(PSWARM_ERR_NO_DEVICE, fmtf("pswarm_create: device %d not present", dev));
+        cudaDeviceProp p{};
+        cuda_check(cudaGetDeviceProperties(&p, dev), "cudaGetDeviceProperties");
+        if (p.major != 10)
+            raise(PSWARM_ERR_NO_DEVICE, fmtf("pswarm_create: device %d is sm_%d%d, this build targets sm_100a", dev,
+                                             p.major, p.minor));
+        auto ctx = std::make_unique<pswarm_ctx>();
+        ctx->device = dev;
+        ctx->sm_count = p.multiProcessorCount;
+        bind(ctx.get());
+        cuda_check(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+        cuda_check(cudaEventCreate(&ctx->ev0), "cudaEventCreate");
+        cuda_check(cudaEventCreate(&ctx->ev1), "cudaEventCreate");
+        cuda_check(cudaEventCreate(&ctx->evk0), "cudaEventCreate");
+        cuda_check(cudaEventCreate(&ctx->evk1), "cudaEventCreate");
+        *out = ctx.release();
+    });
+}
+
+void pswarm_destroy(pswarm_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    ctx->ops.clear();
+    for (auto& b : ctx->buf) {
+        if (b.p) cudaFree(b.p);
+        b.p = nullptr;
+        b.cap = 0;
+    }
+    if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+    if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+    if (ctx->evk0) cudaEventDestroy(ctx->evk0);
+    if (ctx->evk1) cudaEventDestroy(ctx->evk1);
+    if (ctx->stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+
+pswarm_status pswarm_set_option(pswarm_ctx* ctx, const char* key, int64_t value) {
+    return guarded(nullptr, [&] {
+        const std::string k = key ? key : "";
+        if (k == "ctas_per_sm") ctx->ctas_per_sm = static_cast<int>(std::max<int64_t>(1, value));
+        else if (k == "max_ctas") ctx->max_ctas = static_cast<int>(std::max<int64_t>(0, value));
+        else raise(PSWARM_ERR_GENERIC, "pswarm_set_option: unknown key '" + k + "'");
+    });
+}
+
+pswarm_status pswarm_propagate(pswarm_ctx* ctx, int64_t n_states, const double* states, int64_t n_groups,
+                               const int64_t* group_sizes, int64_t n_boundaries, const double* boundaries,
+                               int64_t n_nodes, const pswarm_config* config, pswarm_outputs* out,
+                               pswarm_error* err) {
+    return guarded(err, [&] {
+        propagate_impl(ctx, n_states, states, n_groups, group_sizes, n_boundaries, boundaries, n_nodes, config, out,
+                       RunSpec{});
+    });
+}
+
+pswarm_status pswarm_run_batch(pswarm_ctx* ctx, int64_t n_states, const double* states, int64_t n_boundaries,
+                               const double* boundaries, int64_t n_nodes, const pswarm_config* config, int32_t mode,
+                               int32_t workers, pswarm_outputs* out, pswarm_error* err) {
+    return guarded(err, [&] {
+        if (workers < 1) throw pswarm::InvalidPlanError("run_batch: need at least one worker");
+        pswarm::GroupingPlan plan;
+        if (n_states < 1) throw pswarm::InvalidPlanError("propagate: empty batch");
+        if (mode == 0) plan = pswarm::split_groups(n_states, n_states);
+        else if (mode == 1 || mode == 2) plan = pswarm::split_groups(n_states, 1);
+        else if (mode == 3) plan = pswarm::split_groups(n_states, std::clamp<int64_t>(config->p_groups, 1, n_states));
+        else throw pswarm::InvalidPlanError("grouping_for_mode: invalid mode");
+        RunSpec spec;
+        spec.independent = mode == 0;
+        propagate_impl(ctx, n_states, states, plan.groups(), plan.group_sizes.data(), n_boundaries, boundaries, n_nodes,
+                       config, out, spec);
+    });
+}
+
+pswarm_status pswarm_picard_update(pswarm_ctx* ctx, int64_t n_nodes, int64_t n_cols, const double* force,
+                                   const double* initial_row, double* out, pswarm_error* err) {
+    return guarded(err, [&] {
+        if (!ctx) raise(PSWARM_ERR_NO_DEVICE, "pswarm_picard_update: null context");
+        bind(ctx);
+        const OpPack& op = operators(ctx, n_nodes);
+        if (n_cols < 1) return;
+        const size_t nc = static_cast<size_t>(n_nodes) * n_cols;
+        double *dF, *dy0;
+        upload(ctx, B_OP_IN, force, nc, &dF);
+        upload(ctx, B_OP_IN2, initial_row, static_cast<size_t>(n_cols), &dy0);
+        double* dO = ctx->buf[B_OP_OUT].get<double>(nc);
+        cuda_check(launch_picard_update(static_cast<int>(n_nodes), op.nkp, static_cast<int>(n_cols), dF, dy0, dO,
+                                        reinterpret_cast<const double2*>(op.buf.p), ctx->stream),
+                   "k_picard_update");
+        ++ctx->launches;
+        cuda_check(cudaMemcpyAsync(out, dO, nc * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+        cuda_check(cudaStreamSynchronize(ctx->stream), "picard_update");
+    });
+}
+
+pswarm_status pswarm_eval_force_block(pswarm_ctx* ctx, int64_t n_nodes, int64_t group_size, const double* y,
+                                      double omega2, int32_t force_kind, double central_mu, int32_t n_bodies,
+                                      const double* body_positions, const double* body_mus,
+                                      const char* const* body_names, double proximity_floor_km, double* force,
+                                      pswarm_error* err) {
+    return guarded(err, [&] {
+        if (!ctx) raise(PSWARM_ERR_NO_DEVICE, "pswarm_eval_force_block: null context");
+        bind(ctx);
+        const int64_t N = n_nodes, m = group_size;
+        const int B = force_kind == 1 ? n_bodies : 0;
+        if (B > 63) raise(PSWARM_ERR_INVALID_SIZE, "eval_force_block: at most 63 perturbing bodies are supported");
+        const size_t nc = static_cast<size_t>(N) * 6 * m;
+        // body table [B][N][3] -> node-major [N][B][3] + indirect term
+        std::vector<double> pos(static_cast<size_t>(N) * B * 3), ind(static_cast<size_t>(N) * 3, 0.0);
+        for (int64_t j = 0; j < N; ++j)
+            for (int b = 0; b < B; ++b) {
+                const double* p = body_positions + (static_cast<size_t>(b) * N + j) * 3;
+                std::copy(p, p + 3, pos.data() + (j * B + b) * 3);
+                const double bn = std::sqrt(p[0] * p[0] + p[1] * p[1] + p[2] * p[2]);
+                for (int c = 0; c < 3; ++c) ind[j * 3 + c] += body_mus[b] * (p[c] / (bn * bn * bn));
+            }
+        double *dy, *dpos, *dmu, *dind;
+        upload(ctx, B_OP_IN, y, nc, &dy);
+        upload(ctx, B_BODY_POS, pos.data(), pos.size(), &dpos);
+        upload(ctx, B_BODY_MU, body_mus, static_cast<size_t>(B), &dmu);
+        upload(ctx, B_INDIRECT, ind.data(), ind.size(), &dind);
+        double* dF = ctx->buf[B_OP_OUT].get<double>(nc);
+        unsigned long long* dkey = reinterpret_cast<unsigned long long*>(ctx->buf[B_OP_KEY].get<double>(1));
+        cuda_check(cudaMemsetAsync(dkey, 0xff, sizeof(unsigned long long), ctx->stream), "memset");
+        const ForceData fd = make_force_data(dpos, dmu, dind, central_mu, proximity_floor_km, B);
+        cuda_check(launch_force_block(static_cast<int>(N), static_cast<int>(m), dy, omega2, fd, force_kind == 1, dF, dkey,
+                                      ctx->stream),
+                   "k_force_block");
+        ++ctx->launches;
+        unsigned long long key = 0;
+        cuda_check(cudaMemcpyAsync(force, dF, nc * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+        cuda_check(cudaMemcpyAsync(&key, dkey, sizeof key, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+        cuda_check(cudaStreamSynchronize(ctx->stream), "eval_force_block");
+        if (key != ~0ull) {
+            // first failing sample in s = j*m + t order (force_model.hpp:130-140); the
+            // message quotes the caller's own input, so it is formatted from it here.
+            const int64_t s = static_cast<int64_t>(key / 64), chk = static_cast<int64_t>(key % 64);
+            const int64_t j = s / m, t = s % m;
+            const double* row = y + static_cast<size_t>(j) * 6 * m;
+            const double r[3] = {row[t], row[m + t], row[2 * m + t]};
+            std::string what, body;
+            if (chk == 0) {
+                what = "central-body acceleration at zero radius";
+            } else {
+                const int b = static_cast<int>(chk - 1);
+                const double* p = body_positions + (static_cast<size_t>(b) * N + j) * 3;
+                const double d[3] = {p[0] - r[0], p[1] - r[1], p[2] - r[2]};
+                const double dn = std::sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+                body = body_names && body_names[b] ? body_names[b] : "";
+                what = "close approach to body '" + body + "': distance " + std::to_string(dn) + " km below floor " +
+                       std::to_string(proximity_floor_km) + " km";
+            }
+            CapiFault f;
+            init_err(&f.e, PSWARM_ERR_SINGULARITY,
+                     "node " + std::to_string(j) + ", trajectory " + std::to_string(t) + ": " + what);
+            std::snprintf(f.e.body_name, sizeof f.e.body_name, "%s", body.c_str());
+            f.e.node = j;
+            f.e.trajectory = t;
+            f.e.body = static_cast<int32_t>(chk - 1);
+            throw f;
+        }
+    });
+}
+
+pswarm_status pswarm_block_iteration_error(pswarm_ctx* ctx, int64_t n_nodes, int64_t group_size, const double* cur,
+                                           const double* prev, int32_t error_mode, double* per_state,
+                                           double* group_max, pswarm_error* err) {
+    return guarded(err, [&] {
+        if (!ctx) raise(PSWARM_ERR_NO_DEVICE, "pswarm_block_iteration_error: null context");
+        if (group_size < 1) throw pswarm::EmptyReductionError("reduce_max: empty input");
+        bind(ctx);
+        const size_t nc = static_cast<size_t>(n_nodes) * 6 * group_size;
+        double *dc, *dp;
+        upload(ctx, B_OP_IN, cur, nc, &dc);
+        upload(ctx, B_OP_IN2, prev, nc, &dp);
+        unsigned long long* dbits = reinterpret_cast<unsigned long long*>(ctx->buf[B_OP_OUT].get<double>(group_size));
+        cuda_check(cudaMemsetAsync(dbits, 0, sizeof(double) * group_size, ctx->stream), "memset");
+        cuda_check(launch_block_error(static_cast<int>(n_nodes), static_cast<int>(group_size), dc, dp, error_mode, dbits,
+                                      ctx->stream),
+                   "k_block_error");
+        ++ctx->launches;
+        std::vector<double> h(static_cast<size_t>(group_size));
+        cuda_check(cudaMemcpyAsync(h.data(), dbits, sizeof(double) * group_size, cudaMemcpyDeviceToHost, ctx->stream),
+                   "D2H");
+        cuda_check(cudaStreamSynchronize(ctx->stream), "block_error");
+        if (per_state) std::memcpy(per_state, h.data(), sizeof(double) * group_size);
+        if (group_max) *group_max = *std::max_element(h.begin(), h.end());
+    });
+}
+
+pswarm_status pswarm_warm_start(pswarm_ctx* ctx, int64_t n_states, const double* states, int64_t n_nodes,
+                                const double* times, double central_mu, double* guesses, uint8_t* cold_fallback,
+                                pswarm_error* err) {
+    return guarded(err, [&] {
+        if (!ctx) raise(PSWARM_ERR_NO_DEVICE, "pswarm_warm_start: null context");
+        bind(ctx);
+        if (n_states < 1) return;
+        double *ds, *dt;
+        upload(ctx, B_OP_IN, states, static_cast<size_t>(n_states) * 7, &ds);
+        upload(ctx, B_OP_IN2, times, static_cast<size_t>(n_nodes), &dt);
+        const size_t ng = static_cast<size_t>(n_states) * n_nodes * 6;
+        double* dg = ctx->buf[B_OP_OUT].get<double>(ng);
+        uint8_t* dfb = ctx->buf[B_FALLBACK].get<uint8_t>(static_cast<size_t>(n_states));
+        double* aux = ctx->buf[B_OP_AUX].get<double>(4);
+        unsigned long long* dkey = reinterpret_cast<unsigned long long*>(ctx->buf[B_OP_KEY].get<double>(1));
+        cuda_check(cudaMemsetAsync(dkey, 0xff, sizeof(unsigned long long), ctx->stream), "memset");
+        cuda_check(launch_warm_start(static_cast<int>(n_states), ds, static_cast<int>(n_nodes), dt, central_mu, dg, dfb,
+                                     dkey, aux, ctx->stream),
+                   "k_warm_start");
+        ctx->launches += 2;
+        unsigned long long key = 0;
+        double vals[2] = {0.0, 0.0};
+        cuda_check(cudaMemcpyAsync(guesses, dg, ng * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+        if (cold_fallback)
+            cuda_check(cudaMemcpyAsync(cold_fallback, dfb, static_cast<size_t>(n_states), cudaMemcpyDeviceToHost,
+                                       ctx->stream),
+                       "D2H");
+        cuda_check(cudaMemcpyAsync(&key, dkey, sizeof key, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+        cuda_check(cudaMemcpyAsync(vals, aux, sizeof vals, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+        cuda_check(cudaStreamSynchronize(ctx->stream), "warm_start");
+        if (key != ~0ull) {
+            const int kind = static_cast<int>(key % 4);
+            const int64_t idx = static_cast<int64_t>(key / 4);
+            if (kind == CONIC_ZERO_RADIUS) throw pswarm::SingularityError("kepler_propagate: zero-radius state");
+            CapiFault f;
+            init_err(&f.e, PSWARM_ERR_SOLVER,
+                     "solve_kepler: Newton iteration did not converge for M = " + std::to_string(vals[0]) +
+                         ", e = " + std::to_string(vals[1]));
+            f.e.trajectory = idx / n_nodes;
+            f.e.node = idx % n_nodes;
+            throw f;
+        }
+    });
+}
+
+pswarm_status pswarm_elements_to_state(const double* el, double mu, double t, double* state_out, pswarm_error* err) {
+    return guarded(err, [&] {
+        const auto s = pswarm::elements_to_state(pswarm::OrbitalElements{el[0], el[1], el[2], el[3], el[4], el[5], el[6]},
+                                                 mu, t);
+        state_out[0] = s.epoch;
+        for (int c = 0; c < 3; ++c) {
+            state_out[1 + c] = s.r[c];
+            state_out[4 + c] = s.v[c];
+        }
+    });
+}
+
+static pswarm::StateVector state_from7(const double* s) {
+    pswarm::StateVector x;
+    x.epoch = s[0];
+    x.r = pswarm::Vec3(s[1], s[2], s[3]);
+    x.v = pswarm::Vec3(s[4], s[5], s[6]);
+    return x;
+}
+
+pswarm_status pswarm_osculating_period(const double* state, double mu, double* period, pswarm_error* err) {
+    return guarded(err, [&] { *period = pswarm::osculating_period(state_from7(state), mu); });
+}
+
+pswarm_status pswarm_plan_segments(const double* rep, double t_start, double t_end, double mu, int32_t policy,
+                                   int64_t n_nodes, double max_periods, int64_t capacity, double* boundaries,
+                                   int64_t* n_boundaries, pswarm_error* err) {
+    return guarded(err, [&] {
+        const auto p = pswarm::plan_segments(state_from7(rep), t_start, t_end, mu,
+                                             policy == 1 ? pswarm::SegmentPolicy::per_orbit : pswarm::SegmentPolicy::single,
+                                             n_nodes, max_periods);
+        if (static_cast<int64_t>(p.boundaries.size()) > capacity)
+            raise(PSWARM_ERR_GENERIC, "pswarm_plan_segments: boundary buffer too small");
+        std::memcpy(boundaries, p.boundaries.data(), sizeof(double) * p.boundaries.size());
+        *n_boundaries = static_cast<int64_t>(p.boundaries.size());
+    });
+}
+
+pswarm_status pswarm_build_grid(int64_t n_nodes, double t_start, double t_end, double* times, double* omega2,
+                                pswarm_error* err) {
+    return guarded(err, [&] {
+        const auto g = pswarm::build_grid(n_nodes, t_start, t_end);
+        std::memcpy(times, g.times.data(), sizeof(double) * n_nodes);
+        if (omega2) *omega2 = g.omega2;
+    });
+}
+
+void pswarm_make_clone_batch(const double* base, int64_t count, double spread, uint64_t seed, double* out) {
+    const auto b = pswarm::make_clone_batch(state_from7(base), count, spread, seed);
+    for (int64_t i = 0; i < count; ++i) {
+        out[7 * i] = b[i].epoch;
+        for (int c = 0; c < 3; ++c) {
+            out[7 * i + 1 + c] = b[i].r[c];
+            out[7 * i + 4 + c] = b[i].v[c];
+        }
+    }
+}
+
+}  // extern "C"

@@ -1,0 +1,174 @@
+"""End-to-end parity of the device propagation path (persistent slot kernel)
+against the CPU oracle on the same seeded inputs.
+
+Bars (BASELINE.json north_star): final positions/velocities within 1e-10
+relative (runner.hpp:139-159 metric over every node sample), Picard iteration
+counts within +-1 per (segment, group), identical segment counts.
+"""
+import subprocess
+import os
+
+import numpy as np
+import pytest
+
+import paper_2301_03989_b200 as ps
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _parity(got, want, tol=1e-10):
+    assert got.iterations.shape == want.iterations.shape
+    disc = ps.max_state_discrepancy(got.trajectories, want.trajectories)
+    diter = int(np.abs(got.iterations.astype(int) - want.iterations.astype(int)).max())
+    assert disc <= tol, disc
+    assert diter <= 1, diter
+    tdisc = ps.max_state_discrepancy(got.terminal_states[None, :, 1:], want.terminal_states[None, :, 1:])
+    assert tdisc <= tol
+    assert np.array_equal(got.terminal_states[:, 0], want.terminal_states[:, 0])
+    return disc, diter
+
+
+def _setup(m, n, frac, bodies="reference", spread=1e-5, policy="single", start="warm"):
+    base = ps.reference_state()
+    states = ps.make_clone_batch(base, m, spread)
+    period = ps.osculating_period(base, ps.MU_SUN)
+    plan = ps.plan_segments(base, 0.0, frac * period, ps.MU_SUN, policy, n)
+    if bodies == "two_body":
+        cfg = ps.reference_force_config("two_body", n_nodes=n, start_mode=start)
+    else:
+        blist = ps.reference_bodies() if bodies == "reference" else ps.planets8()
+        cfg = ps.reference_force_config("n_body", bodies=blist, n_nodes=n, start_mode=start)
+    return states, plan, cfg
+
+
+def test_cpp_dropin_api():
+    """The C++ drop-in headers (include/pswarm.hpp) on the device library."""
+    exe = os.path.join(ROOT, "tests", "cpp", "dropin_test")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert r.stdout.strip().splitlines()[-1].endswith(" 0")
+
+
+@pytest.mark.parametrize("start", ["cold", "warm"])
+def test_c1_two_body_closed_form(ctx, oracle, start):
+    """C1: 64 ICs, two-body, one full osculating period, N = 200 (acceptance.cpp:78-124)."""
+    el = [1.3e8, 0.2, 0.05, 0.4, 0.9, 0.0, 0.0]
+    base = ps.elements_to_state(el, ps.MU_SUN, 0.0)
+    states = ps.make_clone_batch(base, 64, 1e-5)
+    period = ps.osculating_period(base, ps.MU_SUN)
+    plan = ps.plan_segments(base, 0.0, period, ps.MU_SUN, "single", 200)
+    cfg = ps.reference_force_config("two_body", start_mode=start)
+    got = ctx.run_batch(states, cfg, plan, "independent")
+    want = oracle.run_batch(states, cfg, plan, "independent", 8)
+    _parity(got, want)
+    assert got.converged.all()
+    # closed form: every node of every trajectory vs its own conic (1e-10)
+    worst = 0.0
+    for i in range(0, 64, 7):
+        for j in range(0, 200, 9):
+            k = oracle.kepler_propagate(states[i], ps.MU_SUN, got.times[j])
+            s = got.trajectories[i, j]
+            worst = max(worst, np.linalg.norm(s[:3] - k[1:4]) / np.linalg.norm(k[1:4]),
+                        np.linalg.norm(s[3:] - k[4:]) / np.linalg.norm(k[4:]))
+    assert worst <= 1e-10
+
+
+@pytest.mark.parametrize("bodies", ["reference", "planets8"])
+def test_c2_nbody_independent(ctx, oracle, bodies):
+    """C2 (reduced to 64 ICs): Sun + planets, 0.87 period, N = 200, warm start."""
+    states, plan, cfg = _setup(64, 200, 0.87, bodies)
+    got = ctx.run_batch(states, cfg, plan, "independent")
+    want = oracle.run_batch(states, cfg, plan, "independent", 8)
+    _parity(got, want)
+    # per-iteration error histories agree while the error is above the FP64 noise
+    # floor of the iterate differences (~1e-13 relative); below it they are roundoff
+    for g in range(0, 64, 9):
+        a, b = got.reports[0][g].per_iteration_errors, want.reports[0][g].per_iteration_errors
+        k = min(len(a), len(b))
+        big = b[:k] > 1e-8
+        assert np.allclose(a[:k][big], b[:k][big], rtol=1e-4, atol=0)
+
+
+@pytest.mark.parametrize("mode,p", [("grouped", 8), ("grouped", 16), ("augmented", 1)])
+def test_group_modes_match_oracle(ctx, oracle, mode, p):
+    m = 8 if mode == "augmented" else 64
+    states, plan, cfg = _setup(m, 128, 0.6)
+    cfg.p_groups = p
+    got = ctx.run_batch(states, cfg, plan, mode)
+    want = oracle.run_batch(states, cfg, plan, mode, 4)
+    _parity(got, want)
+
+
+def test_multisegment_per_orbit(ctx, oracle):
+    """C3 (reduced): 2.5 periods per-orbit -> segments 1/1/0.5, exact chaining."""
+    states, plan, cfg = _setup(32, 96, 2.5, policy="per_orbit")
+    assert plan.segments() == 3
+    got = ctx.run_batch(states, cfg, plan, "independent")
+    want = oracle.run_batch(states, cfg, plan, "independent", 8)
+    _parity(got, want)
+    n = 96
+    for s in range(1, 3):
+        assert got.times[s * (n - 1)] == plan.boundaries[s]
+    assert np.array_equal(got.terminal_states[:, 1:], got.trajectories[:, -1, :])
+
+
+def test_backward_round_trip(ctx):
+    """test_propagator.cpp:192-212: forward then backward recovers the batch (1e-9)."""
+    states, plan, cfg = _setup(16, 64, 0.7, bodies="two_body")
+    fwd = ctx.run_batch(states, cfg, plan, "independent")
+    t_end = plan.boundaries[-1]
+    back_plan = ps.plan_segments(fwd.terminal_states[0], t_end, 0.0, ps.MU_SUN, "single", 64)
+    back = ctx.run_batch(fwd.terminal_states, cfg, back_plan, "independent")
+    d = ps.max_state_discrepancy(back.terminal_states[None, :, 1:], states[None, :, 1:])
+    assert d <= 1e-9
+
+
+def test_warm_beats_cold(ctx):
+    states, plan, cfg = _setup(6, 96, 0.6)
+    warm = ctx.run_batch(states, cfg, plan, "independent")
+    cfg.start_mode = "cold"
+    cold = ctx.run_batch(states, cfg, plan, "independent")
+    assert (warm.iterations < cold.iterations).all()
+
+
+def test_nonconvergence_partial(ctx, oracle):
+    states, plan, cfg = _setup(4, 64, 0.8, bodies="two_body", start="cold")
+    cfg.max_iterations = 3
+    with pytest.raises(ps.PropagationIncompleteError) as e:
+        ctx.propagate(states, [2, 2], plan, cfg)
+    with pytest.raises(ps.PropagationIncompleteError) as e_ref:
+        oracle.propagate(states, [2, 2], plan, cfg)
+    assert (e.value.segment, e.value.group) == (0, 0) == (e_ref.value.segment, e_ref.value.group)
+    assert not e.value.partial.reports[0][0].converged
+
+
+def test_timeout(ctx):
+    states, plan, cfg = _setup(4, 64, 0.1)
+    cfg.timeout_s = 1e-9
+    with pytest.raises(ps.TimeoutError):
+        ctx.propagate(states, [4], plan, cfg)
+
+
+def test_mixed_epochs_rejected(ctx):
+    states, plan, cfg = _setup(3, 16, 0.1, bodies="two_body")
+    states[2, 0] = 10.0
+    with pytest.raises(ps.AlignmentError, match="state 2"):
+        ctx.propagate(states, [3], plan, cfg)
+
+
+def test_divergence_reports_first_non_finite(ctx, oracle):
+    """A trajectory through the Sun's centre blows up; the first non-finite
+    (node, column) in row-major order is reported (picard.hpp:26-36)."""
+    states, plan, cfg = _setup(3, 32, 0.5, bodies="two_body", start="cold")
+    states[1, 4:7] = 0.0  # radial plunge
+    errs = []
+    for impl in (ctx, oracle):
+        try:
+            impl.propagate(states, [3], plan, cfg)
+            errs.append(None)
+        except ps.Error as ex:  # DivergenceError or SingularityError depending on the path
+            errs.append(ex)
+    assert type(errs[0]) is type(errs[1])
+    assert str(errs[0]) == str(errs[1])
