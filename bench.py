@@ -1,0 +1,293 @@
+#!/usr/bin/env python3
+"""Throughput benchmark: trajectories propagated/sec (N-body PC) on B200.
+
+Workload (BASELINE.json configs[1], "C2"): 1,000 perturbed clones of the
+reference spacecraft state (a = 1.25e8 km, e = 0.12; make_clone_batch spread
+1e-5, seed 20220411) per GPU, Sun + 8 planets Newtonian N-body, N = 200
+Chebyshev-Lobatto nodes, one 0.87-period segment, warm start, tol 1e-12
+relative, per-trajectory convergence masking (RunMode::independent).
+
+One step = one propagation of the whole batch through the C-ABI
+(pswarm_run_batch): host ICs in -> terminal states in host memory out.
+  value     trajectories/s over the device solve phase (inputs resident in HBM),
+            whole job, max over ranks (weak scaling: 1,000 ICs per GPU)
+  e2e       trajectories/s of the full C-ABI call with host buffers (H2D of the
+            ICs, solve, D2H of terminal states; + NCCL gather when N > 1)
+  roofline  algorithmic FP64 flops of the PC kernel (F_it =
+            12N^2 + (75+20B)N + 12 per trajectory-iteration) / kernel time vs the
+            measured FP64 (DMMA) peak in profiles/fp64_peak_r01.json
+`--impl reference` times the CPU oracle (Eigen-free restatement of the
+reference, all host cores) on the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "trajectories propagated/sec (N-body PC) at 1/2/4/8 B200 vs CPU host cores"
+UNIT = "trajectories/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--per-gpu", type=int, default=1000, help="trajectories per GPU (weak scaling)")
+    ap.add_argument("--nodes", type=int, default=200)
+    ap.add_argument("--bodies", default="planets8", choices=["planets8", "reference"])
+    ap.add_argument("--span", type=float, default=0.87, help="span in osculating periods")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def workload(args, world, rank):
+    import paper_2301_03989_b200 as ps
+    base = ps.reference_state()
+    period = ps.osculating_period(base, ps.MU_SUN)
+    total = args.per_gpu * world
+    states = ps.make_clone_batch(base, total, 1e-5)
+    lo, hi = rank * args.per_gpu, (rank + 1) * args.per_gpu  # singleton groups: any split is group-aligned
+    plan = ps.plan_segments(base, 0.0, args.span * period, ps.MU_SUN, "single", args.nodes)
+    bodies = ps.planets8() if args.bodies == "planets8" else ps.reference_bodies()
+    cfg = ps.reference_force_config("n_body", bodies=bodies, n_nodes=args.nodes)
+    return states, (lo, hi), plan, cfg
+
+
+def config_dict(args, world):
+    return {
+        "workload": (f"C2: {args.per_gpu}-IC Earth-Venus arc per GPU (reference spacecraft a=1.25e8 km e=0.12, "
+                     f"clone spread 1e-5), Sun + {8 if args.bodies == 'planets8' else 2} planets Newtonian N-body, "
+                     f"N={args.nodes} nodes, {args.span} period single segment, warm start, tol 1e-12, "
+                     "per-trajectory convergence masking (independent mode)"),
+        "trajectories_per_gpu": args.per_gpu, "trajectories_total": args.per_gpu * world, "nodes": args.nodes,
+        "bodies": 8 if args.bodies == "planets8" else 2, "segments": 1, "dtype": "f64",
+        "parallelism": f"dp{world} (trajectory shards, no collective in the iteration loop)",
+        "l2": "flushed between steps (512 MiB device write, outside the timed region)",
+    }
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index):
+        self.path = f"/tmp/bench_clocks_{os.getpid()}.csv"
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(index), f"--query-gpu={q}", "--format=csv,noheader",
+                                          "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1].split()[0]))
+                mx.append(float(f[2].split()[0]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        os.unlink(self.path)
+        under = [s for s in sm if s > 0.5 * max(sm)] if sm else []
+        return {"sm_mhz": statistics.median(under) if under else None, "sm_max_mhz": max(mx) if mx else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def fp64_peak():
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "fp64_peak_r01.json")))
+        return max(d["dmma_w16_tflops"], d["dmma_w8_tflops"]), "measured (tools/fp64_peak.cu DMMA.8x8x4 loop)"
+    except (OSError, KeyError, ValueError):
+        return 37.0, "fallback (B200 FP64 nominal)"
+
+
+def ncu_traffic():
+    """dram bytes per launch of the PC kernel from the committed ncu capture, or None."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
+        return d.get("bench_kernel", {}).get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        return None
+
+
+def run_reference(args):
+    """CPU oracle on the same workload, all host threads (rank 0 only)."""
+    from oracle.oracle_py import Oracle
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    states, (lo, hi), plan, cfg = workload(args, 1, 0)
+    orc = Oracle()
+    cores = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        orc.run_batch(states, cfg, plan, "independent", cores, samples=False)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        orc.run_batch(states, cfg, plan, "independent", cores, samples=False)
+        times.append(time.perf_counter() - t0)
+    ms = 1e3 * statistics.mean(times)
+    v = len(states) / (ms * 1e-3)
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": round(v, 2), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config_dict(args, 1),
+        "e2e": {"value": round(v, 2), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "cpu_baseline": {"value": round(v, 2), "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"full workload ({len(states)} trajectories) per step, run_batch independent mode "
+                                   f"with {cores} worker threads (oracle/pswarm_ref.hpp restatement; the reference "
+                                   "needs Eigen, absent here)"},
+    }), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+
+    import paper_2301_03989_b200 as ps
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    ctx = ps.Context(local)
+    states, (lo, hi), plan, cfg = workload(args, world, rank)
+    shard = torch.from_numpy(states[lo:hi].copy()).pin_memory().numpy()  # pinned host ICs
+    M = hi - lo
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    gathered = torch.empty((M * world, 7), dtype=torch.float64, device=dev) if world > 1 else None
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+        torch.cuda.synchronize(dev)
+
+    def step():
+        r = ctx.run_batch(shard, cfg, plan, "independent", samples=False, history=False)
+        if world > 1:  # final gather of terminal states over NVLink (NCCL)
+            term = torch.from_numpy(r.terminal_states).to(dev, non_blocking=False)
+            dist.all_gather_into_tensor(gathered, term)
+            if rank == 0:
+                gathered.cpu()
+        return r
+
+    for _ in range(args.warmup):
+        step()
+    clocks = Clocks(local)
+    wall, dev_ms, ker_ms, iters, launches = [], [], [], [], 0
+    for _ in range(args.steps):
+        flush.fill_(1.0)  # L2 flush (outside the timed region)
+        barrier()
+        t0 = time.perf_counter()
+        r = step()
+        barrier()
+        wall.append(time.perf_counter() - t0)
+        dev_ms.append(r.device_ms)
+        ker_ms.append(r.kernel_ms)
+        iters.append(r.trajectory_iterations)
+        launches += 1  # k_pc_segment launches per step (one segment)
+    clk = clocks.stop()
+
+    def gmax(x):
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    wall_ms = gmax(1e3 * statistics.mean(wall))
+    dms = gmax(statistics.mean(dev_ms))
+    kms_mean = statistics.mean(ker_ms)
+    total = M * world
+    value = total / (dms * 1e-3)
+    e2e = total / (wall_ms * 1e-3)
+    B = len(cfg.bodies)
+    n = args.nodes
+    f_it = 12 * n * n + (75 + 20 * B) * n + 12
+    flops = f_it * statistics.mean(iters)
+    achieved = flops / (kms_mean * 1e-3) / 1e12
+    peak, peak_src = fp64_peak()
+
+    out = None
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            cpu = cpu_baseline(args, states[lo:hi], plan, cfg, r_check=ctx.run_batch(shard, cfg, plan, "independent"))
+        out = {
+            "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(dms, 4), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded clone cloud, analytic planets)",
+            "config": config_dict(args, world),
+            "e2e": {"value": round(e2e, 1), "unit": UNIT, "ms_per_step": round(wall_ms, 4),
+                    "h2d_bytes_per_step": int(M * 7 * 8), "d2h_bytes_per_step": int(M * 7 * 8),
+                    "path": "pswarm_run_batch C-ABI, pinned host buffers" + (" + NCCL all_gather" if world > 1 else "")},
+            "roofline": {"bound": "tensor", "achieved": round(achieved, 3), "peak": round(peak, 3), "unit": "TFLOP/s",
+                         "frac": round(achieved / peak, 4), "traffic": ncu_traffic(),
+                         "kernel": "k_pc_segment", "kernel_ms": round(kms_mean, 4),
+                         "flops_per_launch": flops, "peak_source": peak_src,
+                         "note": "FP64 DMMA/DFMA share one pipe on B200 (tools/fp64_peak.cu mixed test)"},
+            "cpu_baseline": cpu,
+            "clocks": clk,
+            "gpu_launches": launches,
+            "picard_iterations_per_trajectory": round(statistics.mean(iters) / M, 3),
+        }
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.barrier(device_ids=[local])
+        dist.destroy_process_group()
+
+
+def cpu_baseline(args, states, plan, cfg, r_check):
+    """CPU oracle (all host cores) on the same workload; also checks parity of this run."""
+    import paper_2301_03989_b200 as ps
+    from oracle.oracle_py import Oracle
+    orc = Oracle()
+    cores = os.cpu_count() or 1
+    times = []
+    ref = None
+    for _ in range(2):
+        t0 = time.perf_counter()
+        ref = orc.run_batch(states, cfg, plan, "independent", cores)
+        times.append(time.perf_counter() - t0)
+    v = len(states) / min(times)
+    disc = ps.max_state_discrepancy(r_check.trajectories, ref.trajectories)
+    diter = int(np.abs(r_check.iterations.astype(int) - ref.iterations.astype(int)).max())
+    return {"value": round(v, 2), "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"full workload ({len(states)} trajectories), best of 2, run_batch independent mode, "
+                      f"{cores} threads (oracle/pswarm_ref.hpp)",
+            "parity_vs_gpu": {"max_rel_state_discrepancy": disc, "max_abs_iteration_diff": diter}}
+
+
+if __name__ == "__main__":
+    main()

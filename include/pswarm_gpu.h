@@ -135,9 +135,15 @@ const char* pswarm_status_name(int32_t status);
 pswarm_status pswarm_create(int32_t device, pswarm_ctx** out, pswarm_error* err);
 void pswarm_destroy(pswarm_ctx* ctx);
 
-/* Tuning knobs: "ctas_per_sm" (persistent CTAs per SM, default 1) and
- * "max_ctas" (cap on the persistent grid, 0 = SM count * ctas_per_sm). */
+/* Tuning knobs: "ctas_per_sm" (persistent CTAs per SM, default 1), "max_ctas" (cap
+ * on the persistent grid, 0 = SM count * ctas_per_sm), "profile_phases" (1 = record
+ * per-phase SM cycles of the solve kernel, read with pswarm_get_phase_cycles). */
 pswarm_status pswarm_set_option(pswarm_ctx* ctx, const char* key, int64_t value);
+
+/* Diagnostics: SM cycles summed over CTAs per kernel phase of the last call
+ * (0 claim, 1 warm start, 2 force, 3 DMMA, 4 anchor barrier, 5 epilogue, 6 staged
+ * epilogue, 7 decisions, 8 retire, 9 = CTA count). */
+pswarm_status pswarm_get_phase_cycles(pswarm_ctx* ctx, uint64_t* out, int32_t n);
 
 /* ---- batch API (the drop-in boundary) ---------------------------------- */
 

@@ -300,6 +300,17 @@ class Context:
         if self.lib.pswarm_set_option(self.ptr, key.encode(), int(value)) != _abi.OK:
             raise Error(f"unknown option {key}")
 
+    PHASE_NAMES = ("claim", "warm_start", "force", "dmma", "anchor_barrier", "epilogue", "staged_epilogue",
+                   "decisions", "retire")
+
+    def phase_cycles(self) -> dict:
+        """Per-phase SM cycles of the last solve (requires set_option('profile_phases', 1))."""
+        buf = (C.c_uint64 * 10)()
+        self.lib.pswarm_get_phase_cycles(self.ptr, buf, 10)
+        d = {n: int(buf[k]) for k, n in enumerate(self.PHASE_NAMES)}
+        d["ctas"] = int(buf[9])
+        return d
+
     # ---- batch API ------------------------------------------------------
     def propagate(self, states, group_sizes, plan: SegmentPlan, config: PropagationConfig, *,
                   samples=True, history=True, terminal=True) -> PropagationResult:

@@ -10,8 +10,8 @@
 //                       components), K = N, operator streamed from L2, F from smem.
 //
 // Layout conventions (DESIGN.md §Data layout):
-//   Ybuf  smem  [node j][component c][slot t], row stride YS doubles (bank-conflict-free
-//               double2 epilogue stores);
+//   Ybuf  smem  [node j][component c ^ (j&1)][slot t], row stride 48 doubles (the pair
+//               swap on odd rows makes the double2 epilogue stores bank-conflict-free);
 //   Fbuf  smem  fragment-native B operand: [kstep][ntile pair][lane][2] doubles, so every
 //               B-fragment fetch of a warp is one contiguous 512-byte LDS.128;
 //   Upack gmem  fragment-native A operand: [mtile][kstep pair][lane] double2 (LDG.128).
@@ -24,7 +24,6 @@ namespace pswarm_dev {
 
 constexpr int SLOTS = 8;             // trajectories per CTA tile
 constexpr int COLS = 6 * SLOTS;      // 48 block columns: column = comp*8 + slot
-constexpr int YS = 56;               // Ybuf row stride in doubles (48 + 8 pad)
 constexpr double PI = 3.141592653589793238462643383279502884;
 
 // ---------------------------------------------------------------- DMMA ---
@@ -117,6 +116,54 @@ __device__ __forceinline__ int kepler_propagate(const double r[3], const double 
     return CONIC_OK;
 }
 
+/// Position of an analytic body at epoch t (elements_to_state, kepler.hpp:102-131); the
+/// host has already validated the elements (bound conic).
+__device__ __forceinline__ int elements_position(const double* el, double mu, double t, double out[3], double* m_fail) {
+    const double a = el[0], e = el[1], inc = el[2], raan = el[3], argp = el[4], m0 = el[5], ep = el[6];
+    const double n = sqrt(mu / (a * a * a));
+    const double m = m0 + n * (t - ep);
+    double ea;
+    if (solve_kepler(m, e, &ea) != CONIC_OK) {
+        *m_fail = m;
+        return CONIC_SOLVER;
+    }
+    double se, ce, so, co, si, ci, sw, cw;
+    sincos(ea, &se, &ce);
+    sincos(raan, &so, &co);
+    sincos(inc, &si, &ci);
+    sincos(argp, &sw, &cw);
+    const double beta = sqrt(1.0 - e * e);
+    const double xp = a * (ce - e), yp = a * beta * se;
+    const double p[3] = {co * cw - so * sw * ci, so * cw + co * sw * ci, sw * si};
+    const double q[3] = {-co * sw - so * cw * ci, -so * sw + co * cw * ci, cw * si};
+    for (int c = 0; c < 3; ++c) out[c] = xp * p[c] + yp * q[c];
+    return CONIC_OK;
+}
+
+/// Clenshaw evaluation of a Chebyshev series (ephemeris.hpp:29-38).
+__device__ __forceinline__ double clenshaw(const double* c, int nc, double x) {
+    double b1 = 0.0, b2 = 0.0;
+    for (int k = nc - 1; k >= 1; --k) {
+        const double b0 = c[k] + 2.0 * x * b1 - b2;
+        b2 = b1;
+        b1 = b0;
+    }
+    return c[0] + x * b1 - b2;
+}
+
+/// 1/sqrt(x) for normal positive x: MUFU.RSQ64H seed (rsqrt.approx.f64, ~2^-23) and
+/// two Newton steps (error < 1 ulp level).  The force arguments are squared distances
+/// of 1e-2..1e20 km^2, far from the denormal/overflow cases CUDA's rsqrt() guards
+/// with a slow-path branch.
+__device__ __forceinline__ double rsqrt_nr(double x) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    const double hx = 0.5 * x;
+    y = y * fma(-hx * y, y, 1.5);
+    y = y * fma(-hx * y, y, 1.5);
+    return y;
+}
+
 // ---------------------------------------------------------------- force ---
 /// Per-segment force data.  body_pos [N][B][3] frozen per node (ephemeris.hpp:89-107);
 /// indirect [N][3] = sum_b mu_b r_b/|r_b|^3, the node-constant half of
@@ -134,8 +181,9 @@ struct ForceData {
 /// Acceleration at node j (force_model.hpp:57-69).  Returns -1 when finite and legal,
 /// else the index of the first failing check in reference order: 0 = central body
 /// (|r| not > 0, force_model.hpp:28), 1 + b = body b closer than the floor (:44).
-__device__ __forceinline__ int accel(double rx, double ry, double rz, int j, const ForceData& fd, double& ax,
-                                     double& ay, double& az) {
+/// `bp` = this node's [B][3] body positions, `ind` = its indirect term (shared or global).
+__device__ __forceinline__ int accel(double rx, double ry, double rz, const double* bp, const double* ind,
+                                     const ForceData& fd, double& ax, double& ay, double& az) {
     const double r2 = rx * rx + ry * ry + rz * rz;
     if (!(r2 > 0.0)) return 0;
     const double ir = rsqrt(r2);
@@ -145,23 +193,23 @@ __device__ __forceinline__ int accel(double rx, double ry, double rz, int j, con
     az = s * rz;
     const int B = fd.n_bodies;
     if (B > 0) {
-        const double* bp = fd.body_pos + static_cast<size_t>(j) * B * 3;
+        int fail = -1;
         for (int b = 0; b < B; ++b) {
-            const double dx = __ldg(bp + 3 * b + 0) - rx;
-            const double dy = __ldg(bp + 3 * b + 1) - ry;
-            const double dz = __ldg(bp + 3 * b + 2) - rz;
+            const double dx = bp[3 * b + 0] - rx;
+            const double dy = bp[3 * b + 1] - ry;
+            const double dz = bp[3 * b + 2] - rz;
             const double d2 = dx * dx + dy * dy + dz * dz;
-            if (d2 < fd.floor2_hi && sqrt(d2) < fd.floor_km) return 1 + b;
+            if (d2 < fd.floor2_hi && fail < 0 && sqrt(d2) < fd.floor_km) fail = 1 + b;
             const double id = rsqrt(d2);
             const double k = __ldg(fd.body_mu + b) * (id * id * id);
             ax += k * dx;
             ay += k * dy;
             az += k * dz;
         }
-        const double* ind = fd.indirect + 3 * j;
-        ax -= __ldg(ind + 0);
-        ay -= __ldg(ind + 1);
-        az -= __ldg(ind + 2);
+        ax -= ind[0];
+        ay -= ind[1];
+        az -= ind[2];
+        return fail;
     }
     return -1;
 }
@@ -170,12 +218,17 @@ __device__ __forceinline__ int accel(double rx, double ry, double rz, int j, con
 __device__ __forceinline__ double check_distance(double rx, double ry, double rz, int j, int check,
                                                  const ForceData& fd) {
     if (check <= 0) return sqrt(rx * rx + ry * ry + rz * rz);
-    const double* bp = fd.body_pos + (static_cast<size_t>(j) * fd.n_bodies + (check - 1)) * 3;
+    const double* bp = fd.body_pos + (static_cast<size_t>(j) * fd.n_bodies + (check - 1)) * 3;  // global copy
     const double dx = bp[0] - rx, dy = bp[1] - ry, dz = bp[2] - rz;
     return sqrt(dx * dx + dy * dy + dz * dz);
 }
 
 // ----------------------------------------------------------- tile GEMM ---
+/// Ybuf address of (node j, component c, slot t): components of odd rows are
+/// pair-swapped so the 8 rows of an MMA fragment hit two 64-byte bank windows
+/// (conflict-free double2 epilogue stores with a 48-double row stride).
+__device__ __forceinline__ int yidx(int j, int c, int t) { return j * COLS + ((c ^ (j & 1)) << 3) + t; }
+
 /// Fragment-native index of B element (k, n) in Fbuf (doubles): B fragment of
 /// mma.m8n8k4 holds B[k = lane%4][n = lane/4]; two n-tiles share one double2.
 __device__ __forceinline__ int fbuf_index(int k, int n) {
@@ -183,48 +236,137 @@ __device__ __forceinline__ int fbuf_index(int k, int n) {
     return (((ks * 3 + (nt >> 1)) * 32) + (nn * 4 + kk)) * 2 + (nt & 1);
 }
 
-/// One warp's share of Y' = U'·F: m-tiles 2w and 2w+1 (16 rows) × 48 columns.
-/// Operator pairs (two k-steps) arrive as one LDG.128 per m-tile from L2 with a
-/// two-deep register prefetch; B fragments are LDS.128 from the fragment-native Fbuf.
+/// Warp work plan of the 8-row x 8-column output tiles (mtiles x 6 n-tiles).
+/// Warp w owns `main` full-width m-tiles [w*main, w*main+main) plus up to XMAX single
+/// extra tiles e = w + k*warps (< extras): m-tile mb + e/6, n-tile e%6.  The host picks
+/// warps as a multiple of 4 so every SM sub-partition (SMSP) issues the same number of
+/// DMMAs — the DMMA pipe is per SMSP, so an uneven warp count idles three of them.
+struct GemmPlan {
+    int warps;   // multiple of 4
+    int main;    // full-width m-tiles per warp (0..2)
+    int mb;      // first extra m-tile = main*warps
+    int extras;  // number of extra (m-tile, n-tile) tiles
+    int mtiles;  // ceil((N+1)/8), row N is the anchor row
+    int xmax;    // extra tiles per warp the kernel variant holds (XMAX or XMAX_SMALL)
+};
+constexpr int XMAX = 2;        // extra tiles per warp, large-N kernels
+constexpr int XMAX_SMALL = 6;  // extra tiles per warp, N < 63 (fewer than 8 m-tiles)
+
+/// Per-warp operator pointers (one per owned tile row-block), hoisted out of the
+/// k loop; pair kp of a tile is at ptr + kp*32.
+template <int XM>
+struct AWarp {
+    const double2* m0;
+    const double2* m1;
+    const double2* x[XM];
+    int xoff[XM];  // B-fragment double offset of the extra tile's n-tile within a k-step
+    bool hx[XM];
+};
+
+template <int XM>
+__device__ __forceinline__ AWarp<XM> a_warp(const double2* __restrict__ upack, int nkp, const GemmPlan& gp, int warp,
+                                            int lane) {
+    AWarp<XM> w;
+    w.m0 = upack + static_cast<size_t>(warp * gp.main) * nkp * 32 + lane;
+    w.m1 = w.m0 + static_cast<size_t>(nkp) * 32;
+#pragma unroll
+    for (int x = 0; x < XM; ++x) {
+        const int e = warp + x * gp.warps;
+        w.hx[x] = e < gp.extras;
+        const int mt = w.hx[x] ? gp.mb + e / 6 : 0;
+        w.x[x] = upack + static_cast<size_t>(mt) * nkp * 32 + lane;
+        const int n = e % 6;
+        w.xoff[x] = ((n >> 1) * 32 + lane) * 2 + (n & 1);  // + ks*192 per k-step
+    }
+    return w;
+}
+
+template <int XM>
+struct APair {  // one k-step pair of A fragments for every tile the warp owns
+    double2 m0, m1, x[XM];
+};
+
+template <int XM>
+__device__ __forceinline__ void load_apair(const AWarp<XM>& w, int nmain, int kp, APair<XM>& p) {
+    if (nmain > 0) p.m0 = __ldg(w.m0 + kp * 32);
+    if (nmain > 1) p.m1 = __ldg(w.m1 + kp * 32);
+#pragma unroll
+    for (int x = 0; x < XM; ++x)
+        if (w.hx[x]) p.x[x] = __ldg(w.x[x] + kp * 32);
+}
+
+/// Prefetched first k-step pair (issued before the force phase to hide L2 latency).
+template <int XM>
+struct APrefetch {
+    APair<XM> p;
+};
+
+template <int XM>
+__device__ __forceinline__ APrefetch<XM> gemm_prefetch(const double2* __restrict__ upack, int nkp, const GemmPlan& gp,
+                                                       int warp, int lane) {
+    APrefetch<XM> f;
+    const AWarp<XM> w = a_warp<XM>(upack, nkp, gp, warp, lane);
+    load_apair<XM>(w, gp.main, 0, f.p);
+    return f;
+}
+
+/// Two k-steps (one operator pair) of the warp's tiles.
+template <int XM>
+__device__ __forceinline__ void gemm_pair(const double* fbuf, const AWarp<XM>& w, int nmain, int lane, int kp,
+                                          const APair<XM>& c, double (&acc)[2][6][2], double (&xacc)[XM][2]) {
+    const double2* fb = reinterpret_cast<const double2*>(fbuf) + lane;
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+        const int ks = 2 * kp + s;
+        const double2 b01 = fb[(ks * 3 + 0) * 32];
+        const double2 b23 = fb[(ks * 3 + 1) * 32];
+        const double2 b45 = fb[(ks * 3 + 2) * 32];
+        const double bv[6] = {b01.x, b01.y, b23.x, b23.y, b45.x, b45.y};
+        double bx[XM];
+#pragma unroll
+        for (int x = 0; x < XM; ++x) bx[x] = w.hx[x] ? fbuf[ks * 192 + w.xoff[x]] : 0.0;
+        if (nmain > 0) {
+            const double a0 = s ? c.m0.y : c.m0.x;
+#pragma unroll
+            for (int n = 0; n < 6; ++n) dmma(acc[0][n][0], acc[0][n][1], a0, bv[n]);
+        }
+        if (nmain > 1) {
+            const double a1 = s ? c.m1.y : c.m1.x;
+#pragma unroll
+            for (int n = 0; n < 6; ++n) dmma(acc[1][n][0], acc[1][n][1], a1, bv[n]);
+        }
+#pragma unroll
+        for (int x = 0; x < XM; ++x)
+            if (w.hx[x]) dmma(xacc[x][0], xacc[x][1], s ? c.x[x].y : c.x[x].x, bx[x]);
+    }
+}
+
+/// One warp's share of Y' = [U; anchor]·F: `main` full-width m-tiles (acc) and up to
+/// XM extra tiles (xacc).  Operator pairs come from L2 as LDG.128, double-buffered in
+/// registers (one pair in flight while the other feeds the DMMAs; a pair is ~400 DMMA
+/// cycles per warp, well above L2 latency); B fragments are contiguous LDS.128 from
+/// the fragment-native Fbuf.
+template <int XM>
 __device__ __forceinline__ void warp_gemm(const double2* __restrict__ upack, int nkp, const double* fbuf,
-                                          int warp, int lane, double (&acc)[2][6][2]) {
+                                          const GemmPlan& gp, int warp, int lane, APrefetch<XM> pre,
+                                          double (&acc)[2][6][2], double (&xacc)[XM][2]) {
 #pragma unroll
     for (int i = 0; i < 2; ++i)
 #pragma unroll
         for (int n = 0; n < 6; ++n) acc[i][n][0] = acc[i][n][1] = 0.0;
-    const double2* a0 = upack + static_cast<size_t>(2 * warp) * nkp * 32 + lane;
-    const double2* a1 = a0 + static_cast<size_t>(nkp) * 32;
-    const double2* fb = reinterpret_cast<const double2*>(fbuf) + lane;
-    double2 p0 = __ldg(a0), p1 = __ldg(a1);
-    double2 q0 = p0, q1 = p1;
-    if (nkp > 1) {
-        q0 = __ldg(a0 + 32);
-        q1 = __ldg(a1 + 32);
-    }
-    for (int kp = 0; kp < nkp; ++kp) {
-        const double2 c0 = p0, c1 = p1;
-        p0 = q0;
-        p1 = q1;
-        if (kp + 2 < nkp) {
-            q0 = __ldg(a0 + (kp + 2) * 32);
-            q1 = __ldg(a1 + (kp + 2) * 32);
-        }
 #pragma unroll
-        for (int s = 0; s < 2; ++s) {
-            const int ks = 2 * kp + s;
-            const double2 b01 = fb[(ks * 3 + 0) * 32];
-            const double2 b23 = fb[(ks * 3 + 1) * 32];
-            const double2 b45 = fb[(ks * 3 + 2) * 32];
-            const double bv[6] = {b01.x, b01.y, b23.x, b23.y, b45.x, b45.y};
-            const double av0 = s ? c0.y : c0.x;
-            const double av1 = s ? c1.y : c1.x;
-#pragma unroll
-            for (int n = 0; n < 6; ++n) {
-                dmma(acc[0][n][0], acc[0][n][1], av0, bv[n]);
-                dmma(acc[1][n][0], acc[1][n][1], av1, bv[n]);
-            }
-        }
+    for (int x = 0; x < XM; ++x) xacc[x][0] = xacc[x][1] = 0.0;
+    const AWarp<XM> w = a_warp<XM>(upack, nkp, gp, warp, lane);
+    const int nmain = gp.main;
+    APair<XM> p0 = pre.p, p1;
+    int kp = 0;
+    for (; kp + 1 < nkp; kp += 2) {
+        load_apair<XM>(w, nmain, kp + 1, p1);
+        gemm_pair<XM>(fbuf, w, nmain, lane, kp, p0, acc, xacc);
+        if (kp + 2 < nkp) load_apair<XM>(w, nmain, kp + 2, p0);
+        gemm_pair<XM>(fbuf, w, nmain, lane, kp + 1, p1, acc, xacc);
     }
+    if (kp < nkp) gemm_pair<XM>(fbuf, w, nmain, lane, kp, p0, acc, xacc);
 }
 
 }  // namespace pswarm_dev

@@ -28,9 +28,9 @@ struct CtaState {
     int slot_member[SLOTS];    // member index within its group
     int sing_key[SLOTS];       // min j*(B+1)+check this tick
     int nf_key[SLOTS];         // min j*8+c non-finite this tick
-    int warm_key[SLOTS];       // min node with a warm-start fault
+    int warm_key[SLOTS];       // min node*4+kind with a warm-start fault
     int warm_kind[SLOTS];
-    unsigned long long slot_err[SLOTS];
+    unsigned long long slot_err[SLOTS];  // max squared error ratio (bit pattern)
     double sing_val[SLOTS];
     double warm_val[SLOTS][2];
     double y0[SLOTS][6];
@@ -48,29 +48,222 @@ struct CtaState {
 
 __device__ __forceinline__ int popc(int x) { return __popc(static_cast<unsigned>(x)); }
 
+// Optional per-phase cycle accounting (pswarm_set_option "profile_phases"): thread 0
+// stamps clock64() at phase ends; the sums land in a.phase_cycles[PHASES].
+#define PHASE(k)                                            \
+    do {                                                    \
+        if (prof && tid == 0) {                             \
+            const long long now_ = clock64();               \
+            pc[(k)] += now_ - t_prev;                       \
+            t_prev = now_;                                  \
+        }                                                   \
+    } while (0)
+
+
+struct SmemLayout {
+    size_t ybuf, fbuf, xstage, eph, state, total;  // byte offsets
+};
+
+__host__ __device__ inline SmemLayout smem_layout(int N, int nkp, int xrows, int B, int stage_eph) {
+    SmemLayout L;
+    L.ybuf = 0;
+    L.fbuf = L.ybuf + sizeof(double) * static_cast<size_t>(N) * COLS;
+    L.xstage = L.fbuf + sizeof(double) * static_cast<size_t>(8 * nkp) * COLS;
+    L.eph = L.xstage + sizeof(double) * static_cast<size_t>(xrows) * COLS;
+    L.state = L.eph + (stage_eph ? sizeof(double) * static_cast<size_t>(N) * (3 * B + 3) : 0);
+    L.total = L.state + sizeof(CtaState);
+    return L;
+}
+
+/// Per-sample finite check (picard.hpp:26-36) and convergence error of one (node, slot)
+/// against the previous iterate (augment.hpp:38-51, component_error of
+/// error_metric.hpp:15-23).  The squared ratio max(|dr|^2/|r|^2, |dv|^2/|v|^2) is kept as
+/// a (numerator, denominator) pair and maximised by cross-multiplication, so a lane
+/// pays one division for all its samples; max commutes with the final sqrt.
+__device__ __forceinline__ void update_sample(const double (&yn)[6], const double (&yo)[6], int j, int error_mode,
+                                              double& bn, double& bd, int& nf) {
+#pragma unroll
+    for (int c = 5; c >= 0; --c)
+        if (!isfinite(yn[c])) nf = min(nf, j * 8 + c);
+    double dr2 = 0.0, r2 = 0.0, dv2 = 0.0, v2 = 0.0;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        const double dr = yn[c] - yo[c], dv = yn[c + 3] - yo[c + 3];
+        dr2 += dr * dr;
+        r2 += yo[c] * yo[c];
+        dv2 += dv * dv;
+        v2 += yo[c + 3] * yo[c + 3];
+    }
+    if (error_mode == 1) {
+        r2 = 1.0;
+        v2 = 1.0;
+    } else {
+        r2 = fmax(r2, 1e-60);
+        v2 = fmax(v2, 1e-60);
+    }
+    if (dr2 * bd > bn * r2) {
+        bn = dr2;
+        bd = r2;
+    }
+    if (dv2 * bd > bn * v2) {
+        bn = dv2;
+        bd = v2;
+    }
+}
+
 }  // namespace
 
-size_t segment_smem_bytes(int N, int nkp) {
-    return sizeof(double) * (static_cast<size_t>(N) * YS + static_cast<size_t>(8 * nkp) * COLS) + sizeof(CtaState);
+size_t segment_smem_bytes(int N, int nkp, int xrows, int B, int stage_eph) {
+    return smem_layout(N, nkp, xrows, B, stage_eph).total;
 }
 
-int segment_threads(int N) {
-    const int mt = (N + 1 + 7) / 8;
-    return 32 * ((mt + 1) / 2);
+GemmPlan make_gemm_plan(int N) {
+    GemmPlan gp{};
+    gp.mtiles = (N + 1 + 7) / 8;
+    if (gp.mtiles < 8) {  // small N: 4 warps, up to XMAX_SMALL single tiles each
+        gp.warps = 4;
+        gp.main = gp.mtiles / 4;
+        gp.mb = gp.main * 4;
+        gp.extras = (gp.mtiles - gp.mb) * 6;
+        gp.xmax = XMAX_SMALL;
+        return gp;
+    }
+    for (int w = 4 * (gp.mtiles / 8);; w += 4) {
+        const int main = gp.mtiles / w < 2 ? gp.mtiles / w : 2;
+        const int extras = (gp.mtiles - main * w) * 6;
+        if ((extras + w - 1) / w <= XMAX) {
+            gp.warps = w;
+            gp.main = main;
+            gp.mb = main * w;
+            gp.extras = extras;
+            gp.xmax = XMAX;
+            break;
+        }
+    }
+    return gp;
 }
 
-template <int MAXT>
-__global__ void __launch_bounds__(MAXT, 1) k_pc_segment(const SegArgs a) {
-    extern __shared__ __align__(16) double smem[];
-    const int N = a.N;
-    double* ybuf = smem;
-    double* fbuf = ybuf + static_cast<size_t>(N) * YS;
-    const int KP = 8 * a.nkp;
-    CtaState& st = *reinterpret_cast<CtaState*>(fbuf + static_cast<size_t>(KP) * COLS);
-    const int tid = threadIdx.x, nthr = blockDim.x, warp = tid >> 5, lane = tid & 31;
+int extra_rows(int N, const GemmPlan& gp) {
+    const int r = N - gp.mb * 8;
+    return r > 0 ? r : 0;
+}
+
+/// Force for FS slots of node jq (+ optionally one extra sample (jx, tx)) as
+/// independent chains: a = -mu r/|r|^3 + sum_b mu_b (d_b/|d_b|^3) - indirect(j),
+/// F = omega2 [v; a] written in MMA B-fragment order (force_model.hpp:93-142).
+/// Singularity guards run exactly, in reference order, on a rare slow path.
+template <int FS, bool X>
+__device__ __forceinline__ void force_chains(const SegArgs& a, const double* ybuf, double* fbuf, CtaState& st,
+                                             const double* pos_base, const double* ind_base, int act, int jq, int t0,
+                                             int jx, int tx) {
+    constexpr int K = FS + (X ? 1 : 0);
     const int B = a.fd.n_bodies;
+    int jj[K], tt[K];
+    double rx[K], ry[K], rz[K], ax[K], ay[K], az[K];
+    bool on[K];
+    bool flag = false;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        jj[k] = k < FS ? jq : jx;
+        tt[k] = k < FS ? t0 + k : tx;
+        on[k] = (act >> tt[k]) & 1;
+        rx[k] = on[k] ? ybuf[yidx(jj[k], 0, tt[k])] : 1.0e8;  // benign stand-in keeps idle slots finite
+        ry[k] = on[k] ? ybuf[yidx(jj[k], 1, tt[k])] : 0.0;
+        rz[k] = on[k] ? ybuf[yidx(jj[k], 2, tt[k])] : 0.0;
+        const double r2 = rx[k] * rx[k] + ry[k] * ry[k] + rz[k] * rz[k];
+        flag |= !(r2 > 0.0);
+        const double ir = rsqrt_nr(r2);
+        const double sc = -a.fd.central_mu * (ir * ir * ir);
+        ax[k] = sc * rx[k];
+        ay[k] = sc * ry[k];
+        az[k] = sc * rz[k];
+    }
+    const double* bq = pos_base + static_cast<size_t>(jq) * 3 * B;
+    const double* bx_ = pos_base + static_cast<size_t>(jx) * 3 * B;
+    for (int b = 0; b < B; ++b) {
+        const double mu_b = __ldg(a.fd.body_mu + b);
+        const double qx = bq[3 * b], qy = bq[3 * b + 1], qz = bq[3 * b + 2];
+        double ex = 0.0, ey = 0.0, ez = 0.0;
+        if (X) {
+            ex = bx_[3 * b];
+            ey = bx_[3 * b + 1];
+            ez = bx_[3 * b + 2];
+        }
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const double px = k < FS ? qx : ex, py = k < FS ? qy : ey, pz = k < FS ? qz : ez;
+            const double dx = px - rx[k], dy = py - ry[k], dz = pz - rz[k];
+            const double d2 = dx * dx + dy * dy + dz * dz;
+            flag |= d2 < a.fd.floor2_hi;
+            const double id = rsqrt_nr(d2);
+            const double kk = mu_b * (id * id * id);
+            ax[k] += kk * dx;
+            ay[k] += kk * dy;
+            az[k] += kk * dz;
+        }
+    }
+    if (B > 0) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const double* ind = ind_base + 3 * jj[k];
+            ax[k] -= ind[0];
+            ay[k] -= ind[1];
+            az[k] -= ind[2];
+        }
+    }
+    if (flag) {  // rare: exact guard order of table_acceleration (force_model.hpp:57-69)
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            if (!on[k]) continue;
+            int fail = (rx[k] * rx[k] + ry[k] * ry[k] + rz[k] * rz[k] > 0.0) ? -1 : 0;
+            const double* bp = pos_base + static_cast<size_t>(jj[k]) * 3 * B;
+            for (int b = 0; b < B && fail < 0; ++b) {
+                const double dx = bp[3 * b] - rx[k], dy = bp[3 * b + 1] - ry[k], dz = bp[3 * b + 2] - rz[k];
+                if (sqrt(dx * dx + dy * dy + dz * dz) < a.fd.floor_km) fail = 1 + b;
+            }
+            if (fail >= 0) atomicMin(&st.sing_key[tt[k]], jj[k] * (B + 1) + fail);
+        }
+    }
+    const double w2 = a.omega2;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        const int j = jj[k], t = tt[k];
+        fbuf[fbuf_index(j, 0 * 8 + t)] = on[k] ? w2 * ybuf[yidx(j, 3, t)] : 0.0;
+        fbuf[fbuf_index(j, 1 * 8 + t)] = on[k] ? w2 * ybuf[yidx(j, 4, t)] : 0.0;
+        fbuf[fbuf_index(j, 2 * 8 + t)] = on[k] ? w2 * ybuf[yidx(j, 5, t)] : 0.0;
+        fbuf[fbuf_index(j, 3 * 8 + t)] = on[k] ? w2 * ax[k] : 0.0;
+        fbuf[fbuf_index(j, 4 * 8 + t)] = on[k] ? w2 * ay[k] : 0.0;
+        fbuf[fbuf_index(j, 5 * 8 + t)] = on[k] ? w2 * az[k] : 0.0;
+    }
+}
+
+template <int MAXT, int XM, bool STAGE, int FS>
+__global__ void __launch_bounds__(MAXT, 1) k_pc_segment(const SegArgs a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int N = a.N;
+    const int B = a.fd.n_bodies;
+    const GemmPlan gp = a.gp;
+    const SmemLayout L = smem_layout(N, a.nkp, a.xrows, B, a.stage_eph);
+    double* ybuf = reinterpret_cast<double*>(smem_raw + L.ybuf);
+    double* fbuf = reinterpret_cast<double*>(smem_raw + L.fbuf);
+    double* xstage = reinterpret_cast<double*>(smem_raw + L.xstage);
+    double* eph = reinterpret_cast<double*>(smem_raw + L.eph);
+    CtaState& st = *reinterpret_cast<CtaState*>(smem_raw + L.state);
+    const int KP = 8 * a.nkp;
+    const int tid = threadIdx.x, nthr = blockDim.x, warp = tid >> 5, lane = tid & 31;
+    const int g = lane >> 2, q = lane & 3;
+    const bool prof = a.phase_cycles != nullptr;
+    long long pc[PHASES] = {};
+    long long t_prev = clock64();
 
     for (int i = tid; i < KP * COLS; i += nthr) fbuf[i] = 0.0;
+    // frozen per-segment ephemeris [N][B][3] + indirect [N][3] staged once per launch
+    if (STAGE && B > 0) {
+        for (int i = tid; i < N * 3 * B; i += nthr) eph[i] = a.fd.body_pos[i];
+        for (int i = tid; i < N * 3; i += nthr) eph[N * 3 * B + i] = a.fd.indirect[i];
+    }
+    const double* pos_base = STAGE ? eph : a.fd.body_pos;
+    const double* ind_base = STAGE ? eph + N * 3 * B : a.fd.indirect;
     if (tid == 0) {
         for (int t = 0; t < SLOTS; ++t) {
             st.slot_traj[t] = -1;
@@ -85,26 +278,27 @@ __global__ void __launch_bounds__(MAXT, 1) k_pc_segment(const SegArgs a) {
     for (;;) {
         // ------------------------------------------------ claim + bookkeeping
         if (tid == 0) {
-            st.new_mask = 0;
-            int free_slots = SLOTS - popc(st.active_mask);
+            int new_mask = 0;
+            int am = st.active_mask;
+            const int free_slots = SLOTS - popc(am);
             if (!st.queue_done && free_slots >= a.gmax) {
                 const int k = free_slots / a.gmax;
                 const int g0 = atomicAdd(a.queue, k);
                 const int g1 = min(g0 + k, a.P);
                 if (g0 + k >= a.P) st.queue_done = 1;
-                for (int g = g0; g < g1; ++g) {
+                for (int gi = g0; gi < g1; ++gi) {
                     int lg = 0;
                     while (st.grp_id[lg] >= 0) ++lg;
-                    const int off = static_cast<int>(a.group_off[g]);
-                    const int size = static_cast<int>(a.group_off[g + 1]) - off;
-                    st.grp_id[lg] = g;
+                    const int off = static_cast<int>(a.group_off[gi]);
+                    const int size = static_cast<int>(a.group_off[gi + 1]) - off;
+                    st.grp_id[lg] = gi;
                     st.grp_size[lg] = size;
                     st.grp_iter[lg] = 0;
                     int t = 0;
                     for (int mbr = 0; mbr < size; ++mbr) {
-                        while ((st.active_mask >> t) & 1) ++t;
-                        st.active_mask |= 1 << t;
-                        st.new_mask |= 1 << t;
+                        while ((am >> t) & 1) ++t;
+                        am |= 1 << t;
+                        new_mask |= 1 << t;
                         st.slot_traj[t] = off + mbr;
                         st.slot_grp[t] = lg;
                         st.slot_member[t] = mbr;
@@ -112,26 +306,27 @@ __global__ void __launch_bounds__(MAXT, 1) k_pc_segment(const SegArgs a) {
                     }
                 }
             }
+            st.active_mask = am;
+            st.new_mask = new_mask;
             if (a.deadline_ns != 0ull && globaltimer_ns() > a.deadline_ns) st.timeout = 1;
-            for (int t = 0; t < SLOTS; ++t) {
-                st.slot_err[t] = 0ull;
-                st.sing_key[t] = INT_MAX;
-                st.nf_key[t] = INT_MAX;
-            }
-            st.retire_mask = 0;
-            st.free_mask = 0;
+        }
+        if (tid < SLOTS) {
+            st.slot_err[tid] = 0ull;
+            st.sing_key[tid] = INT_MAX;
+            st.nf_key[tid] = INT_MAX;
         }
         __syncthreads();
+        PHASE(0);
         if (st.active_mask == 0) break;
         if (st.timeout) {
             if (tid == 0) {
                 for (int lg = 0; lg < SLOTS; ++lg) {
-                    const int g = st.grp_id[lg];
-                    if (g < 0) continue;
-                    a.faults[g].status = FAULT_TIMEOUT;
-                    a.faults[g].iteration = st.grp_iter[lg];
-                    a.rep_iter[g] = st.grp_iter[lg];
-                    a.rep_conv[g] = 0;
+                    const int gi = st.grp_id[lg];
+                    if (gi < 0) continue;
+                    a.faults[gi].status = FAULT_TIMEOUT;
+                    a.faults[gi].iteration = st.grp_iter[lg];
+                    a.rep_iter[gi] = st.grp_iter[lg];
+                    a.rep_conv[gi] = 0;
                 }
             }
             break;
@@ -140,8 +335,8 @@ __global__ void __launch_bounds__(MAXT, 1) k_pc_segment(const SegArgs a) {
         // ------------------------------------------------ load + warm start
         const int new_mask = st.new_mask;
         if (new_mask) {
-            for (int t = tid; t < SLOTS * 6; t += nthr) {
-                const int s = t / 6, c = t % 6;
+            for (int i = tid; i < SLOTS * 6; i += nthr) {
+                const int s = i / 6, c = i % 6;
                 if ((new_mask >> s) & 1) st.y0[s][c] = a.state_in[static_cast<size_t>(st.slot_traj[s]) * 6 + c];
             }
             __syncthreads();
@@ -164,13 +359,11 @@ __global__ void __launch_bounds__(MAXT, 1) k_pc_segment(const SegArgs a) {
                     if (j == 0 && a.cold_fallback)
                         a.cold_fallback[st.slot_traj[t]] = (chk == CONIC_NON_ELLIPTIC) ? 1 : 0;
                 }
-                double* yp = ybuf + static_cast<size_t>(j) * YS + t;
-                yp[0] = ro[0];
-                yp[8] = ro[1];
-                yp[16] = ro[2];
-                yp[24] = vo[0];
-                yp[32] = vo[1];
-                yp[40] = vo[2];
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    ybuf[yidx(j, c, t)] = ro[c];
+                    ybuf[yidx(j, c + 3, t)] = vo[c];
+                }
             }
             __syncthreads();
             // rare path: describe warm-start faults (re-evaluate the failing node)
@@ -185,71 +378,88 @@ __global__ void __launch_bounds__(MAXT, 1) k_pc_segment(const SegArgs a) {
                 st.warm_val[t][0] = mf;
                 st.warm_val[t][1] = ef;
             }
-            __syncthreads();
         }
+        PHASE(1);
 
         // ------------------------------------------------ force -> Fbuf
+        // Thread = one node x FS slots (body positions read once, FS independent
+        // dependency chains); when N*8/FS exceeds the thread count the leftover
+        // samples ride along as one extra chain in the first warps, so every warp is
+        // busy for a single pass (the force shares the FP64 pipe with DMMA).
         const int act = st.active_mask;
-        const double w2 = a.omega2;
-        for (int i = tid; i < N * SLOTS; i += nthr) {
-            const int j = i >> 3, t = i & 7;
-            double f[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-            if ((act >> t) & 1) {
-                const double* yp = ybuf + static_cast<size_t>(j) * YS + t;
-                const double rx = yp[0], ry = yp[8], rz = yp[16];
-                double ax = 0.0, ay = 0.0, az = 0.0;
-                const int chk = accel(rx, ry, rz, j, a.fd, ax, ay, az);
-                if (chk >= 0) atomicMin(&st.sing_key[t], j * (B + 1) + chk);
-                f[0] = w2 * yp[24];
-                f[1] = w2 * yp[32];
-                f[2] = w2 * yp[40];
-                f[3] = w2 * ax;
-                f[4] = w2 * ay;
-                f[5] = w2 * az;
+        {
+            const int items = N * (SLOTS / FS);
+            const int extra = items > nthr ? (items - nthr) * FS : 0;  // leftover single samples
+            for (int it0 = tid; it0 < (items > nthr ? nthr : items); it0 += nthr) {
+                const int jq = it0 / (SLOTS / FS), t0 = (it0 % (SLOTS / FS)) * FS;
+                if (tid < extra) {
+                    const int sx = nthr * FS + tid;
+                    force_chains<FS, true>(a, ybuf, fbuf, st, pos_base, ind_base, act, jq, t0, sx >> 3, sx & 7);
+                } else {
+                    force_chains<FS, false>(a, ybuf, fbuf, st, pos_base, ind_base, act, jq, t0, 0, 0);
+                }
             }
-#pragma unroll
-            for (int c = 0; c < 6; ++c) fbuf[fbuf_index(j, c * 8 + t)] = f[c];
         }
+        // operator prefetch (L2 -> registers) overlaps the barrier wait
+        const APrefetch<XM> pre = gemm_prefetch<XM>(a.upack, a.nkp, gp, warp, lane);
+        PHASE(2);
         __syncthreads();
         if (tid < SLOTS && st.sing_key[tid] != INT_MAX) {
             const int t = tid, key = st.sing_key[t], j = key / (B + 1), chk = key % (B + 1);
-            const double* yp = ybuf + static_cast<size_t>(j) * YS + t;
-            st.sing_val[t] = check_distance(yp[0], yp[8], yp[16], j, chk, a.fd);
+            st.sing_val[t] = check_distance(ybuf[yidx(j, 0, t)], ybuf[yidx(j, 1, t)], ybuf[yidx(j, 2, t)], j, chk, a.fd);
         }
 
         // ------------------------------------------------ DMMA update
-        double acc[2][6][2];
-        warp_gemm(a.upack, a.nkp, fbuf, warp, lane, acc);
+        double acc[2][6][2], xacc[XM][2];
+        warp_gemm<XM>(a.upack, a.nkp, fbuf, gp, warp, lane, pre, acc, xacc);
+        PHASE(3);
+        // anchor row N -> b0/2 = (anchor_op·F + 2 y0)/2 (pc_matrices.hpp:138, :145)
         {
-            const int amt = N >> 3, ag = N & 7;
-            if (warp == (amt >> 1) && (lane >> 2) == ag) {
-                const int i = amt & 1, q = lane & 3;
+            const int amt = N >> 3;
+            if (g == (N & 7)) {
 #pragma unroll
-                for (int c = 0; c < 6; ++c)
+                for (int i = 0; i < 2; ++i) {
+                    if (i < gp.main && warp * gp.main + i == amt) {
 #pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        const int t = 2 * q + h;
-                        const double an = i ? acc[1][c][h] : acc[0][c][h];  // static register selection
-                        st.b0h[c * 8 + t] = 0.5 * (an + 2.0 * st.y0[t][c]);
+                        for (int c = 0; c < 6; ++c)
+#pragma unroll
+                            for (int h = 0; h < 2; ++h) {
+                                const int t = 2 * q + h;
+                                const double an = i ? acc[1][c][h] : acc[0][c][h];
+                                st.b0h[c * 8 + t] = 0.5 * (an + 2.0 * st.y0[t][c]);
+                            }
                     }
+                }
+#pragma unroll
+                for (int x = 0; x < XM; ++x) {
+                    const int e = warp + x * gp.warps;
+                    if (e < gp.extras && gp.mb + e / 6 == amt) {
+                        const int c = e % 6;
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const int t = 2 * q + h;
+                            st.b0h[c * 8 + t] = 0.5 * (xacc[x][h] + 2.0 * st.y0[t][c]);
+                        }
+                    }
+                }
             }
         }
         __syncthreads();
+        PHASE(4);
 
-        // ------------------------------------------------ epilogue: Y' , finite, error
+        // ------------------------------------------------ epilogue: main rows in registers
         {
-            const int g = lane >> 2, q = lane & 3;
-            double emax[2] = {0.0, 0.0};
+            double bn[2] = {0.0, 0.0}, bd[2] = {1.0, 1.0};
             int nf[2] = {INT_MAX, INT_MAX};
 #pragma unroll
             for (int i = 0; i < 2; ++i) {
-                const int j = (2 * warp + i) * 8 + g;
+                if (i >= gp.main) continue;
+                const int j = (warp * gp.main + i) * 8 + g;
                 if (j >= N) continue;
-                double* yrow = ybuf + static_cast<size_t>(j) * YS + 2 * q;
                 double yn[2][6], yo[2][6];
 #pragma unroll
                 for (int c = 0; c < 6; ++c) {
-                    const double2 prev = *reinterpret_cast<const double2*>(yrow + c * 8);
+                    const double2 prev = *reinterpret_cast<const double2*>(ybuf + yidx(j, c, 2 * q));
                     yo[0][c] = prev.x;
                     yo[1][c] = prev.y;
                     yn[0][c] = acc[i][c][0] + st.b0h[c * 8 + 2 * q];
@@ -257,47 +467,39 @@ __global__ void __launch_bounds__(MAXT, 1) k_pc_segment(const SegArgs a) {
                 }
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
-                    const int t = 2 * q + h;
-                    if (!((act >> t) & 1)) {
+                    if (!((act >> (2 * q + h)) & 1)) {
 #pragma unroll
                         for (int c = 0; c < 6; ++c) yn[h][c] = yo[h][c];
                         continue;
                     }
-#pragma unroll
-                    for (int c = 5; c >= 0; --c)
-                        if (!isfinite(yn[h][c])) nf[h] = min(nf[h], j * 8 + c);
-                    double dr2 = 0.0, r2 = 0.0, dv2 = 0.0, v2 = 0.0;
-#pragma unroll
-                    for (int c = 0; c < 3; ++c) {
-                        const double dr = yn[h][c] - yo[h][c], dv = yn[h][c + 3] - yo[h][c + 3];
-                        dr2 += dr * dr;
-                        r2 += yo[h][c] * yo[h][c];
-                        dv2 += dv * dv;
-                        v2 += yo[h][c + 3] * yo[h][c + 3];
-                    }
-                    double pos, vel;
-                    if (a.error_mode == 1) {
-                        pos = sqrt(dr2);
-                        vel = sqrt(dv2);
-                    } else {
-                        pos = sqrt(dr2) / fmax(sqrt(r2), 1e-30);
-                        vel = sqrt(dv2) / fmax(sqrt(v2), 1e-30);
-                    }
-                    emax[h] = fmax(emax[h], fmax(pos, vel));
+                    update_sample(yn[h], yo[h], j, a.error_mode, bn[h], bd[h], nf[h]);
                 }
 #pragma unroll
                 for (int c = 0; c < 6; ++c)
-                    *reinterpret_cast<double2*>(yrow + c * 8) = make_double2(yn[0][c], yn[1][c]);
+                    *reinterpret_cast<double2*>(ybuf + yidx(j, c, 2 * q)) = make_double2(yn[0][c], yn[1][c]);
             }
+            // extra tiles: one component per tile -> stage Y' for the cross-warp epilogue
+#pragma unroll
+            for (int x = 0; x < XM; ++x) {
+                const int e = warp + x * gp.warps;
+                if (e >= gp.extras) continue;
+                const int j = (gp.mb + e / 6) * 8 + g, c = e % 6;
+                if (j >= N) continue;
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+                    xstage[(j - gp.mb * 8) * COLS + c * 8 + 2 * q + h] = xacc[x][h] + st.b0h[c * 8 + 2 * q + h];
+            }
+            double emax[2];
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
+                emax[h] = bn[h] / bd[h];
 #pragma unroll
                 for (int off = 4; off < 32; off <<= 1) {
                     emax[h] = fmax(emax[h], __shfl_xor_sync(0xffffffffu, emax[h], off));
                     nf[h] = min(nf[h], __shfl_xor_sync(0xffffffffu, nf[h], off));
                 }
             }
-            if (g == 0) {
+            if (g == 0 && gp.main > 0) {
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     const int t = 2 * q + h;
@@ -309,55 +511,104 @@ __global__ void __launch_bounds__(MAXT, 1) k_pc_segment(const SegArgs a) {
             }
         }
         __syncthreads();
+        PHASE(5);
 
-        // ------------------------------------------------ group decisions
-        if (tid == 0) {
-            for (int lg = 0; lg < SLOTS; ++lg) {
-                const int gid = st.grp_id[lg];
-                if (gid < 0) continue;
-                const int size = st.grp_size[lg];
-                double gerr = 0.0;
-                long long sing_s = LLONG_MAX;
-                int sing_t = -1;
-                long long nf_key = LLONG_MAX;
-                long long warm_k = LLONG_MAX;
-                int warm_t = -1;
-                for (int t = 0; t < SLOTS; ++t) {
-                    if (!((st.active_mask >> t) & 1) || st.slot_grp[t] != lg) continue;
-                    const int mbr = st.slot_member[t];
-                    gerr = fmax(gerr, __longlong_as_double(static_cast<long long>(st.slot_err[t])));
-                    if (((new_mask >> t) & 1) && st.warm_key[t] != INT_MAX) {
-                        // warm_start walks trajectories in batch order (propagator.hpp:86)
-                        if (st.slot_traj[t] < warm_k) {
-                            warm_k = st.slot_traj[t];
-                            warm_t = t;
-                        }
-                    }
-                    if (st.sing_key[t] != INT_MAX) {
-                        const long long j = st.sing_key[t] / (B + 1);
-                        const long long s = j * size + mbr;  // sample order s = j*m + t
-                        if (s < sing_s) {
-                            sing_s = s;
-                            sing_t = t;
-                        }
-                    }
-                    if (st.nf_key[t] != INT_MAX) {
-                        const long long j = st.nf_key[t] >> 3, c = st.nf_key[t] & 7;
-                        const long long key = j * (6LL * size) + c * size + mbr;  // row-major (j, col)
-                        nf_key = min(nf_key, key);
+        // ------------------------------------------------ epilogue: extra rows from the stage
+        if (tid < a.xrows * SLOTS) {
+            const int r = tid >> 3, t = tid & 7, j = gp.mb * 8 + r;
+            if ((act >> t) & 1) {
+                double yn[6], yo[6];
+#pragma unroll
+                for (int c = 0; c < 6; ++c) {
+                    yn[c] = xstage[r * COLS + c * 8 + t];
+                    yo[c] = ybuf[yidx(j, c, t)];
+                }
+                double bn = 0.0, bd = 1.0;
+                int nf = INT_MAX;
+                update_sample(yn, yo, j, a.error_mode, bn, bd, nf);
+                const double e2 = bn / bd;
+#pragma unroll
+                for (int c = 0; c < 6; ++c) ybuf[yidx(j, c, t)] = yn[c];
+                atomicMax(&st.slot_err[t], static_cast<unsigned long long>(__double_as_longlong(e2)));
+                if (nf != INT_MAX) atomicMin(&st.nf_key[t], nf);
+            }
+        }
+        __syncthreads();
+        PHASE(6);
+
+        // ------------------------------------------------ group decisions (warp 0, lane = slot)
+        // The lowest active slot of each group leads it: gathers the member maxima /
+        // first-fault keys, applies the stopping rule of pc_solve (picard.hpp:66-81)
+        // and writes the group's report.  Leaders of different groups run in parallel.
+        if (warp == 0) {
+            const int am = st.active_mask;
+            const int t = lane;
+            const bool act_t = t < SLOTS && ((am >> t) & 1);
+            // each lane loads its own slot record once; leaders gather with shuffles
+            const int my_grp = act_t ? st.slot_grp[t] : -1;
+            const int my_mbr = act_t ? st.slot_member[t] : 0;
+            const double my_e2 = act_t ? __longlong_as_double(static_cast<long long>(st.slot_err[t])) : 0.0;
+            const int my_sk = act_t ? st.sing_key[t] : INT_MAX;
+            const int my_nk = act_t ? st.nf_key[t] : INT_MAX;
+            const int my_wk = (act_t && ((new_mask >> t) & 1)) ? st.warm_key[t] : INT_MAX;
+            const int my_tr = act_t ? st.slot_traj[t] : INT_MAX;
+            const int lg = my_grp;
+            const int gid = act_t ? st.grp_id[lg] : -1;
+            const int size = act_t ? st.grp_size[lg] : 1;
+            int it = act_t ? st.grp_iter[lg] : 0;
+            bool leader = act_t;
+            double gerr2 = 0.0;
+            long long sing_s = LLONG_MAX, nf_best = LLONG_MAX;
+            int sing_t = -1, warm_t = -1, warm_tr = INT_MAX, members = 0;
+            if (a.gmax == 1) {  // singleton groups (independent mode): each lane owns its group
+                members = act_t ? 1 << t : 0;
+                gerr2 = my_e2;
+                if (my_wk != INT_MAX) warm_t = t;
+                if (my_sk != INT_MAX) sing_t = t;
+                if (my_nk != INT_MAX) nf_best = static_cast<long long>(my_nk >> 3) * 6 + (my_nk & 7);
+            } else
+#pragma unroll
+            for (int u = 0; u < SLOTS; ++u) {
+                const int ug = __shfl_sync(0xffffffffu, my_grp, u);
+                const int um = __shfl_sync(0xffffffffu, my_mbr, u);
+                const double ue = __shfl_sync(0xffffffffu, my_e2, u);
+                const int usk = __shfl_sync(0xffffffffu, my_sk, u);
+                const int unk = __shfl_sync(0xffffffffu, my_nk, u);
+                const int uwk = __shfl_sync(0xffffffffu, my_wk, u);
+                const int utr = __shfl_sync(0xffffffffu, my_tr, u);
+                if (!act_t || ug != lg) continue;
+                if (u < t) leader = false;
+                members |= 1 << u;
+                gerr2 = fmax(gerr2, ue);
+                if (uwk != INT_MAX && utr < warm_tr) {  // warm_start walks the batch in order (propagator.hpp:86)
+                    warm_tr = utr;
+                    warm_t = u;
+                }
+                if (usk != INT_MAX) {
+                    const long long smp = static_cast<long long>(usk / (B + 1)) * size + um;  // s = j*m + t
+                    if (smp < sing_s) {
+                        sing_s = smp;
+                        sing_t = u;
                     }
                 }
+                if (unk != INT_MAX) {  // row-major (node, column = comp*m + member)
+                    const long long key = static_cast<long long>(unk >> 3) * (6LL * size) +
+                                          static_cast<long long>(unk & 7) * size + um;
+                    nf_best = min(nf_best, key);
+                }
+            }
+            int free_bits = 0, retire_bits = 0;
+            if (leader) {
+                const double gerr = sqrt(gerr2);
                 GroupFault* fl = a.faults + gid;
-                int it = st.grp_iter[lg];
                 bool retire = false, ok = false, conv = false;
                 if (warm_t >= 0) {
-                    const int t = warm_t;
-                    fl->status = st.warm_kind[t] == CONIC_ZERO_RADIUS ? FAULT_WARM_ZERO_RADIUS : FAULT_WARM_SOLVER;
+                    fl->status = st.warm_kind[warm_t] == CONIC_ZERO_RADIUS ? FAULT_WARM_ZERO_RADIUS : FAULT_WARM_SOLVER;
                     fl->iteration = 0;
-                    fl->trajectory = st.slot_traj[t];
-                    fl->node = st.warm_key[t] / 4;
-                    fl->value = st.warm_val[t][0];
-                    fl->value2 = st.warm_val[t][1];
+                    fl->trajectory = st.slot_traj[warm_t];
+                    fl->node = st.warm_key[warm_t] / 4;
+                    fl->value = st.warm_val[warm_t][0];
+                    fl->value2 = st.warm_val[warm_t][1];
                     retire = true;
                 } else {
                     it += 1;
@@ -371,11 +622,11 @@ __global__ void __launch_bounds__(MAXT, 1) k_pc_segment(const SegArgs a) {
                         fl->trajectory = st.slot_member[sing_t];
                         fl->value = st.sing_val[sing_t];
                         retire = true;
-                    } else if (nf_key != LLONG_MAX) {
+                    } else if (nf_best != LLONG_MAX) {
                         fl->status = FAULT_DIVERGENCE;
                         fl->iteration = it;
-                        fl->node = nf_key / (6LL * size);
-                        fl->column = nf_key % (6LL * size);
+                        fl->node = nf_best / (6LL * size);
+                        fl->column = nf_best % (6LL * size);
                         retire = true;
                     } else {
                         if (a.rep_hist) a.rep_hist[static_cast<size_t>(gid) * a.max_it + (it - 1)] = gerr;
@@ -390,16 +641,20 @@ __global__ void __launch_bounds__(MAXT, 1) k_pc_segment(const SegArgs a) {
                     a.rep_iter[gid] = it;
                     a.rep_err[gid] = gerr;
                     a.rep_conv[gid] = conv ? 1 : 0;
-                    for (int t = 0; t < SLOTS; ++t) {
-                        if (!((st.active_mask >> t) & 1) || st.slot_grp[t] != lg) continue;
-                        st.free_mask |= 1 << t;
-                        if (ok) st.retire_mask |= 1 << t;
-                    }
+                    free_bits = members;
+                    retire_bits = ok ? members : 0;
                     st.grp_id[lg] = -1;
                 }
             }
+            free_bits = __reduce_or_sync(0xffffffffu, static_cast<unsigned>(free_bits));
+            retire_bits = __reduce_or_sync(0xffffffffu, static_cast<unsigned>(retire_bits));
+            if (lane == 0) {
+                st.free_mask = free_bits;
+                st.retire_mask = retire_bits;
+            }
         }
         __syncthreads();
+        PHASE(7);
 
         // ------------------------------------------------ retire: samples + chained state
         const int retire = st.retire_mask;
@@ -408,50 +663,118 @@ __global__ void __launch_bounds__(MAXT, 1) k_pc_segment(const SegArgs a) {
             for (int i = tid; i < N * SLOTS; i += nthr) {
                 const int j = i >> 3, t = i & 7;
                 if (!((retire >> t) & 1)) continue;
-                const double* yp = ybuf + static_cast<size_t>(j) * YS + t;
                 const size_t tr = static_cast<size_t>(st.slot_traj[t]);
                 if (a.samples && j >= j_begin) {
                     double* o = a.samples + (tr * a.R + a.row0 + j) * 6;
 #pragma unroll
-                    for (int c = 0; c < 6; ++c) o[c] = yp[c * 8];
+                    for (int c = 0; c < 6; ++c) o[c] = ybuf[yidx(j, c, t)];
                 }
                 if (j == N - 1) {
 #pragma unroll
-                    for (int c = 0; c < 6; ++c) a.state_out[tr * 6 + c] = yp[c * 8];
+                    for (int c = 0; c < 6; ++c) a.state_out[tr * 6 + c] = ybuf[yidx(j, c, t)];
                 }
             }
         }
         if (tid == 0) {
-            st.active_mask &= ~st.free_mask;
+            const int fm = st.free_mask;
+            st.active_mask &= ~fm;
             for (int t = 0; t < SLOTS; ++t)
-                if ((st.free_mask >> t) & 1) st.slot_traj[t] = -1;
+                if ((fm >> t) & 1) st.slot_traj[t] = -1;
         }
         __syncthreads();
+        PHASE(8);
+    }
+    if (prof && tid == 0) {
+        pc[9] += 1;  // CTA count
+        for (int k = 0; k < PHASES; ++k) atomicAdd(a.phase_cycles + k, static_cast<unsigned long long>(pc[k]));
     }
 }
 
-template <int MAXT>
-static cudaError_t launch_segment_t(const SegArgs& a, int grid, cudaStream_t s) {
-    const size_t smem = segment_smem_bytes(a.N, a.nkp);
-    cudaError_t e = cudaFuncSetAttribute(k_pc_segment<MAXT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
+template <int MAXT, int XM, int FS>
+static cudaError_t launch_segment_t(const SegArgs& a, int grid, size_t smem, cudaStream_t s) {
+    auto kern = a.stage_eph ? k_pc_segment<MAXT, XM, true, FS> : k_pc_segment<MAXT, XM, false, FS>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    k_pc_segment<MAXT><<<grid, 32 * a.warps, smem, s>>>(a);
+    kern<<<grid, 32 * a.gp.warps, smem, s>>>(a);
     return cudaGetLastError();
 }
 
-/// Two register budgets: up to 13 warps (N <= 207, e.g. the default N = 200) the
-/// kernel gets 128+ registers per thread; up to 17 warps (N <= 264) it gets 120.
+/// Register budgets: up to 12 warps (N <= 207, e.g. the default N = 200) the kernel gets
+/// up to 168 registers per thread; up to 16 warps (N <= 264) 128; small N (< 63) runs
+/// 4 warps with up to 6 single tiles each.
 cudaError_t launch_segment(const SegArgs& a, int grid, cudaStream_t s) {
-    if (32 * a.warps <= 416) return launch_segment_t<416>(a, grid, s);
-    return launch_segment_t<544>(a, grid, s);
+    const size_t smem = segment_smem_bytes(a.N, a.nkp, a.xrows, a.fd.n_bodies, a.stage_eph);
+    if (a.gp.xmax == XMAX_SMALL) return launch_segment_t<128, XMAX_SMALL, 4>(a, grid, smem, s);
+    if (a.gp.warps <= 12) return launch_segment_t<384, XMAX, 4>(a, grid, smem, s);
+    return launch_segment_t<512, XMAX, 4>(a, grid, smem, s);
+}
+
+// ============================================================== ephemeris ==
+
+__global__ void k_ephemeris(int N, const double* __restrict__ times, double central_mu, BodyTable bt,
+                            double* __restrict__ pos, double* __restrict__ indirect, unsigned long long* fault_key) {
+    const int j = blockIdx.x, b = threadIdx.x;
+    const double t = times[j];
+    if (b < bt.B) {
+        double p[3] = {0.0, 0.0, 0.0};
+        if (bt.kind[b] == 0) {
+            double mf;
+            if (elements_position(bt.elements + 7 * b, central_mu, t, p, &mf) != CONIC_OK)
+                atomicMin(fault_key, (static_cast<unsigned long long>(b) * N + j) * 4ull + 3ull);
+        } else {
+            int hit = -1;
+            for (int sg = bt.seg_off[b]; sg < bt.seg_off[b + 1]; ++sg) {
+                const double t0 = bt.seg_bounds[2 * sg], t1 = bt.seg_bounds[2 * sg + 1];
+                const bool fwd = t0 <= t1;
+                if ((fwd && t >= t0 && t <= t1) || (!fwd && t <= t0 && t >= t1)) {
+                    hit = sg;
+                    break;
+                }
+            }
+            if (hit < 0) {
+                atomicMin(fault_key, (static_cast<unsigned long long>(b) * N + j) * 4ull + 1ull);
+            } else {
+                const double t0 = bt.seg_bounds[2 * hit], t1 = bt.seg_bounds[2 * hit + 1];
+                const double tau = (2.0 * t - (t0 + t1)) / (t1 - t0);
+                const int nc = bt.ncoef[b];
+                const double* c = bt.coeffs + bt.coeff_off[hit];
+                for (int k = 0; k < 3; ++k) p[k] = clenshaw(c + k * nc, nc, tau);
+            }
+        }
+        double* o = pos + (static_cast<size_t>(j) * bt.B + b) * 3;
+        o[0] = p[0];
+        o[1] = p[1];
+        o[2] = p[2];
+    }
+    __syncthreads();
+    if (b == 0) {  // fixed summation order over bodies (deterministic)
+        double s[3] = {0.0, 0.0, 0.0};
+        for (int k = 0; k < bt.B; ++k) {
+            const double* q = pos + (static_cast<size_t>(j) * bt.B + k) * 3;
+            const double bn = sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2]);
+            const double bn3 = bn * bn * bn;
+            const double mu = bt.mu[k];
+            for (int c = 0; c < 3; ++c) s[c] += mu * (q[c] / bn3);
+        }
+        for (int c = 0; c < 3; ++c) indirect[j * 3 + c] = s[c];
+    }
+}
+
+cudaError_t launch_ephemeris(int N, const double* times, double central_mu, const BodyTable& bt, double* pos,
+                             double* indirect, unsigned long long* fault_key, cudaStream_t s) {
+    if (bt.B <= 0) return cudaSuccess;
+    const int threads = 32 * ((bt.B + 31) / 32);
+    k_ephemeris<<<N, threads, 0, s>>>(N, times, central_mu, bt, pos, indirect, fault_key);
+    return cudaGetLastError();
 }
 
 // ===================================================================== ops ==
 
-/// Y = [U; anchor]·F tile per CTA (48 arbitrary columns), all W warps in one CTA.
-__global__ void __launch_bounds__(544, 1)
-    k_picard_update(int N, int nkp, int C, const double* __restrict__ F, const double* __restrict__ y0,
+/// Y = [U; anchor]·F tile per CTA (48 arbitrary columns), same warp plan as the
+/// segment kernel; every output element is written straight from its fragment.
+template <int MAXT, int XM>
+__global__ void __launch_bounds__(MAXT, 1)
+    k_picard_update(int N, int nkp, GemmPlan gp, int C, const double* __restrict__ F, const double* __restrict__ y0,
                     double* __restrict__ out, const double2* __restrict__ upack) {
     extern __shared__ __align__(16) double smem[];
     double* fbuf = smem;
@@ -459,30 +782,44 @@ __global__ void __launch_bounds__(544, 1)
     const int KP = 8 * nkp;
     const int col0 = blockIdx.x * COLS;
     const int tid = threadIdx.x, nthr = blockDim.x, warp = tid >> 5, lane = tid & 31;
+    const int g = lane >> 2, q = lane & 3;
     for (int i = tid; i < KP * COLS; i += nthr) {
         const int k = i / COLS, n = i % COLS, col = col0 + n;
         fbuf[fbuf_index(k, n)] = (k < N && col < C) ? F[static_cast<size_t>(k) * C + col] : 0.0;
     }
+    const APrefetch<XM> pre = gemm_prefetch<XM>(upack, nkp, gp, warp, lane);
     __syncthreads();
-    double acc[2][6][2];
-    warp_gemm(upack, nkp, fbuf, warp, lane, acc);
-    const int g = lane >> 2, q = lane & 3;
-    const int amt = N >> 3, ag = N & 7;
-    if (warp == (amt >> 1) && g == ag) {
-        const int i = amt & 1;
+    double acc[2][6][2], xacc[XM][2];
+    warp_gemm<XM>(upack, nkp, fbuf, gp, warp, lane, pre, acc, xacc);
+    const int amt = N >> 3;
+    if (g == (N & 7)) {
 #pragma unroll
-        for (int c = 0; c < 6; ++c)
+        for (int i = 0; i < 2; ++i)
+            if (i < gp.main && warp * gp.main + i == amt)
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int n = c * 8 + 2 * q + h, col = col0 + n;
-                const double an = i ? acc[1][c][h] : acc[0][c][h];
-                b0h[n] = col < C ? 0.5 * (an + 2.0 * y0[col]) : 0.0;
-            }
+                for (int c = 0; c < 6; ++c)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int n = c * 8 + 2 * q + h, col = col0 + n;
+                        const double an = i ? acc[1][c][h] : acc[0][c][h];
+                        b0h[n] = col < C ? 0.5 * (an + 2.0 * y0[col]) : 0.0;
+                    }
+#pragma unroll
+        for (int x = 0; x < XM; ++x) {
+            const int e = warp + x * gp.warps;
+            if (e < gp.extras && gp.mb + e / 6 == amt)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int n = (e % 6) * 8 + 2 * q + h, col = col0 + n;
+                    b0h[n] = col < C ? 0.5 * (xacc[x][h] + 2.0 * y0[col]) : 0.0;
+                }
+        }
     }
     __syncthreads();
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
-        const int j = (2 * warp + i) * 8 + g;
+        if (i >= gp.main) continue;
+        const int j = (warp * gp.main + i) * 8 + g;
         if (j >= N) continue;
 #pragma unroll
         for (int c = 0; c < 6; ++c)
@@ -492,16 +829,28 @@ __global__ void __launch_bounds__(544, 1)
                 if (col < C) out[static_cast<size_t>(j) * C + col] = acc[i][c][h] + b0h[n];
             }
     }
+#pragma unroll
+    for (int x = 0; x < XM; ++x) {
+        const int e = warp + x * gp.warps;
+        if (e >= gp.extras) continue;
+        const int j = (gp.mb + e / 6) * 8 + g;
+        if (j >= N) continue;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int n = (e % 6) * 8 + 2 * q + h, col = col0 + n;
+            if (col < C) out[static_cast<size_t>(j) * C + col] = xacc[x][h] + b0h[n];
+        }
+    }
 }
 
 cudaError_t launch_picard_update(int N, int nkp, int C, const double* F, const double* y0, double* out,
                                  const double2* upack, cudaStream_t s) {
+    const GemmPlan gp = make_gemm_plan(N);
     const size_t smem = sizeof(double) * (static_cast<size_t>(8 * nkp) * COLS + COLS);
-    cudaError_t e = cudaFuncSetAttribute(k_picard_update, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
+    auto kern = gp.xmax == XMAX_SMALL ? k_picard_update<128, XMAX_SMALL> : k_picard_update<512, XMAX>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    const int threads = segment_threads(N);
-    k_picard_update<<<(C + COLS - 1) / COLS, threads, smem, s>>>(N, nkp, C, F, y0, out, upack);
+    kern<<<(C + COLS - 1) / COLS, 32 * gp.warps, smem, s>>>(N, nkp, gp, C, F, y0, out, upack);
     return cudaGetLastError();
 }
 
@@ -514,7 +863,8 @@ __global__ void k_force_block(int N, int m, const double* __restrict__ y, double
     const size_t row = static_cast<size_t>(j) * 6 * m;
     const double rx = y[row + t], ry = y[row + m + t], rz = y[row + 2 * m + t];
     double ax = 0.0, ay = 0.0, az = 0.0;
-    const int chk = accel(rx, ry, rz, j, fd, ax, ay, az);
+    const int chk = accel(rx, ry, rz, fd.body_pos + static_cast<size_t>(j) * 3 * fd.n_bodies, fd.indirect + 3 * j, fd,
+                          ax, ay, az);
     if (chk >= 0) atomicMin(fault_key, static_cast<unsigned long long>(s) * 64ull + static_cast<unsigned long long>(chk));
     force[row + t] = omega2 * y[row + 3 * m + t];
     force[row + m + t] = omega2 * y[row + 4 * m + t];

@@ -32,11 +32,17 @@ struct GroupFault {
     double value2;       // eccentricity (solver)
 };
 
+/// Phase accounting slots: 0 claim, 1 warm start, 2 force, 3 DMMA, 4 anchor/b0 barrier,
+/// 5 epilogue (main rows), 6 epilogue (staged rows), 7 decisions, 8 retire, 9 CTA count.
+constexpr int PHASES = 10;
+
 /// Arguments of one segment launch of the persistent slot kernel.
 struct SegArgs {
     int N;          // nodes
     int nkp;        // k-step pairs: K padded to 8*nkp
-    int warps;      // warps per CTA = ceil(ceil((N+1)/8)/2)
+    GemmPlan gp;    // warp plan of the DMMA tiles (warps per CTA = gp.warps)
+    int xrows;      // node rows covered by extra tiles (staged epilogue)
+    int stage_eph;  // 1: per-segment ephemeris staged in shared memory
     int M;          // trajectories
     int P;          // groups
     int gmax;       // largest group (<= SLOTS)
@@ -66,10 +72,32 @@ struct SegArgs {
     double* rep_hist;           // [P][max_it] or nullptr
     GroupFault* faults;         // [P]
     uint8_t* cold_fallback;     // [M] or nullptr
+    unsigned long long* phase_cycles;  // [PHASES] diagnostics or nullptr
 };
 
-size_t segment_smem_bytes(int N, int nkp);
-int segment_threads(int N);
+/// Perturbing bodies on the device (ephemeris.hpp:44-73): analytic elements or
+/// tabulated Chebyshev segments, flattened.
+struct BodyTable {
+    int B;
+    const int* kind;          // [B] 0 analytic, 1 tabulated
+    const double* elements;   // [B][7]
+    const double* mu;         // [B]
+    const int* seg_off;       // [B+1] first segment of each body
+    const double* seg_bounds; // [S][2]
+    const long long* coeff_off;  // [S] offset of the segment's [3][nc] block in coeffs
+    const int* ncoef;         // [B]
+    const double* coeffs;
+};
+
+/// Frozen per-segment ephemeris on the device: body positions [N][B][3] at the node
+/// times and the indirect term [N][3] (ephemeris.hpp:89-107, force_model.hpp:50-51).
+/// fault_key = min over (body, node) of (b*N + j)*4 + kind (1 coverage, 3 solver).
+cudaError_t launch_ephemeris(int N, const double* times, double central_mu, const BodyTable& bt, double* pos,
+                             double* indirect, unsigned long long* fault_key, cudaStream_t s);
+
+GemmPlan make_gemm_plan(int N);
+int extra_rows(int N, const GemmPlan& gp);
+size_t segment_smem_bytes(int N, int nkp, int xrows, int B, int stage_eph);
 cudaError_t launch_segment(const SegArgs& a, int grid, cudaStream_t s);
 
 cudaError_t launch_picard_update(int N, int nkp, int C, const double* F, const double* y0, double* out,

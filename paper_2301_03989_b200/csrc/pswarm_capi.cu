@@ -6,6 +6,7 @@
 // reference's exceptions.  There is no CPU fallback anywhere in this file.
 #include <algorithm>
 #include <chrono>
+#include <climits>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -135,13 +136,14 @@ struct DevBuf {
 struct OpPack {
     DevBuf buf;
     int nkp = 0;
-    int warps = 0;
+    GemmPlan gp{};
 };
 
 enum BufId {
     B_STATE_A, B_STATE_B, B_GROUP_OFF, B_TIMES, B_BODY_POS, B_BODY_MU, B_INDIRECT, B_QUEUE,
     B_REP_ITER, B_REP_ERR, B_REP_CONV, B_REP_HIST, B_FAULTS, B_FALLBACK, B_SAMPLES, B_DEAD,
-    B_OP_IN, B_OP_IN2, B_OP_OUT, B_OP_AUX, B_OP_KEY, B_COUNT
+    B_OP_IN, B_OP_IN2, B_OP_OUT, B_OP_AUX, B_OP_KEY,
+    B_BT_KIND, B_BT_SOFF, B_BT_NC, B_BT_EL, B_BT_BND, B_BT_COFF, B_BT_CF, B_PHASES, B_COUNT
 };
 
 }  // namespace
@@ -156,6 +158,8 @@ struct pswarm_ctx {
     int64_t launches = 0;
     int ctas_per_sm = 1;
     int max_ctas = 0;  // 0 = SM count * ctas_per_sm
+    int profile_phases = 0;
+    unsigned long long phase_host[pswarm_dev::PHASES] = {};
 };
 
 namespace {
@@ -168,10 +172,9 @@ const OpPack& operators(pswarm_ctx* ctx, Index n) {
     if (it != ctx->ops.end()) return *it->second;
     if (n > 264) raise(PSWARM_ERR_INVALID_SIZE, fmtf("device operators support up to 264 nodes, got %lld", (long long)n));
     const auto mats = pswarm::cached_matrices(n);  // InvalidSizeError for n < 3
-    const int mt = static_cast<int>((n + 1 + 7) / 8);
-    const int warps = (mt + 1) / 2;
+    const GemmPlan gp = make_gemm_plan(static_cast<int>(n));
     const int nkp = static_cast<int>((n + 7) / 8);
-    const int rows = 16 * warps;
+    const int rows = 8 * gp.mtiles;
     auto A = [&](int r, int k) -> double {
         if (k >= n) return 0.0;
         if (r < n) return mats->update_op(r, k);
@@ -189,74 +192,52 @@ const OpPack& operators(pswarm_ctx* ctx, Index n) {
             }
     auto p = std::make_unique<OpPack>();
     p->nkp = nkp;
-    p->warps = warps;
+    p->gp = gp;
     double* d = p->buf.get<double>(host.size());
     cuda_check(cudaMemcpy(d, host.data(), host.size() * sizeof(double), cudaMemcpyHostToDevice), "upload operators");
     return *ctx->ops.emplace(n, std::move(p)).first->second;
 }
 
-pswarm::BodySpec body_from(const pswarm_body& b) {
-    pswarm::BodySpec o;
-    o.name = b.name ? b.name : "";
-    o.mu = b.mu;
-    if (b.kind == 0) {
-        o.ephemeris = pswarm::OrbitalElements{b.elements[0], b.elements[1], b.elements[2], b.elements[3],
-                                              b.elements[4], b.elements[5], b.elements[6]};
-    } else {
-        pswarm::ChebyshevEphemeris eph;
-        for (int32_t s = 0; s < b.n_segments; ++s) {
-            pswarm::ChebyshevSegment seg;
-            seg.t_start = b.seg_bounds[2 * s];
-            seg.t_end = b.seg_bounds[2 * s + 1];
-            seg.coeffs_x.resize(b.n_coeffs);
-            seg.coeffs_y.resize(b.n_coeffs);
-            seg.coeffs_z.resize(b.n_coeffs);
-            const double* c = b.coeffs + static_cast<size_t>(s) * 3 * b.n_coeffs;
-            for (int32_t k = 0; k < b.n_coeffs; ++k) {
-                seg.coeffs_x[k] = c[k];
-                seg.coeffs_y[k] = c[b.n_coeffs + k];
-                seg.coeffs_z[k] = c[2 * b.n_coeffs + k];
-            }
-            eph.segments.push_back(std::move(seg));
-        }
-        o.ephemeris = std::move(eph);
-    }
-    return o;
-}
-
-/// Host-side per-segment force constants: frozen body table [N][B][3] and the
-/// node-constant indirect term sum_b mu_b r_b/|r_b|^3 (force_model.hpp:50-51).
-struct SegmentEphemeris {
-    std::vector<double> pos, indirect, mus;
+/// Device body table of one call: flattened analytic elements / tabulated Chebyshev
+/// segments (ephemeris.hpp:44-73) plus the names used in error messages.
+struct BodyUpload {
+    std::vector<int> kind, seg_off, ncoef;
+    std::vector<double> elements, mu, bounds, coeffs;
+    std::vector<long long> coeff_off;
     std::vector<std::string> names;
+    int first_invalid = -1;  // first analytic body that elements_to_state rejects (kepler.hpp:103-106)
+    std::string invalid_msg;
 };
 
-SegmentEphemeris build_segment_ephemeris(const std::vector<pswarm::BodySpec>& bodies, const pswarm::ChebyshevGrid& g,
-                                         double central_mu) {
-    SegmentEphemeris e;
-    const Index n = g.n_nodes, B = static_cast<Index>(bodies.size());
-    e.pos.assign(static_cast<size_t>(n * B * 3), 0.0);
-    e.indirect.assign(static_cast<size_t>(n * 3), 0.0);
-    for (const auto& b : bodies) {
-        e.mus.push_back(b.mu);
-        e.names.push_back(b.name);
+BodyUpload flatten_bodies(const pswarm_config& cfg, int nb) {
+    BodyUpload u;
+    u.seg_off.push_back(0);
+    for (int b = 0; b < nb; ++b) {
+        const pswarm_body& pb = cfg.bodies[b];
+        u.names.push_back(pb.name ? pb.name : "");
+        u.mu.push_back(pb.mu);
+        u.kind.push_back(pb.kind == 0 ? 0 : 1);
+        for (int k = 0; k < 7; ++k) u.elements.push_back(pb.kind == 0 ? pb.elements[k] : 0.0);
+        u.ncoef.push_back(pb.kind == 0 ? 0 : pb.n_coeffs);
+        if (pb.kind == 0) {
+            const double ae = pb.elements[0], ee = pb.elements[1];
+            if (u.first_invalid < 0 && (!(ae > 0.0) || ee < 0.0 || ee >= 1.0 - 1e-8)) {
+                u.first_invalid = b;
+                u.invalid_msg = "elements_to_state: elements do not define a bound conic (a = " + std::to_string(ae) +
+                                ", e = " + std::to_string(ee) + ")";
+            }
+        } else {
+            for (int sg = 0; sg < pb.n_segments; ++sg) {
+                u.bounds.push_back(pb.seg_bounds[2 * sg]);
+                u.bounds.push_back(pb.seg_bounds[2 * sg + 1]);
+                u.coeff_off.push_back(static_cast<long long>(u.coeffs.size()));
+                const double* c = pb.coeffs + static_cast<size_t>(sg) * 3 * pb.n_coeffs;
+                u.coeffs.insert(u.coeffs.end(), c, c + 3 * pb.n_coeffs);
+            }
+        }
+        u.seg_off.push_back(static_cast<int>(u.coeff_off.size()));
     }
-    for (Index b = 0; b < B; ++b)  // body-major like build_ephemeris_cache (ephemeris.hpp:96-105)
-        for (Index j = 0; j < n; ++j) {
-            const pswarm::Vec3 p = pswarm::body_position(bodies[b], central_mu, g.times[j]);
-            double* o = e.pos.data() + (j * B + b) * 3;
-            o[0] = p.x();
-            o[1] = p.y();
-            o[2] = p.z();
-        }
-    for (Index j = 0; j < n; ++j)
-        for (Index b = 0; b < B; ++b) {
-            const double* p = e.pos.data() + (j * B + b) * 3;
-            const double bn = std::sqrt(p[0] * p[0] + p[1] * p[1] + p[2] * p[2]);
-            const double bn3 = bn * bn * bn;
-            for (int c = 0; c < 3; ++c) e.indirect[j * 3 + c] += e.mus[b] * (p[c] / bn3);
-        }
-    return e;
+    return u;
 }
 
 ForceData make_force_data(const double* pos, const double* mus, const double* indirect, double central_mu,
@@ -322,8 +303,7 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
     const int max_it = std::max(cfg->max_iterations, 0);
     const int nb = cfg->force_kind == 1 ? cfg->n_bodies : 0;
     if (nb > 63) raise(PSWARM_ERR_INVALID_SIZE, "propagate: at most 63 perturbing bodies are supported");
-    std::vector<pswarm::BodySpec> bodies;
-    for (int b = 0; b < nb; ++b) bodies.push_back(body_from(cfg->bodies[b]));
+    const BodyUpload bu = flatten_bodies(*cfg, nb);
 
     const auto deadline = cfg->timeout_s > 0.0
                               ? std::chrono::steady_clock::now() +
@@ -374,12 +354,41 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
         gpu_deadline = t0 + static_cast<unsigned long long>(std::max<int64_t>(left.count(), 1));
     }
 
-    const size_t smem = segment_smem_bytes(static_cast<int>(N), op.nkp);
+    const int xrows = extra_rows(static_cast<int>(N), op.gp);
+    // stage the frozen ephemeris in shared memory when it fits next to the state blocks
+    const int stage_eph = (nb > 0 && segment_smem_bytes(static_cast<int>(N), op.nkp, xrows, nb, 1) <= 227 * 1024) ? 1 : 0;
+    if (segment_smem_bytes(static_cast<int>(N), op.nkp, xrows, nb, stage_eph) > 227 * 1024)
+        raise(PSWARM_ERR_INVALID_SIZE, fmtf("propagate: %lld nodes exceed the per-SM shared memory of the slot kernel",
+                                            (long long)N));
     const int per_cta = std::max<int64_t>(1, SLOTS / gmax);
     const int64_t want_ctas = (P + per_cta - 1) / per_cta;
     const int cap = ctx->max_ctas > 0 ? ctx->max_ctas : ctx->sm_count * ctx->ctas_per_sm;
     const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want_ctas, cap)));
 
+    BodyTable bt{};
+    double *d_pos = nullptr, *d_ind = nullptr, *d_mu = nullptr;
+    unsigned long long* d_ekey = reinterpret_cast<unsigned long long*>(ctx->buf[B_OP_AUX].get<double>(2));
+    if (nb > 0) {
+        int *d_kind, *d_soff, *d_nc;
+        double *d_el, *d_bnd, *d_cf;
+        long long* d_coff;
+        upload(ctx, B_BT_KIND, bu.kind.data(), bu.kind.size(), &d_kind);
+        upload(ctx, B_BT_SOFF, bu.seg_off.data(), bu.seg_off.size(), &d_soff);
+        upload(ctx, B_BT_NC, bu.ncoef.data(), bu.ncoef.size(), &d_nc);
+        upload(ctx, B_BT_EL, bu.elements.data(), bu.elements.size(), &d_el);
+        upload(ctx, B_BODY_MU, bu.mu.data(), bu.mu.size(), &d_mu);
+        upload(ctx, B_BT_BND, bu.bounds.data(), bu.bounds.size(), &d_bnd);
+        upload(ctx, B_BT_COFF, bu.coeff_off.data(), bu.coeff_off.size(), &d_coff);
+        upload(ctx, B_BT_CF, bu.coeffs.data(), bu.coeffs.size(), &d_cf);
+        bt = BodyTable{nb, d_kind, d_el, d_mu, d_soff, d_bnd, d_coff, d_nc, d_cf};
+        d_pos = ctx->buf[B_BODY_POS].get<double>(static_cast<size_t>(N) * nb * 3);
+        d_ind = ctx->buf[B_INDIRECT].get<double>(static_cast<size_t>(N) * 3);
+    }
+    unsigned long long* d_phase = nullptr;
+    if (ctx->profile_phases) {
+        d_phase = ctx->buf[B_PHASES].get<unsigned long long>(PHASES);
+        cuda_check(cudaMemsetAsync(d_phase, 0, sizeof(unsigned long long) * PHASES, st), "memset");
+    }
     cuda_check(cudaEventRecord(ctx->ev0, st), "event");
     int64_t seg_done = 0;
     double kernel_ms = 0.0;
@@ -391,7 +400,6 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
 
     for (int64_t seg = 0; seg < S; ++seg) {
         const auto g = pswarm::build_grid(N, boundaries[seg], boundaries[seg + 1]);
-        const auto eph = build_segment_ephemeris(bodies, g, cfg->central_mu);
         for (Index j = (seg == 0 ? 0 : 1); j < N; ++j) h_times[seg * (N - 1) + j] = g.times[j];
         if (std::chrono::steady_clock::now() > deadline) {
             init_err(&fail, PSWARM_ERR_TIMEOUT, "solve_group: wall-clock budget exhausted in group 0");
@@ -400,11 +408,14 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
             fail_status = PSWARM_ERR_TIMEOUT;
             break;
         }
-        double *d_times, *d_pos = nullptr, *d_mu = nullptr, *d_ind = nullptr;
+        double* d_times;
         upload(ctx, B_TIMES, g.times.data(), static_cast<size_t>(N), &d_times);
-        upload(ctx, B_BODY_POS, eph.pos.data(), eph.pos.size(), &d_pos);
-        upload(ctx, B_BODY_MU, eph.mus.data(), eph.mus.size(), &d_mu);
-        upload(ctx, B_INDIRECT, eph.indirect.data(), eph.indirect.size(), &d_ind);
+        if (nb > 0) {  // frozen per-node ephemeris of this segment, evaluated on the device
+            cuda_check(cudaMemsetAsync(d_ekey, 0xff, sizeof(unsigned long long), st), "memset");
+            cuda_check(launch_ephemeris(static_cast<int>(N), d_times, cfg->central_mu, bt, d_pos, d_ind, d_ekey, st),
+                       "k_ephemeris");
+            ++ctx->launches;
+        }
         cuda_check(cudaMemsetAsync(d_queue, 0, sizeof(int), st), "memset");
         cuda_check(cudaMemsetAsync(d_faults, 0, sizeof(GroupFault) * P, st), "memset");
         cuda_check(cudaMemsetAsync(d_iter, 0, sizeof(int32_t) * P, st), "memset");
@@ -414,7 +425,9 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
         SegArgs a{};
         a.N = static_cast<int>(N);
         a.nkp = op.nkp;
-        a.warps = op.warps;
+        a.gp = op.gp;
+        a.xrows = xrows;
+        a.stage_eph = stage_eph;
         a.M = static_cast<int>(M);
         a.P = static_cast<int>(P);
         a.gmax = static_cast<int>(gmax);
@@ -443,6 +456,7 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
         a.rep_hist = d_hist ? d_hist + static_cast<size_t>(seg) * P * max_it : nullptr;
         a.faults = d_faults;
         a.cold_fallback = d_fb;
+        a.phase_cycles = d_phase;
         if (max_it > 0) {
             cuda_check(cudaEventRecord(ctx->evk0, st), "event");
             cuda_check(launch_segment(a, grid, st), "k_pc_segment launch");
@@ -454,7 +468,36 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
         cuda_check(cudaMemcpyAsync(h_conv.data() + seg * P, d_conv, P, cudaMemcpyDeviceToHost, st), "D2H");
         cuda_check(cudaMemcpyAsync(h_faults.data(), d_faults, sizeof(GroupFault) * P, cudaMemcpyDeviceToHost, st), "D2H");
         cuda_check(cudaMemcpyAsync(h_fb.data() + seg * M, d_fb, M, cudaMemcpyDeviceToHost, st), "D2H");
+        unsigned long long ekey = ~0ull;
+        if (nb > 0) cuda_check(cudaMemcpyAsync(&ekey, d_ekey, sizeof ekey, cudaMemcpyDeviceToHost, st), "D2H");
         cuda_check(cudaStreamSynchronize(st), "segment solve");
+        // ---- ephemeris faults come first: build_ephemeris_cache precedes the solve
+        //      (propagator.hpp:252); body-major order (ephemeris.hpp:96-105)
+        {
+            const long long eb = ekey == ~0ull ? LLONG_MAX : static_cast<long long>((ekey / 4) / N);
+            if (seg == 0 && bu.first_invalid >= 0 && bu.first_invalid < eb) {
+                init_err(&fail, PSWARM_ERR_NON_ELLIPTIC, bu.invalid_msg);
+                fail.segment = seg;
+                fail_status = fail.status;
+                break;
+            }
+            if (ekey != ~0ull) {
+                const int kind = static_cast<int>(ekey % 4);
+                const int b = static_cast<int>((ekey / 4) / N), j = static_cast<int>((ekey / 4) % N);
+                if (kind == 1) {
+                    init_err(&fail, PSWARM_ERR_COVERAGE,
+                             "ephemeris for body '" + bu.names[b] + "' does not cover epoch " + std::to_string(g.times[j]));
+                    fail.value = g.times[j];
+                } else {
+                    init_err(&fail, PSWARM_ERR_SOLVER, "solve_kepler: Newton iteration did not converge for body '" +
+                                                           bu.names[b] + "'");
+                }
+                fail.segment = seg;
+                fail.body = b;
+                fail_status = fail.status;
+                break;
+            }
+        }
         if (max_it > 0) {
             float kms = 0.f;
             cudaEventElapsedTime(&kms, ctx->evk0, ctx->evk1);
@@ -523,7 +566,7 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
                 if (f.body < 0) {
                     what = "central-body acceleration at zero radius";
                 } else {
-                    body = eph.names[f.body];
+                    body = bu.names[f.body];
                     what = "close approach to body '" + body + "': distance " + std::to_string(f.value) +
                            " km below floor " + std::to_string(cfg->proximity_floor_km) + " km";
                 }
@@ -596,6 +639,10 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
             cuda_check(cudaMemcpyAsync(s6.data(), d_in, sizeof(double) * M * 6, cudaMemcpyDeviceToHost, st),
                        "D2H terminal");
         }
+        if (d_phase)
+            cuda_check(cudaMemcpyAsync(ctx->phase_host, d_phase, sizeof(unsigned long long) * PHASES,
+                                       cudaMemcpyDeviceToHost, st),
+                       "D2H phases");
         cuda_check(cudaStreamSynchronize(st), "outputs");
         if (out->terminal_states && fail_status == PSWARM_OK)
             for (int64_t i = 0; i < M; ++i) {
@@ -699,7 +746,15 @@ pswarm_status pswarm_set_option(pswarm_ctx* ctx, const char* key, int64_t value)
         const std::string k = key ? key : "";
         if (k == "ctas_per_sm") ctx->ctas_per_sm = static_cast<int>(std::max<int64_t>(1, value));
         else if (k == "max_ctas") ctx->max_ctas = static_cast<int>(std::max<int64_t>(0, value));
+        else if (k == "profile_phases") ctx->profile_phases = value != 0;
         else raise(PSWARM_ERR_GENERIC, "pswarm_set_option: unknown key '" + k + "'");
+    });
+}
+
+pswarm_status pswarm_get_phase_cycles(pswarm_ctx* ctx, uint64_t* out, int32_t n) {
+    return guarded(nullptr, [&] {
+        if (!ctx) raise(PSWARM_ERR_NO_DEVICE, "pswarm_get_phase_cycles: null context");
+        for (int k = 0; k < n && k < PHASES; ++k) out[k] = ctx->phase_host[k];
     });
 }
 

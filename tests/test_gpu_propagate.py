@@ -159,16 +159,30 @@ def test_mixed_epochs_rejected(ctx):
 
 
 def test_divergence_reports_first_non_finite(ctx, oracle):
-    """A trajectory through the Sun's centre blows up; the first non-finite
-    (node, column) in row-major order is reported (picard.hpp:26-36)."""
+    """A state at |r| = 1e-110 passes the zero-radius guard but its 1/|r|^3 overflows,
+    so the first update is non-finite; the first (node, column) in row-major order
+    is reported with the group prefix (picard.hpp:26-36, augment.hpp:132-135)."""
     states, plan, cfg = _setup(3, 32, 0.5, bodies="two_body", start="cold")
-    states[1, 4:7] = 0.0  # radial plunge
+    states[1, 1:4] = [1e-110, 0.0, 0.0]
+    with pytest.raises(ps.DivergenceError) as e:
+        ctx.propagate(states, [3], plan, cfg)
+    with pytest.raises(ps.DivergenceError) as e_ref:
+        oracle.propagate(states, [3], plan, cfg)
+    assert str(e.value) == str(e_ref.value)
+    assert (e.value.node, e.value.column) == (e_ref.value.node, e_ref.value.column)
+    assert str(e.value).startswith("group 0: picard iteration produced a non-finite value")
+
+
+def test_singularity_in_solve_names_body(ctx, oracle):
+    """Trajectory 2 starts 0.4 km from venus-like at its epoch: the force guard
+    raises SingularityError naming node, trajectory-in-group and body."""
+    states, plan, cfg = _setup(4, 16, 0.05, start="cold")
+    pos = oracle.body_positions(ps.reference_bodies(), ps.MU_SUN, np.array([0.0]))
+    states[2, 1:4] = pos[0, 0] + np.array([0.4, 0.0, 0.0])
     errs = []
     for impl in (ctx, oracle):
-        try:
-            impl.propagate(states, [3], plan, cfg)
-            errs.append(None)
-        except ps.Error as ex:  # DivergenceError or SingularityError depending on the path
-            errs.append(ex)
-    assert type(errs[0]) is type(errs[1])
-    assert str(errs[0]) == str(errs[1])
+        with pytest.raises(ps.SingularityError) as e:
+            impl.propagate(states, [4], plan, cfg)
+        errs.append(e.value)
+    assert str(errs[0]) == str(errs[1]) and errs[0].body == "venus-like"
+    assert "trajectory 2" in str(errs[0])

@@ -50,6 +50,33 @@ __global__ void dfma_loop(double* out, int iters, double seed) {
   out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+// Half the warps issue DMMA chains, the other half DFMA chains: if the tensor
+// (DMMA) and FP64 (DFMA) pipes are separate, the aggregate exceeds either alone.
+__global__ void mixed_loop(double* out, int iters, double seed) {
+  const int warp = threadIdx.x >> 5;
+  double s = 0.0;
+  if (warp & 1) {
+    double c[8][2];
+    for (int i = 0; i < 8; ++i) { c[i][0] = 0.0; c[i][1] = 0.0; }
+    const double a = seed * (threadIdx.x + 1), b = 1.0 / (threadIdx.x + 3);
+    for (int it = 0; it < iters; ++it) {
+      #pragma unroll
+      for (int i = 0; i < 8; ++i) dmma(c[i][0], c[i][1], a, b);
+    }
+    for (int i = 0; i < 8; ++i) s += c[i][0] + c[i][1];
+  } else {
+    double c[8];
+    for (int i = 0; i < 8; ++i) c[i] = seed * i;
+    const double a = 1.0 + 1e-9 * threadIdx.x, b = 1e-12;
+    for (int it = 0; it < iters * 4; ++it) {
+      #pragma unroll
+      for (int i = 0; i < 8; ++i) c[i] = fma(c[i], a, b);
+    }
+    for (int i = 0; i < 8; ++i) s += c[i];
+  }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
 // A (8x4) row-major, B (4x8) "col", C 8x8: verify assumed fragment layout.
 __global__ void layout_check(const double* A, const double* B, double* C) {
   const int lane = threadIdx.x;
@@ -110,6 +137,13 @@ int main() {
     char nm[64]; std::snprintf(nm, sizeof nm, "dfma_t%d", threads);
     bench(nm, [&] { dfma_loop<8><<<blocks, threads>>>(out, iters, 1e-3); },
           double(blocks) * threads * iters * 8 * 2.0);
+  }
+  // mixed: per DMMA warp 8*512 flops/iter; per DFMA warp 4*8*2*32 = 2048 flops/iter
+  for (int warps : {8, 16}) {
+    const int blocks = sms * 2;
+    char nm[64]; std::snprintf(nm, sizeof nm, "mixed_w%d", warps);
+    const double per_block = (warps / 2) * (8 * 512.0) + (warps / 2) * (4 * 8 * 2 * 32.0);
+    bench(nm, [&] { mixed_loop<<<blocks, 32 * warps>>>(out, iters, 1e-3); }, double(blocks) * per_block * iters);
   }
   std::printf("}\n");
   return 0;
