@@ -56,13 +56,15 @@ def workload(args, world, rank):
     import paper_2301_03989_b200 as ps
     base = ps.reference_state()
     period = ps.osculating_period(base, ps.MU_SUN)
+    from paper_2301_03989_b200.distributed import shard_groups
     total = args.per_gpu * world
     states = ps.make_clone_batch(base, total, 1e-5)
-    lo, hi = rank * args.per_gpu, (rank + 1) * args.per_gpu  # singleton groups: any split is group-aligned
+    shards = shard_groups([1] * total, world)  # independent mode: singleton groups
+    lo, hi = shards[rank][2], shards[rank][3]
     plan = ps.plan_segments(base, 0.0, args.span * period, ps.MU_SUN, "single", args.nodes)
     bodies = ps.planets8() if args.bodies == "planets8" else ps.reference_bodies()
     cfg = ps.reference_force_config("n_body", bodies=bodies, n_nodes=args.nodes)
-    return states, (lo, hi), plan, cfg
+    return states, (lo, hi), plan, cfg, shards
 
 
 def config_dict(args, world):
@@ -141,7 +143,7 @@ def run_reference(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
-    states, (lo, hi), plan, cfg = workload(args, 1, 0)
+    states, (lo, hi), plan, cfg, _ = workload(args, 1, 0)
     orc = Oracle()
     cores = os.cpu_count() or 1
     for _ in range(args.warmup):
@@ -183,11 +185,11 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     ctx = ps.Context(local)
-    states, (lo, hi), plan, cfg = workload(args, world, rank)
+    from paper_2301_03989_b200.distributed import gather_terminal
+    states, (lo, hi), plan, cfg, shards = workload(args, world, rank)
     shard = torch.from_numpy(states[lo:hi].copy()).pin_memory().numpy()  # pinned host ICs
     M = hi - lo
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
-    gathered = torch.empty((M * world, 7), dtype=torch.float64, device=dev) if world > 1 else None
 
     def barrier():
         if world > 1:
@@ -197,10 +199,7 @@ def main():
     def step():
         r = ctx.run_batch(shard, cfg, plan, "independent", samples=False, history=False)
         if world > 1:  # final gather of terminal states over NVLink (NCCL)
-            term = torch.from_numpy(r.terminal_states).to(dev, non_blocking=False)
-            dist.all_gather_into_tensor(gathered, term)
-            if rank == 0:
-                gathered.cpu()
+            gather_terminal(r.terminal_states, shards, rank, world, device=dev)
         return r
 
     for _ in range(args.warmup):

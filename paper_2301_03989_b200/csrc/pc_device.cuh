@@ -155,6 +155,17 @@ __device__ __forceinline__ double clenshaw(const double* c, int nc, double x) {
 /// two Newton steps (error < 1 ulp level).  The force arguments are squared distances
 /// of 1e-2..1e20 km^2, far from the denormal/overflow cases CUDA's rsqrt() guards
 /// with a slow-path branch.
+__device__ __forceinline__ double rsqrt_seed(double x) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    return y;
+}
+
+/// One Newton-Raphson step for 1/sqrt(x): y (1.5 - 0.5 x y^2).
+__device__ __forceinline__ double rsqrt_newton(double x, double y) {
+    return y * fma(-0.5 * x * y, y, 1.5);
+}
+
 __device__ __forceinline__ double rsqrt_nr(double x) {
     double y;
     asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
@@ -342,10 +353,8 @@ __device__ __forceinline__ void gemm_pair(const double* fbuf, const AWarp<XM>& w
 }
 
 /// One warp's share of Y' = [U; anchor]·F: `main` full-width m-tiles (acc) and up to
-/// XM extra tiles (xacc).  Operator pairs come from L2 as LDG.128, double-buffered in
-/// registers (one pair in flight while the other feeds the DMMAs; a pair is ~400 DMMA
-/// cycles per warp, well above L2 latency); B fragments are contiguous LDS.128 from
-/// the fragment-native Fbuf.
+/// XM extra tiles (xacc).  Operator pairs come from L2 as LDG.128, triple-buffered in
+/// registers; B fragments are contiguous LDS.128 from the fragment-native Fbuf.
 template <int XM>
 __device__ __forceinline__ void warp_gemm(const double2* __restrict__ upack, int nkp, const double* fbuf,
                                           const GemmPlan& gp, int warp, int lane, APrefetch<XM> pre,
@@ -358,15 +367,21 @@ __device__ __forceinline__ void warp_gemm(const double2* __restrict__ upack, int
     for (int x = 0; x < XM; ++x) xacc[x][0] = xacc[x][1] = 0.0;
     const AWarp<XM> w = a_warp<XM>(upack, nkp, gp, warp, lane);
     const int nmain = gp.main;
-    APair<XM> p0 = pre.p, p1;
+    // three register buffers, two operator pairs in flight (L2 latency under full-chip
+    // load exceeds one pair of DMMA issue time)
+    APair<XM> p0 = pre.p, p1, p2;
+    if (nkp > 1) load_apair<XM>(w, nmain, 1, p1);
     int kp = 0;
-    for (; kp + 1 < nkp; kp += 2) {
-        load_apair<XM>(w, nmain, kp + 1, p1);
+    for (; kp + 2 < nkp; kp += 3) {
+        load_apair<XM>(w, nmain, kp + 2, p2);
         gemm_pair<XM>(fbuf, w, nmain, lane, kp, p0, acc, xacc);
-        if (kp + 2 < nkp) load_apair<XM>(w, nmain, kp + 2, p0);
+        if (kp + 3 < nkp) load_apair<XM>(w, nmain, kp + 3, p0);
         gemm_pair<XM>(fbuf, w, nmain, lane, kp + 1, p1, acc, xacc);
+        if (kp + 4 < nkp) load_apair<XM>(w, nmain, kp + 4, p1);
+        gemm_pair<XM>(fbuf, w, nmain, lane, kp + 2, p2, acc, xacc);
     }
     if (kp < nkp) gemm_pair<XM>(fbuf, w, nmain, lane, kp, p0, acc, xacc);
+    if (kp + 1 < nkp) gemm_pair<XM>(fbuf, w, nmain, lane, kp + 1, p1, acc, xacc);
 }
 
 }  // namespace pswarm_dev

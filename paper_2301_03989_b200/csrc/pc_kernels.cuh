@@ -95,6 +95,46 @@ struct BodyTable {
 cudaError_t launch_ephemeris(int N, const double* times, double central_mu, const BodyTable& bt, double* pos,
                              double* indirect, unsigned long long* fault_key, cudaStream_t s);
 
+/// Arguments of the wide-group path (groups larger than one CTA's 8 slots).
+struct WideArgs {
+    int N, nkp;
+    GemmPlan gp;
+    int xrows;
+    int M, P, seg, cold_start, error_mode, max_it;
+    double tol, omega2, epoch;
+    ForceData fd;
+    const double2* upack;
+    const double* times;
+    const int64_t* group_off;     // [P+1]
+    const int* traj_group;        // [M]
+    const double* state_in;       // [M][6]
+    double* state_out;            // [M][6]
+    double* Y;                    // [tiles][N][48] state blocks in HBM
+    double* samples;
+    int64_t R, row0;
+    int* g_active;                // [P]
+    int* g_iter;                  // [P]
+    unsigned long long* g_err2;   // [P] max squared error ratio (bits) of the running iteration
+    unsigned long long* g_nf;     // [P] first non-finite (node, column) key
+    unsigned long long* g_sing;   // [P] first singular sample key (s << 6 | check)
+    unsigned long long* t_sing_key;  // [M]
+    double* t_sing_val;           // [M]
+    int32_t* rep_iter;
+    double* rep_err;
+    uint8_t* rep_conv;
+    double* rep_hist;
+    GroupFault* faults;
+    uint8_t* cold_fallback;
+    unsigned long long* warm_key; // min trajectory*4 + kind of a warm-start fault
+    int* active_count;            // groups still iterating after the last finalize
+};
+
+size_t wide_iter_smem_bytes(int N, int nkp, int xrows);
+cudaError_t launch_wide_start(const WideArgs& a, cudaStream_t s);
+cudaError_t launch_wide_iter(const WideArgs& a, int grid, cudaStream_t s);
+cudaError_t launch_wide_finalize(const WideArgs& a, cudaStream_t s);
+cudaError_t launch_wide_output(const WideArgs& a, cudaStream_t s);
+
 GemmPlan make_gemm_plan(int N);
 int extra_rows(int N, const GemmPlan& gp);
 size_t segment_smem_bytes(int N, int nkp, int xrows, int B, int stage_eph);

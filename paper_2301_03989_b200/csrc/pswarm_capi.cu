@@ -5,6 +5,7 @@
 // frozen ephemeris, packed operators) and turns device fault records into the
 // reference's exceptions.  There is no CPU fallback anywhere in this file.
 #include <algorithm>
+#include <iterator>
 #include <chrono>
 #include <climits>
 #include <cmath>
@@ -143,7 +144,8 @@ enum BufId {
     B_STATE_A, B_STATE_B, B_GROUP_OFF, B_TIMES, B_BODY_POS, B_BODY_MU, B_INDIRECT, B_QUEUE,
     B_REP_ITER, B_REP_ERR, B_REP_CONV, B_REP_HIST, B_FAULTS, B_FALLBACK, B_SAMPLES, B_DEAD,
     B_OP_IN, B_OP_IN2, B_OP_OUT, B_OP_AUX, B_OP_KEY,
-    B_BT_KIND, B_BT_SOFF, B_BT_NC, B_BT_EL, B_BT_BND, B_BT_COFF, B_BT_CF, B_PHASES, B_COUNT
+    B_BT_KIND, B_BT_SOFF, B_BT_NC, B_BT_EL, B_BT_BND, B_BT_COFF, B_BT_CF, B_PHASES,
+    B_W_TG, B_W_Y, B_W_ACT, B_W_ITER, B_W_ERR, B_W_NF, B_W_SING, B_W_TSK, B_W_TSV, B_W_WK, B_W_CNT, B_COUNT
 };
 
 }  // namespace
@@ -160,6 +162,12 @@ struct pswarm_ctx {
     int max_ctas = 0;  // 0 = SM count * ctas_per_sm
     int profile_phases = 0;
     unsigned long long phase_host[pswarm_dev::PHASES] = {};
+    // wide-group path
+    cudaEvent_t wide_ev[4] = {};
+    int* wide_count_host = nullptr;  // pinned ring of active-group counts
+    unsigned long long wide_warm_key = ~0ull;
+    double wide_warm_vals[2] = {0.0, 0.0};
+    bool wide_timeout = false;
 };
 
 namespace {
@@ -261,6 +269,100 @@ void upload(pswarm_ctx* ctx, BufId id, const T* host, size_t count, T** dev) {
     if (count) cuda_check(cudaMemcpyAsync(*dev, host, count * sizeof(T), cudaMemcpyHostToDevice, ctx->stream), "H2D");
 }
 
+// ------------------------------------------------------------- wide groups
+/// One segment of groups larger than a CTA's slots: warm start into HBM, then
+/// lockstep iterations (k_wide_iter + k_wide_finalize) until no group is active,
+/// with at most two iterations in flight before the host reads the active count.
+void run_wide_segment(pswarm_ctx* ctx, const SegArgs& s, const std::vector<int64_t>& h_off,
+                      std::chrono::steady_clock::time_point deadline) {
+    cudaStream_t st = ctx->stream;
+    const int M = s.M, P = s.P, N = s.N;
+    const int tiles = (M + SLOTS - 1) / SLOTS;
+    WideArgs a{};
+    a.N = N;
+    a.nkp = s.nkp;
+    a.gp = s.gp;
+    a.xrows = s.xrows;
+    a.M = M;
+    a.P = P;
+    a.seg = s.seg;
+    a.cold_start = s.cold_start;
+    a.error_mode = s.error_mode;
+    a.max_it = s.max_it;
+    a.tol = s.tol;
+    a.omega2 = s.omega2;
+    a.epoch = s.epoch;
+    a.fd = s.fd;
+    a.upack = s.upack;
+    a.times = s.times;
+    a.group_off = s.group_off;
+    a.state_in = s.state_in;
+    a.state_out = s.state_out;
+    a.samples = s.samples;
+    a.R = s.R;
+    a.row0 = s.row0;
+    a.rep_iter = s.rep_iter;
+    a.rep_err = s.rep_err;
+    a.rep_conv = s.rep_conv;
+    a.rep_hist = s.rep_hist;
+    a.faults = s.faults;
+    a.cold_fallback = s.cold_fallback;
+    std::vector<int> tg(static_cast<size_t>(M));
+    for (int g = 0; g < P; ++g)
+        for (int64_t i = h_off[g]; i < h_off[g + 1]; ++i) tg[i] = g;
+    int* d_tg;
+    upload(ctx, B_W_TG, tg.data(), tg.size(), &d_tg);
+    a.traj_group = d_tg;
+    a.Y = ctx->buf[B_W_Y].get<double>(static_cast<size_t>(tiles) * N * COLS);
+    a.g_active = ctx->buf[B_W_ACT].get<int>(P);
+    a.g_iter = ctx->buf[B_W_ITER].get<int>(P);
+    a.g_err2 = ctx->buf[B_W_ERR].get<unsigned long long>(P);
+    a.g_nf = ctx->buf[B_W_NF].get<unsigned long long>(P);
+    a.g_sing = ctx->buf[B_W_SING].get<unsigned long long>(P);
+    a.t_sing_key = ctx->buf[B_W_TSK].get<unsigned long long>(M);
+    a.t_sing_val = ctx->buf[B_W_TSV].get<double>(M);
+    a.warm_key = ctx->buf[B_W_WK].get<unsigned long long>(2);
+    a.active_count = ctx->buf[B_W_CNT].get<int>(8);
+    std::vector<int> ones(static_cast<size_t>(P), 1);
+    cuda_check(cudaMemcpyAsync(a.g_active, ones.data(), sizeof(int) * P, cudaMemcpyHostToDevice, st), "H2D");
+    cuda_check(cudaMemsetAsync(a.g_iter, 0, sizeof(int) * P, st), "memset");
+    cuda_check(cudaMemsetAsync(a.g_err2, 0, sizeof(unsigned long long) * P, st), "memset");
+    cuda_check(cudaMemsetAsync(a.g_nf, 0xff, sizeof(unsigned long long) * P, st), "memset");
+    cuda_check(cudaMemsetAsync(a.g_sing, 0xff, sizeof(unsigned long long) * P, st), "memset");
+    cuda_check(cudaMemsetAsync(a.warm_key, 0xff, sizeof(unsigned long long), st), "memset");
+    cuda_check(cudaEventRecord(ctx->evk0, st), "event");
+    cuda_check(launch_wide_start(a, st), "k_wide_start");
+    ++ctx->launches;
+    const int grid = std::max(1, std::min(tiles, ctx->sm_count));
+    ctx->wide_timeout = false;
+    constexpr int RING = 4;
+    for (int it = 1; it <= a.max_it; ++it) {
+        if (it > 2) {  // read the active count of iteration it-2 (two launches in flight)
+            cuda_check(cudaEventSynchronize(ctx->wide_ev[(it - 2) % RING]), "wide poll");
+            if (ctx->wide_count_host[(it - 2) % RING] == 0) break;
+        }
+        if (std::chrono::steady_clock::now() > deadline) {
+            ctx->wide_timeout = true;
+            break;
+        }
+        cuda_check(cudaMemsetAsync(a.active_count, 0, sizeof(int), st), "memset");
+        cuda_check(launch_wide_iter(a, grid, st), "k_wide_iter");
+        cuda_check(launch_wide_finalize(a, st), "k_wide_finalize");
+        ctx->launches += 2;
+        cuda_check(cudaMemcpyAsync(ctx->wide_count_host + it % RING, a.active_count, sizeof(int),
+                                   cudaMemcpyDeviceToHost, st),
+                   "D2H count");
+        cuda_check(cudaEventRecord(ctx->wide_ev[it % RING], st), "event");
+    }
+    cuda_check(launch_wide_output(a, st), "k_wide_output");
+    ++ctx->launches;
+    cuda_check(cudaEventRecord(ctx->evk1, st), "event");
+    cuda_check(cudaMemcpyAsync(&ctx->wide_warm_key, a.warm_key, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st),
+               "D2H");
+    cuda_check(cudaStreamSynchronize(st), "wide segment");
+    ctx->wide_warm_vals[0] = ctx->wide_warm_vals[1] = 0.0;
+}
+
 // ----------------------------------------------------------------- propagate
 struct RunSpec {
     bool independent = false;  // run_batch independent mode: reference error order is per trajectory
@@ -292,10 +394,7 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
     if (states[0] != boundaries[0])
         throw pswarm::AlignmentError("propagate: batch epoch does not match the first segment boundary");
     if (cfg->tolerance <= 0.0) throw pswarm::Error("pc_solve: tolerance must be positive");
-    if (gmax > SLOTS)
-        raise(PSWARM_ERR_INVALID_PLAN,
-              fmtf("propagate: groups larger than %d trajectories need the wide-group path (largest group %lld)", SLOTS,
-                   (long long)gmax));
+    const bool wide = gmax > SLOTS;  // groups spanning CTAs: lockstep iterations through HBM
     if (N < 3) throw pswarm::InvalidSizeError("build_matrices: need at least 3 nodes, got " + std::to_string(N));
     if (!ctx) raise(PSWARM_ERR_NO_DEVICE, "propagate: no device context (the B200 path has no CPU fallback)");
     bind(ctx);
@@ -319,10 +418,10 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
     double* d_in = nullptr;
     upload(ctx, B_STATE_A, s6.data(), s6.size(), &d_in);
     double* d_out = ctx->buf[B_STATE_B].get<double>(s6.size());
-    std::vector<int64_t> off(static_cast<size_t>(P) + 1, 0);
-    for (int64_t g = 0; g < P; ++g) off[g + 1] = off[g] + group_sizes[g];
+    std::vector<int64_t> h_off(static_cast<size_t>(P) + 1, 0);
+    for (int64_t g = 0; g < P; ++g) h_off[g + 1] = h_off[g] + group_sizes[g];
     int64_t* d_off = nullptr;
-    upload(ctx, B_GROUP_OFF, off.data(), off.size(), &d_off);
+    upload(ctx, B_GROUP_OFF, h_off.data(), h_off.size(), &d_off);
     const int64_t R = 1 + S * (N - 1);
     double* d_samples = out && out->samples ? ctx->buf[B_SAMPLES].get<double>(static_cast<size_t>(M) * R * 6) : nullptr;
     int* d_queue = ctx->buf[B_QUEUE].get<int>(4);
@@ -357,10 +456,10 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
     const int xrows = extra_rows(static_cast<int>(N), op.gp);
     // stage the frozen ephemeris in shared memory when it fits next to the state blocks
     const int stage_eph = (nb > 0 && segment_smem_bytes(static_cast<int>(N), op.nkp, xrows, nb, 1) <= 227 * 1024) ? 1 : 0;
-    if (segment_smem_bytes(static_cast<int>(N), op.nkp, xrows, nb, stage_eph) > 227 * 1024)
+    if (!wide && segment_smem_bytes(static_cast<int>(N), op.nkp, xrows, nb, stage_eph) > 227 * 1024)
         raise(PSWARM_ERR_INVALID_SIZE, fmtf("propagate: %lld nodes exceed the per-SM shared memory of the slot kernel",
                                             (long long)N));
-    const int per_cta = std::max<int64_t>(1, SLOTS / gmax);
+    const int per_cta = std::max<int64_t>(1, SLOTS / std::min<int64_t>(gmax, SLOTS));
     const int64_t want_ctas = (P + per_cta - 1) / per_cta;
     const int cap = ctx->max_ctas > 0 ? ctx->max_ctas : ctx->sm_count * ctx->ctas_per_sm;
     const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want_ctas, cap)));
@@ -457,11 +556,13 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
         a.faults = d_faults;
         a.cold_fallback = d_fb;
         a.phase_cycles = d_phase;
-        if (max_it > 0) {
+        if (max_it > 0 && !wide) {
             cuda_check(cudaEventRecord(ctx->evk0, st), "event");
             cuda_check(launch_segment(a, grid, st), "k_pc_segment launch");
             cuda_check(cudaEventRecord(ctx->evk1, st), "event");
             ++ctx->launches;
+        } else if (max_it > 0) {
+            run_wide_segment(ctx, a, h_off, deadline);
         }
         cuda_check(cudaMemcpyAsync(h_iter.data() + seg * P, d_iter, sizeof(int32_t) * P, cudaMemcpyDeviceToHost, st), "D2H");
         cuda_check(cudaMemcpyAsync(h_err.data() + seg * P, d_err, sizeof(double) * P, cudaMemcpyDeviceToHost, st), "D2H");
@@ -504,6 +605,23 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
             kernel_ms += kms;
         }
         for (int64_t gi = 0; gi < P; ++gi) traj_iters += static_cast<int64_t>(h_iter[seg * P + gi]) * group_sizes[gi];
+        if (wide && ctx->wide_timeout) {  // deadline between lockstep iterations (augment.hpp:117-121)
+            for (int64_t gi = 0; gi < P; ++gi)
+                if (!h_conv[seg * P + gi]) {
+                    h_faults[gi].status = FAULT_TIMEOUT;
+                    break;
+                }
+        }
+        if (wide && ctx->wide_warm_key != ~0ull) {  // warm-start fault of the wide path -> group record
+            const int64_t tr = static_cast<int64_t>(ctx->wide_warm_key / 4);
+            const int64_t gi = std::upper_bound(h_off.begin(), h_off.end(), tr) - h_off.begin() - 1;
+            GroupFault& f = h_faults[gi];
+            f = GroupFault{};
+            f.status = (ctx->wide_warm_key % 4) == CONIC_ZERO_RADIUS ? FAULT_WARM_ZERO_RADIUS : FAULT_WARM_SOLVER;
+            f.trajectory = tr;
+            f.value = ctx->wide_warm_vals[0];
+            f.value2 = ctx->wide_warm_vals[1];
+        }
 
         // ---- faults, in the order the serial reference would raise them
         int64_t warm_traj = -1, warm_g = -1, first_g = -1;
@@ -719,6 +837,8 @@ pswarm_status pswarm_create(int32_t device, pswarm_ctx** out, pswarm_error* err)
         cuda_check(cudaEventCreate(&ctx->ev1), "cudaEventCreate");
         cuda_check(cudaEventCreate(&ctx->evk0), "cudaEventCreate");
         cuda_check(cudaEventCreate(&ctx->evk1), "cudaEventCreate");
+        for (auto& e : ctx->wide_ev) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+        cuda_check(cudaHostAlloc(&ctx->wide_count_host, 4 * sizeof(int), cudaHostAllocDefault), "cudaHostAlloc");
         *out = ctx.release();
     });
 }
@@ -737,6 +857,9 @@ void pswarm_destroy(pswarm_ctx* ctx) {
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
     if (ctx->evk0) cudaEventDestroy(ctx->evk0);
     if (ctx->evk1) cudaEventDestroy(ctx->evk1);
+    for (auto& e : ctx->wide_ev)
+        if (e) cudaEventDestroy(e);
+    if (ctx->wide_count_host) cudaFreeHost(ctx->wide_count_host);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
 }

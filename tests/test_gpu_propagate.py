@@ -91,14 +91,43 @@ def test_c2_nbody_independent(ctx, oracle, bodies):
         assert np.allclose(a[:k][big], b[:k][big], rtol=1e-4, atol=0)
 
 
-@pytest.mark.parametrize("mode,p", [("grouped", 8), ("grouped", 16), ("augmented", 1)])
-def test_group_modes_match_oracle(ctx, oracle, mode, p):
-    m = 8 if mode == "augmented" else 64
+@pytest.mark.parametrize("mode,p,m", [("grouped", 8, 64), ("grouped", 16, 64), ("augmented", 1, 8),
+                                      ("augmented", 1, 64), ("grouped", 2, 64), ("grouped", 3, 50)])
+def test_group_modes_match_oracle(ctx, oracle, mode, p, m):
+    """Groups within one CTA (<= 8 members, slot kernel) and wide groups (lockstep
+    iterations through HBM): a group stops only when its worst member converges."""
     states, plan, cfg = _setup(m, 128, 0.6)
     cfg.p_groups = p
     got = ctx.run_batch(states, cfg, plan, mode)
     want = oracle.run_batch(states, cfg, plan, mode, 4)
     _parity(got, want)
+    # mode invariance against independent masking (test_runner.cpp:45-59: < 1e-12)
+    ind = ctx.run_batch(states, cfg, plan, "independent")
+    assert ps.max_state_discrepancy(got.trajectories, ind.trajectories) < 1e-12
+
+
+def test_wide_group_multisegment_and_errors(ctx, oracle):
+    """Wide groups across segments (exact chaining) and non-convergence reporting."""
+    states, plan, cfg = _setup(40, 64, 1.7, policy="per_orbit")
+    got = ctx.propagate(states, [17, 23], plan, cfg)
+    want = oracle.propagate(states, [17, 23], plan, cfg)
+    _parity(got, want)
+    cfg.max_iterations = 4
+    with pytest.raises(ps.PropagationIncompleteError) as e:
+        ctx.propagate(states, [17, 23], plan, cfg)
+    with pytest.raises(ps.PropagationIncompleteError) as e_ref:
+        oracle.propagate(states, [17, 23], plan, cfg)
+    assert (e.value.segment, e.value.group) == (e_ref.value.segment, e_ref.value.group)
+
+
+def test_wide_group_divergence_coordinates(ctx, oracle):
+    states, plan, cfg = _setup(20, 32, 0.5, bodies="two_body", start="cold")
+    states[13, 1:4] = [1e-110, 0.0, 0.0]
+    with pytest.raises(ps.DivergenceError) as e:
+        ctx.propagate(states, [20], plan, cfg)
+    with pytest.raises(ps.DivergenceError) as e_ref:
+        oracle.propagate(states, [20], plan, cfg)
+    assert str(e.value) == str(e_ref.value)
 
 
 def test_multisegment_per_orbit(ctx, oracle):
