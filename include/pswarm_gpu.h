@@ -137,7 +137,9 @@ void pswarm_destroy(pswarm_ctx* ctx);
 
 /* Tuning knobs: "ctas_per_sm" (persistent CTAs per SM, default 1), "max_ctas" (cap
  * on the persistent grid, 0 = SM count * ctas_per_sm), "profile_phases" (1 = record
- * per-phase SM cycles of the solve kernel, read with pswarm_get_phase_cycles). */
+ * per-phase SM cycles of the generic slot kernel, read with pswarm_get_phase_cycles),
+ * "slot_kernel" (0 auto, 1 force the generic slot kernel, 2 prefer the
+ * warp-specialised one). */
 pswarm_status pswarm_set_option(pswarm_ctx* ctx, const char* key, int64_t value);
 
 /* Diagnostics: SM cycles summed over CTAs per kernel phase of the last call

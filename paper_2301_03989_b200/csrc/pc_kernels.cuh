@@ -135,6 +135,12 @@ cudaError_t launch_wide_iter(const WideArgs& a, int grid, cudaStream_t s);
 cudaError_t launch_wide_finalize(const WideArgs& a, cudaStream_t s);
 cudaError_t launch_wide_output(const WideArgs& a, cudaStream_t s);
 
+/// Warp-specialised slot kernel (pc_slots2.cu) for groups of <= 4 trajectories.
+size_t ws_smem_bytes(int N, int nkp, int xrows, int B, int stage_eph);
+int ws_main_tiles(int N);
+int ws_extra_rows(int N);
+cudaError_t launch_segment_ws(const SegArgs& a, int grid, cudaStream_t s);
+
 GemmPlan make_gemm_plan(int N);
 int extra_rows(int N, const GemmPlan& gp);
 size_t segment_smem_bytes(int N, int nkp, int xrows, int B, int stage_eph);

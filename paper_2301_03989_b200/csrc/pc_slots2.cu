@@ -1,0 +1,691 @@
+// Warp-specialised slot kernel (k_pc_ws): the fast path of the persistent solve for
+// groups of at most 4 trajectories (independent mode = singleton groups).
+//
+// The 8 trajectory slots of a CTA are split into two halves of 4.  Sixteen warps
+// form two groups that run the halves out of phase:
+//   MMA group (warps 0-7):  [DMMA update of half h] -> [epilogue of half h: + b0/2,
+//                           finite check, error] -> signal "Y_h ready"
+//   FP group  (warps 8-15): [decisions / retire / refill / warm start of half h]
+//                           -> [force of half h] -> signal "F_h ready"
+// so the FP64-vector work of one half (force, conics) overlaps the DMMA work of the
+// other half instead of idling the shared FP64 pipe between phases (on B200 the DMMA
+// and DFMA paths share one FP64 datapath, tools/fp64_peak.cu).  Hand-off is through
+// named barriers (bar.arrive / bar.sync, 512 threads).  Semantics are identical to
+// k_pc_segment (pc_kernels.cu): pc_solve's loop (picard.hpp:66-81) per group with
+// per-trajectory masking and refill.
+//
+// Half layout (per half: 4 slots x 6 components = 24 block columns = 3 MMA n-tiles):
+//   n-tile p holds components 2p, 2p+1; column within the tile = slot*2 + (comp & 1),
+//   so C-fragment lane (g, q) holds all six components of slot q of row g.
+#include <climits>
+
+#include "pc_kernels.cuh"
+#include "pc_tile.cuh"
+
+namespace pswarm_dev {
+
+namespace {
+
+constexpr int HS = 4;            // slots per half
+constexpr int HC = 6 * HS;       // columns per half
+constexpr int YS2 = 2 * HC + 4;  // Ybuf row stride (doubles): 52 -> conflict-free epilogue rows
+constexpr int MMA_WARPS = 8, FP_WARPS = 8;
+constexpr int MMA_THREADS = 32 * MMA_WARPS, FP_THREADS = 32 * FP_WARPS, WS_THREADS = MMA_THREADS + FP_THREADS;
+constexpr int BAR_F0 = 1, BAR_Y0 = 3, BAR_MMA = 5, BAR_FP = 6;  // F_h = 1+h, Y_h = 3+h
+
+__device__ __forceinline__ int y2(int j, int h, int c, int s) { return j * YS2 + h * HC + c * HS + s; }
+/// B-fragment index of F(node j, comp c, slot s) within a half's Fbuf.
+__device__ __forceinline__ int f2(int j, int c, int s) {
+    return (((j >> 2) * 3 + (c >> 1)) * 32) + ((s * 2 + (c & 1)) * 4 + (j & 3));
+}
+
+__device__ __forceinline__ void bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void bar_arrive(int id, int n) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+struct WsState {
+    int slot_traj[SLOTS];
+    int slot_grp[SLOTS];
+    int slot_member[SLOTS];
+    int sing_key[SLOTS];
+    int nf_key[SLOTS];
+    int warm_key[SLOTS];
+    int warm_kind[SLOTS];
+    unsigned long long slot_err[SLOTS];
+    double sing_val[SLOTS];
+    double warm_val[SLOTS][2];
+    double y0[SLOTS][6];
+    double b0h[2][HC];
+    int grp_id[SLOTS];
+    int grp_size[SLOTS];
+    int grp_iter[SLOTS];
+    int active_mask;     // both halves
+    int new_mask[2];     // slots claimed at the last refill of each half
+    int free_mask;
+    int retire_mask;
+    int half_active[2];  // MMA group skips an empty half
+    int queue_done;
+    int timeout;
+    int exit_flag;
+};
+
+struct WsLayout {
+    size_t ybuf, fbuf0, fbuf1, xstage, eph, state, total;
+};
+
+__host__ __device__ inline WsLayout ws_layout(int N, int nkp, int xrows, int B, int stage_eph) {
+    WsLayout L;
+    L.ybuf = 0;
+    L.fbuf0 = L.ybuf + sizeof(double) * static_cast<size_t>(N) * YS2;
+    const size_t fb = sizeof(double) * static_cast<size_t>(8 * nkp) * HC;
+    L.fbuf1 = L.fbuf0 + fb;
+    L.xstage = L.fbuf1 + fb;
+    L.eph = L.xstage + sizeof(double) * static_cast<size_t>(xrows) * HC;
+    L.state = L.eph + (stage_eph ? sizeof(double) * static_cast<size_t>(N) * (3 * B + 3) : 0);
+    L.total = L.state + sizeof(WsState);
+    return L;
+}
+
+/// Tile plan of one half (26 m-tiles x 3 n-tiles at N = 200) over the 8 MMA warps:
+/// `main` consecutive full-width m-tiles per warp + up to XMW single extra tiles.
+struct HalfPlan {
+    int main, mb, extras;
+};
+
+template <int MAIN, int XMW>
+struct APairH {
+    double2 m[MAIN];
+    double2 x[XMW];
+};
+
+/// One warp's share of Y'_h = [U; anchor] F_h over all K (LDG.128 operator pairs,
+/// double-buffered; B fragments are LDS.64 of the fragment-native half Fbuf).
+template <int MAIN, int XMW>
+__device__ __forceinline__ void gemm_half(const double2* __restrict__ upack, int nkp, const double* fb,
+                                          const HalfPlan& hp, int warp, int lane, double (&acc)[MAIN][3][2],
+                                          double (&xacc)[XMW][2]) {
+#pragma unroll
+    for (int i = 0; i < MAIN; ++i)
+#pragma unroll
+        for (int p = 0; p < 3; ++p) acc[i][p][0] = acc[i][p][1] = 0.0;
+    const double2* am[MAIN];
+    const double2* ax[XMW];
+    bool hx[XMW];
+    int xp[XMW];
+#pragma unroll
+    for (int i = 0; i < MAIN; ++i) am[i] = upack + static_cast<size_t>(warp * MAIN + i) * nkp * 32 + lane;
+#pragma unroll
+    for (int x = 0; x < XMW; ++x) {
+        const int e = warp + x * MMA_WARPS;
+        hx[x] = e < hp.extras;
+        ax[x] = upack + static_cast<size_t>(hx[x] ? hp.mb + e / 3 : 0) * nkp * 32 + lane;
+        xp[x] = e % 3;
+    }
+    auto load = [&](int kp, APairH<MAIN, XMW>& p) {
+#pragma unroll
+        for (int i = 0; i < MAIN; ++i) p.m[i] = __ldg(am[i] + kp * 32);
+#pragma unroll
+        for (int x = 0; x < XMW; ++x)
+            if (hx[x]) p.x[x] = __ldg(ax[x] + kp * 32);
+    };
+    auto compute = [&](int kp, const APairH<MAIN, XMW>& c) {
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+            const int ks = 2 * kp + s;
+            const double* fk = fb + ks * 96 + lane;
+            const double b0 = fk[0], b1 = fk[32], b2 = fk[64];
+            const double bv[3] = {b0, b1, b2};
+#pragma unroll
+            for (int i = 0; i < MAIN; ++i) {
+                const double a = s ? c.m[i].y : c.m[i].x;
+#pragma unroll
+                for (int p = 0; p < 3; ++p) dmma(acc[i][p][0], acc[i][p][1], a, bv[p]);
+            }
+#pragma unroll
+            for (int x = 0; x < XMW; ++x)
+                if (hx[x]) {
+                    const double bx = xp[x] == 0 ? b0 : (xp[x] == 1 ? b1 : b2);
+                    dmma(xacc[x][0], xacc[x][1], s ? c.x[x].y : c.x[x].x, bx);
+                }
+        }
+    };
+#pragma unroll
+    for (int x = 0; x < XMW; ++x) xacc[x][0] = xacc[x][1] = 0.0;
+    APairH<MAIN, XMW> p0, p1;
+    load(0, p0);
+    int kp = 0;
+    for (; kp + 1 < nkp; kp += 2) {
+        load(kp + 1, p1);
+        compute(kp, p0);
+        if (kp + 2 < nkp) load(kp + 2, p0);
+        compute(kp + 1, p1);
+    }
+    if (kp < nkp) compute(kp, p0);
+}
+
+/// Force of half h for node j, its 4 slots as independent chains (force_model.hpp:93-142).
+__device__ __forceinline__ void force_half(const ForceData& fd, double w2, const double* ybuf, double* fb, int* sing_key,
+                                           const double* pos_base, const double* ind_base, int act_h, int h, int j) {
+    const int B = fd.n_bodies;
+    double rx[HS], ry[HS], rz[HS], ax[HS], ay[HS], az[HS], r2[HS], ir[HS];
+    bool on[HS];
+    bool flag = false;
+#pragma unroll
+    for (int s = 0; s < HS; ++s) {
+        on[s] = (act_h >> s) & 1;
+        rx[s] = on[s] ? ybuf[y2(j, h, 0, s)] : 1.0e8;
+        ry[s] = on[s] ? ybuf[y2(j, h, 1, s)] : 0.0;
+        rz[s] = on[s] ? ybuf[y2(j, h, 2, s)] : 0.0;
+        r2[s] = rx[s] * rx[s] + ry[s] * ry[s] + rz[s] * rz[s];
+        flag |= !(r2[s] > 0.0);
+    }
+#pragma unroll
+    for (int s = 0; s < HS; ++s) ir[s] = rsqrt_newton(r2[s], rsqrt_newton(r2[s], rsqrt_seed(r2[s])));
+#pragma unroll
+    for (int s = 0; s < HS; ++s) {
+        const double sc = -fd.central_mu * (ir[s] * ir[s] * ir[s]);
+        ax[s] = sc * rx[s];
+        ay[s] = sc * ry[s];
+        az[s] = sc * rz[s];
+    }
+    const double* bp = pos_base + static_cast<size_t>(j) * 3 * B;
+    for (int b = 0; b < B; ++b) {
+        const double mu_b = __ldg(fd.body_mu + b);
+        const double qx = bp[3 * b], qy = bp[3 * b + 1], qz = bp[3 * b + 2];
+        double dx[HS], dy[HS], dz[HS], d2[HS], y[HS];
+#pragma unroll
+        for (int s = 0; s < HS; ++s) {
+            dx[s] = qx - rx[s];
+            dy[s] = qy - ry[s];
+            dz[s] = qz - rz[s];
+            d2[s] = dx[s] * dx[s] + dy[s] * dy[s] + dz[s] * dz[s];
+            flag |= d2[s] < fd.floor2_hi;
+        }
+#pragma unroll
+        for (int s = 0; s < HS; ++s) y[s] = rsqrt_newton(d2[s], rsqrt_seed(d2[s]));
+#pragma unroll
+        for (int s = 0; s < HS; ++s) {
+            const double kk = mu_b * (y[s] * y[s] * y[s]);
+            ax[s] += kk * dx[s];
+            ay[s] += kk * dy[s];
+            az[s] += kk * dz[s];
+        }
+    }
+    if (B > 0) {
+        const double ix = ind_base[3 * j], iy = ind_base[3 * j + 1], iz = ind_base[3 * j + 2];
+#pragma unroll
+        for (int s = 0; s < HS; ++s) {
+            ax[s] -= ix;
+            ay[s] -= iy;
+            az[s] -= iz;
+        }
+    }
+    if (flag) {  // rare: exact guard order of table_acceleration (force_model.hpp:57-69)
+#pragma unroll
+        for (int s = 0; s < HS; ++s) {
+            if (!on[s]) continue;
+            int fail = (rx[s] * rx[s] + ry[s] * ry[s] + rz[s] * rz[s] > 0.0) ? -1 : 0;
+            for (int b = 0; b < B && fail < 0; ++b) {
+                const double dx = bp[3 * b] - rx[s], dy = bp[3 * b + 1] - ry[s], dz = bp[3 * b + 2] - rz[s];
+                if (sqrt(dx * dx + dy * dy + dz * dz) < fd.floor_km) fail = 1 + b;
+            }
+            if (fail >= 0) atomicMin(&sing_key[h * HS + s], j * (B + 1) + fail);
+        }
+    }
+#pragma unroll
+    for (int s = 0; s < HS; ++s) {
+        fb[f2(j, 0, s)] = on[s] ? w2 * ybuf[y2(j, h, 3, s)] : 0.0;
+        fb[f2(j, 1, s)] = on[s] ? w2 * ybuf[y2(j, h, 4, s)] : 0.0;
+        fb[f2(j, 2, s)] = on[s] ? w2 * ybuf[y2(j, h, 5, s)] : 0.0;
+        fb[f2(j, 3, s)] = on[s] ? w2 * ax[s] : 0.0;
+        fb[f2(j, 4, s)] = on[s] ? w2 * ay[s] : 0.0;
+        fb[f2(j, 5, s)] = on[s] ? w2 * az[s] : 0.0;
+    }
+}
+
+}  // namespace
+
+size_t ws_smem_bytes(int N, int nkp, int xrows, int B, int stage_eph) {
+    return ws_layout(N, nkp, xrows, B, stage_eph).total;
+}
+
+int ws_main_tiles(int N) {
+    const int mt = (N + 1 + 7) / 8;
+    return mt / MMA_WARPS;
+}
+
+int ws_extra_rows(int N) {
+    const int mb = ws_main_tiles(N) * MMA_WARPS;
+    const int r = N - mb * 8;
+    return r > 0 ? r : 0;
+}
+
+template <int MAIN, int XMW, bool STAGE>
+__global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int N = a.N, B = a.fd.n_bodies;
+    const int xrows = a.xrows;
+    const WsLayout L = ws_layout(N, a.nkp, xrows, B, STAGE ? 1 : 0);
+    double* ybuf = reinterpret_cast<double*>(smem_raw + L.ybuf);
+    double* fbh[2] = {reinterpret_cast<double*>(smem_raw + L.fbuf0), reinterpret_cast<double*>(smem_raw + L.fbuf1)};
+    double* xstage = reinterpret_cast<double*>(smem_raw + L.xstage);
+    double* eph = reinterpret_cast<double*>(smem_raw + L.eph);
+    WsState& st = *reinterpret_cast<WsState*>(smem_raw + L.state);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int KP = 8 * a.nkp;
+    const int mtiles = (N + 1 + 7) / 8;
+    HalfPlan hp;
+    hp.main = MAIN;
+    hp.mb = MAIN * MMA_WARPS;
+    hp.extras = (mtiles - hp.mb) * 3;
+
+    for (int i = tid; i < 2 * KP * HC; i += WS_THREADS) fbh[0][i] = 0.0;  // both halves (contiguous)
+    if (STAGE && B > 0) {
+        for (int i = tid; i < N * 3 * B; i += WS_THREADS) eph[i] = a.fd.body_pos[i];
+        for (int i = tid; i < N * 3; i += WS_THREADS) eph[N * 3 * B + i] = a.fd.indirect[i];
+    }
+    const double* pos_base = STAGE ? eph : a.fd.body_pos;
+    const double* ind_base = STAGE ? eph + N * 3 * B : a.fd.indirect;
+    if (tid == 0) {
+        for (int t = 0; t < SLOTS; ++t) {
+            st.slot_traj[t] = -1;
+            st.grp_id[t] = -1;
+            st.sing_key[t] = INT_MAX;
+            st.nf_key[t] = INT_MAX;
+            st.slot_err[t] = 0ull;
+        }
+        st.active_mask = 0;
+        st.new_mask[0] = st.new_mask[1] = 0;
+        st.half_active[0] = st.half_active[1] = 0;
+        st.queue_done = 0;
+        st.timeout = 0;
+        st.exit_flag = 0;
+    }
+    __syncthreads();
+
+    if (warp < MMA_WARPS) {
+        // ============================================================ MMA group
+        const int g = lane >> 2, q = lane & 3;
+        for (int h = 0;; h ^= 1) {
+            bar_sync(BAR_F0 + h, WS_THREADS);
+            if (st.exit_flag) break;
+            if (st.half_active[h]) {
+                double acc[MAIN][3][2], xacc[XMW][2];
+                gemm_half<MAIN, XMW>(a.upack, a.nkp, fbh[h], hp, warp, lane, acc, xacc);
+                const int amt = N >> 3;
+                if (g == (N & 7)) {  // anchor row -> b0/2 (pc_matrices.hpp:138, :145)
+#pragma unroll
+                    for (int i = 0; i < MAIN; ++i)
+                        if (warp * MAIN + i == amt)
+#pragma unroll
+                            for (int p = 0; p < 3; ++p)
+#pragma unroll
+                                for (int e = 0; e < 2; ++e)
+                                    st.b0h[h][p * 8 + 2 * q + e] = 0.5 * (acc[i][p][e] + 2.0 * st.y0[h * HS + q][2 * p + e]);
+#pragma unroll
+                    for (int x = 0; x < XMW; ++x) {
+                        const int ex = warp + x * MMA_WARPS;
+                        if (ex < hp.extras && hp.mb + ex / 3 == amt) {
+                            const int p = ex % 3;
+#pragma unroll
+                            for (int e = 0; e < 2; ++e)
+                                st.b0h[h][p * 8 + 2 * q + e] = 0.5 * (xacc[x][e] + 2.0 * st.y0[h * HS + q][2 * p + e]);
+                        }
+                    }
+                }
+                bar_sync(BAR_MMA, MMA_THREADS);
+                const int act_h = (st.active_mask >> (h * HS)) & 0xF;
+                double bn = 0.0, bd = 1.0;
+                int nf = INT_MAX;
+#pragma unroll
+                for (int i = 0; i < MAIN; ++i) {
+                    const int j = (warp * MAIN + i) * 8 + g;
+                    if (j >= N || !((act_h >> q) & 1)) continue;
+                    double yn[6], yo[6];
+#pragma unroll
+                    for (int p = 0; p < 3; ++p)
+#pragma unroll
+                        for (int e = 0; e < 2; ++e) {
+                            const int c = 2 * p + e;
+                            yo[c] = ybuf[y2(j, h, c, q)];
+                            yn[c] = acc[i][p][e] + st.b0h[h][p * 8 + 2 * q + e];
+                        }
+                    update_sample(yn, yo, j, a.error_mode, bn, bd, nf);
+#pragma unroll
+                    for (int c = 0; c < 6; ++c) ybuf[y2(j, h, c, q)] = yn[c];
+                }
+#pragma unroll
+                for (int x = 0; x < XMW; ++x) {  // extra tiles -> stage (components spread over warps)
+                    const int ex = warp + x * MMA_WARPS;
+                    if (ex >= hp.extras) continue;
+                    const int j = (hp.mb + ex / 3) * 8 + g, p = ex % 3;
+                    if (j >= N) continue;
+#pragma unroll
+                    for (int e = 0; e < 2; ++e)
+                        xstage[(j - hp.mb * 8) * HC + q * 6 + 2 * p + e] = xacc[x][e] + st.b0h[h][p * 8 + 2 * q + e];
+                }
+                double e2 = bn / bd;
+#pragma unroll
+                for (int off = 4; off < 32; off <<= 1) {
+                    e2 = fmax(e2, __shfl_xor_sync(0xffffffffu, e2, off));
+                    nf = min(nf, __shfl_xor_sync(0xffffffffu, nf, off));
+                }
+                if (g == 0 && ((act_h >> q) & 1)) {
+                    atomicMax(&st.slot_err[h * HS + q], static_cast<unsigned long long>(__double_as_longlong(e2)));
+                    if (nf != INT_MAX) atomicMin(&st.nf_key[h * HS + q], nf);
+                }
+                bar_sync(BAR_MMA, MMA_THREADS);
+                if (tid < xrows * HS) {  // staged rows
+                    const int r = tid >> 2, s = tid & 3, j = hp.mb * 8 + r;
+                    if ((act_h >> s) & 1) {
+                        double yn[6], yo[6];
+#pragma unroll
+                        for (int c = 0; c < 6; ++c) {
+                            yn[c] = xstage[r * HC + s * 6 + c];
+                            yo[c] = ybuf[y2(j, h, c, s)];
+                        }
+                        double sbn = 0.0, sbd = 1.0;
+                        int snf = INT_MAX;
+                        update_sample(yn, yo, j, a.error_mode, sbn, sbd, snf);
+#pragma unroll
+                        for (int c = 0; c < 6; ++c) ybuf[y2(j, h, c, s)] = yn[c];
+                        atomicMax(&st.slot_err[h * HS + s], static_cast<unsigned long long>(__double_as_longlong(sbn / sbd)));
+                        if (snf != INT_MAX) atomicMin(&st.nf_key[h * HS + s], snf);
+                    }
+                }
+            }
+            __threadfence_block();
+            bar_arrive(BAR_Y0 + h, WS_THREADS);
+        }
+    } else {
+        // ============================================================= FP group
+        const int ft = tid - MMA_THREADS;  // 0..255
+        const int fw = ft >> 5;
+        bool first[2] = {true, true};
+        for (int h = 0;; h ^= 1) {
+            if (!first[h]) bar_sync(BAR_Y0 + h, WS_THREADS);  // epilogue of half h done
+            // ---- decisions for half h (warp 0 of the FP group, lane = slot of the half)
+            if (!first[h] && fw == 0) {
+                const int am = st.active_mask;
+                const int s = lane, t = h * HS + s;
+                const bool act_t = s < HS && ((am >> t) & 1);
+                const int my_grp = act_t ? st.slot_grp[t] : -1;
+                const int my_mbr = act_t ? st.slot_member[t] : 0;
+                const double my_e2 = act_t ? __longlong_as_double(static_cast<long long>(st.slot_err[t])) : 0.0;
+                const int my_sk = act_t ? st.sing_key[t] : INT_MAX;
+                const int my_nk = act_t ? st.nf_key[t] : INT_MAX;
+                const int my_wk = (act_t && ((st.new_mask[h] >> t) & 1)) ? st.warm_key[t] : INT_MAX;
+                const int my_tr = act_t ? st.slot_traj[t] : INT_MAX;
+                const int lg = my_grp;
+                const int gid = act_t ? st.grp_id[lg] : -1;
+                const int size = act_t ? st.grp_size[lg] : 1;
+                int it = act_t ? st.grp_iter[lg] : 0;
+                bool leader = act_t;
+                double gerr2 = 0.0;
+                long long sing_s = LLONG_MAX, nf_best = LLONG_MAX;
+                int sing_t = -1, warm_t = -1, warm_tr = INT_MAX, members = 0;
+#pragma unroll
+                for (int u = 0; u < HS; ++u) {
+                    const int ug = __shfl_sync(0xffffffffu, my_grp, u);
+                    const int um = __shfl_sync(0xffffffffu, my_mbr, u);
+                    const double ue = __shfl_sync(0xffffffffu, my_e2, u);
+                    const int usk = __shfl_sync(0xffffffffu, my_sk, u);
+                    const int unk = __shfl_sync(0xffffffffu, my_nk, u);
+                    const int uwk = __shfl_sync(0xffffffffu, my_wk, u);
+                    const int utr = __shfl_sync(0xffffffffu, my_tr, u);
+                    if (!act_t || ug != lg) continue;
+                    const int ut = h * HS + u;
+                    if (u < s) leader = false;
+                    members |= 1 << ut;
+                    gerr2 = fmax(gerr2, ue);
+                    if (uwk != INT_MAX && utr < warm_tr) {
+                        warm_tr = utr;
+                        warm_t = ut;
+                    }
+                    if (usk != INT_MAX) {
+                        const long long smp = static_cast<long long>(usk / (B + 1)) * size + um;
+                        if (smp < sing_s) {
+                            sing_s = smp;
+                            sing_t = ut;
+                        }
+                    }
+                    if (unk != INT_MAX) {
+                        const long long key = static_cast<long long>(unk >> 3) * (6LL * size) +
+                                              static_cast<long long>(unk & 7) * size + um;
+                        nf_best = min(nf_best, key);
+                    }
+                }
+                int free_bits = 0, retire_bits = 0;
+                if (leader) {
+                    const double gerr = sqrt(gerr2);
+                    GroupFault* fl = a.faults + gid;
+                    bool retire = false, ok = false, conv = false;
+                    if (warm_t >= 0) {
+                        fl->status = st.warm_kind[warm_t] == CONIC_ZERO_RADIUS ? FAULT_WARM_ZERO_RADIUS : FAULT_WARM_SOLVER;
+                        fl->iteration = 0;
+                        fl->trajectory = st.slot_traj[warm_t];
+                        fl->node = st.warm_key[warm_t] / 4;
+                        fl->value = st.warm_val[warm_t][0];
+                        fl->value2 = st.warm_val[warm_t][1];
+                        retire = true;
+                    } else {
+                        it += 1;
+                        st.grp_iter[lg] = it;
+                        if (sing_t >= 0) {
+                            const int key = st.sing_key[sing_t];
+                            fl->status = FAULT_SINGULARITY;
+                            fl->iteration = it;
+                            fl->node = key / (B + 1);
+                            fl->body = key % (B + 1) - 1;
+                            fl->trajectory = st.slot_member[sing_t];
+                            fl->value = st.sing_val[sing_t];
+                            retire = true;
+                        } else if (nf_best != LLONG_MAX) {
+                            fl->status = FAULT_DIVERGENCE;
+                            fl->iteration = it;
+                            fl->node = nf_best / (6LL * size);
+                            fl->column = nf_best % (6LL * size);
+                            retire = true;
+                        } else {
+                            if (a.rep_hist) a.rep_hist[static_cast<size_t>(gid) * a.max_it + (it - 1)] = gerr;
+                            if (gerr <= a.tol) {
+                                retire = ok = conv = true;
+                            } else if (it >= a.max_it) {
+                                retire = ok = true;
+                            }
+                        }
+                    }
+                    if (retire) {
+                        a.rep_iter[gid] = it;
+                        a.rep_err[gid] = gerr;
+                        a.rep_conv[gid] = conv ? 1 : 0;
+                        free_bits = members;
+                        retire_bits = ok ? members : 0;
+                        st.grp_id[lg] = -1;
+                    }
+                }
+                free_bits = __reduce_or_sync(0xffffffffu, static_cast<unsigned>(free_bits));
+                retire_bits = __reduce_or_sync(0xffffffffu, static_cast<unsigned>(retire_bits));
+                if (lane == 0) {
+                    st.free_mask = free_bits;
+                    st.retire_mask = retire_bits;
+                }
+                if (s < HS) {  // reset this half's accumulators for its next iteration
+                    st.slot_err[t] = 0ull;
+                    st.sing_key[t] = INT_MAX;
+                    st.nf_key[t] = INT_MAX;
+                }
+            }
+            bar_sync(BAR_FP, FP_THREADS);
+            // ---- retire outputs of half h
+            if (!first[h] && st.retire_mask) {
+                const int retire = st.retire_mask;
+                const int j_begin = a.seg == 0 ? 0 : 1;
+                for (int i = ft; i < N * HS; i += FP_THREADS) {
+                    const int j = i >> 2, s = i & 3, t = h * HS + s;
+                    if (!((retire >> t) & 1)) continue;
+                    const size_t tr = static_cast<size_t>(st.slot_traj[t]);
+                    if (a.samples && j >= j_begin) {
+                        double* o = a.samples + (tr * a.R + a.row0 + j) * 6;
+#pragma unroll
+                        for (int c = 0; c < 6; ++c) o[c] = ybuf[y2(j, h, c, s)];
+                    }
+                    if (j == N - 1) {
+#pragma unroll
+                        for (int c = 0; c < 6; ++c) a.state_out[tr * 6 + c] = ybuf[y2(j, h, c, s)];
+                    }
+                }
+            }
+            // ---- free + claim into half h (thread 0 of the FP group)
+            if (ft == 0) {
+                int am = st.active_mask;
+                if (!first[h]) {
+                    const int fm = st.free_mask;
+                    am &= ~fm;
+                    for (int t = 0; t < SLOTS; ++t)
+                        if ((fm >> t) & 1) st.slot_traj[t] = -1;
+                }
+                int new_mask = 0;
+                const int hmask = 0xF << (h * HS);
+                const int free_h = HS - __popc(static_cast<unsigned>(am & hmask));
+                if (!st.queue_done && free_h >= a.gmax) {
+                    const int k = free_h / a.gmax;
+                    const int g0 = atomicAdd(a.queue, k);
+                    const int g1 = min(g0 + k, a.P);
+                    if (g0 + k >= a.P) st.queue_done = 1;
+                    for (int gi = g0; gi < g1; ++gi) {
+                        int lg = 0;
+                        while (st.grp_id[lg] >= 0) ++lg;
+                        const int off = static_cast<int>(a.group_off[gi]);
+                        const int size = static_cast<int>(a.group_off[gi + 1]) - off;
+                        st.grp_id[lg] = gi;
+                        st.grp_size[lg] = size;
+                        st.grp_iter[lg] = 0;
+                        int t = h * HS;
+                        for (int mbr = 0; mbr < size; ++mbr) {
+                            while ((am >> t) & 1) ++t;
+                            am |= 1 << t;
+                            new_mask |= 1 << t;
+                            st.slot_traj[t] = off + mbr;
+                            st.slot_grp[t] = lg;
+                            st.slot_member[t] = mbr;
+                            st.warm_key[t] = INT_MAX;
+                        }
+                    }
+                }
+                if (a.deadline_ns != 0ull && globaltimer_ns() > a.deadline_ns) st.timeout = 1;
+                st.active_mask = am;
+                st.new_mask[h] = new_mask;
+                st.half_active[h] = (am & hmask) != 0;
+            }
+            bar_sync(BAR_FP, FP_THREADS);
+            const int am = st.active_mask;
+            if (st.timeout || (am == 0 && st.queue_done)) {  // done: release the MMA group and leave
+                if (ft == 0) {
+                    if (st.timeout)
+                        for (int lg = 0; lg < SLOTS; ++lg) {
+                            const int gi = st.grp_id[lg];
+                            if (gi < 0) continue;
+                            a.faults[gi].status = FAULT_TIMEOUT;
+                            a.faults[gi].iteration = st.grp_iter[lg];
+                            a.rep_iter[gi] = st.grp_iter[lg];
+                            a.rep_conv[gi] = 0;
+                        }
+                    st.exit_flag = 1;
+                }
+                bar_sync(BAR_FP, FP_THREADS);
+                __threadfence_block();
+                bar_arrive(BAR_F0 + h, WS_THREADS);
+                // the MMA group still finishes the other half it was released for:
+                // consume its Y arrive so no named barrier is left half-open
+                if (!first[h ^ 1]) bar_sync(BAR_Y0 + (h ^ 1), WS_THREADS);
+                break;
+            }
+            // ---- load + warm start of new slots in half h
+            const int new_mask = st.new_mask[h];
+            if (new_mask) {
+                for (int i = ft; i < SLOTS * 6; i += FP_THREADS) {
+                    const int s = i / 6, c = i % 6;
+                    if ((new_mask >> s) & 1) st.y0[s][c] = a.state_in[static_cast<size_t>(st.slot_traj[s]) * 6 + c];
+                }
+                bar_sync(BAR_FP, FP_THREADS);
+                for (int i = ft; i < N * HS; i += FP_THREADS) {
+                    const int j = i >> 2, s = i & 3, t = h * HS + s;
+                    if (!((new_mask >> t) & 1)) continue;
+                    const double r[3] = {st.y0[t][0], st.y0[t][1], st.y0[t][2]};
+                    const double v[3] = {st.y0[t][3], st.y0[t][4], st.y0[t][5]};
+                    double ro[3] = {r[0], r[1], r[2]}, vo[3] = {v[0], v[1], v[2]};
+                    if (!a.cold_start) {
+                        const int chk = conic_check(r, v, a.fd.central_mu);
+                        if (chk == CONIC_ZERO_RADIUS) {
+                            atomicMin(&st.warm_key[t], j * 4 + CONIC_ZERO_RADIUS);
+                        } else if (chk == CONIC_OK) {
+                            double mf, ef;
+                            if (kepler_propagate(r, v, a.fd.central_mu, a.times[j] - a.epoch, ro, vo, &mf, &ef) !=
+                                CONIC_OK)
+                                atomicMin(&st.warm_key[t], j * 4 + CONIC_SOLVER);
+                        }
+                        if (j == 0 && a.cold_fallback)
+                            a.cold_fallback[st.slot_traj[t]] = (chk == CONIC_NON_ELLIPTIC) ? 1 : 0;
+                    }
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        ybuf[y2(j, h, c, s)] = ro[c];
+                        ybuf[y2(j, h, c + 3, s)] = vo[c];
+                    }
+                }
+                bar_sync(BAR_FP, FP_THREADS);
+                if (ft < SLOTS && ((new_mask >> ft) & 1) && st.warm_key[ft] != INT_MAX) {
+                    const int t = ft, j = st.warm_key[t] / 4;
+                    st.warm_kind[t] = st.warm_key[t] % 4;
+                    const double r[3] = {st.y0[t][0], st.y0[t][1], st.y0[t][2]};
+                    const double v[3] = {st.y0[t][3], st.y0[t][4], st.y0[t][5]};
+                    double ro[3], vo[3], mf = 0.0, ef = 0.0;
+                    if (st.warm_kind[t] == CONIC_SOLVER)
+                        kepler_propagate(r, v, a.fd.central_mu, a.times[j] - a.epoch, ro, vo, &mf, &ef);
+                    st.warm_val[t][0] = mf;
+                    st.warm_val[t][1] = ef;
+                }
+            }
+            // ---- force of half h
+            const int act_h = (am >> (h * HS)) & 0xF;
+            if (act_h)
+                for (int j = ft; j < N; j += FP_THREADS)
+                    force_half(a.fd, a.omega2, ybuf, fbh[h], st.sing_key, pos_base, ind_base, act_h, h, j);
+            bar_sync(BAR_FP, FP_THREADS);
+            if (ft < HS && st.sing_key[h * HS + ft] != INT_MAX) {
+                const int t = h * HS + ft, key = st.sing_key[t], j = key / (B + 1), chk = key % (B + 1);
+                st.sing_val[t] =
+                    check_distance(ybuf[y2(j, h, 0, ft)], ybuf[y2(j, h, 1, ft)], ybuf[y2(j, h, 2, ft)], j, chk, a.fd);
+            }
+            __threadfence_block();
+            first[h] = false;
+            bar_arrive(BAR_F0 + h, WS_THREADS);
+        }
+    }
+}
+
+template <int MAIN, int XMW>
+static cudaError_t launch_ws_t(const SegArgs& a, int grid, size_t smem, cudaStream_t s) {
+    auto kern = a.stage_eph ? k_pc_ws<MAIN, XMW, true> : k_pc_ws<MAIN, XMW, false>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    kern<<<grid, WS_THREADS, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_segment_ws(const SegArgs& a, int grid, cudaStream_t s) {
+    const int main = ws_main_tiles(a.N);
+    const int mtiles = (a.N + 1 + 7) / 8;
+    if ((mtiles - main * MMA_WARPS) * 3 > MMA_WARPS * (main == 2 ? 3 : 1)) return cudaErrorNotSupported;
+    const size_t smem = ws_smem_bytes(a.N, a.nkp, a.xrows, a.fd.n_bodies, a.stage_eph);
+    switch (main) {
+    case 2: return launch_ws_t<2, 3>(a, grid, smem, s);
+    case 3: return launch_ws_t<3, 1>(a, grid, smem, s);
+    case 4: return launch_ws_t<4, 1>(a, grid, smem, s);
+    default: return cudaErrorNotSupported;
+    }
+}
+
+}  // namespace pswarm_dev

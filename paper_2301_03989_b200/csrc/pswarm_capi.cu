@@ -161,6 +161,7 @@ struct pswarm_ctx {
     int ctas_per_sm = 1;
     int max_ctas = 0;  // 0 = SM count * ctas_per_sm
     int profile_phases = 0;
+    int slot_kernel = 0;  // 0 auto, 1 generic k_pc_segment, 2 warp-specialised k_pc_ws
     unsigned long long phase_host[pswarm_dev::PHASES] = {};
     // wide-group path
     cudaEvent_t wide_ev[4] = {};
@@ -453,10 +454,21 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
         gpu_deadline = t0 + static_cast<unsigned long long>(std::max<int64_t>(left.count(), 1));
     }
 
-    const int xrows = extra_rows(static_cast<int>(N), op.gp);
+    // kernel choice: warp-specialised slot kernel (groups <= 4, N in its tile range),
+    // the generic slot kernel (groups <= 8), or the wide-group path
+    constexpr size_t SMEM_MAX = 227 * 1024;
+    const int Ni = static_cast<int>(N);
+    const int ws_main = ws_main_tiles(Ni);
+    const bool use_ws = !wide && gmax <= 4 && ws_main >= 2 && ws_main <= 4 && ctx->slot_kernel != 1 &&
+                        ws_smem_bytes(Ni, op.nkp, ws_extra_rows(Ni), nb, 0) <= SMEM_MAX;
+    const int xrows = use_ws ? ws_extra_rows(Ni) : extra_rows(Ni, op.gp);
     // stage the frozen ephemeris in shared memory when it fits next to the state blocks
-    const int stage_eph = (nb > 0 && segment_smem_bytes(static_cast<int>(N), op.nkp, xrows, nb, 1) <= 227 * 1024) ? 1 : 0;
-    if (!wide && segment_smem_bytes(static_cast<int>(N), op.nkp, xrows, nb, stage_eph) > 227 * 1024)
+    const int stage_eph =
+        nb > 0 && (use_ws ? ws_smem_bytes(Ni, op.nkp, xrows, nb, 1) : segment_smem_bytes(Ni, op.nkp, xrows, nb, 1)) <=
+                      SMEM_MAX
+            ? 1
+            : 0;
+    if (!wide && !use_ws && segment_smem_bytes(Ni, op.nkp, xrows, nb, stage_eph) > SMEM_MAX)
         raise(PSWARM_ERR_INVALID_SIZE, fmtf("propagate: %lld nodes exceed the per-SM shared memory of the slot kernel",
                                             (long long)N));
     const int per_cta = std::max<int64_t>(1, SLOTS / std::min<int64_t>(gmax, SLOTS));
@@ -558,7 +570,7 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
         a.phase_cycles = d_phase;
         if (max_it > 0 && !wide) {
             cuda_check(cudaEventRecord(ctx->evk0, st), "event");
-            cuda_check(launch_segment(a, grid, st), "k_pc_segment launch");
+            cuda_check(use_ws ? launch_segment_ws(a, grid, st) : launch_segment(a, grid, st), "slot kernel launch");
             cuda_check(cudaEventRecord(ctx->evk1, st), "event");
             ++ctx->launches;
         } else if (max_it > 0) {
@@ -870,6 +882,7 @@ pswarm_status pswarm_set_option(pswarm_ctx* ctx, const char* key, int64_t value)
         if (k == "ctas_per_sm") ctx->ctas_per_sm = static_cast<int>(std::max<int64_t>(1, value));
         else if (k == "max_ctas") ctx->max_ctas = static_cast<int>(std::max<int64_t>(0, value));
         else if (k == "profile_phases") ctx->profile_phases = value != 0;
+        else if (k == "slot_kernel") ctx->slot_kernel = static_cast<int>(value);
         else raise(PSWARM_ERR_GENERIC, "pswarm_set_option: unknown key '" + k + "'");
     });
 }

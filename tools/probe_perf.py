@@ -5,6 +5,8 @@ import numpy as np
 import paper_2301_03989_b200 as ps
 
 ctx = ps.Context(0)
+if os.environ.get('SLOT_KERNEL'):
+    ctx.set_option('slot_kernel', int(os.environ['SLOT_KERNEL']))
 base = ps.reference_state()
 period = ps.osculating_period(base, ps.MU_SUN)
 for M, bodies, n in [(1000, "planets8", 200), (1000, "reference", 200), (10000, "planets8", 200), (100000, "planets8", 200)]:
