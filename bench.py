@@ -205,7 +205,8 @@ def main():
     for _ in range(args.warmup):
         step()
     clocks = Clocks(local)
-    wall, dev_ms, ker_ms, iters, launches = [], [], [], [], 0
+    wall, dev_ms, ker_ms, iters = [], [], [], []
+    launches0 = ctx.run_batch(shard[:1], cfg, plan, "independent", samples=False, history=False).gpu_launches
     for _ in range(args.steps):
         flush.fill_(1.0)  # L2 flush (outside the timed region)
         barrier()
@@ -216,8 +217,8 @@ def main():
         dev_ms.append(r.device_ms)
         ker_ms.append(r.kernel_ms)
         iters.append(r.trajectory_iterations)
-        launches += 1  # k_pc_segment launches per step (one segment)
     clk = clocks.stop()
+    launches = r.gpu_launches - launches0  # context's cumulative count of its own kernel launches
 
     def gmax(x):
         t = torch.tensor([x], dtype=torch.float64, device=dev)
@@ -253,7 +254,7 @@ def main():
                     "path": "pswarm_run_batch C-ABI, pinned host buffers" + (" + NCCL all_gather" if world > 1 else "")},
             "roofline": {"bound": "tensor", "achieved": round(achieved, 3), "peak": round(peak, 3), "unit": "TFLOP/s",
                          "frac": round(achieved / peak, 4), "traffic": ncu_traffic(),
-                         "kernel": "k_pc_segment", "kernel_ms": round(kms_mean, 4),
+                         "kernel": ctx.kernel_name(), "kernel_ms": round(kms_mean, 4),
                          "flops_per_launch": flops, "peak_source": peak_src,
                          "note": "FP64 DMMA/DFMA share one pipe on B200 (tools/fp64_peak.cu mixed test)"},
             "cpu_baseline": cpu,

@@ -142,10 +142,16 @@ void pswarm_destroy(pswarm_ctx* ctx);
  * warp-specialised one). */
 pswarm_status pswarm_set_option(pswarm_ctx* ctx, const char* key, int64_t value);
 
-/* Diagnostics: SM cycles summed over CTAs per kernel phase of the last call
- * (0 claim, 1 warm start, 2 force, 3 DMMA, 4 anchor barrier, 5 epilogue, 6 staged
- * epilogue, 7 decisions, 8 retire, 9 = CTA count). */
+/* Diagnostics: SM cycles summed over CTAs per kernel phase of the last call.
+ * Generic slot kernel: 0 claim, 1 warm start, 2 force, 3 DMMA, 4 anchor barrier,
+ * 5 epilogue, 6 staged epilogue, 7 decisions, 8 retire.  Warp-specialised kernel
+ * (MMA group / FP group leaders): 0 wait for F, 1 DMMA, 2 epilogue, 3 staged rows,
+ * 4 wait for Y, 5 decisions, 6 retire + claim, 7 warm start, 8 force.  9 = CTA count. */
 pswarm_status pswarm_get_phase_cycles(pswarm_ctx* ctx, uint64_t* out, int32_t n);
+
+/* Diagnostics: name of the solver kernel the last propagate/run_batch call used
+ * ("k_pc_ws", "k_pc_segment", "k_wide_iter" or "" before the first call). */
+const char* pswarm_last_kernel(pswarm_ctx* ctx);
 
 /* ---- batch API (the drop-in boundary) ---------------------------------- */
 

@@ -117,6 +117,7 @@ SIGNATURES = [
     ("pswarm_destroy", None, [C.c_void_p]),
     ("pswarm_set_option", C.c_int32, [C.c_void_p, C.c_char_p, C.c_int64]),
     ("pswarm_get_phase_cycles", C.c_int32, [C.c_void_p, C.POINTER(C.c_uint64), C.c_int32]),
+    ("pswarm_last_kernel", C.c_char_p, [C.c_void_p]),
     ("pswarm_propagate", C.c_int32,
      [C.c_void_p, C.c_int64, _dp, C.c_int64, _ip, C.c_int64, _dp, C.c_int64, C.POINTER(PswarmConfig),
       C.POINTER(PswarmOutputs), _ep]),

@@ -311,6 +311,10 @@ class Context:
         d["ctas"] = int(buf[9])
         return d
 
+    def kernel_name(self) -> str:
+        """Solver kernel used by the last propagate/run_batch call."""
+        return self.lib.pswarm_last_kernel(self.ptr).decode()
+
     # ---- batch API ------------------------------------------------------
     def propagate(self, states, group_sizes, plan: SegmentPlan, config: PropagationConfig, *,
                   samples=True, history=True, terminal=True) -> PropagationResult:

@@ -39,6 +39,18 @@ __device__ __forceinline__ int f2(int j, int c, int s) {
     return (((j >> 2) * 3 + (c >> 1)) * 32) + ((s * 2 + (c & 1)) * 4 + (j & 3));
 }
 
+// Optional phase accounting (pswarm_set_option "profile_phases"): MMA-group lane 0 of
+// warp 0 stamps slots 0-3 (wait F, DMMA, epilogue, staged rows), FP-group thread 0 slots
+// 4-8 (wait Y, decisions, retire+claim, warm start, force); slot 9 counts CTAs.
+#define WS_PHASE(k)                                  \
+    do {                                             \
+        if (prof && stamp) {                         \
+            const long long now_ = clock64();        \
+            pc[(k)] += now_ - t_prev;                \
+            t_prev = now_;                           \
+        }                                            \
+    } while (0)
+
 __device__ __forceinline__ void bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 __device__ __forceinline__ void bar_arrive(int id, int n) {
     asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
@@ -152,16 +164,20 @@ __device__ __forceinline__ void gemm_half(const double2* __restrict__ upack, int
     };
 #pragma unroll
     for (int x = 0; x < XMW; ++x) xacc[x][0] = xacc[x][1] = 0.0;
-    APairH<MAIN, XMW> p0, p1;
+    APairH<MAIN, XMW> p0, p1, p2;  // two operator pairs in flight (L2 latency under load)
     load(0, p0);
+    if (nkp > 1) load(1, p1);
     int kp = 0;
-    for (; kp + 1 < nkp; kp += 2) {
-        load(kp + 1, p1);
+    for (; kp + 2 < nkp; kp += 3) {
+        load(kp + 2, p2);
         compute(kp, p0);
-        if (kp + 2 < nkp) load(kp + 2, p0);
+        if (kp + 3 < nkp) load(kp + 3, p0);
         compute(kp + 1, p1);
+        if (kp + 4 < nkp) load(kp + 4, p1);
+        compute(kp + 2, p2);
     }
     if (kp < nkp) compute(kp, p0);
+    if (kp + 1 < nkp) compute(kp + 1, p1);
 }
 
 /// Force of half h for node j, its 4 slots as independent chains (force_model.hpp:93-142).
@@ -268,19 +284,24 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
     const int xrows = a.xrows;
     const WsLayout L = ws_layout(N, a.nkp, xrows, B, STAGE ? 1 : 0);
     double* ybuf = reinterpret_cast<double*>(smem_raw + L.ybuf);
-    double* fbh[2] = {reinterpret_cast<double*>(smem_raw + L.fbuf0), reinterpret_cast<double*>(smem_raw + L.fbuf1)};
+    const size_t fb_bytes = L.fbuf1 - L.fbuf0;
+    double* fb0 = reinterpret_cast<double*>(smem_raw + L.fbuf0);
     double* xstage = reinterpret_cast<double*>(smem_raw + L.xstage);
     double* eph = reinterpret_cast<double*>(smem_raw + L.eph);
     WsState& st = *reinterpret_cast<WsState*>(smem_raw + L.state);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int KP = 8 * a.nkp;
     const int mtiles = (N + 1 + 7) / 8;
+    const bool prof = a.phase_cycles != nullptr;
+    const bool stamp = tid == 0 || tid == MMA_THREADS;
+    long long pc[PHASES] = {};
+    long long t_prev = clock64();
     HalfPlan hp;
     hp.main = MAIN;
     hp.mb = MAIN * MMA_WARPS;
     hp.extras = (mtiles - hp.mb) * 3;
 
-    for (int i = tid; i < 2 * KP * HC; i += WS_THREADS) fbh[0][i] = 0.0;  // both halves (contiguous)
+    for (int i = tid; i < 2 * KP * HC; i += WS_THREADS) fb0[i] = 0.0;  // both halves (contiguous)
     if (STAGE && B > 0) {
         for (int i = tid; i < N * 3 * B; i += WS_THREADS) eph[i] = a.fd.body_pos[i];
         for (int i = tid; i < N * 3; i += WS_THREADS) eph[N * 3 * B + i] = a.fd.indirect[i];
@@ -309,10 +330,13 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
         const int g = lane >> 2, q = lane & 3;
         for (int h = 0;; h ^= 1) {
             bar_sync(BAR_F0 + h, WS_THREADS);
+            WS_PHASE(0);
             if (st.exit_flag) break;
             if (st.half_active[h]) {
                 double acc[MAIN][3][2], xacc[XMW][2];
-                gemm_half<MAIN, XMW>(a.upack, a.nkp, fbh[h], hp, warp, lane, acc, xacc);
+                gemm_half<MAIN, XMW>(a.upack, a.nkp, reinterpret_cast<const double*>(smem_raw + L.fbuf0 + h * fb_bytes),
+                                     hp, warp, lane, acc, xacc);
+                WS_PHASE(1);
                 const int amt = N >> 3;
                 if (g == (N & 7)) {  // anchor row -> b0/2 (pc_matrices.hpp:138, :145)
 #pragma unroll
@@ -376,6 +400,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
                     if (nf != INT_MAX) atomicMin(&st.nf_key[h * HS + q], nf);
                 }
                 bar_sync(BAR_MMA, MMA_THREADS);
+                WS_PHASE(2);
                 if (tid < xrows * HS) {  // staged rows
                     const int r = tid >> 2, s = tid & 3, j = hp.mb * 8 + r;
                     if ((act_h >> s) & 1) {
@@ -395,8 +420,8 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
                     }
                 }
             }
-            __threadfence_block();
-            bar_arrive(BAR_Y0 + h, WS_THREADS);
+            WS_PHASE(3);
+            bar_arrive(BAR_Y0 + h, WS_THREADS);  // bar.arrive/bar.sync order smem among participants
         }
     } else {
         // ============================================================= FP group
@@ -405,6 +430,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
         bool first[2] = {true, true};
         for (int h = 0;; h ^= 1) {
             if (!first[h]) bar_sync(BAR_Y0 + h, WS_THREADS);  // epilogue of half h done
+            WS_PHASE(4);
             // ---- decisions for half h (warp 0 of the FP group, lane = slot of the half)
             if (!first[h] && fw == 0) {
                 const int am = st.active_mask;
@@ -518,6 +544,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
                 }
             }
             bar_sync(BAR_FP, FP_THREADS);
+            WS_PHASE(5);
             // ---- retire outputs of half h
             if (!first[h] && st.retire_mask) {
                 const int retire = st.retire_mask;
@@ -580,6 +607,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
                 st.half_active[h] = (am & hmask) != 0;
             }
             bar_sync(BAR_FP, FP_THREADS);
+            WS_PHASE(6);
             const int am = st.active_mask;
             if (st.timeout || (am == 0 && st.queue_done)) {  // done: release the MMA group and leave
                 if (ft == 0) {
@@ -595,7 +623,6 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
                     st.exit_flag = 1;
                 }
                 bar_sync(BAR_FP, FP_THREADS);
-                __threadfence_block();
                 bar_arrive(BAR_F0 + h, WS_THREADS);
                 // the MMA group still finishes the other half it was released for:
                 // consume its Y arrive so no named barrier is left half-open
@@ -648,21 +675,28 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
                     st.warm_val[t][1] = ef;
                 }
             }
+            WS_PHASE(7);
             // ---- force of half h
             const int act_h = (am >> (h * HS)) & 0xF;
             if (act_h)
                 for (int j = ft; j < N; j += FP_THREADS)
-                    force_half(a.fd, a.omega2, ybuf, fbh[h], st.sing_key, pos_base, ind_base, act_h, h, j);
+                    force_half(a.fd, a.omega2, ybuf, reinterpret_cast<double*>(smem_raw + L.fbuf0 + h * fb_bytes),
+                               st.sing_key, pos_base, ind_base, act_h, h, j);
             bar_sync(BAR_FP, FP_THREADS);
             if (ft < HS && st.sing_key[h * HS + ft] != INT_MAX) {
                 const int t = h * HS + ft, key = st.sing_key[t], j = key / (B + 1), chk = key % (B + 1);
                 st.sing_val[t] =
                     check_distance(ybuf[y2(j, h, 0, ft)], ybuf[y2(j, h, 1, ft)], ybuf[y2(j, h, 2, ft)], j, chk, a.fd);
             }
-            __threadfence_block();
             first[h] = false;
+            WS_PHASE(8);
             bar_arrive(BAR_F0 + h, WS_THREADS);
         }
+    }
+    if (prof && stamp) {
+        if (tid == 0) pc[9] = 1;
+        for (int k = 0; k < PHASES; ++k)
+            if (pc[k]) atomicAdd(a.phase_cycles + k, static_cast<unsigned long long>(pc[k]));
     }
 }
 

@@ -161,6 +161,7 @@ struct pswarm_ctx {
     int ctas_per_sm = 1;
     int max_ctas = 0;  // 0 = SM count * ctas_per_sm
     int profile_phases = 0;
+    const char* last_kernel = "";
     int slot_kernel = 0;  // 0 auto, 1 generic k_pc_segment, 2 warp-specialised k_pc_ws
     unsigned long long phase_host[pswarm_dev::PHASES] = {};
     // wide-group path
@@ -462,6 +463,7 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
     const bool use_ws = !wide && gmax <= 4 && ws_main >= 2 && ws_main <= 4 && ctx->slot_kernel != 1 &&
                         ws_smem_bytes(Ni, op.nkp, ws_extra_rows(Ni), nb, 0) <= SMEM_MAX;
     const int xrows = use_ws ? ws_extra_rows(Ni) : extra_rows(Ni, op.gp);
+    ctx->last_kernel = wide ? "k_wide_iter" : use_ws ? "k_pc_ws" : "k_pc_segment";
     // stage the frozen ephemeris in shared memory when it fits next to the state blocks
     const int stage_eph =
         nb > 0 && (use_ws ? ws_smem_bytes(Ni, op.nkp, xrows, nb, 1) : segment_smem_bytes(Ni, op.nkp, xrows, nb, 1)) <=
@@ -893,6 +895,8 @@ pswarm_status pswarm_get_phase_cycles(pswarm_ctx* ctx, uint64_t* out, int32_t n)
         for (int k = 0; k < n && k < PHASES; ++k) out[k] = ctx->phase_host[k];
     });
 }
+
+const char* pswarm_last_kernel(pswarm_ctx* ctx) { return ctx ? ctx->last_kernel : ""; }
 
 pswarm_status pswarm_propagate(pswarm_ctx* ctx, int64_t n_states, const double* states, int64_t n_groups,
                                const int64_t* group_sizes, int64_t n_boundaries, const double* boundaries,
