@@ -140,13 +140,55 @@ class IterationReport:
     per_iteration_errors: np.ndarray
 
 
+class _Reports(Sequence):
+    """reports[segment][group] -> IterationReport, built on access from the flat
+    per-(segment, group) arrays the C-ABI fills (a batch of 10^5 groups would
+    otherwise pay for 10^5 Python objects per call)."""
+
+    class _Row(Sequence):
+        def __init__(self, src, s):
+            self.src, self.s = src, s
+
+        def __len__(self):
+            return self.src.P
+
+        def __getitem__(self, g):
+            if isinstance(g, slice):
+                return [self[i] for i in range(*g.indices(len(self)))]
+            src, s = self.src, self.s
+            if g < 0:
+                g += src.P
+            if not 0 <= g < src.P:
+                raise IndexError(g)
+            it = int(src.iters[s, g])
+            h = src.hist[s, g, :min(it, src.max_it)].copy() if src.hist is not None else np.zeros(0)
+            return IterationReport(it, float(src.ferr[s, g]), bool(src.conv[s, g]), h)
+
+    def __init__(self, iters, ferr, conv, hist, max_it, n_segments):
+        self.iters, self.ferr, self.conv, self.hist, self.max_it = iters, ferr, conv, hist, max_it
+        self.P = iters.shape[1]
+        self.S = n_segments
+
+    def __len__(self):
+        return self.S
+
+    def __getitem__(self, s):
+        if isinstance(s, slice):
+            return [self[i] for i in range(*s.indices(len(self)))]
+        if s < 0:
+            s += self.S
+        if not 0 <= s < self.S:
+            raise IndexError(s)
+        return _Reports._Row(self, s)
+
+
 @dataclass
 class PropagationResult:
     """PropagationResult (propagator.hpp:151-169) plus device timing."""
     times: np.ndarray
     trajectories: Optional[np.ndarray]  # [M, R, 6]
     terminal_states: Optional[np.ndarray]  # [M, 7]
-    reports: List[List[IterationReport]]
+    reports: Sequence  # reports[segment][group] -> IterationReport
     group_sizes: np.ndarray
     segments: SegmentPlan
     warnings: List[str]
@@ -238,14 +280,7 @@ class _Outputs:
     def result(self, group_sizes, plan: SegmentPlan, complete: bool, independent: bool) -> PropagationResult:
         o = self.out
         S_rep = int(o.segments_reported)
-        reports = []
-        for s in range(S_rep):
-            row = []
-            for g in range(self.P):
-                it = int(self.iters[s, g])
-                h = self.hist[s, g, :min(it, self.max_it)].copy() if self.hist is not None else np.zeros(0)
-                row.append(IterationReport(it, float(self.ferr[s, g]), bool(self.conv[s, g]), h))
-            reports.append(row)
+        reports = _Reports(self.iters, self.ferr, self.conv, self.hist, self.max_it, S_rep)
         warnings = []
         for s in range(S_rep):
             for i in np.nonzero(self.fb[s])[0]:

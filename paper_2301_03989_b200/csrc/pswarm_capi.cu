@@ -145,7 +145,40 @@ enum BufId {
     B_REP_ITER, B_REP_ERR, B_REP_CONV, B_REP_HIST, B_FAULTS, B_FALLBACK, B_SAMPLES, B_DEAD,
     B_OP_IN, B_OP_IN2, B_OP_OUT, B_OP_AUX, B_OP_KEY,
     B_BT_KIND, B_BT_SOFF, B_BT_NC, B_BT_EL, B_BT_BND, B_BT_COFF, B_BT_CF, B_PHASES,
-    B_W_TG, B_W_Y, B_W_ACT, B_W_ITER, B_W_ERR, B_W_NF, B_W_SING, B_W_TSK, B_W_TSV, B_W_WK, B_W_CNT, B_COUNT
+    B_W_TG, B_W_Y, B_W_ACT, B_W_ITER, B_W_ERR, B_W_NF, B_W_SING, B_W_TSK, B_W_TSV, B_W_WK, B_W_CNT,
+    B_IN_PACK, B_REPORT, B_COUNT
+};
+
+/// Page-locked host staging (grow-only): every host<->device transfer of a solve goes
+/// through one of these so the copies are true async DMA, one per direction and segment.
+struct PinnedBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    template <typename T>
+    T* get(size_t bytes) {
+        bytes = std::max<size_t>(bytes, 64);
+        if (bytes > cap) {
+            if (p) cudaFreeHost(p);
+            p = nullptr;
+            cap = 0;
+            cuda_check(cudaHostAlloc(&p, bytes, cudaHostAllocDefault), "cudaHostAlloc");
+            cap = bytes;
+        }
+        return static_cast<T*>(p);
+    }
+    ~PinnedBuf() {
+        if (p) cudaFreeHost(p);
+    }
+};
+
+/// Byte layout of a packed transfer: 16-byte aligned sub-arrays.
+struct Pack {
+    size_t total = 0;
+    size_t add(size_t bytes) {
+        const size_t o = total;
+        total += (bytes + 15) & ~static_cast<size_t>(15);
+        return o;
+    }
 };
 
 }  // namespace
@@ -164,6 +197,7 @@ struct pswarm_ctx {
     const char* last_kernel = "";
     int slot_kernel = 0;  // 0 auto, 1 generic k_pc_segment, 2 warp-specialised k_pc_ws
     unsigned long long phase_host[pswarm_dev::PHASES] = {};
+    PinnedBuf pin_in, pin_rep, pin_term;
     // wide-group path
     cudaEvent_t wide_ev[4] = {};
     int* wide_count_host = nullptr;  // pinned ring of active-group counts
@@ -413,34 +447,78 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
                               : std::chrono::steady_clock::time_point::max();
 
     cudaStream_t st = ctx->stream;
-    // ---- device buffers
-    std::vector<double> s6(static_cast<size_t>(M) * 6);
-    for (int64_t i = 0; i < M; ++i)
-        for (int c = 0; c < 6; ++c) s6[i * 6 + c] = states[7 * i + 1 + c];
-    double* d_in = nullptr;
-    upload(ctx, B_STATE_A, s6.data(), s6.size(), &d_in);
-    double* d_out = ctx->buf[B_STATE_B].get<double>(s6.size());
-    std::vector<int64_t> h_off(static_cast<size_t>(P) + 1, 0);
-    for (int64_t g = 0; g < P; ++g) h_off[g + 1] = h_off[g] + group_sizes[g];
-    int64_t* d_off = nullptr;
-    upload(ctx, B_GROUP_OFF, h_off.data(), h_off.size(), &d_off);
     const int64_t R = 1 + S * (N - 1);
+    // ---- Chebyshev-Gauss-Lobatto grids of every segment (host, exact reference arithmetic)
+    std::vector<double> h_times(static_cast<size_t>(R), 0.0), seg_omega2(static_cast<size_t>(S));
+    std::vector<double> grid_times(static_cast<size_t>(S * N));
+    for (int64_t seg = 0; seg < S; ++seg) {
+        const auto g = pswarm::build_grid(N, boundaries[seg], boundaries[seg + 1]);
+        seg_omega2[seg] = g.omega2;
+        std::memcpy(grid_times.data() + seg * N, g.times.data(), sizeof(double) * N);
+        for (Index j = (seg == 0 ? 0 : 1); j < N; ++j) h_times[seg * (N - 1) + j] = g.times[j];
+    }
+    // ---- one packed host->device transfer: states, group offsets, grids, body table
+    Pack in;
+    const size_t o_s6 = in.add(sizeof(double) * M * 6), o_off = in.add(sizeof(int64_t) * (P + 1)),
+                 o_times = in.add(sizeof(double) * S * N), o_kind = in.add(sizeof(int) * bu.kind.size()),
+                 o_soff = in.add(sizeof(int) * bu.seg_off.size()), o_nc = in.add(sizeof(int) * bu.ncoef.size()),
+                 o_el = in.add(sizeof(double) * bu.elements.size()), o_mu = in.add(sizeof(double) * bu.mu.size()),
+                 o_bnd = in.add(sizeof(double) * bu.bounds.size()),
+                 o_coff = in.add(sizeof(long long) * bu.coeff_off.size()),
+                 o_cf = in.add(sizeof(double) * bu.coeffs.size());
+    char* hin = ctx->pin_in.get<char>(in.total);
+    {
+        double* s6 = reinterpret_cast<double*>(hin + o_s6);
+        for (int64_t i = 0; i < M; ++i)
+            for (int c = 0; c < 6; ++c) s6[i * 6 + c] = states[7 * i + 1 + c];
+        int64_t* off = reinterpret_cast<int64_t*>(hin + o_off);
+        off[0] = 0;
+        for (int64_t g = 0; g < P; ++g) off[g + 1] = off[g] + group_sizes[g];
+        auto put = [&](size_t o, const auto& v) {
+            if (!v.empty()) std::memcpy(hin + o, v.data(), v.size() * sizeof(v[0]));
+        };
+        put(o_times, grid_times);
+        put(o_kind, bu.kind);
+        put(o_soff, bu.seg_off);
+        put(o_nc, bu.ncoef);
+        put(o_el, bu.elements);
+        put(o_mu, bu.mu);
+        put(o_bnd, bu.bounds);
+        put(o_coff, bu.coeff_off);
+        put(o_cf, bu.coeffs);
+    }
+    char* din = ctx->buf[B_IN_PACK].get<char>(in.total);
+    cuda_check(cudaMemcpyAsync(din, hin, in.total, cudaMemcpyHostToDevice, st), "H2D inputs");
+    std::vector<int64_t> h_off(reinterpret_cast<int64_t*>(hin + o_off), reinterpret_cast<int64_t*>(hin + o_off) + P + 1);
+    double* d_in = reinterpret_cast<double*>(din + o_s6);
+    const int64_t* d_off = reinterpret_cast<const int64_t*>(din + o_off);
+    double* d_out = ctx->buf[B_STATE_B].get<double>(static_cast<size_t>(M) * 6);
+    if (d_in == d_out) raise(PSWARM_ERR_GENERIC, "propagate: state buffers alias");
     double* d_samples = out && out->samples ? ctx->buf[B_SAMPLES].get<double>(static_cast<size_t>(M) * R * 6) : nullptr;
-    int* d_queue = ctx->buf[B_QUEUE].get<int>(4);
-    int32_t* d_iter = ctx->buf[B_REP_ITER].get<int32_t>(P);
-    double* d_err = ctx->buf[B_REP_ERR].get<double>(P);
-    uint8_t* d_conv = ctx->buf[B_REP_CONV].get<uint8_t>(P);
     const bool want_hist = out && out->error_history && max_it > 0;
     double* d_hist = want_hist ? ctx->buf[B_REP_HIST].get<double>(static_cast<size_t>(S) * P * max_it) : nullptr;
-    GroupFault* d_faults = ctx->buf[B_FAULTS].get<GroupFault>(P);
-    uint8_t* d_fb = ctx->buf[B_FALLBACK].get<uint8_t>(static_cast<size_t>(M));
     if (d_hist) cuda_check(cudaMemsetAsync(d_hist, 0xff, sizeof(double) * S * P * max_it, st), "memset");
+    // ---- per-segment report block: zeroed with one memset, read back with one copy
+    Pack rp;
+    const size_t r_queue = rp.add(16), r_iter = rp.add(sizeof(int32_t) * P), r_conv = rp.add(P), r_fb = rp.add(M),
+                 r_faults = rp.add(sizeof(GroupFault) * P), r_err = rp.add(sizeof(double) * P), r_zero = rp.total,
+                 r_ekey = rp.add(sizeof(unsigned long long));
+    char* drep = ctx->buf[B_REPORT].get<char>(rp.total);
+    char* hrep = ctx->pin_rep.get<char>(rp.total);
+    int* d_queue = reinterpret_cast<int*>(drep + r_queue);
+    int32_t* d_iter = reinterpret_cast<int32_t*>(drep + r_iter);
+    double* d_err = reinterpret_cast<double*>(drep + r_err);
+    uint8_t* d_conv = reinterpret_cast<uint8_t*>(drep + r_conv);
+    GroupFault* d_faults = reinterpret_cast<GroupFault*>(drep + r_faults);
+    uint8_t* d_fb = reinterpret_cast<uint8_t*>(drep + r_fb);
+    unsigned long long* d_ekey = reinterpret_cast<unsigned long long*>(drep + r_ekey);
+    double* h_term = out && out->terminal_states ? ctx->pin_term.get<double>(sizeof(double) * M * 6) : nullptr;
+    bool term_ready = false;
 
     std::vector<int32_t> h_iter(static_cast<size_t>(S * P), 0);
     std::vector<double> h_err(static_cast<size_t>(S * P), 0.0);
     std::vector<uint8_t> h_conv(static_cast<size_t>(S * P), 0), h_fb(static_cast<size_t>(S * M), 0);
     std::vector<GroupFault> h_faults(static_cast<size_t>(P));
-    std::vector<double> h_times(static_cast<size_t>(R), 0.0);
 
     // device deadline in %globaltimer units
     unsigned long long gpu_deadline = 0;
@@ -480,20 +558,17 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
 
     BodyTable bt{};
     double *d_pos = nullptr, *d_ind = nullptr, *d_mu = nullptr;
-    unsigned long long* d_ekey = reinterpret_cast<unsigned long long*>(ctx->buf[B_OP_AUX].get<double>(2));
     if (nb > 0) {
-        int *d_kind, *d_soff, *d_nc;
-        double *d_el, *d_bnd, *d_cf;
-        long long* d_coff;
-        upload(ctx, B_BT_KIND, bu.kind.data(), bu.kind.size(), &d_kind);
-        upload(ctx, B_BT_SOFF, bu.seg_off.data(), bu.seg_off.size(), &d_soff);
-        upload(ctx, B_BT_NC, bu.ncoef.data(), bu.ncoef.size(), &d_nc);
-        upload(ctx, B_BT_EL, bu.elements.data(), bu.elements.size(), &d_el);
-        upload(ctx, B_BODY_MU, bu.mu.data(), bu.mu.size(), &d_mu);
-        upload(ctx, B_BT_BND, bu.bounds.data(), bu.bounds.size(), &d_bnd);
-        upload(ctx, B_BT_COFF, bu.coeff_off.data(), bu.coeff_off.size(), &d_coff);
-        upload(ctx, B_BT_CF, bu.coeffs.data(), bu.coeffs.size(), &d_cf);
-        bt = BodyTable{nb, d_kind, d_el, d_mu, d_soff, d_bnd, d_coff, d_nc, d_cf};
+        d_mu = reinterpret_cast<double*>(din + o_mu);
+        bt = BodyTable{nb,
+                       reinterpret_cast<int*>(din + o_kind),
+                       reinterpret_cast<double*>(din + o_el),
+                       d_mu,
+                       reinterpret_cast<int*>(din + o_soff),
+                       reinterpret_cast<double*>(din + o_bnd),
+                       reinterpret_cast<long long*>(din + o_coff),
+                       reinterpret_cast<int*>(din + o_nc),
+                       reinterpret_cast<double*>(din + o_cf)};
         d_pos = ctx->buf[B_BODY_POS].get<double>(static_cast<size_t>(N) * nb * 3);
         d_ind = ctx->buf[B_INDIRECT].get<double>(static_cast<size_t>(N) * 3);
     }
@@ -512,8 +587,7 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
     init_err(&fail, PSWARM_OK, "");
 
     for (int64_t seg = 0; seg < S; ++seg) {
-        const auto g = pswarm::build_grid(N, boundaries[seg], boundaries[seg + 1]);
-        for (Index j = (seg == 0 ? 0 : 1); j < N; ++j) h_times[seg * (N - 1) + j] = g.times[j];
+        const double* seg_times = grid_times.data() + seg * N;
         if (std::chrono::steady_clock::now() > deadline) {
             init_err(&fail, PSWARM_ERR_TIMEOUT, "solve_group: wall-clock budget exhausted in group 0");
             fail.segment = seg;
@@ -521,19 +595,14 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
             fail_status = PSWARM_ERR_TIMEOUT;
             break;
         }
-        double* d_times;
-        upload(ctx, B_TIMES, g.times.data(), static_cast<size_t>(N), &d_times);
+        const double* d_times = reinterpret_cast<const double*>(din + o_times) + seg * N;
+        cuda_check(cudaMemsetAsync(drep, 0, r_zero, st), "memset reports");
+        cuda_check(cudaMemsetAsync(d_ekey, 0xff, sizeof(unsigned long long), st), "memset");
         if (nb > 0) {  // frozen per-node ephemeris of this segment, evaluated on the device
-            cuda_check(cudaMemsetAsync(d_ekey, 0xff, sizeof(unsigned long long), st), "memset");
             cuda_check(launch_ephemeris(static_cast<int>(N), d_times, cfg->central_mu, bt, d_pos, d_ind, d_ekey, st),
                        "k_ephemeris");
             ++ctx->launches;
         }
-        cuda_check(cudaMemsetAsync(d_queue, 0, sizeof(int), st), "memset");
-        cuda_check(cudaMemsetAsync(d_faults, 0, sizeof(GroupFault) * P, st), "memset");
-        cuda_check(cudaMemsetAsync(d_iter, 0, sizeof(int32_t) * P, st), "memset");
-        cuda_check(cudaMemsetAsync(d_conv, 0, P, st), "memset");
-        cuda_check(cudaMemsetAsync(d_fb, 0, M, st), "memset");
 
         SegArgs a{};
         a.N = static_cast<int>(N);
@@ -550,7 +619,7 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
         a.max_it = max_it;
         a.record_history = d_hist ? 1 : 0;
         a.tol = cfg->tolerance;
-        a.omega2 = g.omega2;
+        a.omega2 = seg_omega2[seg];
         a.epoch = boundaries[seg];
         a.deadline_ns = gpu_deadline;
         a.fd = make_force_data(d_pos, d_mu, d_ind, cfg->central_mu, cfg->proximity_floor_km, nb);
@@ -578,14 +647,19 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
         } else if (max_it > 0) {
             run_wide_segment(ctx, a, h_off, deadline);
         }
-        cuda_check(cudaMemcpyAsync(h_iter.data() + seg * P, d_iter, sizeof(int32_t) * P, cudaMemcpyDeviceToHost, st), "D2H");
-        cuda_check(cudaMemcpyAsync(h_err.data() + seg * P, d_err, sizeof(double) * P, cudaMemcpyDeviceToHost, st), "D2H");
-        cuda_check(cudaMemcpyAsync(h_conv.data() + seg * P, d_conv, P, cudaMemcpyDeviceToHost, st), "D2H");
-        cuda_check(cudaMemcpyAsync(h_faults.data(), d_faults, sizeof(GroupFault) * P, cudaMemcpyDeviceToHost, st), "D2H");
-        cuda_check(cudaMemcpyAsync(h_fb.data() + seg * M, d_fb, M, cudaMemcpyDeviceToHost, st), "D2H");
-        unsigned long long ekey = ~0ull;
-        if (nb > 0) cuda_check(cudaMemcpyAsync(&ekey, d_ekey, sizeof ekey, cudaMemcpyDeviceToHost, st), "D2H");
+        cuda_check(cudaMemcpyAsync(hrep, drep, rp.total, cudaMemcpyDeviceToHost, st), "D2H reports");
+        if (h_term && seg == S - 1) {  // terminal states ride along with the last segment's reports
+            cuda_check(cudaMemcpyAsync(h_term, d_out, sizeof(double) * M * 6, cudaMemcpyDeviceToHost, st), "D2H terminal");
+            term_ready = true;
+        }
         cuda_check(cudaStreamSynchronize(st), "segment solve");
+        std::memcpy(h_iter.data() + seg * P, hrep + r_iter, sizeof(int32_t) * P);
+        std::memcpy(h_err.data() + seg * P, hrep + r_err, sizeof(double) * P);
+        std::memcpy(h_conv.data() + seg * P, hrep + r_conv, P);
+        std::memcpy(h_faults.data(), hrep + r_faults, sizeof(GroupFault) * P);
+        std::memcpy(h_fb.data() + seg * M, hrep + r_fb, M);
+        unsigned long long ekey;
+        std::memcpy(&ekey, hrep + r_ekey, sizeof ekey);
         // ---- ephemeris faults come first: build_ephemeris_cache precedes the solve
         //      (propagator.hpp:252); body-major order (ephemeris.hpp:96-105)
         {
@@ -601,8 +675,9 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
                 const int b = static_cast<int>((ekey / 4) / N), j = static_cast<int>((ekey / 4) % N);
                 if (kind == 1) {
                     init_err(&fail, PSWARM_ERR_COVERAGE,
-                             "ephemeris for body '" + bu.names[b] + "' does not cover epoch " + std::to_string(g.times[j]));
-                    fail.value = g.times[j];
+                             "ephemeris for body '" + bu.names[b] + "' does not cover epoch " +
+                                 std::to_string(seg_times[j]));
+                    fail.value = seg_times[j];
                 } else {
                     init_err(&fail, PSWARM_ERR_SOLVER, "solve_kepler: Newton iteration did not converge for body '" +
                                                            bu.names[b] + "'");
@@ -767,8 +842,8 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
         if (out->samples)
             cuda_check(cudaMemcpyAsync(out->samples, d_samples, sizeof(double) * M * R * 6, cudaMemcpyDeviceToHost, st),
                        "D2H samples");
-        if (out->terminal_states && fail_status == PSWARM_OK) {
-            cuda_check(cudaMemcpyAsync(s6.data(), d_in, sizeof(double) * M * 6, cudaMemcpyDeviceToHost, st),
+        if (out->terminal_states && fail_status == PSWARM_OK && !term_ready) {
+            cuda_check(cudaMemcpyAsync(h_term, d_in, sizeof(double) * M * 6, cudaMemcpyDeviceToHost, st),
                        "D2H terminal");
         }
         if (d_phase)
@@ -779,7 +854,7 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
         if (out->terminal_states && fail_status == PSWARM_OK)
             for (int64_t i = 0; i < M; ++i) {
                 out->terminal_states[7 * i] = boundaries[S];
-                for (int c = 0; c < 6; ++c) out->terminal_states[7 * i + 1 + c] = s6[i * 6 + c];
+                for (int c = 0; c < 6; ++c) out->terminal_states[7 * i + 1 + c] = h_term[i * 6 + c];
             }
         float ms = 0.f;
         cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
