@@ -139,14 +139,16 @@ void pswarm_destroy(pswarm_ctx* ctx);
  * on the persistent grid, 0 = SM count * ctas_per_sm), "profile_phases" (1 = record
  * per-phase SM cycles of the generic slot kernel, read with pswarm_get_phase_cycles),
  * "slot_kernel" (0 auto, 1 force the generic slot kernel, 2 prefer the
- * warp-specialised one). */
+ * warp-specialised one), "poison_outputs" (1 = NaN-fill the device output buffers
+ * before every solve, so an unwritten sample can never read back as a stale value). */
 pswarm_status pswarm_set_option(pswarm_ctx* ctx, const char* key, int64_t value);
 
-/* Diagnostics: SM cycles summed over CTAs per kernel phase of the last call.
+/* Diagnostics: SM cycles summed over CTAs per kernel phase of the last call (12 slots).
  * Generic slot kernel: 0 claim, 1 warm start, 2 force, 3 DMMA, 4 anchor barrier,
  * 5 epilogue, 6 staged epilogue, 7 decisions, 8 retire.  Warp-specialised kernel
- * (MMA group / FP group leaders): 0 wait for F, 1 DMMA, 2 epilogue, 3 staged rows,
- * 4 wait for Y, 5 decisions, 6 retire + claim, 7 warm start, 8 force.  9 = CTA count. */
+ * (MMA group / FP group leaders): 0 wait for F, 1 DMMA, 2 epilogue, 3 wait for b0,
+ * 4 wait for Y, 5 staged rows + decisions, 6 retire + claim, 7 warm start, 8 force,
+ * 9 b0.  Slot 11 = CTA count. */
 pswarm_status pswarm_get_phase_cycles(pswarm_ctx* ctx, uint64_t* out, int32_t n);
 
 /* Diagnostics: name of the solver kernel the last propagate/run_batch call used

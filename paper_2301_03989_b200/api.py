@@ -337,13 +337,18 @@ class Context:
 
     PHASE_NAMES = ("claim", "warm_start", "force", "dmma", "anchor_barrier", "epilogue", "staged_epilogue",
                    "decisions", "retire")
+    WS_PHASE_NAMES = ("mma_wait_f", "mma_dmma", "mma_epilogue", "mma_wait_b0", "fp_wait_y", "fp_staged_decisions",
+                      "fp_retire_claim", "fp_warm_start", "fp_force", "fp_b0")
+    N_PHASES = 12
 
     def phase_cycles(self) -> dict:
-        """Per-phase SM cycles of the last solve (requires set_option('profile_phases', 1))."""
-        buf = (C.c_uint64 * 10)()
-        self.lib.pswarm_get_phase_cycles(self.ptr, buf, 10)
-        d = {n: int(buf[k]) for k, n in enumerate(self.PHASE_NAMES)}
-        d["ctas"] = int(buf[9])
+        """Per-phase SM cycles of the last solve (requires set_option('profile_phases', 1)),
+        named after the solver kernel that ran."""
+        buf = (C.c_uint64 * self.N_PHASES)()
+        self.lib.pswarm_get_phase_cycles(self.ptr, buf, self.N_PHASES)
+        names = self.WS_PHASE_NAMES if self.kernel_name() == "k_pc_ws" else self.PHASE_NAMES
+        d = {n: int(buf[k]) for k, n in enumerate(names)}
+        d["ctas"] = int(buf[self.N_PHASES - 1])
         return d
 
     def kernel_name(self) -> str:

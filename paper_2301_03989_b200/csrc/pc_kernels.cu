@@ -552,6 +552,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_pc_segment(const SegArgs a) {
                     for (int c = 0; c < 6; ++c) a.state_out[tr * 6 + c] = ybuf[yidx(j, c, t)];
                 }
             }
+            __syncthreads();  // slot_traj is cleared below
         }
         if (tid == 0) {
             const int fm = st.free_mask;
@@ -563,7 +564,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_pc_segment(const SegArgs a) {
         PHASE(8);
     }
     if (prof && tid == 0) {
-        pc[9] += 1;  // CTA count
+        pc[PHASES - 1] += 1;  // CTA count
         for (int k = 0; k < PHASES; ++k) atomicAdd(a.phase_cycles + k, static_cast<unsigned long long>(pc[k]));
     }
 }

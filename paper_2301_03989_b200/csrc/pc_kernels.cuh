@@ -32,9 +32,10 @@ struct GroupFault {
     double value2;       // eccentricity (solver)
 };
 
-/// Phase accounting slots: 0 claim, 1 warm start, 2 force, 3 DMMA, 4 anchor/b0 barrier,
-/// 5 epilogue (main rows), 6 epilogue (staged rows), 7 decisions, 8 retire, 9 CTA count.
-constexpr int PHASES = 10;
+/// Phase accounting slots (generic kernel): 0 claim, 1 warm start, 2 force, 3 DMMA,
+/// 4 anchor/b0 barrier, 5 epilogue (main rows), 6 epilogue (staged rows), 7 decisions,
+/// 8 retire; warp-specialised kernel: see pc_slots2.cu.  Slot PHASES-1 = CTA count.
+constexpr int PHASES = 12;
 
 /// Arguments of one segment launch of the persistent slot kernel.
 struct SegArgs {
@@ -139,6 +140,7 @@ cudaError_t launch_wide_output(const WideArgs& a, cudaStream_t s);
 size_t ws_smem_bytes(int N, int nkp, int xrows, int B, int stage_eph);
 int ws_main_tiles(int N);
 int ws_extra_rows(int N);
+bool ws_supported(int N);
 cudaError_t launch_segment_ws(const SegArgs& a, int grid, cudaStream_t s);
 
 GemmPlan make_gemm_plan(int N);

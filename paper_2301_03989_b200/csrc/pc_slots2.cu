@@ -17,6 +17,7 @@
 // Half layout (per half: 4 slots x 6 components = 24 block columns = 3 MMA n-tiles):
 //   n-tile p holds components 2p, 2p+1; column within the tile = slot*2 + (comp & 1),
 //   so C-fragment lane (g, q) holds all six components of slot q of row g.
+#include <algorithm>
 #include <climits>
 
 #include "pc_kernels.cuh"
@@ -31,7 +32,7 @@ constexpr int HC = 6 * HS;       // columns per half
 constexpr int YS2 = 2 * HC + 4;  // Ybuf row stride (doubles): 52 -> conflict-free epilogue rows
 constexpr int MMA_WARPS = 8, FP_WARPS = 8;
 constexpr int MMA_THREADS = 32 * MMA_WARPS, FP_THREADS = 32 * FP_WARPS, WS_THREADS = MMA_THREADS + FP_THREADS;
-constexpr int BAR_F0 = 1, BAR_Y0 = 3, BAR_MMA = 5, BAR_FP = 6;  // F_h = 1+h, Y_h = 3+h
+constexpr int BAR_F0 = 1, BAR_Y0 = 3, BAR_FP = 6, BAR_B0 = 7;  // F_h = 1+h, Y_h = 3+h, B_h = 7+h
 
 __device__ __forceinline__ int y2(int j, int h, int c, int s) { return j * YS2 + h * HC + c * HS + s; }
 /// B-fragment index of F(node j, comp c, slot s) within a half's Fbuf.
@@ -40,14 +41,14 @@ __device__ __forceinline__ int f2(int j, int c, int s) {
 }
 
 // Optional phase accounting (pswarm_set_option "profile_phases"): MMA-group lane 0 of
-// warp 0 stamps slots 0-3 (wait F, DMMA, epilogue, staged rows), FP-group thread 0 slots
-// 4-8 (wait Y, decisions, retire+claim, warm start, force); slot 9 counts CTAs.
+// warp 0 stamps slots 0-3 (wait F, DMMA, epilogue, wait b0), FP-group thread 0 slots
+// 4-9 (wait Y, staged rows + decisions, retire + claim, warm start, force, b0).
 #define WS_PHASE(k)                                  \
     do {                                             \
         if (prof && stamp) {                         \
             const long long now_ = clock64();        \
-            pc[(k)] += now_ - t_prev;                \
-            t_prev = now_;                           \
+            s_pc[(k)] += now_ - s_prev[grp_];        \
+            s_prev[grp_] = now_;                     \
         }                                            \
     } while (0)
 
@@ -83,8 +84,10 @@ struct WsState {
 };
 
 struct WsLayout {
-    size_t ybuf, fbuf0, fbuf1, xstage, eph, state, total;
+    size_t ybuf, fbuf0, fbuf1, xstage, anchor, b0part, eph, state, total;
 };
+
+constexpr int B0_PARTS = (32 * FP_WARPS) / HC;  // 10 partial sums per b0 column
 
 __host__ __device__ inline WsLayout ws_layout(int N, int nkp, int xrows, int B, int stage_eph) {
     WsLayout L;
@@ -92,8 +95,10 @@ __host__ __device__ inline WsLayout ws_layout(int N, int nkp, int xrows, int B, 
     L.fbuf0 = L.ybuf + sizeof(double) * static_cast<size_t>(N) * YS2;
     const size_t fb = sizeof(double) * static_cast<size_t>(8 * nkp) * HC;
     L.fbuf1 = L.fbuf0 + fb;
-    L.xstage = L.fbuf1 + fb;
-    L.eph = L.xstage + sizeof(double) * static_cast<size_t>(xrows) * HC;
+    L.xstage = L.fbuf1 + fb;  // [2 halves][xrows][HC]
+    L.anchor = L.xstage + sizeof(double) * 2 * static_cast<size_t>(xrows) * HC;
+    L.b0part = L.anchor + sizeof(double) * static_cast<size_t>(8 * nkp);
+    L.eph = L.b0part + sizeof(double) * B0_PARTS * HC;
     L.state = L.eph + (stage_eph ? sizeof(double) * static_cast<size_t>(N) * (3 * B + 3) : 0);
     L.total = L.state + sizeof(WsState);
     return L;
@@ -164,20 +169,33 @@ __device__ __forceinline__ void gemm_half(const double2* __restrict__ upack, int
     };
 #pragma unroll
     for (int x = 0; x < XMW; ++x) xacc[x][0] = xacc[x][1] = 0.0;
-    APairH<MAIN, XMW> p0, p1, p2;  // two operator pairs in flight (L2 latency under load)
-    load(0, p0);
-    if (nkp > 1) load(1, p1);
-    int kp = 0;
-    for (; kp + 2 < nkp; kp += 3) {
-        load(kp + 2, p2);
-        compute(kp, p0);
-        if (kp + 3 < nkp) load(kp + 3, p0);
-        compute(kp + 1, p1);
-        if (kp + 4 < nkp) load(kp + 4, p1);
-        compute(kp + 2, p2);
+    if constexpr (MAIN + XMW <= 4) {
+        APairH<MAIN, XMW> p0, p1, p2;  // two operator pairs in flight (L2 latency under load)
+        load(0, p0);
+        if (nkp > 1) load(1, p1);
+        int kp = 0;
+        for (; kp + 2 < nkp; kp += 3) {
+            load(kp + 2, p2);
+            compute(kp, p0);
+            if (kp + 3 < nkp) load(kp + 3, p0);
+            compute(kp + 1, p1);
+            if (kp + 4 < nkp) load(kp + 4, p1);
+            compute(kp + 2, p2);
+        }
+        if (kp < nkp) compute(kp, p0);
+        if (kp + 1 < nkp) compute(kp + 1, p1);
+    } else {  // wide warps: one pair in flight keeps the accumulators in registers
+        APairH<MAIN, XMW> p0, p1;
+        load(0, p0);
+        int kp = 0;
+        for (; kp + 1 < nkp; kp += 2) {
+            load(kp + 1, p1);
+            compute(kp, p0);
+            if (kp + 2 < nkp) load(kp + 2, p0);
+            compute(kp + 1, p1);
+        }
+        if (kp < nkp) compute(kp, p0);
     }
-    if (kp < nkp) compute(kp, p0);
-    if (kp + 1 < nkp) compute(kp + 1, p1);
 }
 
 /// Force of half h for node j, its 4 slots as independent chains (force_model.hpp:93-142).
@@ -266,14 +284,10 @@ size_t ws_smem_bytes(int N, int nkp, int xrows, int B, int stage_eph) {
     return ws_layout(N, nkp, xrows, B, stage_eph).total;
 }
 
-int ws_main_tiles(int N) {
-    const int mt = (N + 1 + 7) / 8;
-    return mt / MMA_WARPS;
-}
+int ws_main_tiles(int N) { return ((N + 7) / 8) / MMA_WARPS; }
 
 int ws_extra_rows(int N) {
-    const int mb = ws_main_tiles(N) * MMA_WARPS;
-    const int r = N - mb * 8;
+    const int r = N - ws_main_tiles(N) * MMA_WARPS * 8;
     return r > 0 ? r : 0;
 }
 
@@ -287,21 +301,33 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
     const size_t fb_bytes = L.fbuf1 - L.fbuf0;
     double* fb0 = reinterpret_cast<double*>(smem_raw + L.fbuf0);
     double* xstage = reinterpret_cast<double*>(smem_raw + L.xstage);
+    double* anc = reinterpret_cast<double*>(smem_raw + L.anchor);
+    double* b0part = reinterpret_cast<double*>(smem_raw + L.b0part);
     double* eph = reinterpret_cast<double*>(smem_raw + L.eph);
     WsState& st = *reinterpret_cast<WsState*>(smem_raw + L.state);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int KP = 8 * a.nkp;
-    const int mtiles = (N + 1 + 7) / 8;
+    const int mtiles = (N + 7) / 8;  // node rows only: b0 comes from the FP group's anchor GEMV
     const bool prof = a.phase_cycles != nullptr;
     const bool stamp = tid == 0 || tid == MMA_THREADS;
-    long long pc[PHASES] = {};
-    long long t_prev = clock64();
+    // phase counters live in shared memory (no registers / local memory on the hot path)
+    __shared__ long long s_pc[PHASES], s_prev[2];
+    const int grp_ = tid < MMA_THREADS ? 0 : 1;
+    if (tid < PHASES) s_pc[tid] = 0;
+    if (stamp) s_prev[grp_] = clock64();
     HalfPlan hp;
     hp.main = MAIN;
     hp.mb = MAIN * MMA_WARPS;
     hp.extras = (mtiles - hp.mb) * 3;
 
     for (int i = tid; i < 2 * KP * HC; i += WS_THREADS) fb0[i] = 0.0;  // both halves (contiguous)
+    {  // anchor_op row (pc_matrices.hpp:98-100) = row N of the packed operator
+        const double* up = reinterpret_cast<const double*>(a.upack);
+        const int amt = N >> 3, ag = N & 7;
+        for (int k = tid; k < KP; k += WS_THREADS)
+            anc[k] = k < N ? up[2 * ((static_cast<size_t>(amt) * a.nkp + (k >> 3)) * 32 + ag * 4 + (k & 3)) + ((k >> 2) & 1)]
+                           : 0.0;
+    }
     if (STAGE && B > 0) {
         for (int i = tid; i < N * 3 * B; i += WS_THREADS) eph[i] = a.fd.body_pos[i];
         for (int i = tid; i < N * 3; i += WS_THREADS) eph[N * 3 * B + i] = a.fd.indirect[i];
@@ -337,29 +363,14 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
                 gemm_half<MAIN, XMW>(a.upack, a.nkp, reinterpret_cast<const double*>(smem_raw + L.fbuf0 + h * fb_bytes),
                                      hp, warp, lane, acc, xacc);
                 WS_PHASE(1);
-                const int amt = N >> 3;
-                if (g == (N & 7)) {  // anchor row -> b0/2 (pc_matrices.hpp:138, :145)
-#pragma unroll
-                    for (int i = 0; i < MAIN; ++i)
-                        if (warp * MAIN + i == amt)
-#pragma unroll
-                            for (int p = 0; p < 3; ++p)
-#pragma unroll
-                                for (int e = 0; e < 2; ++e)
-                                    st.b0h[h][p * 8 + 2 * q + e] = 0.5 * (acc[i][p][e] + 2.0 * st.y0[h * HS + q][2 * p + e]);
-#pragma unroll
-                    for (int x = 0; x < XMW; ++x) {
-                        const int ex = warp + x * MMA_WARPS;
-                        if (ex < hp.extras && hp.mb + ex / 3 == amt) {
-                            const int p = ex % 3;
-#pragma unroll
-                            for (int e = 0; e < 2; ++e)
-                                st.b0h[h][p * 8 + 2 * q + e] = 0.5 * (xacc[x][e] + 2.0 * st.y0[h * HS + q][2 * p + e]);
-                        }
-                    }
-                }
-                bar_sync(BAR_MMA, MMA_THREADS);
+                bar_sync(BAR_B0 + h, WS_THREADS);  // b0 of half h (FP group)
+                WS_PHASE(3);
+                // epilogue of this warp's rows: + b0/2 (pc_matrices.hpp:145; b0 was formed by
+                // the FP group with the force), finite check, error vs the previous iterate.
+                // No barrier inside the MMA group: a warp that finishes early runs its
+                // epilogue while its SMSP partner still issues DMMAs.
                 const int act_h = (st.active_mask >> (h * HS)) & 0xF;
+                const double* b0 = st.b0h[h];
                 double bn = 0.0, bd = 1.0;
                 int nf = INT_MAX;
 #pragma unroll
@@ -373,12 +384,13 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
                         for (int e = 0; e < 2; ++e) {
                             const int c = 2 * p + e;
                             yo[c] = ybuf[y2(j, h, c, q)];
-                            yn[c] = acc[i][p][e] + st.b0h[h][p * 8 + 2 * q + e];
+                            yn[c] = acc[i][p][e] + b0[p * 8 + 2 * q + e];
                         }
                     update_sample(yn, yo, j, a.error_mode, bn, bd, nf);
 #pragma unroll
                     for (int c = 0; c < 6; ++c) ybuf[y2(j, h, c, q)] = yn[c];
                 }
+                double* xs = xstage + h * xrows * HC;
 #pragma unroll
                 for (int x = 0; x < XMW; ++x) {  // extra tiles -> stage (components spread over warps)
                     const int ex = warp + x * MMA_WARPS;
@@ -386,8 +398,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
                     const int j = (hp.mb + ex / 3) * 8 + g, p = ex % 3;
                     if (j >= N) continue;
 #pragma unroll
-                    for (int e = 0; e < 2; ++e)
-                        xstage[(j - hp.mb * 8) * HC + q * 6 + 2 * p + e] = xacc[x][e] + st.b0h[h][p * 8 + 2 * q + e];
+                    for (int e = 0; e < 2; ++e) xs[(j - hp.mb * 8) * HC + q * 6 + 2 * p + e] = xacc[x][e] + b0[p * 8 + 2 * q + e];
                 }
                 double e2 = bn / bd;
 #pragma unroll
@@ -399,28 +410,10 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
                     atomicMax(&st.slot_err[h * HS + q], static_cast<unsigned long long>(__double_as_longlong(e2)));
                     if (nf != INT_MAX) atomicMin(&st.nf_key[h * HS + q], nf);
                 }
-                bar_sync(BAR_MMA, MMA_THREADS);
                 WS_PHASE(2);
-                if (tid < xrows * HS) {  // staged rows
-                    const int r = tid >> 2, s = tid & 3, j = hp.mb * 8 + r;
-                    if ((act_h >> s) & 1) {
-                        double yn[6], yo[6];
-#pragma unroll
-                        for (int c = 0; c < 6; ++c) {
-                            yn[c] = xstage[r * HC + s * 6 + c];
-                            yo[c] = ybuf[y2(j, h, c, s)];
-                        }
-                        double sbn = 0.0, sbd = 1.0;
-                        int snf = INT_MAX;
-                        update_sample(yn, yo, j, a.error_mode, sbn, sbd, snf);
-#pragma unroll
-                        for (int c = 0; c < 6; ++c) ybuf[y2(j, h, c, s)] = yn[c];
-                        atomicMax(&st.slot_err[h * HS + s], static_cast<unsigned long long>(__double_as_longlong(sbn / sbd)));
-                        if (snf != INT_MAX) atomicMin(&st.nf_key[h * HS + s], snf);
-                    }
-                }
+            } else {
+                bar_sync(BAR_B0 + h, WS_THREADS);  // keep the B_h generations paired
             }
-            WS_PHASE(3);
             bar_arrive(BAR_Y0 + h, WS_THREADS);  // bar.arrive/bar.sync order smem among participants
         }
     } else {
@@ -431,6 +424,29 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
         for (int h = 0;; h ^= 1) {
             if (!first[h]) bar_sync(BAR_Y0 + h, WS_THREADS);  // epilogue of half h done
             WS_PHASE(4);
+            // ---- staged rows of half h (node rows whose components sit in several MMA warps)
+            if (!first[h] && xrows > 0 && st.half_active[h]) {
+                const int act_h = (st.active_mask >> (h * HS)) & 0xF;
+                const double* xs = xstage + h * xrows * HC;
+                for (int i = ft; i < xrows * HS; i += FP_THREADS) {
+                    const int r = i >> 2, s = i & 3, j = MAIN * MMA_WARPS * 8 + r;
+                    if (!((act_h >> s) & 1)) continue;
+                    double yn[6], yo[6];
+#pragma unroll
+                    for (int c = 0; c < 6; ++c) {
+                        yn[c] = xs[r * HC + s * 6 + c];
+                        yo[c] = ybuf[y2(j, h, c, s)];
+                    }
+                    double sbn = 0.0, sbd = 1.0;
+                    int snf = INT_MAX;
+                    update_sample(yn, yo, j, a.error_mode, sbn, sbd, snf);
+#pragma unroll
+                    for (int c = 0; c < 6; ++c) ybuf[y2(j, h, c, s)] = yn[c];
+                    atomicMax(&st.slot_err[h * HS + s], static_cast<unsigned long long>(__double_as_longlong(sbn / sbd)));
+                    if (snf != INT_MAX) atomicMin(&st.nf_key[h * HS + s], snf);
+                }
+                bar_sync(BAR_FP, FP_THREADS);
+            }
             // ---- decisions for half h (warp 0 of the FP group, lane = slot of the half)
             if (!first[h] && fw == 0) {
                 const int am = st.active_mask;
@@ -563,6 +579,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
                         for (int c = 0; c < 6; ++c) a.state_out[tr * 6 + c] = ybuf[y2(j, h, c, s)];
                     }
                 }
+                bar_sync(BAR_FP, FP_THREADS);  // slot_traj is rewritten by the claim below
             }
             // ---- free + claim into half h (thread 0 of the FP group)
             if (ft == 0) {
@@ -690,13 +707,39 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
             }
             first[h] = false;
             WS_PHASE(8);
-            bar_arrive(BAR_F0 + h, WS_THREADS);
+            bar_arrive(BAR_F0 + h, WS_THREADS);  // F_h ready: the MMA group starts its DMMAs
+            // ---- b0 = anchor_op.F + 2 y0 of half h (pc_matrices.hpp:138), overlapped with the
+            //      DMMAs of half h: B0_PARTS strided partial dot products per column, summed in a
+            //      fixed order; the MMA group waits for it (B_h) only before its epilogue
+            if (act_h) {
+                const double* fbh = reinterpret_cast<const double*>(smem_raw + L.fbuf0 + h * fb_bytes);
+                if (ft < B0_PARTS * HC) {
+                    const int col = ft % HC, part = ft / HC;
+                    const int c = 2 * (col >> 3) + (col & 1), s = (col & 7) >> 1;
+                    double sum = 0.0;
+                    for (int j = part; j < N; j += B0_PARTS) sum = fma(anc[j], fbh[f2(j, c, s)], sum);
+                    b0part[part * HC + col] = sum;
+                }
+                bar_sync(BAR_FP, FP_THREADS);
+                if (ft < HC) {
+                    const int c = 2 * (ft >> 3) + (ft & 1), s = (ft & 7) >> 1;
+                    double sum = 0.0;
+#pragma unroll
+                    for (int part = 0; part < B0_PARTS; ++part) sum += b0part[part * HC + ft];
+                    st.b0h[h][ft] = 0.5 * (sum + 2.0 * st.y0[h * HS + s][c]);
+                }
+            }
+            WS_PHASE(9);
+            bar_arrive(BAR_B0 + h, WS_THREADS);
         }
     }
-    if (prof && stamp) {
-        if (tid == 0) pc[9] = 1;
-        for (int k = 0; k < PHASES; ++k)
-            if (pc[k]) atomicAdd(a.phase_cycles + k, static_cast<unsigned long long>(pc[k]));
+    if (prof) {
+        __syncthreads();
+        if (tid == 0) {
+            s_pc[PHASES - 1] = 1;
+            for (int k = 0; k < PHASES; ++k)
+                if (s_pc[k]) atomicAdd(a.phase_cycles + k, static_cast<unsigned long long>(s_pc[k]));
+        }
     }
 }
 
@@ -709,15 +752,30 @@ static cudaError_t launch_ws_t(const SegArgs& a, int grid, size_t smem, cudaStre
     return cudaGetLastError();
 }
 
+/// Extra (m-tile, n-tile) tiles beyond the MAIN full-width m-tiles of every MMA warp.
+static int ws_extras(int N) { return ((N + 7) / 8 - ws_main_tiles(N) * MMA_WARPS) * 3; }
+
+bool ws_supported(int N) {
+    const int main = ws_main_tiles(N);
+    return main >= 1 && main <= 4 && ws_extras(N) <= 3 * MMA_WARPS && (main < 4 || ws_extras(N) <= MMA_WARPS);
+}
+
 cudaError_t launch_segment_ws(const SegArgs& a, int grid, cudaStream_t s) {
+    if (!ws_supported(a.N)) return cudaErrorNotSupported;
     const int main = ws_main_tiles(a.N);
-    const int mtiles = (a.N + 1 + 7) / 8;
-    if ((mtiles - main * MMA_WARPS) * 3 > MMA_WARPS * (main == 2 ? 3 : 1)) return cudaErrorNotSupported;
+    const int xmw = std::max(1, (ws_extras(a.N) + MMA_WARPS - 1) / MMA_WARPS);
     const size_t smem = ws_smem_bytes(a.N, a.nkp, a.xrows, a.fd.n_bodies, a.stage_eph);
-    switch (main) {
-    case 2: return launch_ws_t<2, 3>(a, grid, smem, s);
-    case 3: return launch_ws_t<3, 1>(a, grid, smem, s);
-    case 4: return launch_ws_t<4, 1>(a, grid, smem, s);
+    switch (main * 4 + xmw) {
+    case 5: return launch_ws_t<1, 1>(a, grid, smem, s);
+    case 6: return launch_ws_t<1, 2>(a, grid, smem, s);
+    case 7: return launch_ws_t<1, 3>(a, grid, smem, s);
+    case 9: return launch_ws_t<2, 1>(a, grid, smem, s);
+    case 10: return launch_ws_t<2, 2>(a, grid, smem, s);
+    case 11: return launch_ws_t<2, 3>(a, grid, smem, s);
+    case 13: return launch_ws_t<3, 1>(a, grid, smem, s);
+    case 14: return launch_ws_t<3, 2>(a, grid, smem, s);
+    case 15: return launch_ws_t<3, 3>(a, grid, smem, s);
+    case 17: return launch_ws_t<4, 1>(a, grid, smem, s);
     default: return cudaErrorNotSupported;
     }
 }

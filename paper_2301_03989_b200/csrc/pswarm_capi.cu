@@ -196,6 +196,7 @@ struct pswarm_ctx {
     int profile_phases = 0;
     const char* last_kernel = "";
     int slot_kernel = 0;  // 0 auto, 1 generic k_pc_segment, 2 warp-specialised k_pc_ws
+    int poison_outputs = 0;  // 1: NaN-fill device outputs before each solve (tests)
     unsigned long long phase_host[pswarm_dev::PHASES] = {};
     PinnedBuf pin_in, pin_rep, pin_term;
     // wide-group path
@@ -495,6 +496,10 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
     double* d_out = ctx->buf[B_STATE_B].get<double>(static_cast<size_t>(M) * 6);
     if (d_in == d_out) raise(PSWARM_ERR_GENERIC, "propagate: state buffers alias");
     double* d_samples = out && out->samples ? ctx->buf[B_SAMPLES].get<double>(static_cast<size_t>(M) * R * 6) : nullptr;
+    if (ctx->poison_outputs) {  // test aid: unwritten outputs read back as NaN instead of stale values
+        cuda_check(cudaMemsetAsync(d_out, 0xff, sizeof(double) * M * 6, ctx->stream), "poison");
+        if (d_samples) cuda_check(cudaMemsetAsync(d_samples, 0xff, sizeof(double) * M * R * 6, ctx->stream), "poison");
+    }
     const bool want_hist = out && out->error_history && max_it > 0;
     double* d_hist = want_hist ? ctx->buf[B_REP_HIST].get<double>(static_cast<size_t>(S) * P * max_it) : nullptr;
     if (d_hist) cuda_check(cudaMemsetAsync(d_hist, 0xff, sizeof(double) * S * P * max_it, st), "memset");
@@ -537,8 +542,7 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
     // the generic slot kernel (groups <= 8), or the wide-group path
     constexpr size_t SMEM_MAX = 227 * 1024;
     const int Ni = static_cast<int>(N);
-    const int ws_main = ws_main_tiles(Ni);
-    const bool use_ws = !wide && gmax <= 4 && ws_main >= 2 && ws_main <= 4 && ctx->slot_kernel != 1 &&
+    const bool use_ws = !wide && gmax <= 4 && ws_supported(Ni) && ctx->slot_kernel != 1 &&
                         ws_smem_bytes(Ni, op.nkp, ws_extra_rows(Ni), nb, 0) <= SMEM_MAX;
     const int xrows = use_ws ? ws_extra_rows(Ni) : extra_rows(Ni, op.gp);
     ctx->last_kernel = wide ? "k_wide_iter" : use_ws ? "k_pc_ws" : "k_pc_segment";
@@ -960,6 +964,7 @@ pswarm_status pswarm_set_option(pswarm_ctx* ctx, const char* key, int64_t value)
         else if (k == "max_ctas") ctx->max_ctas = static_cast<int>(std::max<int64_t>(0, value));
         else if (k == "profile_phases") ctx->profile_phases = value != 0;
         else if (k == "slot_kernel") ctx->slot_kernel = static_cast<int>(value);
+        else if (k == "poison_outputs") ctx->poison_outputs = value != 0;
         else raise(PSWARM_ERR_GENERIC, "pswarm_set_option: unknown key '" + k + "'");
     });
 }

@@ -215,3 +215,34 @@ def test_singularity_in_solve_names_body(ctx, oracle):
         errs.append(e.value)
     assert str(errs[0]) == str(errs[1]) and errs[0].body == "venus-like"
     assert "trajectory 2" in str(errs[0])
+
+
+@pytest.mark.parametrize("n", [64, 96, 128, 160, 200, 232, 256])
+def test_c5_node_sweep(ctx, oracle, n):
+    """C5 node-count sweep (64-256 nodes per segment): every warp plan of the slot
+    kernels against the oracle, Sun + 8 planets, 0.6 period."""
+    states, plan, cfg = _setup(24, n, 0.6, "planets8")
+    got = ctx.run_batch(states, cfg, plan, "independent")
+    want = oracle.run_batch(states, cfg, plan, "independent", 8)
+    _parity(got, want)
+    assert got.converged.all()
+
+
+def test_c5_mask_stress_heterogeneous_iterations(ctx, oracle):
+    """C5 convergence-mask stress: four quarters with clone spreads 1e-7 .. 1e-2 give
+    heterogeneous iteration counts; per-trajectory masking refills freed slots, so
+    every trajectory must still match its own oracle solve."""
+    base = ps.reference_state()
+    quarters = [ps.make_clone_batch(base, 40, sp) for sp in (1e-7, 1e-5, 1e-3, 1e-2)]
+    states = np.concatenate(quarters)
+    period = ps.osculating_period(base, ps.MU_SUN)
+    plan = ps.plan_segments(base, 0.0, 0.87 * period, ps.MU_SUN, "single", 200)
+    cfg = ps.reference_force_config("n_body", bodies=ps.planets8(), n_nodes=200)
+    ctx.set_option("max_ctas", 3)  # few CTAs: slots are refilled many times
+    try:
+        got = ctx.run_batch(states, cfg, plan, "independent")
+    finally:
+        ctx.set_option("max_ctas", 0)
+    want = oracle.run_batch(states, cfg, plan, "independent", 8)
+    _parity(got, want)
+    assert want.iterations.min() < want.iterations.max()  # heterogeneous by construction
