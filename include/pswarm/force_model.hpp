@@ -14,13 +14,16 @@
 
 namespace pswarm {
 
-enum class ForceKind { two_body, n_body };
+/// n_body_1pn: EXTENSION (BASELINE config 5, not in the reference): n_body + the EIH first
+/// post-Newtonian correction with the body states frozen per node.
+enum class ForceKind { two_body, n_body, n_body_1pn };
 
 struct ForceModelConfig {  // force_model.hpp:17-24
     ForceKind kind = ForceKind::two_body;
     double central_mu = 0.0;
     std::vector<BodySpec> bodies;
     double proximity_floor_km = 1.0;
+    double c_light = 299792.458;  // km/s, n_body_1pn only
 };
 
 /// omega2-scaled derivative block of a component-major N x 6m state block,

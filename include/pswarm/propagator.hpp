@@ -25,7 +25,7 @@
 
 namespace pswarm {
 
-enum class StartMode { warm, cold };
+enum class StartMode { warm, cold, hot };  // hot: EXTENSION (Macomber hot start)
 enum class SegmentPolicy { single, per_orbit };
 enum class Direction { forward, backward };
 
@@ -229,16 +229,17 @@ struct ConfigMarshal {
         cfg.tolerance = c.tolerance;
         cfg.error_mode = c.error_mode == ErrorMode::absolute ? 1 : 0;
         cfg.max_iterations = c.max_iterations;
-        cfg.start_mode = c.start_mode == StartMode::cold ? 1 : 0;
+        cfg.start_mode = c.start_mode == StartMode::cold ? 1 : c.start_mode == StartMode::hot ? 2 : 0;
         cfg.segment_policy = c.segment_policy == SegmentPolicy::per_orbit ? 1 : 0;
         cfg.max_segment_periods = c.max_segment_periods;
-        cfg.force_kind = c.force.kind == ForceKind::n_body ? 1 : 0;
+        cfg.force_kind = c.force.kind == ForceKind::n_body ? 1 : c.force.kind == ForceKind::n_body_1pn ? 2 : 0;
         cfg.n_bodies = static_cast<int32_t>(bodies.size());
         cfg.central_mu = c.force.central_mu;
         cfg.bodies = bodies.empty() ? nullptr : bodies.data();
         cfg.proximity_floor_km = c.force.proximity_floor_km;
         cfg.p_groups = c.p_groups;
         cfg.timeout_s = c.timeout_s;
+        cfg.c_light = c.force.c_light;
     }
     ConfigMarshal(const ConfigMarshal&) = delete;
 };

@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define PSWARM_ABI_VERSION 1
+#define PSWARM_ABI_VERSION 2
 
 /* Status codes: one per reference exception type (errors.hpp:10-113,
  * propagator.hpp:173-186) plus device-side failures. */
@@ -91,16 +91,19 @@ typedef struct pswarm_config {
     double tolerance;           /* default 1e-12 */
     int32_t error_mode;         /* 0 relative, 1 absolute (error_metric.hpp:12) */
     int32_t max_iterations;     /* default 100 */
-    int32_t start_mode;         /* 0 warm, 1 cold */
+    int32_t start_mode;         /* 0 warm, 1 cold, 2 hot (EXTENSION: warm + the previous segment's
+                                   converged-minus-conic correction, Macomber 2015) */
     int32_t segment_policy;     /* 0 single, 1 per_orbit */
     double max_segment_periods; /* default 1.0 */
-    int32_t force_kind;         /* 0 two_body, 1 n_body */
+    int32_t force_kind;         /* 0 two_body, 1 n_body, 2 n_body_1pn (EXTENSION: n_body + the EIH
+                                   first post-Newtonian correction) */
     int32_t n_bodies;
     double central_mu;
     const pswarm_body* bodies;
     double proximity_floor_km;  /* default 1.0 */
     int64_t p_groups;           /* grouped mode group count */
     double timeout_s;           /* 0 disables the wall-clock guard */
+    double c_light;             /* n_body_1pn: speed of light in km/s (0 = 299792.458) */
 } pswarm_config;
 
 /* Outputs of pswarm_propagate / pswarm_run_batch (PropagationResult,

@@ -127,10 +127,13 @@ Config config_from(const pswarm_config& c) {
     o.tolerance = c.tolerance;
     o.error_mode = c.error_mode == 1 ? ErrorMode::absolute : ErrorMode::relative;
     o.max_iterations = c.max_iterations;
-    o.start_mode = c.start_mode == 1 ? StartMode::cold : StartMode::warm;
+    o.start_mode = c.start_mode == 1 ? StartMode::cold : c.start_mode == 2 ? StartMode::hot : StartMode::warm;
     o.segment_policy = c.segment_policy == 1 ? SegmentPolicy::per_orbit : SegmentPolicy::single;
     o.max_segment_periods = c.max_segment_periods;
-    o.force.kind = c.force_kind == 1 ? ForceKind::n_body : ForceKind::two_body;
+    o.force.kind = c.force_kind == 1   ? ForceKind::n_body
+                   : c.force_kind == 2 ? ForceKind::n_body_1pn
+                                       : ForceKind::two_body;
+    o.force.c_light = c.c_light > 0.0 ? c.c_light : 299792.458;
     o.force.central_mu = c.central_mu;
     for (int32_t b = 0; b < c.n_bodies; ++b) o.force.bodies.push_back(body_from(c.bodies[b]));
     o.force.proximity_floor_km = c.proximity_floor_km;

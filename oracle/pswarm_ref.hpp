@@ -503,6 +503,20 @@ struct ChebSeg {
         const double tau = (2.0 * t - (t_start + t_end)) / (t_end - t_start);
         return {clenshaw(cx, tau), clenshaw(cy, tau), clenshaw(cz, tau)};
     }
+    // EXTENSION (relativistic model, not in the reference): d/dt of the series via the
+    // derivative-coefficient recurrence c'_{k-1} = c'_{k+1} + 2k c_k, c'_0 halved.
+    static std::vector<double> derivative(const std::vector<double>& c) {
+        const Index n = static_cast<Index>(c.size());
+        std::vector<double> d(static_cast<std::size_t>(std::max<Index>(n, 1)), 0.0);
+        for (Index k = n - 1; k >= 1; --k) d[k - 1] = (k + 1 < n ? d[k + 1] : 0.0) + 2.0 * k * c[k];
+        d[0] *= 0.5;
+        return d;
+    }
+    V3 velocity_at(double t) const {
+        const double tau = (2.0 * t - (t_start + t_end)) / (t_end - t_start);
+        const double s = 2.0 / (t_end - t_start);
+        return {s * clenshaw(derivative(cx), tau), s * clenshaw(derivative(cy), tau), s * clenshaw(derivative(cz), tau)};
+    }
 };
 
 struct Body {
@@ -523,6 +537,20 @@ inline V3 body_position(const Body& b, double central_mu, double t) {  // :58-73
     throw CoverageError("ephemeris for body '" + b.name + "' does not cover epoch " + std::to_string(t), t);
 }
 
+/// EXTENSION (relativistic model): heliocentric position and velocity of a body.
+inline std::pair<V3, V3> body_state(const Body& b, double central_mu, double t) {
+    if (!b.tabulated) {
+        const State s = elements_to_state(b.el, central_mu, t);
+        return {s.r, s.v};
+    }
+    for (const auto& s : b.segs) {
+        const bool fwd = s.t_start <= s.t_end;
+        if ((fwd && t >= s.t_start && t <= s.t_end) || (!fwd && t <= s.t_start && t >= s.t_end))
+            return {s.position_at(t), s.velocity_at(t)};
+    }
+    throw CoverageError("ephemeris for body '" + b.name + "' does not cover epoch " + std::to_string(t), t);
+}
+
 struct EphTable {  // :77-86
     std::vector<double> node_times;
     double central_mu = 0.0;
@@ -530,7 +558,106 @@ struct EphTable {  // :77-86
     std::vector<double> mus;
     std::vector<Mat> pos;  // per body N x 3
     Index n_bodies() const { return static_cast<Index>(mus.size()); }
+    // EXTENSION (relativistic model): body velocities, Newtonian heliocentric
+    // accelerations and the potentials of the other massive bodies at each body, frozen per
+    // node like the positions.
+    bool rel = false;
+    double c_light = 0.0;
+    std::vector<Mat> vel, acc;           // per body N x 3
+    std::vector<std::vector<double>> phi;  // per body [N]: mu_sun/|r_b| + sum_{k!=b} mu_k/|r_k - r_b|
+    std::vector<double> phi_sun;         // [N]: sum_k mu_k/|r_k|
 };
+
+/// Massive-body quantities of the EIH test-particle equation at one epoch: positions,
+/// velocities, Newtonian heliocentric accelerations and external potentials (EXTENSION).
+struct RelBodies {
+    std::vector<V3> r, v, a;
+    std::vector<double> mu, phi;
+    double phi_sun = 0.0;
+};
+
+inline void rel_derive(RelBodies& q, double central_mu) {
+    const std::size_t B = q.r.size();
+    q.a.assign(B, V3{});
+    q.phi.assign(B, 0.0);
+    q.phi_sun = 0.0;
+    for (std::size_t b = 0; b < B; ++b) {
+        const double rb = q.r[b].norm();
+        q.phi_sun += q.mu[b] / rb;
+        V3 a = (-(central_mu + q.mu[b]) / (rb * rb * rb)) * q.r[b];
+        double phi = central_mu / rb;
+        for (std::size_t k = 0; k < B; ++k) {
+            if (k == b) continue;
+            const V3 d = q.r[k] - q.r[b];
+            const double dn = d.norm(), rk = q.r[k].norm();
+            a = a + q.mu[k] * (d / (dn * dn * dn) - q.r[k] / (rk * rk * rk));
+            phi += q.mu[k] / dn;
+        }
+        q.a[b] = a;
+        q.phi[b] = phi;
+    }
+}
+
+/// EXTENSION: first post-Newtonian (EIH, beta = gamma = 1) correction for a massless
+/// particle at r, v among the Sun (at the origin, at rest) and the bodies in q
+/// (Explanatory Supplement to the Astronomical Almanac 1992, eq. 8.1),
+/// textbook two-pass form.  The Newtonian part is added separately (table_acc).
+inline V3 eih_correction(V3 r, V3 v, const RelBodies& q, double central_mu, double c_light) {
+    const double c2 = c_light * c_light;
+    const std::size_t B = q.r.size();
+    auto at = [&](std::size_t A, V3& rA, V3& vA, V3& aA, double& muA, double& phiA) {
+        if (A == 0) {
+            rA = V3{};
+            vA = V3{};
+            aA = V3{};
+            muA = central_mu;
+            phiA = q.phi_sun;
+        } else {
+            rA = q.r[A - 1];
+            vA = q.v[A - 1];
+            aA = q.a[A - 1];
+            muA = q.mu[A - 1];
+            phiA = q.phi[A - 1];
+        }
+    };
+    double U = 0.0;  // potential of all massive bodies at the particle
+    for (std::size_t A = 0; A <= B; ++A) {
+        V3 rA, vA, aA;
+        double muA, phiA;
+        at(A, rA, vA, aA, muA, phiA);
+        U += muA / (r - rA).norm();
+    }
+    const double v2 = dot(v, v);
+    V3 out{};
+    for (std::size_t A = 0; A <= B; ++A) {
+        V3 rA, vA, aA;
+        double muA, phiA;
+        at(A, rA, vA, aA, muA, phiA);
+        const V3 d = rA - r;  // r_A - r
+        const double rho = d.norm();
+        const double rho3 = rho * rho * rho;
+        const double proj = dot(r - rA, vA) / rho;
+        const double bracket = -4.0 * U / c2 - phiA / c2 + v2 / c2 + 2.0 * dot(vA, vA) / c2 -
+                               4.0 * dot(v, vA) / c2 - 1.5 * proj * proj / c2 + 0.5 * dot(d, aA) / c2;
+        out = out + (muA / rho3 * bracket) * d;
+        out = out + (muA / rho3 * dot(r - rA, 4.0 * v - 3.0 * vA) / c2) * (v - vA);
+        out = out + (3.5 * muA / rho / c2) * aA;
+    }
+    return out;
+}
+
+/// Massive-body quantities of node j of a table (derived on first use from positions and
+/// velocities).
+inline RelBodies rel_at_node(const EphTable& t, Index j) {
+    RelBodies q;
+    for (Index b = 0; b < t.n_bodies(); ++b) {
+        q.r.push_back({t.pos[b](j, 0), t.pos[b](j, 1), t.pos[b](j, 2)});
+        q.v.push_back({t.vel[b](j, 0), t.vel[b](j, 1), t.vel[b](j, 2)});
+        q.mu.push_back(t.mus[b]);
+    }
+    rel_derive(q, t.central_mu);
+    return q;
+}
 
 inline EphTable build_ephemeris(const std::vector<Body>& bodies, const Grid& g, double central_mu) {  // :89-107
     EphTable t;
@@ -547,6 +674,54 @@ inline EphTable build_ephemeris(const std::vector<Body>& bodies, const Grid& g, 
         t.names.push_back(b.name);
         t.mus.push_back(b.mu);
         t.pos.push_back(std::move(p));
+    }
+    return t;
+}
+
+/// Massive-body quantities of node j read from a finished relativistic table.
+inline RelBodies rel_cached(const EphTable& t, Index j) {
+    RelBodies q;
+    for (Index b = 0; b < t.n_bodies(); ++b) {
+        q.r.push_back({t.pos[b](j, 0), t.pos[b](j, 1), t.pos[b](j, 2)});
+        q.v.push_back({t.vel[b](j, 0), t.vel[b](j, 1), t.vel[b](j, 2)});
+        q.a.push_back({t.acc[b](j, 0), t.acc[b](j, 1), t.acc[b](j, 2)});
+        q.mu.push_back(t.mus[b]);
+        q.phi.push_back(t.phi[b][j]);
+    }
+    q.phi_sun = t.phi_sun[j];
+    return q;
+}
+
+/// EXTENSION: the per-node table of the relativistic model (positions as above, plus
+/// velocities, accelerations and potentials).
+inline EphTable build_ephemeris_rel(const std::vector<Body>& bodies, const Grid& g, double central_mu,
+                                    double c_light) {
+    EphTable t = build_ephemeris(bodies, g, central_mu);
+    t.rel = true;
+    t.c_light = c_light;
+    const std::size_t B = bodies.size();
+    for (std::size_t b = 0; b < B; ++b) {
+        Mat v(g.n, 3);
+        for (Index j = 0; j < g.n; ++j) {
+            const V3 vb = body_state(bodies[b], central_mu, g.times[j]).second;
+            v(j, 0) = vb.x;
+            v(j, 1) = vb.y;
+            v(j, 2) = vb.z;
+        }
+        t.vel.push_back(std::move(v));
+        t.acc.emplace_back(g.n, 3);
+        t.phi.emplace_back(static_cast<std::size_t>(g.n), 0.0);
+    }
+    t.phi_sun.assign(static_cast<std::size_t>(g.n), 0.0);
+    for (Index j = 0; j < g.n; ++j) {
+        RelBodies q = rel_at_node(t, j);
+        for (std::size_t b = 0; b < B; ++b) {
+            t.acc[b](j, 0) = q.a[b].x;
+            t.acc[b](j, 1) = q.a[b].y;
+            t.acc[b](j, 2) = q.a[b].z;
+            t.phi[b][j] = q.phi[b];
+        }
+        t.phi_sun[j] = q.phi_sun;
     }
     return t;
 }
@@ -592,12 +767,16 @@ ChebSeg fit_segment(PosFn&& position, double t0, double t1, Index n) {  // :112-
 // ---------------------------------------------------------------------------
 // Force model (force_model.hpp:14-142)
 // ---------------------------------------------------------------------------
-enum class ForceKind { two_body, n_body };
+/// n_body_1pn = EXTENSION (BASELINE config 5; not in the reference): Newtonian
+/// restricted N-body + the EIH first post-Newtonian correction (eih_correction).
+enum class ForceKind { two_body, n_body, n_body_1pn };
+inline bool has_bodies(ForceKind k) { return k != ForceKind::two_body; }
 struct ForceConfig {
     ForceKind kind = ForceKind::two_body;
     double central_mu = 0.0;
     std::vector<Body> bodies;
     double proximity_floor_km = 1.0;
+    double c_light = 299792.458;  // km/s (relativistic model only)
 };
 
 inline V3 central_acc(V3 r, double mu) {  // :26-32
@@ -621,7 +800,7 @@ inline V3 perturber_acc(V3 r, V3 rb, double mu_b, double floor_km, const std::st
 
 inline V3 table_acc(V3 r, Index node, const EphTable& t, ForceKind kind, double floor_km) {  // :57-69
     V3 a = central_acc(r, t.central_mu);
-    if (kind == ForceKind::n_body) {
+    if (has_bodies(kind)) {
         for (Index b = 0; b < t.n_bodies(); ++b) {
             const V3 rb{t.pos[b](node, 0), t.pos[b](node, 1), t.pos[b](node, 2)};
             a = a + perturber_acc(r, rb, t.mus[b], floor_km, t.names[b]);
@@ -632,9 +811,26 @@ inline V3 table_acc(V3 r, Index node, const EphTable& t, ForceKind kind, double 
 
 inline V3 acceleration_at(V3 r, double t, const ForceConfig& cfg) {  // :78-87
     V3 a = central_acc(r, cfg.central_mu);
-    if (cfg.kind == ForceKind::n_body)
+    if (has_bodies(cfg.kind))
         for (const auto& b : cfg.bodies)
             a = a + perturber_acc(r, body_position(b, cfg.central_mu, t), b.mu, cfg.proximity_floor_km, b.name);
+    return a;
+}
+
+/// EXTENSION: continuous-time acceleration of the relativistic model (RKF78 cross-check).
+inline V3 acceleration_at(V3 r, V3 v, double t, const ForceConfig& cfg) {
+    V3 a = acceleration_at(r, t, cfg);
+    if (cfg.kind == ForceKind::n_body_1pn) {
+        RelBodies q;
+        for (const auto& b : cfg.bodies) {
+            const auto [rb, vb] = body_state(b, cfg.central_mu, t);
+            q.r.push_back(rb);
+            q.v.push_back(vb);
+            q.mu.push_back(b.mu);
+        }
+        rel_derive(q, cfg.central_mu);
+        a = a + eih_correction(r, v, q, cfg.central_mu, cfg.c_light);
+    }
     return a;
 }
 
@@ -656,6 +852,7 @@ inline void eval_force_block(const Mat& y, Index m, const Grid& g, const EphTabl
         V3 a;
         try {
             a = table_acc(r, j, t, cfg.kind, cfg.proximity_floor_km);
+            if (t.rel) a = a + eih_correction(r, v, rel_cached(t, j), t.central_mu, t.c_light);
         } catch (const SingularityError& e) {
             throw SingularityError("node " + std::to_string(j) + ", trajectory " + std::to_string(k) + ": " + e.what(),
                                    e.body);
@@ -922,7 +1119,11 @@ inline std::pair<Block, Report> solve_group(Block block, const Grid& g, const Op
 // ---------------------------------------------------------------------------
 // Propagator (propagator.hpp:24-347)
 // ---------------------------------------------------------------------------
-enum class StartMode { warm, cold };
+/// hot = EXTENSION (BASELINE config 3; excluded by the reference): segment 0 is
+/// warm; a later segment whose span equals the previous one starts from its own conic guess
+/// plus the previous segment's (converged - starting guess) correction per node (Macomber's
+/// hot start), otherwise warm.
+enum class StartMode { warm, cold, hot };
 enum class SegmentPolicy { single, per_orbit };
 enum class Direction { forward, backward };
 
@@ -974,6 +1175,15 @@ inline Mat warm_guess(const State& s, const Grid& g, double mu, bool* fell_back)
         *fell_back = true;
     }
     return out;
+}
+
+/// EXTENSION: a hot start applies to segment seg >= 1 whose span equals the previous span
+/// (to 1e-9 relative), so node j sits at the same phase of the representative orbit.
+inline bool hot_applies(const Segments& sp, Index seg) {
+    if (seg < 1) return false;
+    const double a = sp.boundaries[seg + 1] - sp.boundaries[seg];
+    const double b = sp.boundaries[seg] - sp.boundaries[seg - 1];
+    return std::abs(a - b) <= 1e-9 * std::abs(b);
 }
 
 inline Segments plan_segments(const State& rep, double t0, double t1, double mu, SegmentPolicy policy, Index n,
@@ -1063,11 +1273,15 @@ inline Result propagate(const std::vector<State>& states, const Plan& plan, cons
     res->times.assign(static_cast<std::size_t>(rows), 0.0);
     res->trajectories.assign(static_cast<std::size_t>(n_traj), Mat(rows, state_dim));
     std::vector<State> cur(states);
+    std::vector<Mat> base_prev(cfg.start_mode == StartMode::hot ? static_cast<std::size_t>(n_traj) : 0);
 
     for (Index seg = 0; seg < n_seg; ++seg) {
         const Grid g = build_grid(n, sp.boundaries[seg], sp.boundaries[seg + 1]);
-        const EphTable tab = build_ephemeris(
-            cfg.force.kind == ForceKind::n_body ? cfg.force.bodies : std::vector<Body>{}, g, cfg.force.central_mu);
+        const EphTable tab =
+            cfg.force.kind == ForceKind::n_body_1pn
+                ? build_ephemeris_rel(cfg.force.bodies, g, cfg.force.central_mu, cfg.force.c_light)
+                : build_ephemeris(has_bodies(cfg.force.kind) ? cfg.force.bodies : std::vector<Body>{}, g,
+                                  cfg.force.central_mu);
         std::vector<Mat> guesses(static_cast<std::size_t>(n_traj));
         if (seg == 0 && cfg.start_mode == StartMode::cold) {
             for (Index i = 0; i < n_traj; ++i) guesses[i] = cold_guess(cur[i], n);
@@ -1079,6 +1293,19 @@ inline Result propagate(const std::vector<State>& states, const Plan& plan, cons
                     res->warnings.push_back("segment " + std::to_string(seg) + ", trajectory " + std::to_string(i) +
                                             ": non-elliptic state, cold start used");
             }
+        }
+        // EXTENSION: hot start (see StartMode::hot)
+        std::vector<Mat> base_now;
+        if (cfg.start_mode == StartMode::hot) {
+            base_now = guesses;
+            if (hot_applies(sp, seg))
+                for (Index i = 0; i < n_traj; ++i) {
+                    const Mat& prev = res->trajectories[i];
+                    const Index prow = (seg - 1) * (n - 1);
+                    for (Index j = 0; j < n; ++j)
+                        for (Index c = 0; c < state_dim; ++c)
+                            guesses[i](j, c) += prev(prow + j, c) - base_prev[i](j, c);
+                }
         }
         const Index P = plan.groups();
         std::vector<Block> blocks(static_cast<std::size_t>(P));
@@ -1124,6 +1351,7 @@ inline Result propagate(const std::vector<State>& states, const Plan& plan, cons
             cur[i].r = {tr(last, 0), tr(last, 1), tr(last, 2)};
             cur[i].v = {tr(last, 3), tr(last, 4), tr(last, 5)};
         }
+        if (cfg.start_mode == StartMode::hot) base_prev = std::move(base_now);
     }
     res->terminal_states = std::move(cur);
     return std::move(*res);
@@ -1235,7 +1463,7 @@ inline ForceConfig reference_force(ForceKind kind = ForceKind::n_body) {  // :36
     ForceConfig c;
     c.kind = kind;
     c.central_mu = mu_sun;
-    if (kind == ForceKind::n_body) c.bodies = reference_bodies();
+    if (has_bodies(kind)) c.bodies = reference_bodies();
     return c;
 }
 
@@ -1397,7 +1625,7 @@ inline double compare_trajectories(const Mat& cand, const Mat& ref) {
 /// Newtonian derivative callback for rk_propagate (state -> [v, a(r, t)]).
 inline auto nbody_deriv(const ForceConfig& cfg) {
     return [&cfg](double t, const S6& y) {
-        const V3 a = acceleration_at({y[0], y[1], y[2]}, t, cfg);
+        const V3 a = acceleration_at({y[0], y[1], y[2]}, {y[3], y[4], y[5]}, t, cfg);
         return S6{y[3], y[4], y[5], a.x, a.y, a.z};
     };
 }

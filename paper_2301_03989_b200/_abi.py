@@ -81,6 +81,7 @@ class PswarmConfig(C.Structure):
         ("proximity_floor_km", C.c_double),
         ("p_groups", C.c_int64),
         ("timeout_s", C.c_double),
+        ("c_light", C.c_double),
     ]
 
 

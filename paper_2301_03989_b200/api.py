@@ -100,6 +100,10 @@ class BodySpec:
     segments: Optional[list] = None
 
 
+FORCE_KINDS = {"two_body": 0, "n_body": 1, "n_body_1pn": 2}  # n_body_1pn: EXTENSION (EIH 1PN)
+START_MODES = {"warm": 0, "cold": 1, "hot": 2}  # hot: EXTENSION (Macomber hot start)
+
+
 @dataclass
 class PropagationConfig:
     """PropagationConfig + ForceModelConfig (propagator.hpp:38-49, force_model.hpp:17-24)."""
@@ -116,6 +120,7 @@ class PropagationConfig:
     proximity_floor_km: float = 1.0
     p_groups: int = 1
     timeout_s: float = 0.0
+    c_light: float = 299792.458  # km/s, force_kind "n_body_1pn" only (EXTENSION)
 
 
 @dataclass
@@ -208,7 +213,7 @@ class _ConfigMarshal:
     """Keeps the ctypes view of a PropagationConfig (and its arrays) alive."""
 
     def __init__(self, cfg: PropagationConfig):
-        bodies = list(cfg.bodies) if cfg.force_kind == "n_body" else list(cfg.bodies)
+        bodies = list(cfg.bodies)
         self.keep = []
         arr = (_abi.PswarmBody * max(1, len(bodies)))()
         for k, b in enumerate(bodies):
@@ -241,16 +246,17 @@ class _ConfigMarshal:
         c.tolerance = cfg.tolerance
         c.error_mode = 1 if cfg.error_mode == "absolute" else 0
         c.max_iterations = cfg.max_iterations
-        c.start_mode = 1 if cfg.start_mode == "cold" else 0
+        c.start_mode = START_MODES[cfg.start_mode]
         c.segment_policy = 1 if cfg.segment_policy == "per_orbit" else 0
         c.max_segment_periods = cfg.max_segment_periods
-        c.force_kind = 1 if cfg.force_kind == "n_body" else 0
+        c.force_kind = FORCE_KINDS[cfg.force_kind]
         c.n_bodies = len(bodies)
         c.central_mu = cfg.central_mu
         c.bodies = C.cast(arr, C.POINTER(_abi.PswarmBody))
         c.proximity_floor_km = cfg.proximity_floor_km
         c.p_groups = cfg.p_groups
         c.timeout_s = cfg.timeout_s
+        c.c_light = cfg.c_light
         self.cfg = c
 
 
@@ -427,7 +433,7 @@ class Context:
         names = (C.c_char_p * max(1, B))(*[n.encode() for n in (body_names or [""] * B)])
         out = np.zeros_like(yy)
         err = _abi.PswarmError()
-        kind = 1 if force_kind == "n_body" else 0
+        kind = FORCE_KINDS[force_kind]
         _check(self.lib.pswarm_eval_force_block(self.ptr, N, group_size, _abi.dptr(yy), omega2, kind, central_mu, B,
                                                 _abi.dptr(pos), _abi.dptr(mus), names, proximity_floor_km,
                                                 _abi.dptr(out), C.byref(err)), err)
@@ -548,7 +554,7 @@ def planets8() -> List[BodySpec]:
 def reference_force_config(kind="n_body", bodies=None, **kw) -> PropagationConfig:
     """make_reference_force_model (synthetic.hpp:36-44) folded into a PropagationConfig."""
     cfg = PropagationConfig(force_kind=kind, central_mu=MU_SUN, **kw)
-    if kind == "n_body":
+    if kind != "two_body":
         cfg.bodies = list(bodies) if bodies is not None else reference_bodies()
     return cfg
 

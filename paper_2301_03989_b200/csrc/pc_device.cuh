@@ -140,6 +140,49 @@ __device__ __forceinline__ int elements_position(const double* el, double mu, do
     return CONIC_OK;
 }
 
+/// Position and velocity of an analytic body (elements_to_state, kepler.hpp:102-131);
+/// the velocity feeds the relativistic model only (EXTENSION).
+__device__ __forceinline__ int elements_state(const double* el, double mu, double t, double r[3], double v[3],
+                                              double* m_fail) {
+    const double a = el[0], e = el[1], inc = el[2], raan = el[3], argp = el[4], m0 = el[5], ep = el[6];
+    const double n = sqrt(mu / (a * a * a));
+    const double m = m0 + n * (t - ep);
+    double ea;
+    if (solve_kepler(m, e, &ea) != CONIC_OK) {
+        *m_fail = m;
+        return CONIC_SOLVER;
+    }
+    double se, ce, so, co, si, ci, sw, cw;
+    sincos(ea, &se, &ce);
+    sincos(raan, &so, &co);
+    sincos(inc, &si, &ci);
+    sincos(argp, &sw, &cw);
+    const double beta = sqrt(1.0 - e * e);
+    const double rn = a * (1.0 - e * ce);
+    const double xp = a * (ce - e), yp = a * beta * se;
+    const double vs = sqrt(mu * a) / rn;
+    const double vxp = -vs * se, vyp = vs * beta * ce;
+    const double p[3] = {co * cw - so * sw * ci, so * cw + co * sw * ci, sw * si};
+    const double q[3] = {-co * sw - so * cw * ci, -so * sw + co * cw * ci, cw * si};
+    for (int c = 0; c < 3; ++c) {
+        r[c] = xp * p[c] + yp * q[c];
+        v[c] = vxp * p[c] + vyp * q[c];
+    }
+    return CONIC_OK;
+}
+
+/// d/dx of a Chebyshev series: sum_k k c_k U_{k-1}(x) by Clenshaw on the U recurrence
+/// (EXTENSION: velocities of tabulated bodies for the relativistic model).
+__device__ __forceinline__ double clenshaw_deriv(const double* c, int nc, double x) {
+    double b1 = 0.0, b2 = 0.0;
+    for (int k = nc - 1; k >= 1; --k) {
+        const double b0 = k * c[k] + 2.0 * x * b1 - b2;
+        b2 = b1;
+        b1 = b0;
+    }
+    return b1;
+}
+
 /// Clenshaw evaluation of a Chebyshev series (ephemeris.hpp:29-38).
 __device__ __forceinline__ double clenshaw(const double* c, int nc, double x) {
     double b1 = 0.0, b2 = 0.0;
@@ -187,7 +230,60 @@ struct ForceData {
     double floor_km;
     double floor2_hi;  // floor^2 * (1 + 1e-9): cheap pre-test before the exact sqrt compare
     int n_bodies;      // 0 for two-body
+    int rel;           // 1: n_body_1pn (EXTENSION) -> add rel_correction()
+    double ic2;        // 1 / c^2 (km^-2 s^2)
+    const double* rel_tab;  // [N][B+1][REL_W]: Sun + bodies at each node (k_ephemeris)
 };
+
+// ------------------------------------------------------- relativistic (EXTENSION) ---
+/// Row of the per-node relativistic table: massive body A (A = 0 Sun at the origin)
+/// position, velocity, Newtonian heliocentric acceleration, mu and
+/// K_A = (2 v_A^2 - phi_A) / c^2 with phi_A the potential of the other massive bodies at A.
+constexpr int REL_W = 12;
+
+/// First post-Newtonian (EIH, beta = gamma = 1) correction for a massless particle
+/// (Explanatory Supplement 1992 eq. 8.1) in one pass over the massive
+/// bodies: the -4U/c^2 and v^2/c^2 terms factor out of the Newtonian sum, so
+///   da = (v^2 - 4U)/c^2 a_N + sum_A g_A [K_A - (4 v.v_A + 1.5 (d.v_A)^2/rho^2 - 0.5 d.a_A)/c^2] d
+///        + 1/c^2 sum_A g_A (-d.(4v - 3v_A)) (v - v_A) + 3.5/c^2 sum_A mu_A a_A / rho,
+/// d = r_A - r, g_A = mu_A / rho^3.  The oracle evaluates the textbook two-pass form.
+static __device__ __noinline__ void rel_correction(double rx, double ry, double rz, double vx, double vy, double vz,
+                                            const double* __restrict__ tab, int nb1, double ic2, double* out) {
+    double U = 0.0, nx = 0.0, ny = 0.0, nz = 0.0, bx = 0.0, by = 0.0, bz = 0.0;
+    double wx = 0.0, wy = 0.0, wz = 0.0, qx = 0.0, qy = 0.0, qz = 0.0;
+    for (int A = 0; A < nb1; ++A) {
+        const double* t = tab + A * REL_W;
+        const double dx = t[0] - rx, dy = t[1] - ry, dz = t[2] - rz;
+        const double d2 = dx * dx + dy * dy + dz * dz;
+        const double ir = rsqrt_nr(d2);
+        const double mu = t[9];
+        const double g = mu * ir * ir * ir;
+        U += mu * ir;
+        nx += g * dx;
+        ny += g * dy;
+        nz += g * dz;
+        const double vax = t[3], vay = t[4], vaz = t[5];
+        const double vva = vx * vax + vy * vay + vz * vaz;
+        const double dva = dx * vax + dy * vay + dz * vaz;
+        const double daa = dx * t[6] + dy * t[7] + dz * t[8];
+        const double br = g * (t[10] - ic2 * (4.0 * vva + 1.5 * dva * dva * (ir * ir) - 0.5 * daa));
+        bx += br * dx;
+        by += br * dy;
+        bz += br * dz;
+        const double w = -g * (dx * (4.0 * vx - 3.0 * vax) + dy * (4.0 * vy - 3.0 * vay) + dz * (4.0 * vz - 3.0 * vaz));
+        wx += w * (vx - vax);
+        wy += w * (vy - vay);
+        wz += w * (vz - vaz);
+        const double m = mu * ir;
+        qx += m * t[6];
+        qy += m * t[7];
+        qz += m * t[8];
+    }
+    const double f = ic2 * (vx * vx + vy * vy + vz * vz - 4.0 * U);
+    out[0] = f * nx + bx + ic2 * wx + 3.5 * ic2 * qx;
+    out[1] = f * ny + by + ic2 * wy + 3.5 * ic2 * qy;
+    out[2] = f * nz + bz + ic2 * wz + 3.5 * ic2 * qz;
+}
 
 /// Acceleration at node j (force_model.hpp:57-69).  Returns -1 when finite and legal,
 /// else the index of the first failing check in reference order: 0 = central body

@@ -113,7 +113,7 @@ int extra_rows(int N, const GemmPlan& gp) {
     return r > 0 ? r : 0;
 }
 
-template <int MAXT, int XM, bool STAGE, int FS>
+template <int MAXT, int XM, bool STAGE, int FS, bool REL>
 __global__ void __launch_bounds__(MAXT, 1) k_pc_segment(const SegArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int N = a.N;
@@ -270,10 +270,10 @@ __global__ void __launch_bounds__(MAXT, 1) k_pc_segment(const SegArgs a) {
                 const int jq = it0 / (SLOTS / FS), t0 = (it0 % (SLOTS / FS)) * FS;
                 if (tid < extra) {
                     const int sx = nthr * FS + tid;
-                    force_chains<FS, true>(a.fd, a.omega2, ybuf, fbuf, st.sing_key, pos_base, ind_base, act, jq, t0,
+                    force_chains<FS, true, REL>(a.fd, a.omega2, ybuf, fbuf, st.sing_key, pos_base, ind_base, act, jq, t0,
                                            sx >> 3, sx & 7);
                 } else {
-                    force_chains<FS, false>(a.fd, a.omega2, ybuf, fbuf, st.sing_key, pos_base, ind_base, act, jq, t0,
+                    force_chains<FS, false, REL>(a.fd, a.omega2, ybuf, fbuf, st.sing_key, pos_base, ind_base, act, jq, t0,
                                             0, 0);
                 }
             }
@@ -571,7 +571,8 @@ __global__ void __launch_bounds__(MAXT, 1) k_pc_segment(const SegArgs a) {
 
 template <int MAXT, int XM, int FS>
 static cudaError_t launch_segment_t(const SegArgs& a, int grid, size_t smem, cudaStream_t s) {
-    auto kern = a.stage_eph ? k_pc_segment<MAXT, XM, true, FS> : k_pc_segment<MAXT, XM, false, FS>;
+    auto kern = a.fd.rel ? k_pc_segment<MAXT, XM, false, FS, true>
+                         : (a.stage_eph ? k_pc_segment<MAXT, XM, true, FS, false> : k_pc_segment<MAXT, XM, false, FS, false>);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     kern<<<grid, 32 * a.gp.warps, smem, s>>>(a);
@@ -591,15 +592,18 @@ cudaError_t launch_segment(const SegArgs& a, int grid, cudaStream_t s) {
 // ============================================================== ephemeris ==
 
 __global__ void k_ephemeris(int N, const double* __restrict__ times, double central_mu, BodyTable bt,
-                            double* __restrict__ pos, double* __restrict__ indirect, unsigned long long* fault_key) {
+                            double* __restrict__ pos, double* __restrict__ indirect, unsigned long long* fault_key,
+                            double* __restrict__ vel, double* __restrict__ rel_tab, double ic2) {
     const int j = blockIdx.x, b = threadIdx.x;
     const double t = times[j];
+    const bool rel = rel_tab != nullptr;
     if (b < bt.B) {
-        double p[3] = {0.0, 0.0, 0.0};
+        double p[3] = {0.0, 0.0, 0.0}, v[3] = {0.0, 0.0, 0.0};
         if (bt.kind[b] == 0) {
             double mf;
-            if (elements_position(bt.elements + 7 * b, central_mu, t, p, &mf) != CONIC_OK)
-                atomicMin(fault_key, (static_cast<unsigned long long>(b) * N + j) * 4ull + 3ull);
+            const int st = rel ? elements_state(bt.elements + 7 * b, central_mu, t, p, v, &mf)
+                               : elements_position(bt.elements + 7 * b, central_mu, t, p, &mf);
+            if (st != CONIC_OK) atomicMin(fault_key, (static_cast<unsigned long long>(b) * N + j) * 4ull + 3ull);
         } else {
             int hit = -1;
             for (int sg = bt.seg_off[b]; sg < bt.seg_off[b + 1]; ++sg) {
@@ -618,12 +622,20 @@ __global__ void k_ephemeris(int N, const double* __restrict__ times, double cent
                 const int nc = bt.ncoef[b];
                 const double* c = bt.coeffs + bt.coeff_off[hit];
                 for (int k = 0; k < 3; ++k) p[k] = clenshaw(c + k * nc, nc, tau);
+                if (rel)
+                    for (int k = 0; k < 3; ++k) v[k] = (2.0 / (t1 - t0)) * clenshaw_deriv(c + k * nc, nc, tau);
             }
         }
         double* o = pos + (static_cast<size_t>(j) * bt.B + b) * 3;
         o[0] = p[0];
         o[1] = p[1];
         o[2] = p[2];
+        if (rel) {
+            double* w = vel + (static_cast<size_t>(j) * bt.B + b) * 3;
+            w[0] = v[0];
+            w[1] = v[1];
+            w[2] = v[2];
+        }
     }
     __syncthreads();
     if (b == 0) {  // fixed summation order over bodies (deterministic)
@@ -637,13 +649,55 @@ __global__ void k_ephemeris(int N, const double* __restrict__ times, double cent
         }
         for (int c = 0; c < 3; ++c) indirect[j * 3 + c] = s[c];
     }
+    if (rel && b <= bt.B) {
+        // EXTENSION: relativistic node table row A = b (0 = Sun): Newtonian heliocentric
+        // acceleration of body A and the potential of the other massive bodies at A
+        const double* P = pos + static_cast<size_t>(j) * bt.B * 3;
+        double* row = rel_tab + (static_cast<size_t>(j) * (bt.B + 1) + b) * REL_W;
+        double r[3] = {0.0, 0.0, 0.0}, v[3] = {0.0, 0.0, 0.0}, acc[3] = {0.0, 0.0, 0.0}, phi = 0.0, mu = central_mu;
+        if (b == 0) {
+            for (int k = 0; k < bt.B; ++k) {
+                const double* q = P + 3 * k;
+                phi += bt.mu[k] / sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2]);
+            }
+        } else {
+            const int bb = b - 1;
+            mu = bt.mu[bb];
+            for (int c = 0; c < 3; ++c) {
+                r[c] = P[3 * bb + c];
+                v[c] = vel[(static_cast<size_t>(j) * bt.B + bb) * 3 + c];
+            }
+            const double rb = sqrt(r[0] * r[0] + r[1] * r[1] + r[2] * r[2]);
+            const double k0 = -(central_mu + mu) / (rb * rb * rb);
+            for (int c = 0; c < 3; ++c) acc[c] = k0 * r[c];
+            phi = central_mu / rb;
+            for (int k = 0; k < bt.B; ++k) {
+                if (k == bb) continue;
+                const double* q = P + 3 * k;
+                const double d[3] = {q[0] - r[0], q[1] - r[1], q[2] - r[2]};
+                const double dn = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+                const double rk = sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2]);
+                for (int c = 0; c < 3; ++c) acc[c] += bt.mu[k] * (d[c] / (dn * dn * dn) - q[c] / (rk * rk * rk));
+                phi += bt.mu[k] / dn;
+            }
+        }
+        for (int c = 0; c < 3; ++c) {
+            row[c] = r[c];
+            row[3 + c] = v[c];
+            row[6 + c] = acc[c];
+        }
+        row[9] = mu;
+        row[10] = ic2 * (2.0 * (v[0] * v[0] + v[1] * v[1] + v[2] * v[2]) - phi);
+        row[11] = 0.0;
+    }
 }
 
 cudaError_t launch_ephemeris(int N, const double* times, double central_mu, const BodyTable& bt, double* pos,
-                             double* indirect, unsigned long long* fault_key, cudaStream_t s) {
-    if (bt.B <= 0) return cudaSuccess;
-    const int threads = 32 * ((bt.B + 31) / 32);
-    k_ephemeris<<<N, threads, 0, s>>>(N, times, central_mu, bt, pos, indirect, fault_key);
+                             double* indirect, unsigned long long* fault_key, double* vel, double* rel_tab, double ic2,
+                             cudaStream_t s) {
+    if (bt.B <= 0 && rel_tab == nullptr) return cudaSuccess;
+    const int threads = 32 * ((bt.B + 1 + 31) / 32);
+    k_ephemeris<<<N, threads, 0, s>>>(N, times, central_mu, bt, pos, indirect, fault_key, vel, rel_tab, ic2);
     return cudaGetLastError();
 }
 

@@ -93,8 +93,11 @@ struct BodyTable {
 /// Frozen per-segment ephemeris on the device: body positions [N][B][3] at the node
 /// times and the indirect term [N][3] (ephemeris.hpp:89-107, force_model.hpp:50-51).
 /// fault_key = min over (body, node) of (b*N + j)*4 + kind (1 coverage, 3 solver).
+/// Relativistic model (EXTENSION, rel_tab != nullptr): also body velocities vel [N][B][3]
+/// and the node table rel_tab [N][B+1][REL_W] (Sun row first).
 cudaError_t launch_ephemeris(int N, const double* times, double central_mu, const BodyTable& bt, double* pos,
-                             double* indirect, unsigned long long* fault_key, cudaStream_t s);
+                             double* indirect, unsigned long long* fault_key, double* vel, double* rel_tab, double ic2,
+                             cudaStream_t s);
 
 /// Arguments of the wide-group path (groups larger than one CTA's 8 slots).
 struct WideArgs {

@@ -199,6 +199,7 @@ __device__ __forceinline__ void gemm_half(const double2* __restrict__ upack, int
 }
 
 /// Force of half h for node j, its 4 slots as independent chains (force_model.hpp:93-142).
+template <bool REL>
 __device__ __forceinline__ void force_half(const ForceData& fd, double w2, const double* ybuf, double* fb, int* sing_key,
                                            const double* pos_base, const double* ind_base, int act_h, int h, int j) {
     const int B = fd.n_bodies;
@@ -255,6 +256,18 @@ __device__ __forceinline__ void force_half(const ForceData& fd, double w2, const
             az[s] -= iz;
         }
     }
+    if (REL) {  // EXTENSION: EIH 1PN correction (n_body_1pn)
+        const double* rt = fd.rel_tab + static_cast<size_t>(j) * (B + 1) * REL_W;
+        for (int s = 0; s < HS; ++s) {
+            if (!on[s]) continue;
+            double o[3];
+            rel_correction(rx[s], ry[s], rz[s], ybuf[y2(j, h, 3, s)], ybuf[y2(j, h, 4, s)], ybuf[y2(j, h, 5, s)], rt,
+                           B + 1, fd.ic2, o);
+            ax[s] += o[0];
+            ay[s] += o[1];
+            az[s] += o[2];
+        }
+    }
     if (flag) {  // rare: exact guard order of table_acceleration (force_model.hpp:57-69)
 #pragma unroll
         for (int s = 0; s < HS; ++s) {
@@ -291,7 +304,7 @@ int ws_extra_rows(int N) {
     return r > 0 ? r : 0;
 }
 
-template <int MAIN, int XMW, bool STAGE>
+template <int MAIN, int XMW, bool STAGE, bool REL>
 __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int N = a.N, B = a.fd.n_bodies;
@@ -697,7 +710,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
             const int act_h = (am >> (h * HS)) & 0xF;
             if (act_h)
                 for (int j = ft; j < N; j += FP_THREADS)
-                    force_half(a.fd, a.omega2, ybuf, reinterpret_cast<double*>(smem_raw + L.fbuf0 + h * fb_bytes),
+                    force_half<REL>(a.fd, a.omega2, ybuf, reinterpret_cast<double*>(smem_raw + L.fbuf0 + h * fb_bytes),
                                st.sing_key, pos_base, ind_base, act_h, h, j);
             bar_sync(BAR_FP, FP_THREADS);
             if (ft < HS && st.sing_key[h * HS + ft] != INT_MAX) {
@@ -716,9 +729,14 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
                 if (ft < B0_PARTS * HC) {
                     const int col = ft % HC, part = ft / HC;
                     const int c = 2 * (col >> 3) + (col & 1), s = (col & 7) >> 1;
-                    double sum = 0.0;
-                    for (int j = part; j < N; j += B0_PARTS) sum = fma(anc[j], fbh[f2(j, c, s)], sum);
-                    b0part[part * HC + col] = sum;
+                    double s0 = 0.0, s1 = 0.0;  // two chains: latency under the DMMA stream
+                    int j = part;
+                    for (; j + B0_PARTS < N; j += 2 * B0_PARTS) {
+                        s0 = fma(anc[j], fbh[f2(j, c, s)], s0);
+                        s1 = fma(anc[j + B0_PARTS], fbh[f2(j + B0_PARTS, c, s)], s1);
+                    }
+                    if (j < N) s0 = fma(anc[j], fbh[f2(j, c, s)], s0);
+                    b0part[part * HC + col] = s0 + s1;
                 }
                 bar_sync(BAR_FP, FP_THREADS);
                 if (ft < HC) {
@@ -745,7 +763,9 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
 
 template <int MAIN, int XMW>
 static cudaError_t launch_ws_t(const SegArgs& a, int grid, size_t smem, cudaStream_t s) {
-    auto kern = a.stage_eph ? k_pc_ws<MAIN, XMW, true> : k_pc_ws<MAIN, XMW, false>;
+    // relativistic launches never stage the ephemeris (the host clears stage_eph)
+    auto kern = a.fd.rel ? k_pc_ws<MAIN, XMW, false, true>
+                         : (a.stage_eph ? k_pc_ws<MAIN, XMW, true, false> : k_pc_ws<MAIN, XMW, false, false>);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     kern<<<grid, WS_THREADS, smem, s>>>(a);

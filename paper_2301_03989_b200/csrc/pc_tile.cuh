@@ -48,7 +48,7 @@ __device__ __forceinline__ void update_sample(const double (&yn)[6], const doubl
 /// independent chains: a = -mu r/|r|^3 + sum_b mu_b (d_b/|d_b|^3) - indirect(j),
 /// F = omega2 [v; a] written in MMA B-fragment order (force_model.hpp:93-142).
 /// Singularity guards run exactly, in reference order, on a rare slow path.
-template <int FS, bool X>
+template <int FS, bool X, bool REL = false>
 __device__ __forceinline__ void force_chains(const ForceData& fd, double w2, const double* ybuf, double* fbuf,
                                              int* sing_key, const double* pos_base, const double* ind_base, int act,
                                              int jq, int t0, int jx, int tx) {
@@ -129,6 +129,18 @@ __device__ __forceinline__ void force_chains(const ForceData& fd, double w2, con
             ax[k] -= ind[0];
             ay[k] -= ind[1];
             az[k] -= ind[2];
+        }
+    }
+    if (REL) {  // EXTENSION: EIH 1PN correction (n_body_1pn)
+        for (int k = 0; k < K; ++k) {
+            if (!on[k]) continue;
+            double o[3];
+            rel_correction(rx[k], ry[k], rz[k], ybuf[yidx(jj[k], 3, tt[k])], ybuf[yidx(jj[k], 4, tt[k])],
+                           ybuf[yidx(jj[k], 5, tt[k])], fd.rel_tab + static_cast<size_t>(jj[k]) * (B + 1) * REL_W,
+                           B + 1, fd.ic2, o);
+            ax[k] += o[0];
+            ay[k] += o[1];
+            az[k] += o[2];
         }
     }
     if (flag) {  // rare: exact guard order of table_acceleration (force_model.hpp:57-69)

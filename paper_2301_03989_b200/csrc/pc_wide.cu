@@ -69,7 +69,7 @@ __global__ void k_wide_start(WideArgs a) {
 }
 
 /// One Picard iteration of every tile whose slots belong to active groups.
-template <int MAXT, int XM>
+template <int MAXT, int XM, bool REL>
 __global__ void __launch_bounds__(MAXT, 1) k_wide_iter(WideArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int N = a.N, B = a.fd.n_bodies;
@@ -123,10 +123,10 @@ __global__ void __launch_bounds__(MAXT, 1) k_wide_iter(WideArgs a) {
                 const int jq = it0 / (SLOTS / FS), t0 = (it0 % (SLOTS / FS)) * FS;
                 if (tid < extra) {
                     const int sx = nthr * FS + tid;
-                    force_chains<FS, true>(a.fd, a.omega2, ybuf, fbuf, ws.sing_key, a.fd.body_pos, a.fd.indirect, act,
+                    force_chains<FS, true, REL>(a.fd, a.omega2, ybuf, fbuf, ws.sing_key, a.fd.body_pos, a.fd.indirect, act,
                                            jq, t0, sx >> 3, sx & 7);
                 } else {
-                    force_chains<FS, false>(a.fd, a.omega2, ybuf, fbuf, ws.sing_key, a.fd.body_pos, a.fd.indirect, act,
+                    force_chains<FS, false, REL>(a.fd, a.omega2, ybuf, fbuf, ws.sing_key, a.fd.body_pos, a.fd.indirect, act,
                                             jq, t0, 0, 0);
                 }
             }
@@ -329,25 +329,20 @@ cudaError_t launch_wide_start(const WideArgs& a, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+template <int MAXT, int XM>
+static cudaError_t launch_wide_iter_t(const WideArgs& a, int grid, size_t smem, cudaStream_t s) {
+    auto kern = a.fd.rel ? k_wide_iter<MAXT, XM, true> : k_wide_iter<MAXT, XM, false>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    kern<<<grid, 32 * a.gp.warps, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_wide_iter(const WideArgs& a, int grid, cudaStream_t s) {
     const size_t smem = wide_smem_bytes(a.N, a.nkp, a.xrows);
-    if (a.gp.xmax == XMAX_SMALL) {
-        cudaError_t e = cudaFuncSetAttribute(k_wide_iter<128, XMAX_SMALL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(smem));
-        if (e != cudaSuccess) return e;
-        k_wide_iter<128, XMAX_SMALL><<<grid, 32 * a.gp.warps, smem, s>>>(a);
-    } else if (a.gp.warps <= 12) {
-        cudaError_t e = cudaFuncSetAttribute(k_wide_iter<384, XMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(smem));
-        if (e != cudaSuccess) return e;
-        k_wide_iter<384, XMAX><<<grid, 32 * a.gp.warps, smem, s>>>(a);
-    } else {
-        cudaError_t e = cudaFuncSetAttribute(k_wide_iter<512, XMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(smem));
-        if (e != cudaSuccess) return e;
-        k_wide_iter<512, XMAX><<<grid, 32 * a.gp.warps, smem, s>>>(a);
-    }
-    return cudaGetLastError();
+    if (a.gp.xmax == XMAX_SMALL) return launch_wide_iter_t<128, XMAX_SMALL>(a, grid, smem, s);
+    if (a.gp.warps <= 12) return launch_wide_iter_t<384, XMAX>(a, grid, smem, s);
+    return launch_wide_iter_t<512, XMAX>(a, grid, smem, s);
 }
 
 cudaError_t launch_wide_finalize(const WideArgs& a, cudaStream_t s) {

@@ -146,7 +146,7 @@ enum BufId {
     B_OP_IN, B_OP_IN2, B_OP_OUT, B_OP_AUX, B_OP_KEY,
     B_BT_KIND, B_BT_SOFF, B_BT_NC, B_BT_EL, B_BT_BND, B_BT_COFF, B_BT_CF, B_PHASES,
     B_W_TG, B_W_Y, B_W_ACT, B_W_ITER, B_W_ERR, B_W_NF, B_W_SING, B_W_TSK, B_W_TSV, B_W_WK, B_W_CNT,
-    B_IN_PACK, B_REPORT, B_COUNT
+    B_IN_PACK, B_REPORT, B_BODY_VEL, B_REL_TAB, B_HOT, B_COUNT
 };
 
 /// Page-locked host staging (grow-only): every host<->device transfer of a solve goes
@@ -437,7 +437,13 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
     bind(ctx);
     const OpPack& op = operators(ctx, N);
     const int max_it = std::max(cfg->max_iterations, 0);
-    const int nb = cfg->force_kind == 1 ? cfg->n_bodies : 0;
+    if (cfg->force_kind < 0 || cfg->force_kind > 2)
+        raise(PSWARM_ERR_INVALID_PLAN, "propagate: unknown force kind " + std::to_string(cfg->force_kind));
+    if (cfg->start_mode < 0 || cfg->start_mode > 2)
+        raise(PSWARM_ERR_INVALID_PLAN, "propagate: unknown start mode " + std::to_string(cfg->start_mode));
+    const bool rel = cfg->force_kind == 2;  // EXTENSION: n_body + EIH 1PN
+    const double c_light = cfg->c_light > 0.0 ? cfg->c_light : 299792.458;
+    const int nb = cfg->force_kind >= 1 ? cfg->n_bodies : 0;
     if (nb > 63) raise(PSWARM_ERR_INVALID_SIZE, "propagate: at most 63 perturbing bodies are supported");
     const BodyUpload bu = flatten_bodies(*cfg, nb);
 
@@ -548,7 +554,7 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
     ctx->last_kernel = wide ? "k_wide_iter" : use_ws ? "k_pc_ws" : "k_pc_segment";
     // stage the frozen ephemeris in shared memory when it fits next to the state blocks
     const int stage_eph =
-        nb > 0 && (use_ws ? ws_smem_bytes(Ni, op.nkp, xrows, nb, 1) : segment_smem_bytes(Ni, op.nkp, xrows, nb, 1)) <=
+        nb > 0 && !rel && (use_ws ? ws_smem_bytes(Ni, op.nkp, xrows, nb, 1) : segment_smem_bytes(Ni, op.nkp, xrows, nb, 1)) <=
                       SMEM_MAX
             ? 1
             : 0;
@@ -576,6 +582,14 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
         d_pos = ctx->buf[B_BODY_POS].get<double>(static_cast<size_t>(N) * nb * 3);
         d_ind = ctx->buf[B_INDIRECT].get<double>(static_cast<size_t>(N) * 3);
     }
+    double *d_vel = nullptr, *d_rel = nullptr;
+    if (rel) {  // EXTENSION: body velocities + per-node relativistic table (Sun row first)
+        bt.B = nb;
+        d_vel = ctx->buf[B_BODY_VEL].get<double>(static_cast<size_t>(N) * std::max(nb, 1) * 3);
+        d_rel = ctx->buf[B_REL_TAB].get<double>(static_cast<size_t>(N) * (nb + 1) * REL_W);
+        if (!d_pos) d_pos = ctx->buf[B_BODY_POS].get<double>(static_cast<size_t>(N) * 3);
+        if (!d_ind) d_ind = ctx->buf[B_INDIRECT].get<double>(static_cast<size_t>(N) * 3);
+    }
     unsigned long long* d_phase = nullptr;
     if (ctx->profile_phases) {
         d_phase = ctx->buf[B_PHASES].get<unsigned long long>(PHASES);
@@ -602,8 +616,9 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
         const double* d_times = reinterpret_cast<const double*>(din + o_times) + seg * N;
         cuda_check(cudaMemsetAsync(drep, 0, r_zero, st), "memset reports");
         cuda_check(cudaMemsetAsync(d_ekey, 0xff, sizeof(unsigned long long), st), "memset");
-        if (nb > 0) {  // frozen per-node ephemeris of this segment, evaluated on the device
-            cuda_check(launch_ephemeris(static_cast<int>(N), d_times, cfg->central_mu, bt, d_pos, d_ind, d_ekey, st),
+        if (nb > 0 || rel) {  // frozen per-node ephemeris of this segment, evaluated on the device
+            cuda_check(launch_ephemeris(static_cast<int>(N), d_times, cfg->central_mu, bt, d_pos, d_ind, d_ekey, d_vel,
+                                        d_rel, 1.0 / (c_light * c_light), st),
                        "k_ephemeris");
             ++ctx->launches;
         }
@@ -627,6 +642,11 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
         a.epoch = boundaries[seg];
         a.deadline_ns = gpu_deadline;
         a.fd = make_force_data(d_pos, d_mu, d_ind, cfg->central_mu, cfg->proximity_floor_km, nb);
+        if (rel) {
+            a.fd.rel = 1;
+            a.fd.ic2 = 1.0 / (c_light * c_light);
+            a.fd.rel_tab = d_rel;
+        }
         a.upack = reinterpret_cast<const double2*>(op.buf.p);
         a.times = d_times;
         a.group_off = d_off;
@@ -1036,6 +1056,9 @@ pswarm_status pswarm_eval_force_block(pswarm_ctx* ctx, int64_t n_nodes, int64_t 
         if (!ctx) raise(PSWARM_ERR_NO_DEVICE, "pswarm_eval_force_block: null context");
         bind(ctx);
         const int64_t N = n_nodes, m = group_size;
+        if (force_kind < 0 || force_kind > 1)
+            raise(PSWARM_ERR_INVALID_PLAN, "eval_force_block: the operator entry point takes force kinds 0 (two_body) "
+                                           "and 1 (n_body); n_body_1pn needs body velocities (use propagate)");
         const int B = force_kind == 1 ? n_bodies : 0;
         if (B > 63) raise(PSWARM_ERR_INVALID_SIZE, "eval_force_block: at most 63 perturbing bodies are supported");
         const size_t nc = static_cast<size_t>(N) * 6 * m;

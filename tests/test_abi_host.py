@@ -28,7 +28,8 @@ def test_library_exports_every_declared_symbol():
     for n in names:
         assert hasattr(lib, n), n
     assert {n for n, _, _ in _abi.SIGNATURES} == set(names)
-    assert lib.pswarm_abi_version() == 1
+    abi = int(re.search(r"#define PSWARM_ABI_VERSION (\d+)", open(HEADER).read()).group(1))
+    assert lib.pswarm_abi_version() == abi == 2
 
 
 def test_struct_layouts_match_header():
@@ -37,6 +38,7 @@ def test_struct_layouts_match_header():
     assert C.sizeof(_abi.PswarmError) == 4 + 4 + 5 * 8 + 4 + 4 + 8 + 64 + 512
     assert C.sizeof(_abi.PswarmBody) == 8 + 8 + 4 + 4 + 7 * 8 + 4 + 4 + 8 + 8
     assert C.sizeof(_abi.PswarmOutputs) == 8 * 8 + 8 * 7
+    assert C.sizeof(_abi.PswarmConfig) == 8 + 8 + 4 * 4 + 8 + 4 + 4 + 8 * 7  # ABI 2: + c_light
 
 
 def test_clone_batch_bit_exact(oracle):
