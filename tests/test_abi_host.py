@@ -38,7 +38,7 @@ def test_struct_layouts_match_header():
     assert C.sizeof(_abi.PswarmError) == 4 + 4 + 5 * 8 + 4 + 4 + 8 + 64 + 512
     assert C.sizeof(_abi.PswarmBody) == 8 + 8 + 4 + 4 + 7 * 8 + 4 + 4 + 8 + 8
     assert C.sizeof(_abi.PswarmOutputs) == 8 * 8 + 8 * 7
-    assert C.sizeof(_abi.PswarmConfig) == 8 + 8 + 4 * 4 + 8 + 4 + 4 + 8 * 7  # ABI 2: + c_light
+    assert C.sizeof(_abi.PswarmConfig) == 8 + 8 + 4 * 4 + 8 + 4 + 4 + 8 * 6  # ABI 2: + c_light
 
 
 def test_clone_batch_bit_exact(oracle):
