@@ -183,6 +183,22 @@ __device__ __forceinline__ double clenshaw_deriv(const double* c, int nc, double
     return b1;
 }
 
+/// EXTENSION (hot start, StartMode::hot): the starting guess of a node is its conic (or
+/// cold) base guess plus the previous segment's (converged - base) correction hb when the
+/// segment spans match (apply); hb then keeps this segment's base for hot_retire_node.
+__device__ __forceinline__ void hot_start_node(double* hb, int apply, double ro[3], double vo[3]) {
+    const double base[6] = {ro[0], ro[1], ro[2], vo[0], vo[1], vo[2]};
+    if (apply)
+        for (int c = 0; c < 3; ++c) {
+            ro[c] = base[c] + hb[c];
+            vo[c] = base[3 + c] + hb[3 + c];
+        }
+    for (int c = 0; c < 6; ++c) hb[c] = base[c];
+}
+
+/// EXTENSION (hot start): correction carried to the next segment = converged - base.
+__device__ __forceinline__ void hot_retire_node(double* hb, int c, double y) { hb[c] = y - hb[c]; }
+
 /// Clenshaw evaluation of a Chebyshev series (ephemeris.hpp:29-38).
 __device__ __forceinline__ double clenshaw(const double* c, int nc, double x) {
     double b1 = 0.0, b2 = 0.0;

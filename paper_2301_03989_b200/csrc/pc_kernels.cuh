@@ -74,6 +74,8 @@ struct SegArgs {
     GroupFault* faults;         // [P]
     uint8_t* cold_fallback;     // [M] or nullptr
     unsigned long long* phase_cycles;  // [PHASES] diagnostics or nullptr
+    double* hot;                // [M][N][6] hot-start corrections (EXTENSION) or nullptr
+    int hot_apply;              // 1: this segment starts from base + correction
 };
 
 /// Perturbing bodies on the device (ephemeris.hpp:44-73): analytic elements or
@@ -131,6 +133,8 @@ struct WideArgs {
     uint8_t* cold_fallback;
     unsigned long long* warm_key; // min trajectory*4 + kind of a warm-start fault
     int* active_count;            // groups still iterating after the last finalize
+    double* hot;                  // [M][N][6] hot-start corrections (EXTENSION) or nullptr
+    int hot_apply;
 };
 
 size_t wide_iter_smem_bytes(int N, int nkp, int xrows);

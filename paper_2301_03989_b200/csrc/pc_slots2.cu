@@ -587,6 +587,8 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
 #pragma unroll
                         for (int c = 0; c < 6; ++c) o[c] = ybuf[y2(j, h, c, s)];
                     }
+                    if (a.hot)
+                        for (int c = 0; c < 6; ++c) hot_retire_node(a.hot + (tr * N + j) * 6, c, ybuf[y2(j, h, c, s)]);
                     if (j == N - 1) {
 #pragma unroll
                         for (int c = 0; c < 6; ++c) a.state_out[tr * 6 + c] = ybuf[y2(j, h, c, s)];
@@ -686,6 +688,8 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
                         if (j == 0 && a.cold_fallback)
                             a.cold_fallback[st.slot_traj[t]] = (chk == CONIC_NON_ELLIPTIC) ? 1 : 0;
                     }
+                    if (a.hot)
+                        hot_start_node(a.hot + (static_cast<size_t>(st.slot_traj[t]) * N + j) * 6, a.hot_apply, ro, vo);
 #pragma unroll
                     for (int c = 0; c < 3; ++c) {
                         ybuf[y2(j, h, c, s)] = ro[c];

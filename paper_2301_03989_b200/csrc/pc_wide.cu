@@ -59,6 +59,7 @@ __global__ void k_wide_start(WideArgs a) {
         }
         if (j == 0 && a.cold_fallback) a.cold_fallback[tr] = chk == CONIC_NON_ELLIPTIC ? 1 : 0;
     }
+    if (a.hot) hot_start_node(a.hot + (static_cast<size_t>(tr) * a.N + j) * 6, a.hot_apply, ro, vo);
     double* y = a.Y + static_cast<size_t>(tr >> 3) * a.N * COLS;
     const int t = tr & 7;
 #pragma unroll
@@ -321,6 +322,9 @@ __global__ void k_wide_output(WideArgs a) {
 #pragma unroll
         for (int c = 0; c < 6; ++c) a.state_out[static_cast<size_t>(tr) * 6 + c] = y[yidx(j, c, t)];
     }
+    if (a.hot)
+        for (int c = 0; c < 6; ++c)
+            hot_retire_node(a.hot + (static_cast<size_t>(tr) * a.N + j) * 6, c, y[yidx(j, c, t)]);
 }
 
 cudaError_t launch_wide_start(const WideArgs& a, cudaStream_t s) {

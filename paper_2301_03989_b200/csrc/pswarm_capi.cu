@@ -344,6 +344,8 @@ void run_wide_segment(pswarm_ctx* ctx, const SegArgs& s, const std::vector<int64
     a.rep_hist = s.rep_hist;
     a.faults = s.faults;
     a.cold_fallback = s.cold_fallback;
+    a.hot = s.hot;
+    a.hot_apply = s.hot_apply;
     std::vector<int> tg(static_cast<size_t>(M));
     for (int g = 0; g < P; ++g)
         for (int64_t i = h_off[g]; i < h_off[g + 1]; ++i) tg[i] = g;
@@ -582,6 +584,7 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
         d_pos = ctx->buf[B_BODY_POS].get<double>(static_cast<size_t>(N) * nb * 3);
         d_ind = ctx->buf[B_INDIRECT].get<double>(static_cast<size_t>(N) * 3);
     }
+    double* d_hot = cfg->start_mode == 2 ? ctx->buf[B_HOT].get<double>(static_cast<size_t>(M) * N * 6) : nullptr;
     double *d_vel = nullptr, *d_rel = nullptr;
     if (rel) {  // EXTENSION: body velocities + per-node relativistic table (Sun row first)
         bt.B = nb;
@@ -662,6 +665,10 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
         a.rep_hist = d_hist ? d_hist + static_cast<size_t>(seg) * P * max_it : nullptr;
         a.faults = d_faults;
         a.cold_fallback = d_fb;
+        a.hot = d_hot;  // EXTENSION: hot start corrections, persistent across segments
+        a.hot_apply = d_hot && seg >= 1 &&
+                      std::abs((boundaries[seg + 1] - boundaries[seg]) - (boundaries[seg] - boundaries[seg - 1])) <=
+                          1e-9 * std::abs(boundaries[seg] - boundaries[seg - 1]);
         a.phase_cycles = d_phase;
         if (max_it > 0 && !wide) {
             cuda_check(cudaEventRecord(ctx->evk0, st), "event");

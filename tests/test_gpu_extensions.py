@@ -92,3 +92,50 @@ def test_relativistic_tabulated_ephemeris(ctx, oracle):
     got = ctx.run_batch(states, cfg, plan, "independent")
     want = oracle.run_batch(states, cfg, plan, "independent", 8)
     _parity(got, want)
+
+
+def _hot_setup(m, frac, bodies="reference", kind="n_body", n=200):
+    base = ps.reference_state()
+    states = ps.make_clone_batch(base, m, 1e-5)
+    period = ps.osculating_period(base, ps.MU_SUN)
+    plan = ps.plan_segments(base, 0.0, frac * period, ps.MU_SUN, "per_orbit", n)
+    blist = [] if bodies == "none" else (ps.reference_bodies() if bodies == "reference" else ps.planets8())
+    cfg = ps.reference_force_config(kind, bodies=blist, n_nodes=n, start_mode="hot")
+    return states, plan, cfg
+
+
+def test_c3_hot_start_multisegment(ctx, oracle):
+    """C3 restart semantics with hot starts: per-orbit segments 1/1/1/0.5 periods (the
+    truncated last segment falls back to warm), parity with the oracle and the same fixed
+    point as the reference's warm restart."""
+    states, plan, cfg = _hot_setup(32, 3.5)
+    assert len(plan.boundaries) == 5
+    got = ctx.run_batch(states, cfg, plan, "independent")
+    want = oracle.run_batch(states, cfg, plan, "independent", 8)
+    _parity(got, want)
+    cfg.start_mode = "warm"
+    warm = ctx.run_batch(states, cfg, plan, "independent")
+    assert ps.max_state_discrepancy(got.trajectories, warm.trajectories) <= 1e-10
+    assert np.array_equal(got.iterations[0], warm.iterations[0])  # segment 0 is warm
+
+
+def test_hot_start_pays_on_periodic_correction(ctx, oracle):
+    """Sun-only 1PN: the relativistic correction repeats every orbit, so the hot start
+    cuts the iterations of later segments (oracle/ext_tests.cpp pins the same)."""
+    states, plan, cfg = _hot_setup(16, 3.0, bodies="none", kind="n_body_1pn")
+    got = ctx.run_batch(states, cfg, plan, "independent")
+    want = oracle.run_batch(states, cfg, plan, "independent", 8)
+    _parity(got, want)
+    cfg.start_mode = "warm"
+    warm = ctx.run_batch(states, cfg, plan, "independent")
+    assert 10 * got.iterations[2].sum() < 7 * warm.iterations[2].sum()
+
+
+@pytest.mark.parametrize("mode,p,m", [("grouped", 4, 32), ("augmented", 1, 24)])
+def test_hot_start_group_modes(ctx, oracle, mode, p, m):
+    """Hot start on the generic slot kernel (groups of 8) and the wide-group path."""
+    states, plan, cfg = _hot_setup(m, 2.0, n=128)
+    cfg.p_groups = p
+    got = ctx.run_batch(states, cfg, plan, mode)
+    want = oracle.run_batch(states, cfg, plan, mode, 4)
+    _parity(got, want)
