@@ -38,43 +38,81 @@ METRIC = "trajectories propagated/sec (N-body PC) at 1/2/4/8 B200 vs CPU host co
 UNIT = "trajectories/s"
 
 
+CONFIGS = {
+    # name: (trajectories, per-GPU (weak) or total (strong), bodies, force kind, span periods, policy, start, spreads)
+    "c1": (64, "weak", "none", "two_body", 1.0, "single", "warm", (1e-5,)),
+    "c2": (1000, "weak", "planets8", "n_body", 0.87, "single", "warm", (1e-5,)),
+    "c3": (100000, "strong", "planets8", "n_body", 3.5, "per_orbit", "hot", (1e-5,)),
+    "c4": (1000000, "strong", "planets8", "n_body", 0.87, "single", "warm", (1e-5,)),
+    "c5": (100000, "strong", "planets8", "n_body_1pn", 0.87, "single", "warm", (1e-7, 1e-5, 1e-3, 1e-2)),
+}
+DESCR = {
+    "c1": "C1: heliocentric two-body Keplerian propagation, {m} ICs per GPU (a=1.3e8 km e=0.2), one period",
+    "c2": ("C2: {m}-IC Earth-Venus arc per GPU (reference spacecraft a=1.25e8 km e=0.12, clone spread 1e-5), "
+           "Sun + 8 planets Newtonian N-body, {span} period single segment"),
+    "c3": ("C3: planetary-protection Monte-Carlo cloud, {m} ICs total, Sun + 8 planets, per-orbit segments over "
+           "{span} periods (1/1/1/0.5), hot starts (EXTENSION) on the equal-span segments"),
+    "c4": "C4: {m}-trajectory cloud total sharded over the GPUs, Sun + 8 planets, {span} period single segment",
+    "c5": ("C5: relativistic (EIH 1PN, EXTENSION) Sun + 8 planets, {m} ICs total in four quarters with clone "
+           "spreads 1e-7/1e-5/1e-3/1e-2 (convergence-mask stress), {span} period single segment"),
+}
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--per-gpu", type=int, default=1000, help="trajectories per GPU (weak scaling)")
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS), help="BASELINE.json configs[0..4]")
+    ap.add_argument("--per-gpu", type=int, default=None, help="override the trajectory count")
     ap.add_argument("--nodes", type=int, default=200)
-    ap.add_argument("--bodies", default="planets8", choices=["planets8", "reference"])
-    ap.add_argument("--span", type=float, default=0.87, help="span in osculating periods")
+    ap.add_argument("--bodies", default=None, choices=["planets8", "reference", "none"])
+    ap.add_argument("--span", type=float, default=None, help="span in osculating periods")
+    ap.add_argument("--cpu-sample", type=int, default=2000, help="trajectories in the bounded CPU baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    return ap.parse_args()
+    a = ap.parse_args()
+    m, scaling, bodies, kind, span, policy, start, spreads = CONFIGS[a.config]
+    a.m = a.per_gpu if a.per_gpu is not None else m
+    a.scaling = scaling
+    a.bodies = a.bodies or bodies
+    a.kind = kind
+    a.span = a.span if a.span is not None else span
+    a.policy, a.start, a.spreads = policy, start, spreads
+    return a
 
 
 def workload(args, world, rank):
     import paper_2301_03989_b200 as ps
-    base = ps.reference_state()
-    period = ps.osculating_period(base, ps.MU_SUN)
     from paper_2301_03989_b200.distributed import shard_groups
-    total = args.per_gpu * world
-    states = ps.make_clone_batch(base, total, 1e-5)
+    if args.config == "c1":
+        base = ps.elements_to_state([1.3e8, 0.2, 0.05, 0.4, 0.9, 0.0, 0.0], ps.MU_SUN, 0.0)
+    else:
+        base = ps.reference_state()
+    period = ps.osculating_period(base, ps.MU_SUN)
+    total = args.m * world if args.scaling == "weak" else args.m
+    q = len(args.spreads)
+    states = np.concatenate([ps.make_clone_batch(base, total // q + (1 if k < total % q else 0), sp)
+                             for k, sp in enumerate(args.spreads)])
     shards = shard_groups([1] * total, world)  # independent mode: singleton groups
     lo, hi = shards[rank][2], shards[rank][3]
-    plan = ps.plan_segments(base, 0.0, args.span * period, ps.MU_SUN, "single", args.nodes)
-    bodies = ps.planets8() if args.bodies == "planets8" else ps.reference_bodies()
-    cfg = ps.reference_force_config("n_body", bodies=bodies, n_nodes=args.nodes)
+    plan = ps.plan_segments(base, 0.0, args.span * period, ps.MU_SUN, args.policy, args.nodes)
+    bodies = {"planets8": ps.planets8, "reference": ps.reference_bodies, "none": list}[args.bodies]()
+    kind = "two_body" if args.bodies == "none" and args.kind == "n_body" else args.kind
+    cfg = ps.reference_force_config(kind, bodies=bodies, n_nodes=args.nodes, start_mode=args.start)
     return states, (lo, hi), plan, cfg, shards
 
 
-def config_dict(args, world):
+def config_dict(args, world, plan=None):
+    total = args.m * world if args.scaling == "weak" else args.m
+    nb = {"planets8": 8, "reference": 2, "none": 0}[args.bodies]
     return {
-        "workload": (f"C2: {args.per_gpu}-IC Earth-Venus arc per GPU (reference spacecraft a=1.25e8 km e=0.12, "
-                     f"clone spread 1e-5), Sun + {8 if args.bodies == 'planets8' else 2} planets Newtonian N-body, "
-                     f"N={args.nodes} nodes, {args.span} period single segment, warm start, tol 1e-12, "
-                     "per-trajectory convergence masking (independent mode)"),
-        "trajectories_per_gpu": args.per_gpu, "trajectories_total": args.per_gpu * world, "nodes": args.nodes,
-        "bodies": 8 if args.bodies == "planets8" else 2, "segments": 1, "dtype": "f64",
+        "workload": DESCR[args.config].format(m=args.m, span=args.span) +
+                    f", N={args.nodes} nodes, {args.start} start, tol 1e-12, per-trajectory convergence masking "
+                    "(independent mode)",
+        "name": args.config, "trajectories_per_gpu": total // world, "trajectories_total": total,
+        "nodes": args.nodes, "bodies": nb, "force": args.kind,
+        "segments": None if plan is None else len(plan.boundaries) - 1, "dtype": "f64",
         "parallelism": f"dp{world} (trajectory shards, no collective in the iteration loop)",
         "l2": "flushed between steps (512 MiB device write, outside the timed region)",
     }
@@ -90,7 +128,7 @@ class Clocks:
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(index), f"--query-gpu={q}", "--format=csv,noheader",
-                                          "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+                                          "-lms", "20"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except OSError:
             self.proc = None
 
@@ -144,6 +182,7 @@ def run_reference(args):
     if rank != 0:
         return
     states, (lo, hi), plan, cfg, _ = workload(args, 1, 0)
+    states = cpu_sample(states, args.cpu_sample)
     orc = Oracle()
     cores = os.cpu_count() or 1
     for _ in range(args.warmup):
@@ -158,12 +197,13 @@ def run_reference(args):
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": round(v, 2), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config_dict(args, 1),
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_dict(args, 1, plan),
         "e2e": {"value": round(v, 2), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "cpu_baseline": {"value": round(v, 2), "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"full workload ({len(states)} trajectories) per step, run_batch independent mode "
-                                   f"with {cores} worker threads (oracle/pswarm_ref.hpp restatement; the reference "
-                                   "needs Eigen, absent here)"},
+                         "sample": f"{len(states)} trajectories per step (evenly strided over the workload), "
+                                   f"run_batch independent mode with {cores} worker threads (oracle/pswarm_ref.hpp "
+                                   "restatement; the reference needs Eigen, absent here)"},
     }), flush=True)
 
 
@@ -232,10 +272,7 @@ def main():
     total = M * world
     value = total / (dms * 1e-3)
     e2e = total / (wall_ms * 1e-3)
-    B = len(cfg.bodies)
-    n = args.nodes
-    f_it = 12 * n * n + (75 + 20 * B) * n + 12
-    flops = f_it * statistics.mean(iters)
+    flops = flops_per_trajectory_iteration(args.nodes, len(cfg.bodies), cfg.force_kind) * statistics.mean(iters)
     achieved = flops / (kms_mean * 1e-3) / 1e12
     peak, peak_src = fp64_peak()
 
@@ -243,12 +280,13 @@ def main():
     if rank == 0:
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
-            cpu = cpu_baseline(args, states[lo:hi], plan, cfg, r_check=ctx.run_batch(shard, cfg, plan, "independent"))
+            sample = cpu_sample(states[lo:hi], args.cpu_sample)
+            cpu = cpu_baseline(args, sample, plan, cfg, r_check=ctx.run_batch(sample, cfg, plan, "independent"))
         out = {
             "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": round(dms, 4), "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": round(dms, 4), "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded clone cloud, analytic planets)",
-            "config": config_dict(args, world),
+            "config": config_dict(args, world, plan),
             "e2e": {"value": round(e2e, 1), "unit": UNIT, "ms_per_step": round(wall_ms, 4),
                     "h2d_bytes_per_step": int(M * 7 * 8), "d2h_bytes_per_step": int(M * 7 * 8),
                     "path": "pswarm_run_batch C-ABI, pinned host buffers" + (" + NCCL all_gather" if world > 1 else "")},
@@ -268,6 +306,23 @@ def main():
         dist.destroy_process_group()
 
 
+def cpu_sample(states, k):
+    """Evenly strided subsample (covers every quarter of a mixed-spread cloud)."""
+    if len(states) <= k:
+        return states
+    return np.ascontiguousarray(states[np.linspace(0, len(states) - 1, k).round().astype(int)])
+
+
+def flops_per_trajectory_iteration(n, b, kind):
+    """Algorithmic FP64 flops of one Picard iteration of one trajectory (SURVEY.md §8d;
+    add/sub/mul/div/sqrt = 1, FMA = 2): update 12N^2 + 18N + 12, force (21 + 20B)N, error
+    36N; the relativistic model (EXTENSION) adds (80(B+1) + 20)N."""
+    f = 12 * n * n + (75 + 20 * b) * n + 12
+    if kind == "n_body_1pn":
+        f += (80 * (b + 1) + 20) * n
+    return f
+
+
 def cpu_baseline(args, states, plan, cfg, r_check):
     """CPU oracle (all host cores) on the same workload; also checks parity of this run."""
     import paper_2301_03989_b200 as ps
@@ -284,8 +339,9 @@ def cpu_baseline(args, states, plan, cfg, r_check):
     disc = ps.max_state_discrepancy(r_check.trajectories, ref.trajectories)
     diter = int(np.abs(r_check.iterations.astype(int) - ref.iterations.astype(int)).max())
     return {"value": round(v, 2), "unit": UNIT, "cores": cores, "kind": "port",
-            "sample": f"full workload ({len(states)} trajectories), best of 2, run_batch independent mode, "
-                      f"{cores} threads (oracle/pswarm_ref.hpp)",
+            "sample": f"{len(states)} trajectories (evenly strided over the workload), best of 2, run_batch "
+                      f"independent mode, {cores} threads (oracle/pswarm_ref.hpp); parity below is the GPU on the "
+                      "same sample (independent mode: per-trajectory results do not depend on the batch)",
             "parity_vs_gpu": {"max_rel_state_discrepancy": disc, "max_abs_iteration_diff": diter}}
 
 

@@ -198,6 +198,100 @@ __device__ __forceinline__ void gemm_half(const double2* __restrict__ upack, int
     }
 }
 
+/// Relativistic force of half h for node j (EXTENSION, n_body_1pn): one fused pass over
+/// the massive bodies of the node table (Sun row first) per slot pair yields both the
+/// Newtonian sum and the EIH 1PN terms from the same d, |d|^-1 (see rel_correction for the
+/// factorisation); the reference's singularity guards run exactly on the slow path.
+__device__ __forceinline__ void force_half_rel(const ForceData& fd, double w2, const double* ybuf, double* fb,
+                                               int* sing_key, int act_h, int h, int j) {
+    const int B = fd.n_bodies, nb1 = B + 1;
+    const double ic2 = fd.ic2;
+    const double* rt = fd.rel_tab + static_cast<size_t>(j) * nb1 * REL_W;
+    const double ix = B > 0 ? fd.indirect[3 * j] : 0.0, iy = B > 0 ? fd.indirect[3 * j + 1] : 0.0,
+                 iz = B > 0 ? fd.indirect[3 * j + 2] : 0.0;
+#pragma unroll 1
+    for (int s0 = 0; s0 < HS; s0 += 2) {
+        double rx[2], ry[2], rz[2], vx[2], vy[2], vz[2];
+        double U[2], nx[2], ny[2], nz[2], bx[2], by[2], bz[2], wx[2], wy[2], wz[2], qx[2], qy[2], qz[2];
+        bool on[2];
+        bool flag = false;
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const int s = s0 + k;
+            on[k] = (act_h >> s) & 1;
+            rx[k] = on[k] ? ybuf[y2(j, h, 0, s)] : 1.0e8;
+            ry[k] = on[k] ? ybuf[y2(j, h, 1, s)] : 0.0;
+            rz[k] = on[k] ? ybuf[y2(j, h, 2, s)] : 0.0;
+            vx[k] = on[k] ? ybuf[y2(j, h, 3, s)] : 0.0;
+            vy[k] = on[k] ? ybuf[y2(j, h, 4, s)] : 0.0;
+            vz[k] = on[k] ? ybuf[y2(j, h, 5, s)] : 0.0;
+            U[k] = nx[k] = ny[k] = nz[k] = bx[k] = by[k] = bz[k] = 0.0;
+            wx[k] = wy[k] = wz[k] = qx[k] = qy[k] = qz[k] = 0.0;
+            flag |= !(rx[k] * rx[k] + ry[k] * ry[k] + rz[k] * rz[k] > 0.0);
+        }
+        for (int A = 0; A < nb1; ++A) {
+            const double* t = rt + A * REL_W;
+            const double tx = t[0], ty = t[1], tz = t[2], vax = t[3], vay = t[4], vaz = t[5];
+            const double aax = t[6], aay = t[7], aaz = t[8], mu = t[9], K = t[10];
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                const double dx = tx - rx[k], dy = ty - ry[k], dz = tz - rz[k];
+                const double d2 = dx * dx + dy * dy + dz * dz;
+                if (A > 0) flag |= d2 < fd.floor2_hi;
+                double ir = rsqrt_newton(d2, rsqrt_seed(d2));
+                if (A == 0) ir = rsqrt_newton(d2, ir);  // central term: full precision
+                const double mi = mu * ir, g = mi * ir * ir;
+                U[k] += mi;
+                nx[k] = fma(g, dx, nx[k]);
+                ny[k] = fma(g, dy, ny[k]);
+                nz[k] = fma(g, dz, nz[k]);
+                const double vva = vx[k] * vax + vy[k] * vay + vz[k] * vaz;
+                const double dva = dx * vax + dy * vay + dz * vaz;
+                const double daa = dx * aax + dy * aay + dz * aaz;
+                const double br = g * (K - ic2 * (4.0 * vva + 1.5 * dva * dva * (ir * ir) - 0.5 * daa));
+                bx[k] = fma(br, dx, bx[k]);
+                by[k] = fma(br, dy, by[k]);
+                bz[k] = fma(br, dz, bz[k]);
+                const double w = -g * (dx * (4.0 * vx[k] - 3.0 * vax) + dy * (4.0 * vy[k] - 3.0 * vay) +
+                                       dz * (4.0 * vz[k] - 3.0 * vaz));
+                wx[k] = fma(w, vx[k] - vax, wx[k]);
+                wy[k] = fma(w, vy[k] - vay, wy[k]);
+                wz[k] = fma(w, vz[k] - vaz, wz[k]);
+                qx[k] = fma(mi, aax, qx[k]);
+                qy[k] = fma(mi, aay, qy[k]);
+                qz[k] = fma(mi, aaz, qz[k]);
+            }
+        }
+        if (flag) {  // rare: exact guard order of table_acceleration (force_model.hpp:57-69)
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                if (!on[k]) continue;
+                int fail = (rx[k] * rx[k] + ry[k] * ry[k] + rz[k] * rz[k] > 0.0) ? -1 : 0;
+                for (int b = 0; b < B && fail < 0; ++b) {
+                    const double* q = rt + (b + 1) * REL_W;
+                    const double dx = q[0] - rx[k], dy = q[1] - ry[k], dz = q[2] - rz[k];
+                    if (sqrt(dx * dx + dy * dy + dz * dz) < fd.floor_km) fail = 1 + b;
+                }
+                if (fail >= 0) atomicMin(&sing_key[h * HS + s0 + k], j * (B + 1) + fail);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const int s = s0 + k;
+            const double f = ic2 * (vx[k] * vx[k] + vy[k] * vy[k] + vz[k] * vz[k] - 4.0 * U[k]);
+            const double ax = (nx[k] - ix) + (f * nx[k] + bx[k] + ic2 * wx[k] + 3.5 * ic2 * qx[k]);
+            const double ay = (ny[k] - iy) + (f * ny[k] + by[k] + ic2 * wy[k] + 3.5 * ic2 * qy[k]);
+            const double az = (nz[k] - iz) + (f * nz[k] + bz[k] + ic2 * wz[k] + 3.5 * ic2 * qz[k]);
+            fb[f2(j, 0, s)] = on[k] ? w2 * vx[k] : 0.0;
+            fb[f2(j, 1, s)] = on[k] ? w2 * vy[k] : 0.0;
+            fb[f2(j, 2, s)] = on[k] ? w2 * vz[k] : 0.0;
+            fb[f2(j, 3, s)] = on[k] ? w2 * ax : 0.0;
+            fb[f2(j, 4, s)] = on[k] ? w2 * ay : 0.0;
+            fb[f2(j, 5, s)] = on[k] ? w2 * az : 0.0;
+        }
+    }
+}
+
 /// Force of half h for node j, its 4 slots as independent chains (force_model.hpp:93-142).
 template <bool REL>
 __device__ __forceinline__ void force_half(const ForceData& fd, double w2, const double* ybuf, double* fb, int* sing_key,
@@ -713,9 +807,13 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
             // ---- force of half h
             const int act_h = (am >> (h * HS)) & 0xF;
             if (act_h)
-                for (int j = ft; j < N; j += FP_THREADS)
-                    force_half<REL>(a.fd, a.omega2, ybuf, reinterpret_cast<double*>(smem_raw + L.fbuf0 + h * fb_bytes),
-                               st.sing_key, pos_base, ind_base, act_h, h, j);
+                for (int j = ft; j < N; j += FP_THREADS) {
+                    double* fbh = reinterpret_cast<double*>(smem_raw + L.fbuf0 + h * fb_bytes);
+                    if constexpr (REL)
+                        force_half_rel(a.fd, a.omega2, ybuf, fbh, st.sing_key, act_h, h, j);
+                    else
+                        force_half<false>(a.fd, a.omega2, ybuf, fbh, st.sing_key, pos_base, ind_base, act_h, h, j);
+                }
             bar_sync(BAR_FP, FP_THREADS);
             if (ft < HS && st.sing_key[h * HS + ft] != INT_MAX) {
                 const int t = h * HS + ft, key = st.sing_key[t], j = key / (B + 1), chk = key % (B + 1);
