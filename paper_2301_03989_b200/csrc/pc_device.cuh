@@ -28,9 +28,15 @@ constexpr double PI = 3.141592653589793238462643383279502884;
 
 // ---------------------------------------------------------------- DMMA ---
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+#ifdef PSWARM_DMMA_VOLATILE
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                  : "+d"(c0), "+d"(c1)
                  : "d"(a), "d"(b));
+#else  // pure register op: let the compiler schedule it against the operand loads
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+        : "+d"(c0), "+d"(c1)
+        : "d"(a), "d"(b));
+#endif
 }
 
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
