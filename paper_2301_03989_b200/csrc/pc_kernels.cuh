@@ -54,6 +54,7 @@ struct SegArgs {
     int record_history;
     int pad0;
     double tol;
+    double tol2_lo, tol2_hi;  // tol^2 (1 -+ 1e-13): squared pre-test of err <= tol (picard.hpp:77)
     double omega2;
     double epoch;       // segment start time == times[0]
     unsigned long long deadline_ns;  // %globaltimer deadline, 0 = none

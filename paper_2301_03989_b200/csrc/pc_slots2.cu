@@ -319,6 +319,7 @@ __device__ __forceinline__ void force_half(const ForceData& fd, double w2, const
         az[s] = sc * rz[s];
     }
     const double* bp = pos_base + static_cast<size_t>(j) * 3 * B;
+#pragma unroll 4
     for (int b = 0; b < B; ++b) {
         const double mu_b = __ldg(fd.body_mu + b);
         const double qx = bp[3 * b], qy = bp[3 * b + 1], qz = bp[3 * b + 2];
@@ -607,7 +608,9 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
                 }
                 int free_bits = 0, retire_bits = 0;
                 if (leader) {
-                    const double gerr = sqrt(gerr2);
+                    // sqrt only where the value is needed (history, retire) or the squared test
+                    // is within rounding of tol^2 (tol2_lo/hi carry a 1e-13 relative margin)
+                    auto gerr_of = [&] { return sqrt(gerr2); };
                     GroupFault* fl = a.faults + gid;
                     bool retire = false, ok = false, conv = false;
                     if (warm_t >= 0) {
@@ -637,8 +640,10 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
                             fl->column = nf_best % (6LL * size);
                             retire = true;
                         } else {
-                            if (a.rep_hist) a.rep_hist[static_cast<size_t>(gid) * a.max_it + (it - 1)] = gerr;
-                            if (gerr <= a.tol) {
+                            if (a.rep_hist) a.rep_hist[static_cast<size_t>(gid) * a.max_it + (it - 1)] = gerr_of();
+                            const bool le_tol =
+                                gerr2 <= a.tol2_lo ? true : (gerr2 > a.tol2_hi ? false : gerr_of() <= a.tol);
+                            if (le_tol) {
                                 retire = ok = conv = true;
                             } else if (it >= a.max_it) {
                                 retire = ok = true;
@@ -647,7 +652,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
                     }
                     if (retire) {
                         a.rep_iter[gid] = it;
-                        a.rep_err[gid] = gerr;
+                        a.rep_err[gid] = gerr_of();
                         a.rep_conv[gid] = conv ? 1 : 0;
                         free_bits = members;
                         retire_bits = ok ? members : 0;

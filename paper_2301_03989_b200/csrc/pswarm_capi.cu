@@ -641,6 +641,8 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
         a.max_it = max_it;
         a.record_history = d_hist ? 1 : 0;
         a.tol = cfg->tolerance;
+        a.tol2_lo = cfg->tolerance * cfg->tolerance * (1.0 - 1e-13);
+        a.tol2_hi = cfg->tolerance * cfg->tolerance * (1.0 + 1e-13);
         a.omega2 = seg_omega2[seg];
         a.epoch = boundaries[seg];
         a.deadline_ns = gpu_deadline;
