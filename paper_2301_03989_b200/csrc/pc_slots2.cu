@@ -29,15 +29,21 @@ namespace {
 
 constexpr int HS = 4;            // slots per half
 constexpr int HC = 6 * HS;       // columns per half
-constexpr int YS2 = 2 * HC + 4;  // Ybuf row stride (doubles): 52 -> conflict-free epilogue rows
+// Ybuf row stride (doubles): 50 keeps the epilogue (8 rows x 4 slots per warp) at the
+// 2-wavefront minimum and the force's column reads (32 consecutive rows) at 4 wavefronts
+constexpr int YS2 = 2 * HC + 2;
 constexpr int MMA_WARPS = 8, FP_WARPS = 8;
 constexpr int MMA_THREADS = 32 * MMA_WARPS, FP_THREADS = 32 * FP_WARPS, WS_THREADS = MMA_THREADS + FP_THREADS;
 constexpr int BAR_F0 = 1, BAR_Y0 = 3, BAR_FP = 6, BAR_B0 = 7;  // F_h = 1+h, Y_h = 3+h, B_h = 7+h
 
 __device__ __forceinline__ int y2(int j, int h, int c, int s) { return j * YS2 + h * HC + c * HS + s; }
-/// B-fragment index of F(node j, comp c, slot s) within a half's Fbuf.
+/// B-fragment index of F(node j, comp c, slot s) within a half's Fbuf: per k-step (4 nodes)
+/// three 32-double fragments (one per n-tile) + 4 doubles of padding, so the force
+/// threads' stores (consecutive nodes j, bank set by j & 3 and the k-step) spread over
+/// all banks instead of 4.
+constexpr int FKS = 3 * 32 + 4;  // doubles per k-step
 __device__ __forceinline__ int f2(int j, int c, int s) {
-    return (((j >> 2) * 3 + (c >> 1)) * 32) + ((s * 2 + (c & 1)) * 4 + (j & 3));
+    return (j >> 2) * FKS + (c >> 1) * 32 + ((s * 2 + (c & 1)) * 4 + (j & 3));
 }
 
 // Optional phase accounting (pswarm_set_option "profile_phases"): MMA-group lane 0 of
@@ -87,13 +93,13 @@ struct WsLayout {
     size_t ybuf, fbuf0, fbuf1, xstage, anchor, b0part, eph, state, total;
 };
 
-constexpr int B0_PARTS = (32 * FP_WARPS) / HC;  // 10 partial sums per b0 column
+constexpr int B0_PARTS = FP_WARPS;  // one partial sum per FP warp and b0 column
 
 __host__ __device__ inline WsLayout ws_layout(int N, int nkp, int xrows, int B, int stage_eph) {
     WsLayout L;
     L.ybuf = 0;
     L.fbuf0 = L.ybuf + sizeof(double) * static_cast<size_t>(N) * YS2;
-    const size_t fb = sizeof(double) * static_cast<size_t>(8 * nkp) * HC;
+    const size_t fb = sizeof(double) * static_cast<size_t>(2 * nkp) * FKS;
     L.fbuf1 = L.fbuf0 + fb;
     L.xstage = L.fbuf1 + fb;  // [2 halves][xrows][HC]
     L.anchor = L.xstage + sizeof(double) * 2 * static_cast<size_t>(xrows) * HC;
@@ -150,7 +156,7 @@ __device__ __forceinline__ void gemm_half(const double2* __restrict__ upack, int
 #pragma unroll
         for (int s = 0; s < 2; ++s) {
             const int ks = 2 * kp + s;
-            const double* fk = fb + ks * 96 + lane;
+            const double* fk = fb + ks * FKS + lane;
             const double b0 = fk[0], b1 = fk[32], b2 = fk[64];
             const double bv[3] = {b0, b1, b2};
 #pragma unroll
@@ -295,7 +301,8 @@ __device__ __forceinline__ void force_half_rel(const ForceData& fd, double w2, c
 /// Force of half h for node j, its 4 slots as independent chains (force_model.hpp:93-142).
 template <bool REL>
 __device__ __forceinline__ void force_half(const ForceData& fd, double w2, const double* ybuf, double* fb, int* sing_key,
-                                           const double* pos_base, const double* ind_base, int act_h, int h, int j) {
+                                           const double* pos_base, const double* ind_base, int psj, int psc,
+                                           int act_h, int h, int j) {
     const int B = fd.n_bodies;
     double rx[HS], ry[HS], rz[HS], ax[HS], ay[HS], az[HS], r2[HS], ir[HS];
     bool on[HS];
@@ -318,11 +325,11 @@ __device__ __forceinline__ void force_half(const ForceData& fd, double w2, const
         ay[s] = sc * ry[s];
         az[s] = sc * rz[s];
     }
-    const double* bp = pos_base + static_cast<size_t>(j) * 3 * B;
+    const double* bp = pos_base + static_cast<size_t>(j) * psj;  // element (b, c) at bp[(3b + c) * psc]
 #pragma unroll 4
     for (int b = 0; b < B; ++b) {
         const double mu_b = __ldg(fd.body_mu + b);
-        const double qx = bp[3 * b], qy = bp[3 * b + 1], qz = bp[3 * b + 2];
+        const double qx = bp[(3 * b) * psc], qy = bp[(3 * b + 1) * psc], qz = bp[(3 * b + 2) * psc];
         double dx[HS], dy[HS], dz[HS], d2[HS], y[HS];
 #pragma unroll
         for (int s = 0; s < HS; ++s) {
@@ -343,7 +350,8 @@ __device__ __forceinline__ void force_half(const ForceData& fd, double w2, const
         }
     }
     if (B > 0) {
-        const double ix = ind_base[3 * j], iy = ind_base[3 * j + 1], iz = ind_base[3 * j + 2];
+        const int ij = psc == 1 ? 3 * j : j;  // [N][3] in global memory, [3][N] when staged
+        const double ix = ind_base[ij], iy = ind_base[ij + psc], iz = ind_base[ij + 2 * psc];
 #pragma unroll
         for (int s = 0; s < HS; ++s) {
             ax[s] -= ix;
@@ -369,7 +377,8 @@ __device__ __forceinline__ void force_half(const ForceData& fd, double w2, const
             if (!on[s]) continue;
             int fail = (rx[s] * rx[s] + ry[s] * ry[s] + rz[s] * rz[s] > 0.0) ? -1 : 0;
             for (int b = 0; b < B && fail < 0; ++b) {
-                const double dx = bp[3 * b] - rx[s], dy = bp[3 * b + 1] - ry[s], dz = bp[3 * b + 2] - rz[s];
+                const double dx = bp[(3 * b) * psc] - rx[s], dy = bp[(3 * b + 1) * psc] - ry[s],
+                             dz = bp[(3 * b + 2) * psc] - rz[s];
                 if (sqrt(dx * dx + dy * dy + dz * dz) < fd.floor_km) fail = 1 + b;
             }
             if (fail >= 0) atomicMin(&sing_key[h * HS + s], j * (B + 1) + fail);
@@ -428,7 +437,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
     hp.mb = MAIN * MMA_WARPS;
     hp.extras = (mtiles - hp.mb) * 3;
 
-    for (int i = tid; i < 2 * KP * HC; i += WS_THREADS) fb0[i] = 0.0;  // both halves (contiguous)
+    for (int i = tid; i < 2 * 2 * a.nkp * FKS; i += WS_THREADS) fb0[i] = 0.0;  // both halves (contiguous)
     {  // anchor_op row (pc_matrices.hpp:98-100) = row N of the packed operator
         const double* up = reinterpret_cast<const double*>(a.upack);
         const int amt = N >> 3, ag = N & 7;
@@ -436,12 +445,17 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
             anc[k] = k < N ? up[2 * ((static_cast<size_t>(amt) * a.nkp + (k >> 3)) * 32 + ag * 4 + (k & 3)) + ((k >> 2) & 1)]
                            : 0.0;
     }
-    if (STAGE && B > 0) {
-        for (int i = tid; i < N * 3 * B; i += WS_THREADS) eph[i] = a.fd.body_pos[i];
-        for (int i = tid; i < N * 3; i += WS_THREADS) eph[N * 3 * B + i] = a.fd.indirect[i];
+    if (STAGE && B > 0) {  // node-contiguous [B*3][N] + [3][N]: the force threads (one node each) read conflict-free
+        for (int i = tid; i < N * 3 * B; i += WS_THREADS) {
+            const int j = i / (3 * B), r = i % (3 * B);
+            eph[r * N + j] = a.fd.body_pos[i];
+        }
+        for (int i = tid; i < N * 3; i += WS_THREADS) eph[N * 3 * B + (i % 3) * N + i / 3] = a.fd.indirect[i];
     }
     const double* pos_base = STAGE ? eph : a.fd.body_pos;
     const double* ind_base = STAGE ? eph + N * 3 * B : a.fd.indirect;
+    // element (node j, body b, coordinate c) at pos_base[j * psj + (3b + c) * psc]
+    const int psj = STAGE ? 1 : 3 * B, psc = STAGE ? N : 1;
     if (tid == 0) {
         for (int t = 0; t < SLOTS; ++t) {
             st.slot_traj[t] = -1;
@@ -817,7 +831,8 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
                     if constexpr (REL)
                         force_half_rel(a.fd, a.omega2, ybuf, fbh, st.sing_key, act_h, h, j);
                     else
-                        force_half<false>(a.fd, a.omega2, ybuf, fbh, st.sing_key, pos_base, ind_base, act_h, h, j);
+                        force_half<false>(a.fd, a.omega2, ybuf, fbh, st.sing_key, pos_base, ind_base, psj, psc, act_h,
+                                          h, j);
                 }
             bar_sync(BAR_FP, FP_THREADS);
             if (ft < HS && st.sing_key[h * HS + ft] != INT_MAX) {
@@ -833,24 +848,35 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
             //      fixed order; the MMA group waits for it (B_h) only before its epilogue
             if (act_h) {
                 const double* fbh = reinterpret_cast<const double*>(smem_raw + L.fbuf0 + h * fb_bytes);
-                if (ft < B0_PARTS * HC) {
-                    const int col = ft % HC, part = ft / HC;
-                    const int c = 2 * (col >> 3) + (col & 1), s = (col & 7) >> 1;
-                    double s0 = 0.0, s1 = 0.0;  // two chains: latency under the DMMA stream
-                    int j = part;
-                    for (; j + B0_PARTS < N; j += 2 * B0_PARTS) {
-                        s0 = fma(anc[j], fbh[f2(j, c, s)], s0);
-                        s1 = fma(anc[j + B0_PARTS], fbh[f2(j + B0_PARTS, c, s)], s1);
+                {  // warp fw reads whole 32-double fragments (conflict-free): lane = (col & 7) * 4 + (j & 3)
+                    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+                    const int jl = lane & 3;
+                    for (int kq = fw; kq < a.nkp * 2; kq += FP_WARPS) {
+                        const double w = anc[4 * kq + jl];  // zero past N
+                        const double* fq = fbh + kq * FKS + lane;
+                        s0 = fma(w, fq[0], s0);
+                        s1 = fma(w, fq[32], s1);
+                        s2 = fma(w, fq[64], s2);
                     }
-                    if (j < N) s0 = fma(anc[j], fbh[f2(j, c, s)], s0);
-                    b0part[part * HC + col] = s0 + s1;
+#pragma unroll
+                    for (int off = 1; off < 4; off <<= 1) {  // sum the 4 nodes of a k-step (lanes ^1, ^2)
+                        s0 += __shfl_xor_sync(0xffffffffu, s0, off);
+                        s1 += __shfl_xor_sync(0xffffffffu, s1, off);
+                        s2 += __shfl_xor_sync(0xffffffffu, s2, off);
+                    }
+                    if (jl == 0) {
+                        const int c8 = lane >> 2;
+                        b0part[fw * HC + c8] = s0;
+                        b0part[fw * HC + 8 + c8] = s1;
+                        b0part[fw * HC + 16 + c8] = s2;
+                    }
                 }
                 bar_sync(BAR_FP, FP_THREADS);
                 if (ft < HC) {
                     const int c = 2 * (ft >> 3) + (ft & 1), s = (ft & 7) >> 1;
                     double sum = 0.0;
 #pragma unroll
-                    for (int part = 0; part < B0_PARTS; ++part) sum += b0part[part * HC + ft];
+                    for (int part = 0; part < FP_WARPS; ++part) sum += b0part[part * HC + ft];
                     st.b0h[h][ft] = 0.5 * (sum + 2.0 * st.y0[h * HS + s][c]);
                 }
             }
