@@ -29,14 +29,17 @@ namespace {
 
 constexpr int HS = 4;            // slots per half
 constexpr int HC = 6 * HS;       // columns per half
-// Ybuf row stride (doubles): 50 keeps the epilogue (8 rows x 4 slots per warp) at the
-// 2-wavefront minimum and the force's column reads (32 consecutive rows) at 4 wavefronts
-constexpr int YS2 = 2 * HC + 2;
+// Ybuf row stride 52 doubles (= 4 mod 16): a half-warp touching 4 rows x 4 slots (epilogue,
+// retire, warm start) covers 16 distinct banks; the slot index is XOR-swizzled with
+// (j >> 2) & 3 so the force's 16 consecutive rows of one column do as well.
+constexpr int YS2 = 2 * HC + 4;
 constexpr int MMA_WARPS = 8, FP_WARPS = 8;
 constexpr int MMA_THREADS = 32 * MMA_WARPS, FP_THREADS = 32 * FP_WARPS, WS_THREADS = MMA_THREADS + FP_THREADS;
 constexpr int BAR_F0 = 1, BAR_Y0 = 3, BAR_FP = 6, BAR_B0 = 7;  // F_h = 1+h, Y_h = 3+h, B_h = 7+h
 
-__device__ __forceinline__ int y2(int j, int h, int c, int s) { return j * YS2 + h * HC + c * HS + s; }
+__device__ __forceinline__ int y2(int j, int h, int c, int s) {
+    return j * YS2 + h * HC + c * HS + (s ^ ((j >> 2) & 3));
+}
 /// B-fragment index of F(node j, comp c, slot s) within a half's Fbuf: per k-step (4 nodes)
 /// three 32-double fragments (one per n-tile) + 4 doubles of padding, so the force
 /// threads' stores (consecutive nodes j, bank set by j & 3 and the k-step) spread over
@@ -446,11 +449,11 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
                            : 0.0;
     }
     if (STAGE && B > 0) {  // node-contiguous [B*3][N] + [3][N]: the force threads (one node each) read conflict-free
-        for (int i = tid; i < N * 3 * B; i += WS_THREADS) {
-            const int j = i / (3 * B), r = i % (3 * B);
-            eph[r * N + j] = a.fd.body_pos[i];
+        for (int i = tid; i < N * 3 * B; i += WS_THREADS) {  // smem-contiguous order (conflict-free stores)
+            const int r = i / N, j = i % N;
+            eph[i] = a.fd.body_pos[j * 3 * B + r];
         }
-        for (int i = tid; i < N * 3; i += WS_THREADS) eph[N * 3 * B + (i % 3) * N + i / 3] = a.fd.indirect[i];
+        for (int i = tid; i < N * 3; i += WS_THREADS) eph[N * 3 * B + i] = a.fd.indirect[(i % N) * 3 + i / N];
     }
     const double* pos_base = STAGE ? eph : a.fd.body_pos;
     const double* ind_base = STAGE ? eph + N * 3 * B : a.fd.indirect;
