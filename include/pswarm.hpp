@@ -17,3 +17,4 @@
 #include "pswarm/state.hpp"
 #include "pswarm/synthetic.hpp"
 #include "pswarm/types.hpp"
+#include "pswarm/oracle.hpp"

@@ -79,6 +79,7 @@ class DeviceError : public Error { public: using Error::Error; };
     case PSWARM_ERR_INVALID_PLAN: throw InvalidPlanError(m);
     case PSWARM_ERR_EMPTY_REDUCTION: throw EmptyReductionError(m);
     case PSWARM_ERR_TIMEOUT: throw TimeoutError(m);
+    case PSWARM_ERR_ORACLE: throw OracleError(m);
     case PSWARM_ERR_CUDA:
     case PSWARM_ERR_OOM:
     case PSWARM_ERR_NO_DEVICE: throw DeviceError(m);

@@ -50,6 +50,7 @@ typedef enum pswarm_status {
     PSWARM_ERR_EMPTY_REDUCTION = 12,/* EmptyReductionError */
     PSWARM_ERR_TIMEOUT = 13,        /* TimeoutError */
     PSWARM_ERR_INCOMPLETE = 14,     /* PropagationIncompleteError; partial outputs valid */
+    PSWARM_ERR_ORACLE = 15,         /* OracleError (oracle.hpp: RK step underflow / budget) */
     PSWARM_ERR_CUDA = 20,
     PSWARM_ERR_OOM = 21,
     PSWARM_ERR_NO_DEVICE = 23
@@ -203,6 +204,21 @@ pswarm_status pswarm_block_iteration_error(pswarm_ctx* ctx, int64_t n_nodes, int
 pswarm_status pswarm_warm_start(pswarm_ctx* ctx, int64_t n_states, const double* states, int64_t n_nodes,
                                 const double* times, double central_mu, double* guesses, uint8_t* cold_fallback,
                                 pswarm_error* err);
+
+/* ---- independent verifier (the CLI's --oracle-check, cli.hpp:238-261) --- */
+
+/* oracle_sample_trajectory + compare_trajectories (oracle.hpp:136-183) for every
+ * trajectory at once: adaptive Fehlberg 7(8) (rk_propagate, oracle.hpp:63-132; OracleConfig
+ * rel_tol / abs_tol / max_steps) with the continuous-time force (acceleration_at,
+ * force_model.hpp:78-87; body positions at every stage epoch), one device thread per
+ * trajectory.  states [M][7] with epoch == times[0]; times [R] (propagate's result times);
+ * candidate [M][R][6] (e.g. propagate's samples) or NULL.  Outputs, each may be NULL:
+ * samples_out [M][R][6] = the RK samples, node_error [M][R] = max(position, velocity)
+ * relative discrepancy of candidate vs RK per node, max_error [M] (max_combined). */
+pswarm_status pswarm_oracle_check(pswarm_ctx* ctx, int64_t n_states, const double* states, int64_t n_times,
+                                  const double* times, const pswarm_config* config, double rel_tol, double abs_tol,
+                                  int64_t max_steps, const double* candidate, double* samples_out,
+                                  double* node_error, double* max_error, pswarm_error* err);
 
 /* ---- host utilities (no device needed; same code as the C++ headers) ---- */
 

@@ -7,7 +7,7 @@ and calls the CUDA library ``libpswarm_b200.so`` through the C-ABI declared in
 """
 from .api import (  # noqa: F401
     MU_SUN, AlignmentError, BodySpec, Context, CoverageError, DeviceError, DivergenceError, EmptyReductionError,
-    Error, InvalidPlanError, InvalidSizeError, InvalidSpanError, IterationReport, NonEllipticError,
+    Error, InvalidPlanError, InvalidSizeError, InvalidSpanError, IterationReport, NonEllipticError, OracleError,
     PropagationConfig, PropagationIncompleteError, PropagationResult, SegmentPlan, ShapeError, SingularityError,
     SolverError, TimeoutError, build_grid, default_context, elements_to_state, make_clone_batch,
     max_state_discrepancy, osculating_period, parse_run_mode, plan_segments, planets8, reference_bodies,

@@ -29,6 +29,7 @@ ERR_INVALID_PLAN = 11
 ERR_EMPTY_REDUCTION = 12
 ERR_TIMEOUT = 13
 ERR_INCOMPLETE = 14
+ERR_ORACLE = 15
 ERR_CUDA = 20
 ERR_OOM = 21
 ERR_NO_DEVICE = 23
@@ -132,6 +133,8 @@ SIGNATURES = [
     ("pswarm_block_iteration_error", C.c_int32,
      [C.c_void_p, C.c_int64, C.c_int64, _dp, _dp, C.c_int32, _dp, _dp, _ep]),
     ("pswarm_warm_start", C.c_int32, [C.c_void_p, C.c_int64, _dp, C.c_int64, _dp, C.c_double, _dp, _u8, _ep]),
+    ("pswarm_oracle_check", C.c_int32, [C.c_void_p, C.c_int64, _dp, C.c_int64, _dp, C.POINTER(PswarmConfig),
+                                        C.c_double, C.c_double, C.c_int64, _dp, _dp, _dp, _dp, _ep]),
     ("pswarm_elements_to_state", C.c_int32, [_dp, C.c_double, C.c_double, _dp, _ep]),
     ("pswarm_osculating_period", C.c_int32, [_dp, C.c_double, _dp, _ep]),
     ("pswarm_plan_segments", C.c_int32,

@@ -36,6 +36,7 @@ class SolverError(Error): ...
 class InvalidPlanError(Error): ...
 class EmptyReductionError(Error): ...
 class TimeoutError(Error): ...  # noqa: A001 - reference name
+class OracleError(Error): ...
 class DeviceError(Error):
     """CUDA / device failure or no B200 visible (no reference analogue)."""
 
@@ -68,7 +69,7 @@ _SIMPLE = {
     _abi.ERR_GENERIC: Error, _abi.ERR_INVALID_SPAN: InvalidSpanError, _abi.ERR_INVALID_SIZE: InvalidSizeError,
     _abi.ERR_SHAPE: ShapeError, _abi.ERR_ALIGNMENT: AlignmentError, _abi.ERR_NON_ELLIPTIC: NonEllipticError,
     _abi.ERR_SOLVER: SolverError, _abi.ERR_INVALID_PLAN: InvalidPlanError,
-    _abi.ERR_EMPTY_REDUCTION: EmptyReductionError, _abi.ERR_TIMEOUT: TimeoutError,
+    _abi.ERR_EMPTY_REDUCTION: EmptyReductionError, _abi.ERR_TIMEOUT: TimeoutError, _abi.ERR_ORACLE: OracleError,
     _abi.ERR_CUDA: DeviceError, _abi.ERR_OOM: DeviceError, _abi.ERR_NO_DEVICE: DeviceError,
 }
 
@@ -463,6 +464,26 @@ class Context:
         _check(self.lib.pswarm_warm_start(self.ptr, st.shape[0], _abi.dptr(st), t.size, _abi.dptr(t), central_mu,
                                           _abi.dptr(g), fb.ctypes.data_as(C.POINTER(C.c_uint8)), C.byref(err)), err)
         return g, fb.astype(bool)
+
+    def oracle_check(self, states, config: "PropagationConfig", times, candidate=None, rel_tol=1e-13,
+                     abs_tol=1e-16, max_steps=4000000, samples=True):
+        """The CLI's --oracle-check (cli.hpp:238-261) on the device: RKF7(8)
+        oracle_sample_trajectory + compare_trajectories (oracle.hpp:63-183) for every
+        trajectory.  Returns (rk_samples [M, R, 6] or None, node_error [M, R] or None,
+        max_error [M] or None); the errors need `candidate` (e.g. result.trajectories)."""
+        st = _states(states)
+        t = np.ascontiguousarray(times, dtype=np.float64)
+        M, R = st.shape[0], t.size
+        m = _ConfigMarshal(config)
+        cand = None if candidate is None else np.ascontiguousarray(candidate, dtype=np.float64).reshape(M, R, 6)
+        out = np.zeros((M, R, 6)) if samples else None
+        node = np.zeros((M, R)) if cand is not None else None
+        mx = np.zeros(M) if cand is not None else None
+        err = _abi.PswarmError()
+        _check(self.lib.pswarm_oracle_check(self.ptr, M, _abi.dptr(st), R, _abi.dptr(t), C.byref(m.cfg), rel_tol,
+                                            abs_tol, max_steps, _abi.dptr(cand), _abi.dptr(out), _abi.dptr(node),
+                                            _abi.dptr(mx), C.byref(err)), err)
+        return out, node, mx
 
 
 _default = threading.local()

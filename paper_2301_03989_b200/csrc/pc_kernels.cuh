@@ -144,6 +144,25 @@ cudaError_t launch_wide_iter(const WideArgs& a, int grid, cudaStream_t s);
 cudaError_t launch_wide_finalize(const WideArgs& a, cudaStream_t s);
 cudaError_t launch_wide_output(const WideArgs& a, cudaStream_t s);
 
+/// Batched RKF7(8) verifier (pc_rk.cu; oracle.hpp:63-183): one thread per trajectory.
+struct RkArgs {
+    int M, R;
+    int rel;                     // 1: n_body_1pn derivative (EXTENSION)
+    int pad;
+    long long max_steps;
+    double rel_tol, abs_tol, central_mu, floor_km, c_light;
+    BodyTable bt;
+    const double* states;        // [M][7]
+    const double* times;         // [R], times[0] == epoch
+    const double* candidate;     // [M][R][6] samples to compare, or nullptr
+    double* samples_out;         // [M][R][6] RK samples, or nullptr
+    double* node_err;            // [M][R] max(position, velocity) relative discrepancy, or nullptr
+    double* max_err;             // [M], or nullptr
+    unsigned long long* fault_key;  // min of trajectory << 24 | code << 16 | node
+    double* fault_t;             // [M] epoch reached at a fault
+};
+cudaError_t launch_rk_check(const RkArgs& a, cudaStream_t s);
+
 /// Warp-specialised slot kernel (pc_slots2.cu) for groups of <= 4 trajectories.
 size_t ws_smem_bytes(int N, int nkp, int xrows, int B, int stage_eph);
 int ws_main_tiles(int N);

@@ -105,6 +105,8 @@ pswarm_status guarded(pswarm_error* err, Fn&& fn) {
         init_err(e, PSWARM_ERR_INVALID_PLAN, x.what());
     } catch (const pswarm::TimeoutError& x) {
         init_err(e, PSWARM_ERR_TIMEOUT, x.what());
+    } catch (const pswarm::OracleError& x) {
+        init_err(e, PSWARM_ERR_ORACLE, x.what());
     } catch (const std::bad_alloc&) {
         init_err(e, PSWARM_ERR_OOM, "host allocation failed");
     } catch (const std::exception& x) {
@@ -928,6 +930,7 @@ const char* pswarm_status_name(int32_t s) {
     case PSWARM_ERR_EMPTY_REDUCTION: return "EmptyReductionError";
     case PSWARM_ERR_TIMEOUT: return "TimeoutError";
     case PSWARM_ERR_INCOMPLETE: return "PropagationIncompleteError";
+    case PSWARM_ERR_ORACLE: return "OracleError";
     case PSWARM_ERR_CUDA: return "CudaError";
     case PSWARM_ERR_OOM: return "OutOfMemory";
     case PSWARM_ERR_NO_DEVICE: return "NoDevice";
@@ -1151,6 +1154,106 @@ pswarm_status pswarm_block_iteration_error(pswarm_ctx* ctx, int64_t n_nodes, int
         cuda_check(cudaStreamSynchronize(ctx->stream), "block_error");
         if (per_state) std::memcpy(per_state, h.data(), sizeof(double) * group_size);
         if (group_max) *group_max = *std::max_element(h.begin(), h.end());
+    });
+}
+
+pswarm_status pswarm_oracle_check(pswarm_ctx* ctx, int64_t n_states, const double* states, int64_t n_times,
+                                  const double* times, const pswarm_config* config, double rel_tol, double abs_tol,
+                                  int64_t max_steps, const double* candidate, double* samples_out,
+                                  double* node_error, double* max_error, pswarm_error* err) {
+    return guarded(err, [&] {
+        if (!(rel_tol > 0.0) || !(abs_tol > 0.0))
+            throw pswarm::OracleError("rk_propagate: tolerances must be positive");  // oracle.hpp:66-68
+        const int64_t M = n_states, R = n_times;
+        if (M < 1) return;
+        for (int64_t i = 0; i < M; ++i)
+            if (R < 1 || times[0] != states[7 * i])
+                throw pswarm::OracleError("oracle_sample_trajectory: sample times must begin at the state epoch");
+        if (!ctx) raise(PSWARM_ERR_NO_DEVICE, "pswarm_oracle_check: null context");
+        if (config->force_kind < 0 || config->force_kind > 2)
+            raise(PSWARM_ERR_INVALID_PLAN, "oracle_check: unknown force kind " + std::to_string(config->force_kind));
+        const int nb = config->force_kind >= 1 ? config->n_bodies : 0;
+        if (nb > 16) raise(PSWARM_ERR_INVALID_SIZE, "oracle_check: at most 16 perturbing bodies are supported");
+        bind(ctx);
+        const BodyUpload bu = flatten_bodies(*config, nb);
+        if (bu.first_invalid >= 0) throw pswarm::NonEllipticError(bu.invalid_msg);
+        cudaStream_t st = ctx->stream;
+        DevBuf tmp[8];  // body table of this call
+        auto up = [&](int k, const void* h, size_t bytes) -> void* {
+            void* d = tmp[k].get<char>(bytes);
+            if (bytes) cuda_check(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, st), "H2D");
+            return d;
+        };
+        RkArgs a{};
+        a.M = static_cast<int>(M);
+        a.R = static_cast<int>(R);
+        a.rel = config->force_kind == 2 ? 1 : 0;
+        a.max_steps = max_steps;
+        a.rel_tol = rel_tol;
+        a.abs_tol = abs_tol;
+        a.central_mu = config->central_mu;
+        a.floor_km = config->proximity_floor_km;
+        a.c_light = config->c_light > 0.0 ? config->c_light : 299792.458;
+        a.bt = BodyTable{nb,
+                         static_cast<int*>(up(0, bu.kind.data(), sizeof(int) * bu.kind.size())),
+                         static_cast<double*>(up(1, bu.elements.data(), sizeof(double) * bu.elements.size())),
+                         static_cast<double*>(up(2, bu.mu.data(), sizeof(double) * bu.mu.size())),
+                         static_cast<int*>(up(3, bu.seg_off.data(), sizeof(int) * bu.seg_off.size())),
+                         static_cast<double*>(up(4, bu.bounds.data(), sizeof(double) * bu.bounds.size())),
+                         static_cast<long long*>(up(5, bu.coeff_off.data(), sizeof(long long) * bu.coeff_off.size())),
+                         static_cast<int*>(up(6, bu.ncoef.data(), sizeof(int) * bu.ncoef.size())),
+                         static_cast<double*>(up(7, bu.coeffs.data(), sizeof(double) * bu.coeffs.size()))};
+        double* d_states;
+        double* d_times;
+        upload(ctx, B_OP_IN, states, static_cast<size_t>(M) * 7, &d_states);
+        upload(ctx, B_OP_IN2, times, static_cast<size_t>(R), &d_times);
+        a.states = d_states;
+        a.times = d_times;
+        const size_t ns = static_cast<size_t>(M) * R * 6;
+        double* d_cand = nullptr;
+        if (candidate) upload(ctx, B_SAMPLES, candidate, ns, &d_cand);
+        a.candidate = d_cand;
+        a.samples_out = samples_out ? ctx->buf[B_OP_OUT].get<double>(ns) : nullptr;
+        a.node_err = node_error && candidate ? ctx->buf[B_OP_AUX].get<double>(static_cast<size_t>(M) * R) : nullptr;
+        a.max_err = ctx->buf[B_REP_ERR].get<double>(static_cast<size_t>(M));
+        a.fault_t = ctx->buf[B_DEAD].get<double>(static_cast<size_t>(M));
+        a.fault_key = reinterpret_cast<unsigned long long*>(ctx->buf[B_OP_KEY].get<double>(1));
+        cuda_check(cudaMemsetAsync(a.fault_key, 0xff, sizeof(unsigned long long), st), "memset");
+        cuda_check(launch_rk_check(a, st), "k_rk_check");
+        ++ctx->launches;
+        unsigned long long key = 0;
+        cuda_check(cudaMemcpyAsync(&key, a.fault_key, sizeof key, cudaMemcpyDeviceToHost, st), "D2H");
+        if (a.samples_out)
+            cuda_check(cudaMemcpyAsync(samples_out, a.samples_out, ns * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
+        if (a.node_err)
+            cuda_check(cudaMemcpyAsync(node_error, a.node_err, sizeof(double) * M * R, cudaMemcpyDeviceToHost, st),
+                       "D2H");
+        if (max_error)
+            cuda_check(cudaMemcpyAsync(max_error, a.max_err, sizeof(double) * M, cudaMemcpyDeviceToHost, st), "D2H");
+        cuda_check(cudaStreamSynchronize(st), "oracle_check");
+        if (key != ~0ull) {  // the lowest failing trajectory, in the reference's wording
+            const int64_t tr = static_cast<int64_t>(key >> 24);
+            const int code = static_cast<int>((key >> 16) & 0xff);
+            double tf = 0.0;
+            cuda_check(cudaMemcpy(&tf, a.fault_t + tr, sizeof tf, cudaMemcpyDeviceToHost), "D2H");
+            if (code == 200) throw pswarm::OracleError("rk_propagate: step size underflow at t = " + std::to_string(tf));
+            if (code == 201)
+                throw pswarm::OracleError("rk_propagate: exceeded " + std::to_string(max_steps) + " steps");
+            if (code == 1) throw pswarm::SingularityError("central-body acceleration at zero radius");
+            if (code >= 100) {
+                const int b = code - 100;
+                if (bu.kind[b] == 1)
+                    throw pswarm::CoverageError("ephemeris for body '" + bu.names[b] + "' does not cover epoch " +
+                                                    std::to_string(tf),
+                                                tf);
+                throw pswarm::SolverError("solve_kepler: Newton iteration did not converge for body '" + bu.names[b] +
+                                          "'");
+            }
+            const int b = code - 2;
+            throw pswarm::SingularityError("close approach to body '" + bu.names[b] + "' (trajectory " +
+                                               std::to_string(tr) + ")",
+                                           bu.names[b]);
+        }
     });
 }
 

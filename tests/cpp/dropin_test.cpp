@@ -272,6 +272,21 @@ int main() {
         } catch (const ps::TimeoutError&) {
         }
     });
+    run("oracle_check_batch_acceptance_bar", [] {  // cli.hpp:238-261 + acceptance.cpp:148-172
+        ps::PropagationConfig cfg;
+        cfg.force = ps::make_reference_force_model();
+        const auto st = ps::make_clone_batch(ps::make_reference_state(), 16, 1e-5);
+        const double period = ps::osculating_period(st[0], ps::mu_sun_km3s2);
+        const auto sp = ps::plan_segments(st[0], 0.0, 0.87 * period, ps::mu_sun_km3s2, ps::SegmentPolicy::single, 200);
+        const auto out = ps::run_batch(st, cfg, sp, ps::RunMode::independent);
+        ps::Mat per_node;
+        const auto mx = ps::oracle_check_batch(st, out.result, cfg, {}, &per_node);
+        double worst = 0.0;
+        for (double x : mx) worst = std::max(worst, x);
+        expect(mx.size() == 16 && worst <= 1e-9, "pc vs rkf78 " + std::to_string(worst));
+        expect(per_node.rows() == static_cast<ps::Index>(out.result.times.size()) && per_node.cols() == 16,
+               "per-node shape");
+    });
     std::printf("SUMMARY %d %d\n", n_pass, n_fail);
     return n_fail == 0 ? 0 : 1;
 }
