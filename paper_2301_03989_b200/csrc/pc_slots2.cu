@@ -211,7 +211,7 @@ __device__ __forceinline__ void gemm_half(const double2* __restrict__ upack, int
 /// the massive bodies of the node table (Sun row first) per slot pair yields both the
 /// Newtonian sum and the EIH 1PN terms from the same d, |d|^-1 (see rel_correction for the
 /// factorisation); the reference's singularity guards run exactly on the slow path.
-__device__ __forceinline__ void force_half_rel(const ForceData& fd, double w2, const double* ybuf, double* fb,
+__device__ __forceinline__ void force_half_rel(const ForceData& fd, const double* ybuf, double* fb,
                                                int* sing_key, int act_h, int h, int j) {
     const int B = fd.n_bodies, nb1 = B + 1;
     const double ic2 = fd.ic2;
@@ -291,19 +291,21 @@ __device__ __forceinline__ void force_half_rel(const ForceData& fd, double w2, c
             const double ax = (nx[k] - ix) + (f * nx[k] + bx[k] + ic2 * wx[k] + 3.5 * ic2 * qx[k]);
             const double ay = (ny[k] - iy) + (f * ny[k] + by[k] + ic2 * wy[k] + 3.5 * ic2 * qy[k]);
             const double az = (nz[k] - iz) + (f * nz[k] + bz[k] + ic2 * wz[k] + 3.5 * ic2 * qz[k]);
-            fb[f2(j, 0, s)] = on[k] ? w2 * vx[k] : 0.0;
-            fb[f2(j, 1, s)] = on[k] ? w2 * vy[k] : 0.0;
-            fb[f2(j, 2, s)] = on[k] ? w2 * vz[k] : 0.0;
-            fb[f2(j, 3, s)] = on[k] ? w2 * ax : 0.0;
-            fb[f2(j, 4, s)] = on[k] ? w2 * ay : 0.0;
-            fb[f2(j, 5, s)] = on[k] ? w2 * az : 0.0;
+            fb[f2(j, 0, s)] = on[k] ? vx[k] : 0.0;
+            fb[f2(j, 1, s)] = on[k] ? vy[k] : 0.0;
+            fb[f2(j, 2, s)] = on[k] ? vz[k] : 0.0;
+            fb[f2(j, 3, s)] = on[k] ? ax : 0.0;
+            fb[f2(j, 4, s)] = on[k] ? ay : 0.0;
+            fb[f2(j, 5, s)] = on[k] ? az : 0.0;
         }
     }
 }
 
 /// Force of half h for node j, its 4 slots as independent chains (force_model.hpp:93-142).
+/// F holds [v, a] unscaled: the segment's omega2 (force_model.hpp:122-127) is applied by the
+/// epilogue (Y' = omega2 U F + b0/2 with b0 = omega2 anchor.F + 2 y0), one FMA per entry.
 template <bool REL>
-__device__ __forceinline__ void force_half(const ForceData& fd, double w2, const double* ybuf, double* fb, int* sing_key,
+__device__ __forceinline__ void force_half(const ForceData& fd, const double* ybuf, double* fb, int* sing_key,
                                            const double* pos_base, const double* ind_base, int psj, int psc,
                                            int act_h, int h, int j) {
     const int B = fd.n_bodies;
@@ -389,12 +391,12 @@ __device__ __forceinline__ void force_half(const ForceData& fd, double w2, const
     }
 #pragma unroll
     for (int s = 0; s < HS; ++s) {
-        fb[f2(j, 0, s)] = on[s] ? w2 * ybuf[y2(j, h, 3, s)] : 0.0;
-        fb[f2(j, 1, s)] = on[s] ? w2 * ybuf[y2(j, h, 4, s)] : 0.0;
-        fb[f2(j, 2, s)] = on[s] ? w2 * ybuf[y2(j, h, 5, s)] : 0.0;
-        fb[f2(j, 3, s)] = on[s] ? w2 * ax[s] : 0.0;
-        fb[f2(j, 4, s)] = on[s] ? w2 * ay[s] : 0.0;
-        fb[f2(j, 5, s)] = on[s] ? w2 * az[s] : 0.0;
+        fb[f2(j, 0, s)] = on[s] ? ybuf[y2(j, h, 3, s)] : 0.0;
+        fb[f2(j, 1, s)] = on[s] ? ybuf[y2(j, h, 4, s)] : 0.0;
+        fb[f2(j, 2, s)] = on[s] ? ybuf[y2(j, h, 5, s)] : 0.0;
+        fb[f2(j, 3, s)] = on[s] ? ax[s] : 0.0;
+        fb[f2(j, 4, s)] = on[s] ? ay[s] : 0.0;
+        fb[f2(j, 5, s)] = on[s] ? az[s] : 0.0;
     }
 }
 
@@ -496,6 +498,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
                 // epilogue while its SMSP partner still issues DMMAs.
                 const int act_h = (st.active_mask >> (h * HS)) & 0xF;
                 const double* b0 = st.b0h[h];
+                const double w2 = a.omega2;  // F holds [v, a]; the segment's step scale applies here
                 double bn = 0.0, bd = 1.0;
                 int nf = INT_MAX;
 #pragma unroll
@@ -509,7 +512,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
                         for (int e = 0; e < 2; ++e) {
                             const int c = 2 * p + e;
                             yo[c] = ybuf[y2(j, h, c, q)];
-                            yn[c] = acc[i][p][e] + b0[p * 8 + 2 * q + e];
+                            yn[c] = fma(w2, acc[i][p][e], b0[p * 8 + 2 * q + e]);
                         }
                     update_sample(yn, yo, j, a.error_mode, bn, bd, nf);
 #pragma unroll
@@ -523,7 +526,8 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
                     const int j = (hp.mb + ex / 3) * 8 + g, p = ex % 3;
                     if (j >= N) continue;
 #pragma unroll
-                    for (int e = 0; e < 2; ++e) xs[(j - hp.mb * 8) * HC + q * 6 + 2 * p + e] = xacc[x][e] + b0[p * 8 + 2 * q + e];
+                    for (int e = 0; e < 2; ++e)
+                        xs[(j - hp.mb * 8) * HC + q * 6 + 2 * p + e] = fma(w2, xacc[x][e], b0[p * 8 + 2 * q + e]);
                 }
                 double e2 = bn / bd;
 #pragma unroll
@@ -570,7 +574,10 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
                     atomicMax(&st.slot_err[h * HS + s], static_cast<unsigned long long>(__double_as_longlong(sbn / sbd)));
                     if (snf != INT_MAX) atomicMin(&st.nf_key[h * HS + s], snf);
                 }
-                bar_sync(BAR_FP, FP_THREADS);
+                if (xrows * HS > 32)
+                    bar_sync(BAR_FP, FP_THREADS);
+                else
+                    __syncwarp();  // warp 0 staged every row and also takes the decisions
             }
             // ---- decisions for half h (warp 0 of the FP group, lane = slot of the half)
             if (!first[h] && fw == 0) {
@@ -592,8 +599,18 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
                 double gerr2 = 0.0;
                 long long sing_s = LLONG_MAX, nf_best = LLONG_MAX;
                 int sing_t = -1, warm_t = -1, warm_tr = INT_MAX, members = 0;
+                if (a.gmax == 1 && act_t) {  // singleton groups (independent mode): no cross-lane scan
+                    members = 1 << t;
+                    gerr2 = my_e2;
+                    if (my_wk != INT_MAX) warm_t = t;
+                    if (my_sk != INT_MAX) {
+                        sing_s = my_sk / (B + 1);
+                        sing_t = t;
+                    }
+                    if (my_nk != INT_MAX) nf_best = static_cast<long long>(my_nk >> 3) * 6 + (my_nk & 7);
+                }
 #pragma unroll
-                for (int u = 0; u < HS; ++u) {
+                for (int u = 0; u < (a.gmax == 1 ? 0 : HS); ++u) {
                     const int ug = __shfl_sync(0xffffffffu, my_grp, u);
                     const int um = __shfl_sync(0xffffffffu, my_mbr, u);
                     const double ue = __shfl_sync(0xffffffffu, my_e2, u);
@@ -832,9 +849,9 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
                 for (int j = ft; j < N; j += FP_THREADS) {
                     double* fbh = reinterpret_cast<double*>(smem_raw + L.fbuf0 + h * fb_bytes);
                     if constexpr (REL)
-                        force_half_rel(a.fd, a.omega2, ybuf, fbh, st.sing_key, act_h, h, j);
+                        force_half_rel(a.fd, ybuf, fbh, st.sing_key, act_h, h, j);
                     else
-                        force_half<false>(a.fd, a.omega2, ybuf, fbh, st.sing_key, pos_base, ind_base, psj, psc, act_h,
+                        force_half<false>(a.fd, ybuf, fbh, st.sing_key, pos_base, ind_base, psj, psc, act_h,
                                           h, j);
                 }
             bar_sync(BAR_FP, FP_THREADS);
@@ -880,7 +897,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
                     double sum = 0.0;
 #pragma unroll
                     for (int part = 0; part < FP_WARPS; ++part) sum += b0part[part * HC + ft];
-                    st.b0h[h][ft] = 0.5 * (sum + 2.0 * st.y0[h * HS + s][c]);
+                    st.b0h[h][ft] = 0.5 * fma(a.omega2, sum, 2.0 * st.y0[h * HS + s][c]);
                 }
             }
             WS_PHASE(9);
