@@ -261,12 +261,26 @@ class _ConfigMarshal:
         self.cfg = c
 
 
+def pinned_sample_buffer(n_states: int, plan: "SegmentPlan") -> np.ndarray:
+    """Page-locked [M, R, 6] buffer for `samples=` of propagate/run_batch: with it the
+    library copies each segment's node samples while the next segment computes (the
+    overlapped D2H of pswarm_propagate).  Allocate once and reuse across calls."""
+    import torch
+    R = 1 + (len(plan.boundaries) - 1) * (plan.n_nodes - 1)
+    return torch.zeros((n_states, R, 6), dtype=torch.float64, pin_memory=True).numpy()
+
+
 class _Outputs:
     def __init__(self, M, P, S, N, max_it, samples=True, history=True, terminal=True):
         R = 1 + S * (N - 1)
         self.M, self.P, self.S, self.R, self.max_it = M, P, S, R, max(max_it, 0)
         self.terminal = np.zeros((M, 7)) if terminal else None
-        self.samples = np.zeros((M, R, 6)) if samples else None
+        if isinstance(samples, np.ndarray):  # caller-owned (e.g. pinned_sample_buffer) output
+            if samples.shape != (M, R, 6) or samples.dtype != np.float64 or not samples.flags.c_contiguous:
+                raise ShapeError(f"samples buffer must be float64 C-contiguous of shape {(M, R, 6)}")
+            self.samples = samples
+        else:
+            self.samples = np.zeros((M, R, 6)) if samples else None
         self.times = np.zeros(R)
         self.iters = np.zeros((S, P), dtype=np.int32)
         self.ferr = np.zeros((S, P))

@@ -190,6 +190,8 @@ struct pswarm_ctx {
     int sm_count = 0;
     cudaStream_t stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, evk0 = nullptr, evk1 = nullptr;
+    cudaStream_t copy_stream = nullptr;  // per-segment sample D2H overlapped with the next segment
+    cudaEvent_t ev_seg = nullptr;
     std::map<Index, std::unique_ptr<OpPack>> ops;
     DevBuf buf[B_COUNT];
     int64_t launches = 0;
@@ -602,6 +604,24 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
     }
     cuda_check(cudaEventRecord(ctx->ev0, st), "event");
     int64_t seg_done = 0;
+    // ---- samples into a pinned host buffer: copy each segment's rows as soon as its kernel
+    //      finishes, on a second stream, overlapping the next segment
+    bool overlap_samples = false;
+    if (out && out->samples && S > 1) {
+        cudaPointerAttributes pa{};
+        overlap_samples = cudaPointerGetAttributes(&pa, out->samples) == cudaSuccess && pa.type == cudaMemoryTypeHost;
+        cudaGetLastError();
+        if (overlap_samples && !ctx->copy_stream) {
+            cuda_check(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking), "cudaStreamCreate");
+            cuda_check(cudaEventCreateWithFlags(&ctx->ev_seg, cudaEventDisableTiming), "cudaEventCreate");
+        }
+    }
+    struct CopySync {  // the copy stream never outlives the call (also on error paths)
+        cudaStream_t s;
+        ~CopySync() {
+            if (s) cudaStreamSynchronize(s);
+        }
+    } copy_sync{overlap_samples ? ctx->copy_stream : nullptr};
     double kernel_ms = 0.0;
     int64_t traj_iters = 0;
     std::string fail_msg;
@@ -681,6 +701,15 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
             ++ctx->launches;
         } else if (max_it > 0) {
             run_wide_segment(ctx, a, h_off, deadline);
+        }
+        if (overlap_samples) {  // rows [row0 + jb, row0 + N - 1] of every trajectory, pitch R rows
+            const int64_t jb = seg == 0 ? 0 : 1, row = seg * (N - 1) + jb, nrows = N - jb;
+            const size_t pitch = sizeof(double) * 6 * R;
+            cuda_check(cudaEventRecord(ctx->ev_seg, st), "event");
+            cuda_check(cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_seg, 0), "wait");
+            cuda_check(cudaMemcpy2DAsync(out->samples + row * 6, pitch, d_samples + row * 6, pitch,
+                                         sizeof(double) * 6 * nrows, M, cudaMemcpyDeviceToHost, ctx->copy_stream),
+                       "D2H segment samples");
         }
         cuda_check(cudaMemcpyAsync(hrep, drep, rp.total, cudaMemcpyDeviceToHost, st), "D2H reports");
         if (h_term && seg == S - 1) {  // terminal states ride along with the last segment's reports
@@ -874,9 +903,10 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
             cuda_check(cudaMemcpyAsync(out->error_history, d_hist, sizeof(double) * rep * P * max_it,
                                        cudaMemcpyDeviceToHost, st),
                        "D2H history");
-        if (out->samples)
+        if (out->samples && !overlap_samples)
             cuda_check(cudaMemcpyAsync(out->samples, d_samples, sizeof(double) * M * R * 6, cudaMemcpyDeviceToHost, st),
                        "D2H samples");
+        if (overlap_samples) cuda_check(cudaStreamSynchronize(ctx->copy_stream), "segment samples");
         if (out->terminal_states && fail_status == PSWARM_OK && !term_ready) {
             cuda_check(cudaMemcpyAsync(h_term, d_in, sizeof(double) * M * 6, cudaMemcpyDeviceToHost, st),
                        "D2H terminal");
@@ -978,6 +1008,11 @@ void pswarm_destroy(pswarm_ctx* ctx) {
         b.p = nullptr;
         b.cap = 0;
     }
+    if (ctx->copy_stream) {
+        cudaStreamSynchronize(ctx->copy_stream);
+        cudaStreamDestroy(ctx->copy_stream);
+    }
+    if (ctx->ev_seg) cudaEventDestroy(ctx->ev_seg);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
     if (ctx->evk0) cudaEventDestroy(ctx->evk0);

@@ -246,3 +246,17 @@ def test_c5_mask_stress_heterogeneous_iterations(ctx, oracle):
     want = oracle.run_batch(states, cfg, plan, "independent", 8)
     _parity(got, want)
     assert want.iterations.min() < want.iterations.max()  # heterogeneous by construction
+
+
+def test_pinned_samples_overlapped_copy_identical(ctx):
+    """Node samples into a caller-owned pinned buffer are copied per segment while the
+    next segment computes; the result must be identical to the end-of-call copy."""
+    from paper_2301_03989_b200 import api
+    states, plan, cfg = _setup(40, 64, 2.5, policy="per_orbit")
+    assert len(plan.boundaries) > 2
+    buf = api.pinned_sample_buffer(len(states), plan)
+    a = ctx.run_batch(states, cfg, plan, "independent", samples=buf)
+    b = ctx.run_batch(states, cfg, plan, "independent")
+    assert a.trajectories is buf
+    assert np.array_equal(a.trajectories, b.trajectories)
+    assert np.array_equal(a.terminal_states, b.terminal_states)
