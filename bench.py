@@ -71,6 +71,8 @@ def parse():
     ap.add_argument("--span", type=float, default=None, help="span in osculating periods")
     ap.add_argument("--cpu-sample", type=int, default=2000, help="trajectories in the bounded CPU baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="collective backend for N > 1 (gloo: flow check with ranks sharing a GPU)")
     a = ap.parse_args()
     m, scaling, bodies, kind, span, policy, start, spreads = CONFIGS[a.config]
     a.m = a.per_gpu if a.per_gpu is not None else m
@@ -219,11 +221,17 @@ def main():
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    # one rank per GPU; --dist-backend gloo lets several ranks share a GPU (flow check only)
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
+    nccl = args.dist_backend == "nccl"
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if nccl:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     dev = torch.device("cuda", local)
+    gdev = dev if nccl else None  # gather buffers: device (NVLink) or host (gloo)
     ctx = ps.Context(local)
     from paper_2301_03989_b200.distributed import gather_terminal
     states, (lo, hi), plan, cfg, shards = workload(args, world, rank)
@@ -233,13 +241,13 @@ def main():
 
     def barrier():
         if world > 1:
-            dist.barrier(device_ids=[local])
+            dist.barrier(device_ids=[local]) if nccl else dist.barrier()
         torch.cuda.synchronize(dev)
 
     def step():
         r = ctx.run_batch(shard, cfg, plan, "independent", samples=False, history=False)
         if world > 1:  # final gather of terminal states over NVLink (NCCL)
-            gather_terminal(r.terminal_states, shards, rank, world, device=dev)
+            r.gathered = gather_terminal(r.terminal_states, shards, rank, world, device=gdev)
         return r
 
     for _ in range(args.warmup):
@@ -261,10 +269,14 @@ def main():
     launches = r.gpu_launches - launches0  # context's cumulative count of its own kernel launches
 
     def gmax(x):
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        t = torch.tensor([x], dtype=torch.float64, device=gdev)
         if world > 1:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
+
+    if world > 1:  # the gathered terminal states are the single-process batch order
+        g = r.gathered
+        assert g.shape == (len(states), 7) and np.array_equal(g[lo:hi], r.terminal_states)
 
     wall_ms = gmax(1e3 * statistics.mean(wall))
     dms = gmax(statistics.mean(dev_ms))
@@ -289,7 +301,7 @@ def main():
             "config": config_dict(args, world, plan),
             "e2e": {"value": round(e2e, 1), "unit": UNIT, "ms_per_step": round(wall_ms, 4),
                     "h2d_bytes_per_step": int(M * 7 * 8), "d2h_bytes_per_step": int(M * 7 * 8),
-                    "path": "pswarm_run_batch C-ABI, pinned host buffers" + (" + NCCL all_gather" if world > 1 else "")},
+                    "path": "pswarm_run_batch C-ABI, pinned host buffers" + (f" + {args.dist_backend} all_gather" if world > 1 else "")},
             "roofline": {"bound": "tensor", "achieved": round(achieved, 3), "peak": round(peak, 3), "unit": "TFLOP/s",
                          "frac": round(achieved / peak, 4), "traffic": ncu_traffic(),
                          "kernel": ctx.kernel_name(), "kernel_ms": round(kms_mean, 4),
@@ -302,7 +314,7 @@ def main():
         }
         print(json.dumps(out), flush=True)
     if world > 1:
-        dist.barrier(device_ids=[local])
+        dist.barrier(device_ids=[local]) if nccl else dist.barrier()
         dist.destroy_process_group()
 
 
