@@ -476,6 +476,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_pc_segment(const SegArgs a) {
                     nf_best = min(nf_best, key);
                 }
             }
+            __syncwarp();  // every lane has read the slot / group records the leader rewrites
             int free_bits = 0, retire_bits = 0;
             if (leader) {
                 const double gerr = sqrt(gerr2);

@@ -82,7 +82,8 @@ struct WsState {
     int grp_id[SLOTS];
     int grp_size[SLOTS];
     int grp_iter[SLOTS];
-    int active_mask;     // both halves
+    int act_word[2];     // active slots of half h (bits h*HS..h*HS+3); the MMA group reads
+                         // act_word[h] while the FP group claims into act_word[h ^ 1]
     int new_mask[2];     // slots claimed at the last refill of each half
     int free_mask;
     int retire_mask;
@@ -469,7 +470,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
             st.nf_key[t] = INT_MAX;
             st.slot_err[t] = 0ull;
         }
-        st.active_mask = 0;
+        st.act_word[0] = st.act_word[1] = 0;
         st.new_mask[0] = st.new_mask[1] = 0;
         st.half_active[0] = st.half_active[1] = 0;
         st.queue_done = 0;
@@ -496,7 +497,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
                 // the FP group with the force), finite check, error vs the previous iterate.
                 // No barrier inside the MMA group: a warp that finishes early runs its
                 // epilogue while its SMSP partner still issues DMMAs.
-                const int act_h = (st.active_mask >> (h * HS)) & 0xF;
+                const int act_h = (st.act_word[h] >> (h * HS)) & 0xF;
                 const double* b0 = st.b0h[h];
                 const double w2 = a.omega2;  // F holds [v, a]; the segment's step scale applies here
                 double bn = 0.0, bd = 1.0;
@@ -555,7 +556,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
             WS_PHASE(4);
             // ---- staged rows of half h (node rows whose components sit in several MMA warps)
             if (!first[h] && xrows > 0 && st.half_active[h]) {
-                const int act_h = (st.active_mask >> (h * HS)) & 0xF;
+                const int act_h = (st.act_word[h] >> (h * HS)) & 0xF;
                 const double* xs = xstage + h * xrows * HC;
                 for (int i = ft; i < xrows * HS; i += FP_THREADS) {
                     const int r = i >> 2, s = i & 3, j = MAIN * MMA_WARPS * 8 + r;
@@ -581,7 +582,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
             }
             // ---- decisions for half h (warp 0 of the FP group, lane = slot of the half)
             if (!first[h] && fw == 0) {
-                const int am = st.active_mask;
+                const int am = st.act_word[h];
                 const int s = lane, t = h * HS + s;
                 const bool act_t = s < HS && ((am >> t) & 1);
                 const int my_grp = act_t ? st.slot_grp[t] : -1;
@@ -640,6 +641,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
                         nf_best = min(nf_best, key);
                     }
                 }
+                __syncwarp();  // every lane has read the slot / group records the leader rewrites
                 int free_bits = 0, retire_bits = 0;
                 if (leader) {
                     // sqrt only where the value is needed (history, retire) or the squared test
@@ -731,7 +733,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
             }
             // ---- free + claim into half h (thread 0 of the FP group)
             if (ft == 0) {
-                int am = st.active_mask;
+                int am = st.act_word[0] | st.act_word[1];
                 if (!first[h]) {
                     const int fm = st.free_mask;
                     am &= ~fm;
@@ -767,13 +769,13 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
                     }
                 }
                 if (a.deadline_ns != 0ull && globaltimer_ns() > a.deadline_ns) st.timeout = 1;
-                st.active_mask = am;
+                st.act_word[h] = am & (0xF << (h * HS));
                 st.new_mask[h] = new_mask;
                 st.half_active[h] = (am & hmask) != 0;
             }
             bar_sync(BAR_FP, FP_THREADS);
             WS_PHASE(6);
-            const int am = st.active_mask;
+            const int am = st.act_word[0] | st.act_word[1];
             if (st.timeout || (am == 0 && st.queue_done)) {  // done: release the MMA group and leave
                 if (ft == 0) {
                     if (st.timeout)
