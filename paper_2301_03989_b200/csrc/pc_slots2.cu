@@ -212,21 +212,24 @@ __device__ __forceinline__ void gemm_half(const double2* __restrict__ upack, int
 /// the massive bodies of the node table (Sun row first) per slot pair yields both the
 /// Newtonian sum and the EIH 1PN terms from the same d, |d|^-1 (see rel_correction for the
 /// factorisation); the reference's singularity guards run exactly on the slow path.
+template <int NS>
 __device__ __forceinline__ void force_half_rel(const ForceData& fd, const double* ybuf, double* fb,
-                                               int* sing_key, int act_h, int h, int j) {
+                                               int* sing_key, int act_h, int h, int j, int s_begin) {
+    constexpr int PAIR = NS < 2 ? NS : 2;  // slots per fused pass
     const int B = fd.n_bodies, nb1 = B + 1;
     const double ic2 = fd.ic2;
     const double* rt = fd.rel_tab + static_cast<size_t>(j) * nb1 * REL_W;
     const double ix = B > 0 ? fd.indirect[3 * j] : 0.0, iy = B > 0 ? fd.indirect[3 * j + 1] : 0.0,
                  iz = B > 0 ? fd.indirect[3 * j + 2] : 0.0;
 #pragma unroll 1
-    for (int s0 = 0; s0 < HS; s0 += 2) {
-        double rx[2], ry[2], rz[2], vx[2], vy[2], vz[2];
-        double U[2], nx[2], ny[2], nz[2], bx[2], by[2], bz[2], wx[2], wy[2], wz[2], qx[2], qy[2], qz[2];
-        bool on[2];
+    for (int s0 = s_begin; s0 < s_begin + NS; s0 += PAIR) {
+        double rx[PAIR], ry[PAIR], rz[PAIR], vx[PAIR], vy[PAIR], vz[PAIR];
+        double U[PAIR], nx[PAIR], ny[PAIR], nz[PAIR], bx[PAIR], by[PAIR], bz[PAIR], wx[PAIR], wy[PAIR], wz[PAIR],
+            qx[PAIR], qy[PAIR], qz[PAIR];
+        bool on[PAIR];
         bool flag = false;
 #pragma unroll
-        for (int k = 0; k < 2; ++k) {
+        for (int k = 0; k < PAIR; ++k) {
             const int s = s0 + k;
             on[k] = (act_h >> s) & 1;
             rx[k] = on[k] ? ybuf[y2(j, h, 0, s)] : 1.0e8;
@@ -244,7 +247,7 @@ __device__ __forceinline__ void force_half_rel(const ForceData& fd, const double
             const double tx = t[0], ty = t[1], tz = t[2], vax = t[3], vay = t[4], vaz = t[5];
             const double aax = t[6], aay = t[7], aaz = t[8], mu = t[9], K = t[10];
 #pragma unroll
-            for (int k = 0; k < 2; ++k) {
+            for (int k = 0; k < PAIR; ++k) {
                 const double dx = tx - rx[k], dy = ty - ry[k], dz = tz - rz[k];
                 const double d2 = dx * dx + dy * dy + dz * dz;
                 if (A > 0) flag |= d2 < fd.floor2_hi;
@@ -274,7 +277,7 @@ __device__ __forceinline__ void force_half_rel(const ForceData& fd, const double
         }
         if (flag) {  // rare: exact guard order of table_acceleration (force_model.hpp:57-69)
 #pragma unroll
-            for (int k = 0; k < 2; ++k) {
+            for (int k = 0; k < PAIR; ++k) {
                 if (!on[k]) continue;
                 int fail = (rx[k] * rx[k] + ry[k] * ry[k] + rz[k] * rz[k] > 0.0) ? -1 : 0;
                 for (int b = 0; b < B && fail < 0; ++b) {
@@ -286,7 +289,7 @@ __device__ __forceinline__ void force_half_rel(const ForceData& fd, const double
             }
         }
 #pragma unroll
-        for (int k = 0; k < 2; ++k) {
+        for (int k = 0; k < PAIR; ++k) {
             const int s = s0 + k;
             const double f = ic2 * (vx[k] * vx[k] + vy[k] * vy[k] + vz[k] * vz[k] - 4.0 * U[k]);
             const double ax = (nx[k] - ix) + (f * nx[k] + bx[k] + ic2 * wx[k] + 3.5 * ic2 * qx[k]);
@@ -302,30 +305,30 @@ __device__ __forceinline__ void force_half_rel(const ForceData& fd, const double
     }
 }
 
-/// Force of half h for node j, its 4 slots as independent chains (force_model.hpp:93-142).
+/// Force of half h for node j, slots [s0, s0 + NS) as independent chains (force_model.hpp:93-142).
 /// F holds [v, a] unscaled: the segment's omega2 (force_model.hpp:122-127) is applied by the
 /// epilogue (Y' = omega2 U F + b0/2 with b0 = omega2 anchor.F + 2 y0), one FMA per entry.
-template <bool REL>
+template <int NS>
 __device__ __forceinline__ void force_half(const ForceData& fd, const double* ybuf, double* fb, int* sing_key,
                                            const double* pos_base, const double* ind_base, int psj, int psc,
-                                           int act_h, int h, int j) {
+                                           int act_h, int h, int j, int s0) {
     const int B = fd.n_bodies;
-    double rx[HS], ry[HS], rz[HS], ax[HS], ay[HS], az[HS], r2[HS], ir[HS];
-    bool on[HS];
+    double rx[NS], ry[NS], rz[NS], ax[NS], ay[NS], az[NS], r2[NS], ir[NS];
+    bool on[NS];
     bool flag = false;
 #pragma unroll
-    for (int s = 0; s < HS; ++s) {
-        on[s] = (act_h >> s) & 1;
-        rx[s] = on[s] ? ybuf[y2(j, h, 0, s)] : 1.0e8;
-        ry[s] = on[s] ? ybuf[y2(j, h, 1, s)] : 0.0;
-        rz[s] = on[s] ? ybuf[y2(j, h, 2, s)] : 0.0;
+    for (int s = 0; s < NS; ++s) {
+        on[s] = (act_h >> (s0 + s)) & 1;
+        rx[s] = on[s] ? ybuf[y2(j, h, 0, s0 + s)] : 1.0e8;
+        ry[s] = on[s] ? ybuf[y2(j, h, 1, s0 + s)] : 0.0;
+        rz[s] = on[s] ? ybuf[y2(j, h, 2, s0 + s)] : 0.0;
         r2[s] = rx[s] * rx[s] + ry[s] * ry[s] + rz[s] * rz[s];
         flag |= !(r2[s] > 0.0);
     }
 #pragma unroll
-    for (int s = 0; s < HS; ++s) ir[s] = rsqrt_newton(r2[s], rsqrt_newton(r2[s], rsqrt_seed(r2[s])));
+    for (int s = 0; s < NS; ++s) ir[s] = rsqrt_newton(r2[s], rsqrt_newton(r2[s], rsqrt_seed(r2[s])));
 #pragma unroll
-    for (int s = 0; s < HS; ++s) {
+    for (int s = 0; s < NS; ++s) {
         const double sc = -fd.central_mu * (ir[s] * ir[s] * ir[s]);
         ax[s] = sc * rx[s];
         ay[s] = sc * ry[s];
@@ -336,9 +339,9 @@ __device__ __forceinline__ void force_half(const ForceData& fd, const double* yb
     for (int b = 0; b < B; ++b) {
         const double mu_b = __ldg(fd.body_mu + b);
         const double qx = bp[(3 * b) * psc], qy = bp[(3 * b + 1) * psc], qz = bp[(3 * b + 2) * psc];
-        double dx[HS], dy[HS], dz[HS], d2[HS], y[HS];
+        double dx[NS], dy[NS], dz[NS], d2[NS], y[NS];
 #pragma unroll
-        for (int s = 0; s < HS; ++s) {
+        for (int s = 0; s < NS; ++s) {
             dx[s] = qx - rx[s];
             dy[s] = qy - ry[s];
             dz[s] = qz - rz[s];
@@ -346,9 +349,9 @@ __device__ __forceinline__ void force_half(const ForceData& fd, const double* yb
             flag |= d2[s] < fd.floor2_hi;
         }
 #pragma unroll
-        for (int s = 0; s < HS; ++s) y[s] = rsqrt_newton(d2[s], rsqrt_seed(d2[s]));
+        for (int s = 0; s < NS; ++s) y[s] = rsqrt_newton(d2[s], rsqrt_seed(d2[s]));
 #pragma unroll
-        for (int s = 0; s < HS; ++s) {
+        for (int s = 0; s < NS; ++s) {
             const double kk = mu_b * (y[s] * y[s] * y[s]);
             ax[s] += kk * dx[s];
             ay[s] += kk * dy[s];
@@ -359,27 +362,15 @@ __device__ __forceinline__ void force_half(const ForceData& fd, const double* yb
         const int ij = psc == 1 ? 3 * j : j;  // [N][3] in global memory, [3][N] when staged
         const double ix = ind_base[ij], iy = ind_base[ij + psc], iz = ind_base[ij + 2 * psc];
 #pragma unroll
-        for (int s = 0; s < HS; ++s) {
+        for (int s = 0; s < NS; ++s) {
             ax[s] -= ix;
             ay[s] -= iy;
             az[s] -= iz;
         }
     }
-    if (REL) {  // EXTENSION: EIH 1PN correction (n_body_1pn)
-        const double* rt = fd.rel_tab + static_cast<size_t>(j) * (B + 1) * REL_W;
-        for (int s = 0; s < HS; ++s) {
-            if (!on[s]) continue;
-            double o[3];
-            rel_correction(rx[s], ry[s], rz[s], ybuf[y2(j, h, 3, s)], ybuf[y2(j, h, 4, s)], ybuf[y2(j, h, 5, s)], rt,
-                           B + 1, fd.ic2, o);
-            ax[s] += o[0];
-            ay[s] += o[1];
-            az[s] += o[2];
-        }
-    }
     if (flag) {  // rare: exact guard order of table_acceleration (force_model.hpp:57-69)
 #pragma unroll
-        for (int s = 0; s < HS; ++s) {
+        for (int s = 0; s < NS; ++s) {
             if (!on[s]) continue;
             int fail = (rx[s] * rx[s] + ry[s] * ry[s] + rz[s] * rz[s] > 0.0) ? -1 : 0;
             for (int b = 0; b < B && fail < 0; ++b) {
@@ -387,17 +378,17 @@ __device__ __forceinline__ void force_half(const ForceData& fd, const double* yb
                              dz = bp[(3 * b + 2) * psc] - rz[s];
                 if (sqrt(dx * dx + dy * dy + dz * dz) < fd.floor_km) fail = 1 + b;
             }
-            if (fail >= 0) atomicMin(&sing_key[h * HS + s], j * (B + 1) + fail);
+            if (fail >= 0) atomicMin(&sing_key[h * HS + s0 + s], j * (B + 1) + fail);
         }
     }
 #pragma unroll
-    for (int s = 0; s < HS; ++s) {
-        fb[f2(j, 0, s)] = on[s] ? ybuf[y2(j, h, 3, s)] : 0.0;
-        fb[f2(j, 1, s)] = on[s] ? ybuf[y2(j, h, 4, s)] : 0.0;
-        fb[f2(j, 2, s)] = on[s] ? ybuf[y2(j, h, 5, s)] : 0.0;
-        fb[f2(j, 3, s)] = on[s] ? ax[s] : 0.0;
-        fb[f2(j, 4, s)] = on[s] ? ay[s] : 0.0;
-        fb[f2(j, 5, s)] = on[s] ? az[s] : 0.0;
+    for (int s = 0; s < NS; ++s) {
+        fb[f2(j, 0, s0 + s)] = on[s] ? ybuf[y2(j, h, 3, s0 + s)] : 0.0;
+        fb[f2(j, 1, s0 + s)] = on[s] ? ybuf[y2(j, h, 4, s0 + s)] : 0.0;
+        fb[f2(j, 2, s0 + s)] = on[s] ? ybuf[y2(j, h, 5, s0 + s)] : 0.0;
+        fb[f2(j, 3, s0 + s)] = on[s] ? ax[s] : 0.0;
+        fb[f2(j, 4, s0 + s)] = on[s] ? ay[s] : 0.0;
+        fb[f2(j, 5, s0 + s)] = on[s] ? az[s] : 0.0;
     }
 }
 
@@ -847,15 +838,35 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
             WS_PHASE(7);
             // ---- force of half h
             const int act_h = (am >> (h * HS)) & 0xF;
-            if (act_h)
-                for (int j = ft; j < N; j += FP_THREADS) {
-                    double* fbh = reinterpret_cast<double*>(smem_raw + L.fbuf0 + h * fb_bytes);
-                    if constexpr (REL)
-                        force_half_rel(a.fd, ybuf, fbh, st.sing_key, act_h, h, j);
-                    else
-                        force_half<false>(a.fd, ybuf, fbh, st.sing_key, pos_base, ind_base, psj, psc, act_h,
-                                          h, j);
+            if (act_h) {
+                // slots per force thread: all FP warps stay busy down to N = 64 (the FP warps only
+                // issue in the DMMA stream's gaps, so their count sets the force throughput)
+                double* fbh = reinterpret_cast<double*>(smem_raw + L.fbuf0 + h * fb_bytes);
+                if (N > FP_THREADS / 2) {
+                    for (int j = ft; j < N; j += FP_THREADS) {
+                        if constexpr (REL)
+                            force_half_rel<4>(a.fd, ybuf, fbh, st.sing_key, act_h, h, j, 0);
+                        else
+                            force_half<4>(a.fd, ybuf, fbh, st.sing_key, pos_base, ind_base, psj, psc, act_h, h, j, 0);
+                    }
+                } else if (N > FP_THREADS / 4) {
+                    for (int w = ft; w < 2 * N; w += FP_THREADS) {
+                        const int j = w % N, s0 = (w / N) * 2;
+                        if constexpr (REL)
+                            force_half_rel<2>(a.fd, ybuf, fbh, st.sing_key, act_h, h, j, s0);
+                        else
+                            force_half<2>(a.fd, ybuf, fbh, st.sing_key, pos_base, ind_base, psj, psc, act_h, h, j, s0);
+                    }
+                } else {
+                    for (int w = ft; w < 4 * N; w += FP_THREADS) {
+                        const int j = w % N, s0 = w / N;
+                        if constexpr (REL)
+                            force_half_rel<1>(a.fd, ybuf, fbh, st.sing_key, act_h, h, j, s0);
+                        else
+                            force_half<1>(a.fd, ybuf, fbh, st.sing_key, pos_base, ind_base, psj, psc, act_h, h, j, s0);
+                    }
                 }
+            }
             bar_sync(BAR_FP, FP_THREADS);
             if (ft < HS && st.sing_key[h * HS + ft] != INT_MAX) {
                 const int t = h * HS + ft, key = st.sing_key[t], j = key / (B + 1), chk = key % (B + 1);
