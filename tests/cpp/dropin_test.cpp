@@ -62,8 +62,12 @@ rf::Config ref_config(const ps::PropagationConfig& c) {
     o.n_nodes = c.n_nodes;
     o.tolerance = c.tolerance;
     o.max_iterations = c.max_iterations;
-    o.start_mode = c.start_mode == ps::StartMode::cold ? rf::StartMode::cold : rf::StartMode::warm;
-    o.force = c.force.kind == ps::ForceKind::n_body ? rf::reference_force() : rf::reference_force(rf::ForceKind::two_body);
+    o.start_mode = c.start_mode == ps::StartMode::cold  ? rf::StartMode::cold
+                   : c.start_mode == ps::StartMode::hot ? rf::StartMode::hot
+                                                        : rf::StartMode::warm;
+    o.force = c.force.kind == ps::ForceKind::two_body ? rf::reference_force(rf::ForceKind::two_body)
+                                                      : rf::reference_force();
+    if (c.force.kind == ps::ForceKind::n_body_1pn) o.force.kind = rf::ForceKind::n_body_1pn;
     o.p_groups = c.p_groups;
     return o;
 }
@@ -241,6 +245,27 @@ int main() {
                "independent " + sci(d1) + "/" + std::to_string(i1) + " grouped " + sci(d2) + "/" + std::to_string(i2));
         expect(ps::max_state_discrepancy(grp.result, ind.result) < 1e-12,
                "mode invariance " + sci(ps::max_state_discrepancy(grp.result, ind.result)));
+    });
+    run("extensions_1pn_hot_start_match_oracle", [] {  // BASELINE configs 3 and 5 through the C++ API
+        const auto st = ps::make_clone_batch(ps::make_reference_state(), 16, 1e-5);
+        const double period = ps::osculating_period(st[0], ps::mu_sun_km3s2);
+        const auto sp = ps::plan_segments(st[0], 0.0, 2.5 * period, ps::mu_sun_km3s2, ps::SegmentPolicy::per_orbit, 128);
+        rf::Segments rsp;
+        rsp.boundaries = sp.boundaries;
+        rsp.n_nodes = 128;
+        const auto rst = to_ref(st);
+        for (int variant = 0; variant < 2; ++variant) {
+            ps::PropagationConfig cfg;
+            cfg.n_nodes = 128;
+            cfg.force = ps::make_reference_force_model();
+            if (variant == 0) cfg.force.kind = ps::ForceKind::n_body_1pn;
+            else cfg.start_mode = ps::StartMode::hot;
+            const auto got = ps::run_batch(st, cfg, sp, ps::RunMode::independent);
+            const auto want = rf::run_batch(rst, ref_config(cfg), rsp, rf::RunMode::independent, 4);
+            const double d = discrepancy(got.result, want.result);
+            const int di = max_iter_diff(got.result, want.result);
+            expect(d <= 1e-10 && di <= 1, (variant ? "hot " : "1pn ") + sci(d) + "/" + std::to_string(di));
+        }
     });
     run("propagate_nonconvergence_partial", [] {  // test_propagator.cpp:229-249
         ps::PropagationConfig cfg;
