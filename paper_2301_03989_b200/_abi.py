@@ -147,9 +147,11 @@ _lib = None
 
 
 def load(path: str = LIB_PATH) -> C.CDLL:
-    """Load (once) the in-tree CUDA library; raises OSError when it is missing."""
+    """Load (once) the in-tree CUDA library; raises OSError when it is missing.
+    PSWARM_LIB overrides the path (diagnostic builds of the same library)."""
     global _lib
     if _lib is None:
+        path = os.environ.get("PSWARM_LIB", path)
         if not os.path.exists(path):
             raise OSError(f"{path} not built: run __graft_entry__.build() (nvcc, sm_100a); "
                           "the PC path has no CPU fallback")

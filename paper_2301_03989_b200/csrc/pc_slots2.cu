@@ -20,6 +20,10 @@
 #include <algorithm>
 #include <climits>
 
+#ifndef PSWARM_ABLATE
+#define PSWARM_ABLATE 0  // diagnostic builds only (tools/ablate.sh)
+#endif
+
 #include "pc_kernels.cuh"
 #include "pc_tile.cuh"
 
@@ -114,49 +118,51 @@ __host__ __device__ inline WsLayout ws_layout(int N, int nkp, int xrows, int B, 
     return L;
 }
 
-/// Tile plan of one half (26 m-tiles x 3 n-tiles at N = 200) over the 8 MMA warps:
+/// Tile plan of one half (25 m-tiles x 3 n-tiles at N = 200) over the 8 MMA warps:
 /// `main` consecutive full-width m-tiles per warp + up to XMW single extra tiles.
 struct HalfPlan {
     int main, mb, extras;
 };
 
-template <int MAIN, int XMW>
+template <int MAIN, int NX>
 struct APairH {
     double2 m[MAIN];
-    double2 x[XMW];
+    double2 x[NX > 0 ? NX : 1];
 };
 
-/// One warp's share of Y'_h = [U; anchor] F_h over all K (LDG.128 operator pairs,
-/// double-buffered; B fragments are LDS.64 of the fragment-native half Fbuf).
-template <int MAIN, int XMW>
-__device__ __forceinline__ void gemm_half(const double2* __restrict__ upack, int nkp, const double* fb,
+/// One warp's share of Y'_h = U F_h over all K (LDG.128 operator pairs, double-buffered;
+/// B fragments are LDS.64 of the fragment-native half Fbuf).  NX = this warp's number of
+/// single extra tiles, a compile-time constant: a predicated-off DMMA still costs a pipe
+/// slot (tools/ws_micro.cu: 16.7 k -> 15.2 k cycles per half without it at N = 192).
+template <int MAIN, int NX>
+__device__ __forceinline__ void gemm_core(const double2* __restrict__ upack, int nkp, const double* fb,
                                           const HalfPlan& hp, int warp, int lane, double (&acc)[MAIN][3][2],
-                                          double (&xacc)[XMW][2]) {
+                                          double (*xacc)[2]) {
 #pragma unroll
     for (int i = 0; i < MAIN; ++i)
 #pragma unroll
         for (int p = 0; p < 3; ++p) acc[i][p][0] = acc[i][p][1] = 0.0;
+    constexpr int XA = NX > 0 ? NX : 1;
     const double2* am[MAIN];
-    const double2* ax[XMW];
-    bool hx[XMW];
-    int xp[XMW];
+    const double2* ax[XA];
+    int xp[XA];
+    double xa[XA][2];
 #pragma unroll
     for (int i = 0; i < MAIN; ++i) am[i] = upack + static_cast<size_t>(warp * MAIN + i) * nkp * 32 + lane;
 #pragma unroll
-    for (int x = 0; x < XMW; ++x) {
+    for (int x = 0; x < NX; ++x) {
         const int e = warp + x * MMA_WARPS;
-        hx[x] = e < hp.extras;
-        ax[x] = upack + static_cast<size_t>(hx[x] ? hp.mb + e / 3 : 0) * nkp * 32 + lane;
+        ax[x] = upack + static_cast<size_t>(hp.mb + e / 3) * nkp * 32 + lane;
         xp[x] = e % 3;
+        xa[x][0] = xa[x][1] = 0.0;
     }
-    auto load = [&](int kp, APairH<MAIN, XMW>& p) {
+    auto load = [&](int kp, APairH<MAIN, NX>& p) {
 #pragma unroll
         for (int i = 0; i < MAIN; ++i) p.m[i] = __ldg(am[i] + kp * 32);
 #pragma unroll
-        for (int x = 0; x < XMW; ++x)
-            if (hx[x]) p.x[x] = __ldg(ax[x] + kp * 32);
+        for (int x = 0; x < NX; ++x) p.x[x] = __ldg(ax[x] + kp * 32);
     };
-    auto compute = [&](int kp, const APairH<MAIN, XMW>& c) {
+    auto compute = [&](int kp, const APairH<MAIN, NX>& c) {
 #pragma unroll
         for (int s = 0; s < 2; ++s) {
             const int ks = 2 * kp + s;
@@ -170,17 +176,14 @@ __device__ __forceinline__ void gemm_half(const double2* __restrict__ upack, int
                 for (int p = 0; p < 3; ++p) dmma(acc[i][p][0], acc[i][p][1], a, bv[p]);
             }
 #pragma unroll
-            for (int x = 0; x < XMW; ++x)
-                if (hx[x]) {
-                    const double bx = xp[x] == 0 ? b0 : (xp[x] == 1 ? b1 : b2);
-                    dmma(xacc[x][0], xacc[x][1], s ? c.x[x].y : c.x[x].x, bx);
-                }
+            for (int x = 0; x < NX; ++x) {
+                const double bx = xp[x] == 0 ? b0 : (xp[x] == 1 ? b1 : b2);
+                dmma(xa[x][0], xa[x][1], s ? c.x[x].y : c.x[x].x, bx);
+            }
         }
     };
-#pragma unroll
-    for (int x = 0; x < XMW; ++x) xacc[x][0] = xacc[x][1] = 0.0;
-    if constexpr (MAIN + XMW <= 4) {
-        APairH<MAIN, XMW> p0, p1, p2;  // two operator pairs in flight (L2 latency under load)
+    if constexpr (MAIN + NX <= 4) {
+        APairH<MAIN, NX> p0, p1, p2;  // two operator pairs in flight (L2 latency under load)
         load(0, p0);
         if (nkp > 1) load(1, p1);
         int kp = 0;
@@ -195,7 +198,7 @@ __device__ __forceinline__ void gemm_half(const double2* __restrict__ upack, int
         if (kp < nkp) compute(kp, p0);
         if (kp + 1 < nkp) compute(kp + 1, p1);
     } else {  // wide warps: one pair in flight keeps the accumulators in registers
-        APairH<MAIN, XMW> p0, p1;
+        APairH<MAIN, NX> p0, p1;
         load(0, p0);
         int kp = 0;
         for (; kp + 1 < nkp; kp += 2) {
@@ -205,6 +208,34 @@ __device__ __forceinline__ void gemm_half(const double2* __restrict__ upack, int
             compute(kp + 1, p1);
         }
         if (kp < nkp) compute(kp, p0);
+    }
+#pragma unroll
+    for (int x = 0; x < NX; ++x) {
+        xacc[x][0] = xa[x][0];
+        xacc[x][1] = xa[x][1];
+    }
+}
+
+/// gemm_core for this warp's (uniform) number of extra tiles, 0..XMW.
+template <int MAIN, int XMW>
+__device__ __forceinline__ void gemm_half(const double2* __restrict__ upack, int nkp, const double* fb,
+                                          const HalfPlan& hp, int warp, int lane, double (&acc)[MAIN][3][2],
+                                          double (&xacc)[XMW][2]) {
+    int nx = 0;
+#pragma unroll
+    for (int x = 0; x < XMW; ++x) {
+        xacc[x][0] = xacc[x][1] = 0.0;
+        nx += warp + x * MMA_WARPS < hp.extras ? 1 : 0;
+    }
+    if (nx == 0) {
+        gemm_core<MAIN, 0>(upack, nkp, fb, hp, warp, lane, acc, xacc);
+    } else if (nx == 1 || XMW == 1) {
+        gemm_core<MAIN, 1>(upack, nkp, fb, hp, warp, lane, acc, xacc);
+    } else if constexpr (XMW >= 2) {
+        if (nx == 2 || XMW == 2)
+            gemm_core<MAIN, 2>(upack, nkp, fb, hp, warp, lane, acc, xacc);
+        else if constexpr (XMW >= 3)
+            gemm_core<MAIN, 3>(upack, nkp, fb, hp, warp, lane, acc, xacc);
     }
 }
 
@@ -479,11 +510,21 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
             if (st.exit_flag) break;
             if (st.half_active[h]) {
                 double acc[MAIN][3][2], xacc[XMW][2];
+#if PSWARM_ABLATE == 3  // diagnostic: no DMMA
+                for (int i = 0; i < MAIN; ++i)
+                    for (int p = 0; p < 3; ++p) acc[i][p][0] = acc[i][p][1] = 0.0;
+                for (int x = 0; x < XMW; ++x) xacc[x][0] = xacc[x][1] = 0.0;
+                if (false)
+#endif
                 gemm_half<MAIN, XMW>(a.upack, a.nkp, reinterpret_cast<const double*>(smem_raw + L.fbuf0 + h * fb_bytes),
                                      hp, warp, lane, acc, xacc);
                 WS_PHASE(1);
                 bar_sync(BAR_B0 + h, WS_THREADS);  // b0 of half h (FP group)
                 WS_PHASE(3);
+#if PSWARM_ABLATE == 1  // diagnostic: no epilogue
+                if (acc[0][0][0] == 12345.0) ybuf[0] = xacc[0][0];
+                if (false) {
+#endif
                 // epilogue of this warp's rows: + b0/2 (pc_matrices.hpp:145; b0 was formed by
                 // the FP group with the force), finite check, error vs the previous iterate.
                 // No barrier inside the MMA group: a warp that finishes early runs its
@@ -531,6 +572,9 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
                     atomicMax(&st.slot_err[h * HS + q], static_cast<unsigned long long>(__double_as_longlong(e2)));
                     if (nf != INT_MAX) atomicMin(&st.nf_key[h * HS + q], nf);
                 }
+#if PSWARM_ABLATE == 1
+                }
+#endif
                 WS_PHASE(2);
             } else {
                 bar_sync(BAR_B0 + h, WS_THREADS);  // keep the B_h generations paired
@@ -668,8 +712,8 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
                             retire = true;
                         } else {
                             if (a.rep_hist) a.rep_hist[static_cast<size_t>(gid) * a.max_it + (it - 1)] = gerr_of();
-                            const bool le_tol =
-                                gerr2 <= a.tol2_lo ? true : (gerr2 > a.tol2_hi ? false : gerr_of() <= a.tol);
+                            const bool le_tol = PSWARM_ABLATE == 0 &&  // ablation builds: fixed max_it work
+                                (gerr2 <= a.tol2_lo ? true : (gerr2 > a.tol2_hi ? false : gerr_of() <= a.tol));
                             if (le_tol) {
                                 retire = ok = conv = true;
                             } else if (it >= a.max_it) {
@@ -838,7 +882,11 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
             WS_PHASE(7);
             // ---- force of half h
             const int act_h = (am >> (h * HS)) & 0xF;
+#if PSWARM_ABLATE == 2  // diagnostic: no force
+            if (false) {
+#else
             if (act_h) {
+#endif
                 // slots per force thread: all FP warps stay busy down to N = 64 (the FP warps only
                 // issue in the DMMA stream's gaps, so their count sets the force throughput)
                 double* fbh = reinterpret_cast<double*>(smem_raw + L.fbuf0 + h * fb_bytes);

@@ -8,12 +8,12 @@
 #include "../paper_2301_03989_b200/csrc/pc_slots2.cu"
 using namespace pswarm_dev;
 
-template <int MAIN, int XMW>
+template <int MAIN, int XMW, bool HASX>
 __global__ void __launch_bounds__(512, 1) k_half_loop(const double2* upack, int nkp, int N, int reps, int fp_load,
                                                      double* sink, long long* cycles) {
     extern __shared__ __align__(16) double fbuf[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    for (int i = tid; i < 8 * nkp * HC; i += blockDim.x) fbuf[i] = 1e-3 * (i % 97);
+    for (int i = tid; i < 2 * nkp * FKS; i += blockDim.x) fbuf[i] = 1e-3 * (i % 97);
     __syncthreads();
     HalfPlan hp;
     hp.main = MAIN;
@@ -60,13 +60,15 @@ int main(int argc, char** argv) {
     double2* du; cudaMalloc(&du, hu.size() * 8); cudaMemcpy(du, hu.data(), hu.size() * 8, cudaMemcpyHostToDevice);
     double* sink; cudaMalloc(&sink, 148 * 512 * 8);
     long long* cyc; cudaMalloc(&cyc, 148 * 8);
-    const size_t smem = 8 * nkp * HC * 8;
-    cudaFuncSetAttribute(k_half_loop<3, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const size_t smem = 2 * nkp * FKS * 8;
+    cudaFuncSetAttribute(k_half_loop<3, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_half_loop<3, 1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int reps = 200;
     for (int it = 0; it < 3; ++it) {
         cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
         cudaEventRecord(e0);
-        k_half_loop<3, 1><<<148, 512, smem>>>(du, nkp, N, reps, fp_load, sink, cyc);
+        if (N % 64 == 0 && N < 256) k_half_loop<3, 1, false><<<148, 512, smem>>>(du, nkp, N, reps, fp_load, sink, cyc);
+        else k_half_loop<3, 1, true><<<148, 512, smem>>>(du, nkp, N, reps, fp_load, sink, cyc);
         cudaEventRecord(e1); cudaEventSynchronize(e1);
         float ms; cudaEventElapsedTime(&ms, e0, e1);
         std::vector<long long> hc(148); cudaMemcpy(hc.data(), cyc, 148 * 8, cudaMemcpyDeviceToHost);
