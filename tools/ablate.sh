@@ -1,8 +1,8 @@
 # Diagnostic builds of the library with one phase of k_pc_ws removed (results invalid):
-# 1 = no MMA epilogue, 2 = no force, 3 = no DMMA.  Timing only (tools/probe_ablate.py).
+# 1 = no MMA epilogue (main rows), 2 = no force, 3 = no DMMA, 4 = no b0 GEMV.  Timing only (tools/probe_ablate.py).
 set -e
 cd "$(dirname "$0")/../paper_2301_03989_b200/csrc"
-for k in 1 2 3; do
+for k in 1 2 3 4; do
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++20 -Xcompiler -fPIC,-O3 --expt-relaxed-constexpr \
     -I../../include -I. -DPSWARM_ABLATE=$k -c pc_slots2.cu -o /tmp/pc_slots2_ablate$k.o
   nvcc -gencode arch=compute_100a,code=sm_100a -shared -cudart static -o ../libpswarm_ablate$k.so \

@@ -9,7 +9,7 @@
 using namespace pswarm_dev;
 
 template <int MAIN, int XMW, bool HASX>
-__global__ void __launch_bounds__(512, 1) k_half_loop(const double2* upack, int nkp, int N, int reps, int fp_load,
+__global__ void __launch_bounds__(WS_THREADS, 1) k_half_loop(const double2* upack, int nkp, int N, int reps, int fp_load,
                                                      double* sink, long long* cycles) {
     extern __shared__ __align__(16) double fbuf[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -31,7 +31,7 @@ __global__ void __launch_bounds__(512, 1) k_half_loop(const double2* upack, int 
                 for (int p = 0; p < 3; ++p) s += acc[i][p][0] + acc[i][p][1];
 #pragma unroll
             for (int x = 0; x < XMW; ++x) s += xacc[x][0] + xacc[x][1];
-            asm volatile("bar.sync 1, 256;");
+            asm volatile("bar.sync 1, %0;" ::"n"(MMA_THREADS));
         }
         long long t1 = clock64();
         if (tid == 0) cycles[blockIdx.x] = t1 - t0;
@@ -52,23 +52,29 @@ __global__ void __launch_bounds__(512, 1) k_half_loop(const double2* upack, int 
     sink[blockIdx.x * blockDim.x + tid] = s;
 }
 
+#ifndef MICRO_MAIN
+#define MICRO_MAIN 3
+#define MICRO_XMW 1
+#endif
+constexpr int MM = MICRO_MAIN, XM = MICRO_XMW;
+
 int main(int argc, char** argv) {
     const int fp_load = argc > 1 ? atoi(argv[1]) : 0;
     const int N = argc > 2 ? atoi(argv[2]) : 200, nkp = (N + 7) / 8, mt = (N + 1 + 7) / 8;
     std::vector<double> hu(static_cast<size_t>(mt) * nkp * 64);
     for (size_t i = 0; i < hu.size(); ++i) hu[i] = 1e-4 * ((i * 2654435761u) % 1000);
     double2* du; cudaMalloc(&du, hu.size() * 8); cudaMemcpy(du, hu.data(), hu.size() * 8, cudaMemcpyHostToDevice);
-    double* sink; cudaMalloc(&sink, 148 * 512 * 8);
+    double* sink; cudaMalloc(&sink, 148 * WS_THREADS * 8);
     long long* cyc; cudaMalloc(&cyc, 148 * 8);
     const size_t smem = 2 * nkp * FKS * 8;
-    cudaFuncSetAttribute(k_half_loop<3, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(k_half_loop<3, 1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_half_loop<MM, XM, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_half_loop<MM, XM, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int reps = 200;
     for (int it = 0; it < 3; ++it) {
         cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
         cudaEventRecord(e0);
-        if (N % 64 == 0 && N < 256) k_half_loop<3, 1, false><<<148, 512, smem>>>(du, nkp, N, reps, fp_load, sink, cyc);
-        else k_half_loop<3, 1, true><<<148, 512, smem>>>(du, nkp, N, reps, fp_load, sink, cyc);
+        if (N % 64 == 0 && N < 256) k_half_loop<MM, XM, false><<<148, WS_THREADS, smem>>>(du, nkp, N, reps, fp_load, sink, cyc);
+        else k_half_loop<MM, XM, true><<<148, WS_THREADS, smem>>>(du, nkp, N, reps, fp_load, sink, cyc);
         cudaEventRecord(e1); cudaEventSynchronize(e1);
         float ms; cudaEventElapsedTime(&ms, e0, e1);
         std::vector<long long> hc(148); cudaMemcpy(hc.data(), cyc, 148 * 8, cudaMemcpyDeviceToHost);
