@@ -77,6 +77,9 @@ struct SegArgs {
     unsigned long long* phase_cycles;  // [PHASES] diagnostics or nullptr
     double* hot;                // [M][N][6] hot-start corrections (EXTENSION) or nullptr
     int hot_apply;              // 1: this segment starts from base + correction
+    const double2* upack_fold;  // mirror-folded operator pairs [pair][part][k-pair][lane] or nullptr
+    int nkp_fold;               // k-pairs per folded part
+    const double* anc_fold;     // [8 nkp] anchor weights of the folded F layout
 };
 
 /// Perturbing bodies on the device (ephemeris.hpp:44-73): analytic elements or
@@ -164,10 +167,11 @@ struct RkArgs {
 cudaError_t launch_rk_check(const RkArgs& a, cudaStream_t s);
 
 /// Warp-specialised slot kernel (pc_slots2.cu) for groups of <= 4 trajectories.
-size_t ws_smem_bytes(int N, int nkp, int xrows, int B, int stage_eph);
-int ws_main_tiles(int N);
-int ws_extra_rows(int N);
-bool ws_supported(int N);
+/// fold: mirror-folded update (two half-size contractions, pc_slots2.cu ws_layout notes).
+size_t ws_smem_bytes(int N, int nkp, int xrows, int B, int stage_eph, bool fold);
+int ws_main_tiles(int N, bool fold);
+int ws_extra_rows(int N, bool fold);
+bool ws_supported(int N, bool fold);
 cudaError_t launch_segment_ws(const SegArgs& a, int grid, cudaStream_t s);
 
 GemmPlan make_gemm_plan(int N);

@@ -106,14 +106,26 @@ struct WsLayout {
 
 constexpr int B0_PARTS = FP_WARPS;  // one partial sum per FP warp and b0 column
 
-__host__ __device__ inline WsLayout ws_layout(int N, int nkp, int xrows, int B, int stage_eph) {
+/// Mirror-folded update (fold = 1): U anticommutes with the node reversal
+/// (U[N-1-j][N-1-k] = -U[j][k], Chebyshev-Lobatto nodes are mirrored, chebyshev.hpp:33-43),
+/// so with s_k = F_k + F_{N-1-k} and a_k = F_k - F_{N-1-k} (k < N/2)
+///   Y_j + Y_{N-1-j} = sum_k (U[j][k] - U[j][N-1-k]) a_k,  Y_j - Y_{N-1-j} = sum_k (U[j][k] + U[j][N-1-k]) s_k:
+/// two (N/2) x (N/2) contractions instead of one N x N (half the DMMAs).  Fbuf then holds
+/// s_k at position k and a_{N-1-p} at position p >= N/2; the extra k-steps past N stay zero.
+__host__ __device__ inline int ws_fold_ksteps(int N, int nkp) {
+    const int half = N / 2, nkpf = (half + 7) / 8;
+    const int need = half / 4 + 2 * nkpf;
+    return need > 2 * nkp ? need + (need & 1) : 2 * nkp;
+}
+
+__host__ __device__ inline WsLayout ws_layout(int N, int nkp, int xrows, int B, int stage_eph, int fold) {
     WsLayout L;
     L.ybuf = 0;
     L.fbuf0 = L.ybuf + sizeof(double) * static_cast<size_t>(N) * YS2;
-    const size_t fb = sizeof(double) * static_cast<size_t>(2 * nkp) * FKS;
+    const size_t fb = sizeof(double) * static_cast<size_t>(fold ? ws_fold_ksteps(N, nkp) : 2 * nkp) * FKS;
     L.fbuf1 = L.fbuf0 + fb;
-    L.xstage = L.fbuf1 + fb;  // [2 halves][xrows][HC]
-    L.anchor = L.xstage + sizeof(double) * 2 * static_cast<size_t>(xrows) * HC;
+    L.xstage = L.fbuf1 + fb;  // [2 halves][fold ? 2 : 1][xrows][HC]
+    L.anchor = L.xstage + sizeof(double) * (fold ? 4 : 2) * static_cast<size_t>(xrows) * HC;
     L.b0part = L.anchor + sizeof(double) * static_cast<size_t>(8 * nkp);
     L.eph = L.b0part + sizeof(double) * B0_PARTS * HC;
     L.state = L.eph + (stage_eph ? sizeof(double) * static_cast<size_t>(N) * (3 * B + 3) : 0);
@@ -239,6 +251,117 @@ __device__ __forceinline__ void gemm_half(const double2* __restrict__ upack, int
             gemm_core<MAIN, 2>(upack, nkp, fb, hp, warp, lane, acc, xacc);
         else if constexpr (XMW >= 3)
             gemm_core<MAIN, 3>(upack, nkp, fb, hp, warp, lane, acc, xacc);
+    }
+}
+
+/// Folded counterpart of gemm_core: each of the warp's "tiles" is a pair (rows 8mt..8mt+7
+/// of both half-size operators): acc[.][0] = Y_j + Y_{N-1-j} part (upf part 1, Fbuf
+/// positions >= N/2), acc[.][1] = Y_j - Y_{N-1-j} part (upf part 0, positions < N/2).
+/// upf layout: [pair mt][part][k-pair][lane] double2, nkpf k-pairs per part.
+template <int MAIN, int NX>
+__device__ __forceinline__ void gemm_core_fold(const double2* __restrict__ upf, int nkpf, int half, const double* fb,
+                                               const HalfPlan& hp, int warp, int lane,
+                                               double (&acc)[MAIN][3][2][2], double (*xacc)[2][2]) {
+#pragma unroll
+    for (int i = 0; i < MAIN; ++i)
+#pragma unroll
+        for (int p = 0; p < 3; ++p)
+#pragma unroll
+            for (int u = 0; u < 2; ++u) acc[i][p][u][0] = acc[i][p][u][1] = 0.0;
+    constexpr int XA = NX > 0 ? NX : 1;
+    const double2* am[MAIN][2];
+    const double2* ax[XA][2];
+    int xp[XA];
+    double xa[XA][2][2];
+#pragma unroll
+    for (int i = 0; i < MAIN; ++i)
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+            am[i][u] = upf + (static_cast<size_t>(warp * MAIN + i) * 2 + (1 - u)) * nkpf * 32 + lane;
+#pragma unroll
+    for (int x = 0; x < NX; ++x) {
+        const int e = warp + x * MMA_WARPS;
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            ax[x][u] = upf + (static_cast<size_t>(hp.mb + e / 3) * 2 + (1 - u)) * nkpf * 32 + lane;
+            xa[x][u][0] = xa[x][u][1] = 0.0;
+        }
+        xp[x] = e % 3;
+    }
+    const double* fb_lo = fb + lane;                          // part 0: s at positions < N/2
+    const double* fb_hi = fb + (half >> 2) * FKS + lane;      // part 1: a at positions >= N/2
+    struct Pair {
+        double2 m[MAIN][2];
+        double2 x[XA][2];
+    };
+    auto load = [&](int kp, Pair& c) {
+#pragma unroll
+        for (int i = 0; i < MAIN; ++i)
+#pragma unroll
+            for (int u = 0; u < 2; ++u) c.m[i][u] = __ldg(am[i][u] + kp * 32);
+#pragma unroll
+        for (int x = 0; x < NX; ++x)
+#pragma unroll
+            for (int u = 0; u < 2; ++u) c.x[x][u] = __ldg(ax[x][u] + kp * 32);
+    };
+    auto compute = [&](int kp, const Pair& c) {
+#pragma unroll
+        for (int sub = 0; sub < 2; ++sub) {
+            const int ks = 2 * kp + sub;
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const double* fk = (u ? fb_lo : fb_hi) + ks * FKS;
+                const double b0 = fk[0], b1 = fk[32], b2 = fk[64];
+                const double bv[3] = {b0, b1, b2};
+#pragma unroll
+                for (int i = 0; i < MAIN; ++i) {
+                    const double av = sub ? c.m[i][u].y : c.m[i][u].x;
+#pragma unroll
+                    for (int p = 0; p < 3; ++p) dmma(acc[i][p][u][0], acc[i][p][u][1], av, bv[p]);
+                }
+#pragma unroll
+                for (int x = 0; x < NX; ++x) {
+                    const double bx = xp[x] == 0 ? b0 : (xp[x] == 1 ? b1 : b2);
+                    dmma(xa[x][u][0], xa[x][u][1], sub ? c.x[x][u].y : c.x[x][u].x, bx);
+                }
+            }
+        }
+    };
+    Pair p0, p1;  // one k-pair in flight: two operator parts per tile
+    load(0, p0);
+    int kp = 0;
+    for (; kp + 1 < nkpf; kp += 2) {
+        load(kp + 1, p1);
+        compute(kp, p0);
+        if (kp + 2 < nkpf) load(kp + 2, p0);
+        compute(kp + 1, p1);
+    }
+    if (kp < nkpf) compute(kp, p0);
+#pragma unroll
+    for (int x = 0; x < NX; ++x)
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            xacc[x][u][0] = xa[x][u][0];
+            xacc[x][u][1] = xa[x][u][1];
+        }
+}
+
+template <int MAIN, int XMW>
+__device__ __forceinline__ void gemm_half_fold(const double2* __restrict__ upf, int nkpf, int half, const double* fb,
+                                               const HalfPlan& hp, int warp, int lane,
+                                               double (&acc)[MAIN][3][2][2], double (&xacc)[XMW][2][2]) {
+    int nx = 0;
+#pragma unroll
+    for (int x = 0; x < XMW; ++x) {
+        xacc[x][0][0] = xacc[x][0][1] = xacc[x][1][0] = xacc[x][1][1] = 0.0;
+        nx += warp + x * MMA_WARPS < hp.extras ? 1 : 0;
+    }
+    if (nx == 0) {
+        gemm_core_fold<MAIN, 0>(upf, nkpf, half, fb, hp, warp, lane, acc, xacc);
+    } else if (nx == 1 || XMW == 1) {
+        gemm_core_fold<MAIN, 1>(upf, nkpf, half, fb, hp, warp, lane, acc, xacc);
+    } else if constexpr (XMW >= 2) {
+        gemm_core_fold<MAIN, 2>(upf, nkpf, half, fb, hp, warp, lane, acc, xacc);
     }
 }
 
@@ -428,23 +551,14 @@ __device__ __forceinline__ void force_half(const ForceData& fd, const double* yb
 
 }  // namespace
 
-size_t ws_smem_bytes(int N, int nkp, int xrows, int B, int stage_eph) {
-    return ws_layout(N, nkp, xrows, B, stage_eph).total;
-}
 
-int ws_main_tiles(int N) { return ((N + 7) / 8) / MMA_WARPS; }
-
-int ws_extra_rows(int N) {
-    const int r = N - ws_main_tiles(N) * MMA_WARPS * 8;
-    return r > 0 ? r : 0;
-}
-
-template <int MAIN, int XMW, bool STAGE, bool REL>
+template <int MAIN, int XMW, bool STAGE, bool REL, bool FOLD>
 __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int N = a.N, B = a.fd.n_bodies;
     const int xrows = a.xrows;
-    const WsLayout L = ws_layout(N, a.nkp, xrows, B, STAGE ? 1 : 0);
+    const int half = N / 2;
+    const WsLayout L = ws_layout(N, a.nkp, xrows, B, STAGE ? 1 : 0, FOLD ? 1 : 0);
     double* ybuf = reinterpret_cast<double*>(smem_raw + L.ybuf);
     const size_t fb_bytes = L.fbuf1 - L.fbuf0;
     double* fb0 = reinterpret_cast<double*>(smem_raw + L.fbuf0);
@@ -455,7 +569,8 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
     WsState& st = *reinterpret_cast<WsState*>(smem_raw + L.state);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int KP = 8 * a.nkp;
-    const int mtiles = (N + 7) / 8;  // node rows only: b0 comes from the FP group's anchor GEMV
+    // node rows only (b0 comes from the FP group's anchor GEMV); folded: row pairs
+    const int mtiles = FOLD ? (half + 7) / 8 : (N + 7) / 8;
     const bool prof = a.phase_cycles != nullptr;
     const bool stamp = tid == 0 || tid == MMA_THREADS;
     // phase counters live in shared memory (no registers / local memory on the hot path)
@@ -468,8 +583,11 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
     hp.mb = MAIN * MMA_WARPS;
     hp.extras = (mtiles - hp.mb) * 3;
 
-    for (int i = tid; i < 2 * 2 * a.nkp * FKS; i += WS_THREADS) fb0[i] = 0.0;  // both halves (contiguous)
-    {  // anchor_op row (pc_matrices.hpp:98-100) = row N of the packed operator
+    const int fb_doubles = (FOLD ? ws_fold_ksteps(N, a.nkp) : 2 * a.nkp) * FKS;
+    for (int i = tid; i < 2 * fb_doubles; i += WS_THREADS) fb0[i] = 0.0;  // both halves (contiguous)
+    if (FOLD) {  // anchor weights of the folded F layout (s at k, a at p >= N/2)
+        for (int k = tid; k < KP; k += WS_THREADS) anc[k] = k < N ? a.anc_fold[k] : 0.0;
+    } else {  // anchor_op row (pc_matrices.hpp:98-100) = row N of the packed operator
         const double* up = reinterpret_cast<const double*>(a.upack);
         const int amt = N >> 3, ag = N & 7;
         for (int k = tid; k < KP; k += WS_THREADS)
@@ -512,6 +630,72 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
             WS_PHASE(0);
             if (st.exit_flag) break;
             if (st.half_active[h]) {
+                if constexpr (FOLD) {
+                    double facc[MAIN][3][2][2], fxacc[XMW][2][2];
+                    gemm_half_fold<MAIN, XMW>(a.upack_fold, a.nkp_fold, half,
+                                              reinterpret_cast<const double*>(smem_raw + L.fbuf0 + h * fb_bytes), hp,
+                                              warp, lane, facc, fxacc);
+                    WS_PHASE(1);
+                    bar_sync(BAR_B0 + h, WS_THREADS);  // b0 of half h (FP group)
+                    WS_PHASE(3);
+                    // unfold: Y_j = acc_sum + acc_diff, Y_{N-1-j} = acc_sum - acc_diff (the 1/2 sits in
+                    // the packed operators), then the same epilogue as the dense path for both rows
+                    const int act_h = (st.act_word[h] >> (h * HS)) & 0xF;
+                    const double* b0 = st.b0h[h];
+                    const double w2 = a.omega2;
+                    double bn = 0.0, bd = 1.0;
+                    int nf = INT_MAX;
+#pragma unroll
+                    for (int i = 0; i < MAIN; ++i) {
+                        const int j = (warp * MAIN + i) * 8 + g, jm = N - 1 - j;
+                        if (j >= half || !((act_h >> q) & 1)) continue;
+                        double ylo[6], yhi[6], olo[6], ohi[6];
+#pragma unroll
+                        for (int p = 0; p < 3; ++p)
+#pragma unroll
+                            for (int e = 0; e < 2; ++e) {
+                                const int c = 2 * p + e;
+                                const double bb = b0[p * 8 + 2 * q + e];
+                                ylo[c] = fma(w2, facc[i][p][0][e] + facc[i][p][1][e], bb);
+                                yhi[c] = fma(w2, facc[i][p][0][e] - facc[i][p][1][e], bb);
+                                olo[c] = ybuf[y2(j, h, c, q)];
+                                ohi[c] = ybuf[y2(jm, h, c, q)];
+                            }
+                        update_sample(ylo, olo, j, a.error_mode, bn, bd, nf);
+                        update_sample(yhi, ohi, jm, a.error_mode, bn, bd, nf);
+#pragma unroll
+                        for (int c = 0; c < 6; ++c) {
+                            ybuf[y2(j, h, c, q)] = ylo[c];
+                            ybuf[y2(jm, h, c, q)] = yhi[c];
+                        }
+                    }
+                    double* xs_lo = xstage + (2 * h) * xrows * HC;
+                    double* xs_hi = xs_lo + xrows * HC;
+#pragma unroll
+                    for (int x = 0; x < XMW; ++x) {  // extra pair tiles -> stage (both mirrored rows)
+                        const int ex = warp + x * MMA_WARPS;
+                        if (ex >= hp.extras) continue;
+                        const int j = (hp.mb + ex / 3) * 8 + g, p = ex % 3;
+                        if (j >= half) continue;
+#pragma unroll
+                        for (int e = 0; e < 2; ++e) {
+                            const double bb = b0[p * 8 + 2 * q + e];
+                            const int o = (j - hp.mb * 8) * HC + q * 6 + 2 * p + e;
+                            xs_lo[o] = fma(w2, fxacc[x][0][e] + fxacc[x][1][e], bb);
+                            xs_hi[o] = fma(w2, fxacc[x][0][e] - fxacc[x][1][e], bb);
+                        }
+                    }
+                    double e2 = bn / bd;
+#pragma unroll
+                    for (int off = 4; off < 32; off <<= 1) {
+                        e2 = fmax(e2, __shfl_xor_sync(0xffffffffu, e2, off));
+                        nf = min(nf, __shfl_xor_sync(0xffffffffu, nf, off));
+                    }
+                    if (g == 0 && ((act_h >> q) & 1)) {
+                        atomicMax(&st.slot_err[h * HS + q], static_cast<unsigned long long>(__double_as_longlong(e2)));
+                        if (nf != INT_MAX) atomicMin(&st.nf_key[h * HS + q], nf);
+                    }
+                } else {
                 double acc[MAIN][3][2], xacc[XMW][2];
 #if PSWARM_ABLATE == 3  // diagnostic: no DMMA
                 for (int i = 0; i < MAIN; ++i)
@@ -581,6 +765,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
                     atomicMax(&st.slot_err[h * HS + q], static_cast<unsigned long long>(__double_as_longlong(e2)));
                     if (nf != INT_MAX) atomicMin(&st.nf_key[h * HS + q], nf);
                 }
+                }
                 WS_PHASE(2);
             } else {
                 bar_sync(BAR_B0 + h, WS_THREADS);  // keep the B_h generations paired
@@ -598,9 +783,12 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
             // ---- staged rows of half h (node rows whose components sit in several MMA warps)
             if (!first[h] && xrows > 0 && st.half_active[h]) {
                 const int act_h = (st.act_word[h] >> (h * HS)) & 0xF;
-                const double* xs = xstage + h * xrows * HC;
-                for (int i = ft; i < xrows * HS; i += FP_THREADS) {
-                    const int r = i >> 2, s = i & 3, j = MAIN * MMA_WARPS * 8 + r;
+                const int nitems = xrows * HS * (FOLD ? 2 : 1);  // folded: each pair row and its mirror
+                for (int i = ft; i < nitems; i += FP_THREADS) {
+                    const int mir = FOLD ? i / (xrows * HS) : 0, ii = i - mir * xrows * HS;
+                    const int r = ii >> 2, s = ii & 3;
+                    const int j = mir ? N - 1 - (MAIN * MMA_WARPS * 8 + r) : MAIN * MMA_WARPS * 8 + r;
+                    const double* xs = xstage + (FOLD ? 2 * h + mir : h) * xrows * HC;
                     if (!((act_h >> s) & 1)) continue;
                     double yn[6], yo[6];
 #pragma unroll
@@ -616,7 +804,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
                     atomicMax(&st.slot_err[h * HS + s], static_cast<unsigned long long>(__double_as_longlong(sbn / sbd)));
                     if (snf != INT_MAX) atomicMin(&st.nf_key[h * HS + s], snf);
                 }
-                if (xrows * HS > 32)
+                if (xrows * HS * (FOLD ? 2 : 1) > 32)
                     bar_sync(BAR_FP, FP_THREADS);
                 else
                     __syncwarp();  // warp 0 staged every row and also takes the decisions
@@ -922,6 +1110,20 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
                 }
             }
             bar_sync(BAR_FP, FP_THREADS);
+            if constexpr (FOLD) {  // fold F in place: s_k at position k, a_k = F_k - F_{N-1-k} at N-1-k
+                if (act_h) {
+                    double* fbh = reinterpret_cast<double*>(smem_raw + L.fbuf0 + h * fb_bytes);
+                    for (int i = ft; i < half * HC; i += FP_THREADS) {
+                        const int k = i % half, col = i / half;
+                        const int c = 2 * (col >> 3) + (col & 1), sl = (col & 7) >> 1;
+                        const int lo = f2(k, c, sl), hi = f2(N - 1 - k, c, sl);
+                        const double flo = fbh[lo], fhi = fbh[hi];
+                        fbh[lo] = flo + fhi;
+                        fbh[hi] = flo - fhi;
+                    }
+                }
+                bar_sync(BAR_FP, FP_THREADS);
+            }
             if (ft < HS && st.sing_key[h * HS + ft] != INT_MAX) {
                 const int t = h * HS + ft, key = st.sing_key[t], j = key / (B + 1), chk = key % (B + 1);
                 st.sing_val[t] =
@@ -981,30 +1183,55 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
     }
 }
 
-template <int MAIN, int XMW>
+template <int MAIN, int XMW, bool FOLD = false>
 static cudaError_t launch_ws_t(const SegArgs& a, int grid, size_t smem, cudaStream_t s) {
     // relativistic launches never stage the ephemeris (the host clears stage_eph)
-    auto kern = a.fd.rel ? k_pc_ws<MAIN, XMW, false, true>
-                         : (a.stage_eph ? k_pc_ws<MAIN, XMW, true, false> : k_pc_ws<MAIN, XMW, false, false>);
+    auto kern = a.fd.rel ? k_pc_ws<MAIN, XMW, false, true, FOLD>
+                         : (a.stage_eph ? k_pc_ws<MAIN, XMW, true, false, FOLD> : k_pc_ws<MAIN, XMW, false, false, FOLD>);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     kern<<<grid, WS_THREADS, smem, s>>>(a);
     return cudaGetLastError();
 }
 
+/// Tiles of one half: m-tiles of node rows, or (folded) of row pairs.
+static int ws_mtiles(int N, bool fold) { return fold ? (N / 2 + 7) / 8 : (N + 7) / 8; }
+int ws_main_tiles(int N, bool fold) { return ws_mtiles(N, fold) / MMA_WARPS; }
 /// Extra (m-tile, n-tile) tiles beyond the MAIN full-width m-tiles of every MMA warp.
-static int ws_extras(int N) { return ((N + 7) / 8 - ws_main_tiles(N) * MMA_WARPS) * 3; }
+static int ws_extras(int N, bool fold) { return (ws_mtiles(N, fold) - ws_main_tiles(N, fold) * MMA_WARPS) * 3; }
 
-bool ws_supported(int N) {
-    const int main = ws_main_tiles(N);
-    return main >= 1 && main <= 4 && ws_extras(N) <= 3 * MMA_WARPS && (main < 4 || ws_extras(N) <= MMA_WARPS);
+int ws_extra_rows(int N, bool fold) {
+    const int rows = fold ? N / 2 : N;
+    const int r = rows - ws_main_tiles(N, fold) * MMA_WARPS * 8;
+    return r > 0 ? r : 0;
+}
+
+bool ws_supported(int N, bool fold) {
+    const int main = ws_main_tiles(N, fold);
+    if (fold)  // even k-steps per part, 1-2 pair tiles per warp, <= 2 extra pair tiles
+        return N % 8 == 0 && main >= 1 && main <= 2 && ws_extras(N, true) <= 2 * MMA_WARPS;
+    return main >= 1 && main <= 4 && ws_extras(N, false) <= 3 * MMA_WARPS && (main < 4 || ws_extras(N, false) <= MMA_WARPS);
+}
+
+size_t ws_smem_bytes(int N, int nkp, int xrows, int B, int stage_eph, bool fold) {
+    return ws_layout(N, nkp, xrows, B, stage_eph, fold ? 1 : 0).total;
 }
 
 cudaError_t launch_segment_ws(const SegArgs& a, int grid, cudaStream_t s) {
-    if (!ws_supported(a.N)) return cudaErrorNotSupported;
-    const int main = ws_main_tiles(a.N);
-    const int xmw = std::max(1, (ws_extras(a.N) + MMA_WARPS - 1) / MMA_WARPS);
-    const size_t smem = ws_smem_bytes(a.N, a.nkp, a.xrows, a.fd.n_bodies, a.stage_eph);
+    const bool fold = a.upack_fold != nullptr;
+    if (!ws_supported(a.N, fold)) return cudaErrorNotSupported;
+    const int main = ws_main_tiles(a.N, fold);
+    const int xmw = std::max(1, (ws_extras(a.N, fold) + MMA_WARPS - 1) / MMA_WARPS);
+    const size_t smem = ws_smem_bytes(a.N, a.nkp, a.xrows, a.fd.n_bodies, a.stage_eph, fold);
+    if (fold) {
+        switch (main * 4 + xmw) {
+        case 5: return launch_ws_t<1, 1, true>(a, grid, smem, s);
+        case 6: return launch_ws_t<1, 2, true>(a, grid, smem, s);
+        case 9: return launch_ws_t<2, 1, true>(a, grid, smem, s);
+        case 10: return launch_ws_t<2, 2, true>(a, grid, smem, s);
+        default: return cudaErrorNotSupported;
+        }
+    }
     switch (main * 4 + xmw) {
     case 5: return launch_ws_t<1, 1>(a, grid, smem, s);
     case 6: return launch_ws_t<1, 2>(a, grid, smem, s);

@@ -140,6 +140,10 @@ struct OpPack {
     DevBuf buf;
     int nkp = 0;
     GemmPlan gp{};
+    // mirror-folded operators (even N, N % 8 == 0): [pair][part][k-pair][lane] double2 + the
+    // anchor weights of the folded F layout (pc_slots2.cu ws_layout notes)
+    DevBuf fold, anc_fold;
+    int nkp_fold = 0;
 };
 
 enum BufId {
@@ -201,6 +205,7 @@ struct pswarm_ctx {
     const char* last_kernel = "";
     int slot_kernel = 0;  // 0 auto, 1 generic k_pc_segment, 2 warp-specialised k_pc_ws
     int poison_outputs = 0;  // 1: NaN-fill device outputs before each solve (tests)
+    int fold = 1;            // 1: mirror-folded update when N % 8 == 0 (k_pc_ws_fold)
     unsigned long long phase_host[pswarm_dev::PHASES] = {};
     PinnedBuf pin_in, pin_rep, pin_term;
     // wide-group path
@@ -244,6 +249,36 @@ const OpPack& operators(pswarm_ctx* ctx, Index n) {
     p->gp = gp;
     double* d = p->buf.get<double>(host.size());
     cuda_check(cudaMemcpy(d, host.data(), host.size() * sizeof(double), cudaMemcpyHostToDevice), "upload operators");
+    if (n % 8 == 0) {  // U anticommutes with the node reversal: two half-size operators
+        const int half = static_cast<int>(n / 2), np = (half + 7) / 8, nkpf = (half + 7) / 8;
+        auto G = [&](int part, int r, int k) -> double {  // 1/2 folded into the operator
+            if (r >= half || k >= half) return 0.0;
+            if (part == 0) return 0.5 * (mats->update_op(r, k) + mats->update_op(r, n - 1 - k));  // -> Y_r - Y_{N-1-r}
+            const int pos = half + k;                                                           // a at pos >= N/2
+            return 0.5 * (mats->update_op(r, n - 1 - pos) - mats->update_op(r, pos));          // -> Y_r + Y_{N-1-r}
+        };
+        std::vector<double> hf(static_cast<size_t>(np) * 2 * nkpf * 32 * 2);
+        for (int m = 0; m < np; ++m)
+            for (int part = 0; part < 2; ++part)
+                for (int kp = 0; kp < nkpf; ++kp)
+                    for (int lane = 0; lane < 32; ++lane) {
+                        const int g = lane >> 2, q = lane & 3;
+                        const size_t idx = ((static_cast<size_t>(m) * 2 + part) * nkpf + kp) * 32 + lane;
+                        hf[2 * idx] = G(part, m * 8 + g, kp * 8 + q);
+                        hf[2 * idx + 1] = G(part, m * 8 + g, kp * 8 + 4 + q);
+                    }
+        std::vector<double> af(static_cast<size_t>(8 * nkp), 0.0);
+        for (int k = 0; k < n; ++k)
+            af[k] = k < half ? 0.5 * (mats->anchor_op[k] + mats->anchor_op[n - 1 - k])
+                             : 0.5 * (mats->anchor_op[n - 1 - k] - mats->anchor_op[k]);
+        p->nkp_fold = nkpf;
+        cuda_check(cudaMemcpy(p->fold.get<double>(hf.size()), hf.data(), hf.size() * sizeof(double),
+                              cudaMemcpyHostToDevice),
+                   "upload folded operators");
+        cuda_check(cudaMemcpy(p->anc_fold.get<double>(af.size()), af.data(), af.size() * sizeof(double),
+                              cudaMemcpyHostToDevice),
+                   "upload folded anchor");
+    }
     return *ctx->ops.emplace(n, std::move(p)).first->second;
 }
 
@@ -554,16 +589,20 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
     // the generic slot kernel (groups <= 8), or the wide-group path
     constexpr size_t SMEM_MAX = 227 * 1024;
     const int Ni = static_cast<int>(N);
-    const bool use_ws = !wide && gmax <= 4 && ws_supported(Ni) && ctx->slot_kernel != 1 &&
-                        ws_smem_bytes(Ni, op.nkp, ws_extra_rows(Ni), nb, 0) <= SMEM_MAX;
-    const int xrows = use_ws ? ws_extra_rows(Ni) : extra_rows(Ni, op.gp);
-    ctx->last_kernel = wide ? "k_wide_iter" : use_ws ? "k_pc_ws" : "k_pc_segment";
+    // mirror-folded update when N allows it (half the DMMAs); "fold" option 0 forces the dense one
+    const bool fold = !wide && gmax <= 4 && ctx->fold && op.nkp_fold > 0 && ws_supported(Ni, true) &&
+                      ctx->slot_kernel != 1 &&
+                      ws_smem_bytes(Ni, op.nkp, ws_extra_rows(Ni, true), nb, 0, true) <= SMEM_MAX;
+    const bool use_ws = fold || (!wide && gmax <= 4 && ws_supported(Ni, false) && ctx->slot_kernel != 1 &&
+                                 ws_smem_bytes(Ni, op.nkp, ws_extra_rows(Ni, false), nb, 0, false) <= SMEM_MAX);
+    const int xrows = use_ws ? ws_extra_rows(Ni, fold) : extra_rows(Ni, op.gp);
+    ctx->last_kernel = wide ? "k_wide_iter" : fold ? "k_pc_ws_fold" : use_ws ? "k_pc_ws" : "k_pc_segment";
     // stage the frozen ephemeris in shared memory when it fits next to the state blocks
-    const int stage_eph =
-        nb > 0 && !rel && (use_ws ? ws_smem_bytes(Ni, op.nkp, xrows, nb, 1) : segment_smem_bytes(Ni, op.nkp, xrows, nb, 1)) <=
-                      SMEM_MAX
-            ? 1
-            : 0;
+    const int stage_eph = nb > 0 && !rel &&
+                                  (use_ws ? ws_smem_bytes(Ni, op.nkp, xrows, nb, 1, fold)
+                                          : segment_smem_bytes(Ni, op.nkp, xrows, nb, 1)) <= SMEM_MAX
+                              ? 1
+                              : 0;
     if (!wide && !use_ws && segment_smem_bytes(Ni, op.nkp, xrows, nb, stage_eph) > SMEM_MAX)
         raise(PSWARM_ERR_INVALID_SIZE, fmtf("propagate: %lld nodes exceed the per-SM shared memory of the slot kernel",
                                             (long long)N));
@@ -694,6 +733,9 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
                       std::abs((boundaries[seg + 1] - boundaries[seg]) - (boundaries[seg] - boundaries[seg - 1])) <=
                           1e-9 * std::abs(boundaries[seg] - boundaries[seg - 1]);
         a.phase_cycles = d_phase;
+        a.upack_fold = fold ? reinterpret_cast<const double2*>(op.fold.p) : nullptr;
+        a.nkp_fold = op.nkp_fold;
+        a.anc_fold = fold ? reinterpret_cast<const double*>(op.anc_fold.p) : nullptr;
         if (max_it > 0 && !wide) {
             cuda_check(cudaEventRecord(ctx->evk0, st), "event");
             cuda_check(use_ws ? launch_segment_ws(a, grid, st) : launch_segment(a, grid, st), "slot kernel launch");
@@ -1032,6 +1074,7 @@ pswarm_status pswarm_set_option(pswarm_ctx* ctx, const char* key, int64_t value)
         else if (k == "profile_phases") ctx->profile_phases = value != 0;
         else if (k == "slot_kernel") ctx->slot_kernel = static_cast<int>(value);
         else if (k == "poison_outputs") ctx->poison_outputs = value != 0;
+        else if (k == "fold") ctx->fold = value != 0;
         else raise(PSWARM_ERR_GENERIC, "pswarm_set_option: unknown key '" + k + "'");
     });
 }

@@ -260,3 +260,22 @@ def test_pinned_samples_overlapped_copy_identical(ctx):
     assert a.trajectories is buf
     assert np.array_equal(a.trajectories, b.trajectories)
     assert np.array_equal(a.terminal_states, b.terminal_states)
+
+
+@pytest.mark.parametrize("n", [128, 200, 256])
+@pytest.mark.parametrize("fold", [1, 0])
+def test_mirror_folded_and_dense_updates(ctx, oracle, n, fold):
+    """The slot kernel's Picard update folded over the Chebyshev mirror symmetry
+    (half the DMMAs, default where N % 8 == 0) and the dense update both match the
+    oracle; the kernel that ran is the one selected."""
+    states, plan, cfg = _setup(24, n, 0.87, "planets8")
+    ctx.set_option("fold", fold)
+    try:
+        got = ctx.run_batch(states, cfg, plan, "independent")
+        name = ctx.kernel_name()
+    finally:
+        ctx.set_option("fold", 1)
+    assert name == ("k_pc_ws_fold" if fold else "k_pc_ws")
+    want = oracle.run_batch(states, cfg, plan, "independent", 8)
+    _parity(got, want)
+    assert got.converged.all()
