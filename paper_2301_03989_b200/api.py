@@ -359,7 +359,7 @@ class Context:
     PHASE_NAMES = ("claim", "warm_start", "force", "dmma", "anchor_barrier", "epilogue", "staged_epilogue",
                    "decisions", "retire")
     WS_PHASE_NAMES = ("mma_wait_f", "mma_dmma", "mma_epilogue", "mma_wait_b0", "fp_wait_y", "fp_staged_decisions",
-                      "fp_retire_claim", "fp_warm_start", "fp_force", "fp_b0")
+                      "fp_retire_claim", "fp_warm_start", "fp_force", "fp_b0", "fp_staged")
     N_PHASES = 12
 
     def phase_cycles(self) -> dict:
@@ -367,7 +367,7 @@ class Context:
         named after the solver kernel that ran."""
         buf = (C.c_uint64 * self.N_PHASES)()
         self.lib.pswarm_get_phase_cycles(self.ptr, buf, self.N_PHASES)
-        names = self.WS_PHASE_NAMES if self.kernel_name() == "k_pc_ws" else self.PHASE_NAMES
+        names = self.WS_PHASE_NAMES if self.kernel_name().startswith("k_pc_ws") else self.PHASE_NAMES
         d = {n: int(buf[k]) for k, n in enumerate(names)}
         d["ctas"] = int(buf[self.N_PHASES - 1])
         return d

@@ -124,8 +124,8 @@ __host__ __device__ inline WsLayout ws_layout(int N, int nkp, int xrows, int B, 
     L.fbuf0 = L.ybuf + sizeof(double) * static_cast<size_t>(N) * YS2;
     const size_t fb = sizeof(double) * static_cast<size_t>(fold ? ws_fold_ksteps(N, nkp) : 2 * nkp) * FKS;
     L.fbuf1 = L.fbuf0 + fb;
-    L.xstage = L.fbuf1 + fb;  // [2 halves][fold ? 2 : 1][xrows][HC]
-    L.anchor = L.xstage + sizeof(double) * (fold ? 4 : 2) * static_cast<size_t>(xrows) * HC;
+    L.xstage = L.fbuf1 + fb;  // [2 halves][xrows][HC]
+    L.anchor = L.xstage + sizeof(double) * 2 * static_cast<size_t>(xrows) * HC;
     L.b0part = L.anchor + sizeof(double) * static_cast<size_t>(8 * nkp);
     L.eph = L.b0part + sizeof(double) * B0_PARTS * HC;
     L.state = L.eph + (stage_eph ? sizeof(double) * static_cast<size_t>(N) * (3 * B + 3) : 0);
@@ -254,55 +254,30 @@ __device__ __forceinline__ void gemm_half(const double2* __restrict__ upack, int
     }
 }
 
-/// Folded counterpart of gemm_core: each of the warp's "tiles" is a pair (rows 8mt..8mt+7
-/// of both half-size operators): acc[.][0] = Y_j + Y_{N-1-j} part (upf part 1, Fbuf
-/// positions >= N/2), acc[.][1] = Y_j - Y_{N-1-j} part (upf part 0, positions < N/2).
-/// upf layout: [pair mt][part][k-pair][lane] double2, nkpf k-pairs per part.
-template <int MAIN, int NX>
+/// Folded counterpart of gemm_core: each of the warp's NV tiles is a pair tile (rows
+/// 8mt..8mt+7 of both half-size operators), mt = warp + i * MMA_WARPS (strided, so the four
+/// SMSPs carry equal DMMA streams to within one tile): acc[.][.][0] = Y_j + Y_{N-1-j} part
+/// (upf part 1, Fbuf positions >= N/2), acc[.][.][1] = Y_j - Y_{N-1-j} part (upf part 0,
+/// positions < N/2).  upf layout: [pair mt][part][k-pair][lane] double2, nkpf k-pairs per part.
+template <int NV, int MAIN>
 __device__ __forceinline__ void gemm_core_fold(const double2* __restrict__ upf, int nkpf, int half, const double* fb,
-                                               const HalfPlan& hp, int warp, int lane,
-                                               double (&acc)[MAIN][3][2][2], double (*xacc)[2][2]) {
+                                               int warp, int lane, double (&acc)[MAIN][3][2][2]) {
+    const double2* am[NV][2];
 #pragma unroll
-    for (int i = 0; i < MAIN; ++i)
-#pragma unroll
-        for (int p = 0; p < 3; ++p)
-#pragma unroll
-            for (int u = 0; u < 2; ++u) acc[i][p][u][0] = acc[i][p][u][1] = 0.0;
-    constexpr int XA = NX > 0 ? NX : 1;
-    const double2* am[MAIN][2];
-    const double2* ax[XA][2];
-    int xp[XA];
-    double xa[XA][2][2];
-#pragma unroll
-    for (int i = 0; i < MAIN; ++i)
+    for (int i = 0; i < NV; ++i)
 #pragma unroll
         for (int u = 0; u < 2; ++u)
-            am[i][u] = upf + (static_cast<size_t>(warp * MAIN + i) * 2 + (1 - u)) * nkpf * 32 + lane;
-#pragma unroll
-    for (int x = 0; x < NX; ++x) {
-        const int e = warp + x * MMA_WARPS;
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-            ax[x][u] = upf + (static_cast<size_t>(hp.mb + e / 3) * 2 + (1 - u)) * nkpf * 32 + lane;
-            xa[x][u][0] = xa[x][u][1] = 0.0;
-        }
-        xp[x] = e % 3;
-    }
+            am[i][u] = upf + (static_cast<size_t>(warp + i * MMA_WARPS) * 2 + (1 - u)) * nkpf * 32 + lane;
     const double* fb_lo = fb + lane;                          // part 0: s at positions < N/2
     const double* fb_hi = fb + (half >> 2) * FKS + lane;      // part 1: a at positions >= N/2
     struct Pair {
-        double2 m[MAIN][2];
-        double2 x[XA][2];
+        double2 m[NV][2];
     };
     auto load = [&](int kp, Pair& c) {
 #pragma unroll
-        for (int i = 0; i < MAIN; ++i)
+        for (int i = 0; i < NV; ++i)
 #pragma unroll
             for (int u = 0; u < 2; ++u) c.m[i][u] = __ldg(am[i][u] + kp * 32);
-#pragma unroll
-        for (int x = 0; x < NX; ++x)
-#pragma unroll
-            for (int u = 0; u < 2; ++u) c.x[x][u] = __ldg(ax[x][u] + kp * 32);
     };
     auto compute = [&](int kp, const Pair& c) {
 #pragma unroll
@@ -311,18 +286,12 @@ __device__ __forceinline__ void gemm_core_fold(const double2* __restrict__ upf, 
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
                 const double* fk = (u ? fb_lo : fb_hi) + ks * FKS;
-                const double b0 = fk[0], b1 = fk[32], b2 = fk[64];
-                const double bv[3] = {b0, b1, b2};
+                const double bv[3] = {fk[0], fk[32], fk[64]};
 #pragma unroll
-                for (int i = 0; i < MAIN; ++i) {
+                for (int i = 0; i < NV; ++i) {
                     const double av = sub ? c.m[i][u].y : c.m[i][u].x;
 #pragma unroll
                     for (int p = 0; p < 3; ++p) dmma(acc[i][p][u][0], acc[i][p][u][1], av, bv[p]);
-                }
-#pragma unroll
-                for (int x = 0; x < NX; ++x) {
-                    const double bx = xp[x] == 0 ? b0 : (xp[x] == 1 ? b1 : b2);
-                    dmma(xa[x][u][0], xa[x][u][1], sub ? c.x[x][u].y : c.x[x][u].x, bx);
                 }
             }
         }
@@ -337,31 +306,23 @@ __device__ __forceinline__ void gemm_core_fold(const double2* __restrict__ upf, 
         compute(kp + 1, p1);
     }
     if (kp < nkpf) compute(kp, p0);
-#pragma unroll
-    for (int x = 0; x < NX; ++x)
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-            xacc[x][u][0] = xa[x][u][0];
-            xacc[x][u][1] = xa[x][u][1];
-        }
 }
 
-template <int MAIN, int XMW>
+/// gemm_core_fold for this warp's number of valid pair tiles (0..MAIN).
+template <int MAIN>
 __device__ __forceinline__ void gemm_half_fold(const double2* __restrict__ upf, int nkpf, int half, const double* fb,
-                                               const HalfPlan& hp, int warp, int lane,
-                                               double (&acc)[MAIN][3][2][2], double (&xacc)[XMW][2][2]) {
-    int nx = 0;
+                                               int mtiles, int warp, int lane, double (&acc)[MAIN][3][2][2]) {
 #pragma unroll
-    for (int x = 0; x < XMW; ++x) {
-        xacc[x][0][0] = xacc[x][0][1] = xacc[x][1][0] = xacc[x][1][1] = 0.0;
-        nx += warp + x * MMA_WARPS < hp.extras ? 1 : 0;
-    }
-    if (nx == 0) {
-        gemm_core_fold<MAIN, 0>(upf, nkpf, half, fb, hp, warp, lane, acc, xacc);
-    } else if (nx == 1 || XMW == 1) {
-        gemm_core_fold<MAIN, 1>(upf, nkpf, half, fb, hp, warp, lane, acc, xacc);
-    } else if constexpr (XMW >= 2) {
-        gemm_core_fold<MAIN, 2>(upf, nkpf, half, fb, hp, warp, lane, acc, xacc);
+    for (int i = 0; i < MAIN; ++i)
+#pragma unroll
+        for (int p = 0; p < 3; ++p)
+#pragma unroll
+            for (int u = 0; u < 2; ++u) acc[i][p][u][0] = acc[i][p][u][1] = 0.0;
+    if (PSWARM_ABLATE == 3) return;  // diagnostic: no DMMA
+    if (warp + (MAIN - 1) * MMA_WARPS < mtiles)
+        gemm_core_fold<MAIN, MAIN>(upf, nkpf, half, fb, warp, lane, acc);
+    else if constexpr (MAIN >= 2) {
+        if (warp < mtiles) gemm_core_fold<1, MAIN>(upf, nkpf, half, fb, warp, lane, acc);
     }
 }
 
@@ -631,12 +592,12 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
             if (st.exit_flag) break;
             if (st.half_active[h]) {
                 if constexpr (FOLD) {
-                    double facc[MAIN][3][2][2], fxacc[XMW][2][2];
-                    gemm_half_fold<MAIN, XMW>(a.upack_fold, a.nkp_fold, half,
-                                              reinterpret_cast<const double*>(smem_raw + L.fbuf0 + h * fb_bytes), hp,
-                                              warp, lane, facc, fxacc);
+                    double facc[MAIN][3][2][2];
+                    gemm_half_fold<MAIN>(a.upack_fold, a.nkp_fold, half,
+                                         reinterpret_cast<const double*>(smem_raw + L.fbuf0 + h * fb_bytes), mtiles,
+                                         warp, lane, facc);
                     WS_PHASE(1);
-                    bar_sync(BAR_B0 + h, WS_THREADS);  // b0 of half h (FP group)
+                    bar_sync(BAR_B0 + h, WS_THREADS);  // b0 of half h (FP group, formed before F_h)
                     WS_PHASE(3);
                     // unfold: Y_j = acc_sum + acc_diff, Y_{N-1-j} = acc_sum - acc_diff (the 1/2 sits in
                     // the packed operators), then the same epilogue as the dense path for both rows
@@ -647,7 +608,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
                     int nf = INT_MAX;
 #pragma unroll
                     for (int i = 0; i < MAIN; ++i) {
-                        const int j = (warp * MAIN + i) * 8 + g, jm = N - 1 - j;
+                        const int j = (warp + i * MMA_WARPS) * 8 + g, jm = N - 1 - j;
                         if (j >= half || !((act_h >> q) & 1)) continue;
                         double ylo[6], yhi[6], olo[6], ohi[6];
 #pragma unroll
@@ -667,22 +628,6 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
                         for (int c = 0; c < 6; ++c) {
                             ybuf[y2(j, h, c, q)] = ylo[c];
                             ybuf[y2(jm, h, c, q)] = yhi[c];
-                        }
-                    }
-                    double* xs_lo = xstage + (2 * h) * xrows * HC;
-                    double* xs_hi = xs_lo + xrows * HC;
-#pragma unroll
-                    for (int x = 0; x < XMW; ++x) {  // extra pair tiles -> stage (both mirrored rows)
-                        const int ex = warp + x * MMA_WARPS;
-                        if (ex >= hp.extras) continue;
-                        const int j = (hp.mb + ex / 3) * 8 + g, p = ex % 3;
-                        if (j >= half) continue;
-#pragma unroll
-                        for (int e = 0; e < 2; ++e) {
-                            const double bb = b0[p * 8 + 2 * q + e];
-                            const int o = (j - hp.mb * 8) * HC + q * 6 + 2 * p + e;
-                            xs_lo[o] = fma(w2, fxacc[x][0][e] + fxacc[x][1][e], bb);
-                            xs_hi[o] = fma(w2, fxacc[x][0][e] - fxacc[x][1][e], bb);
                         }
                     }
                     double e2 = bn / bd;
@@ -783,12 +728,9 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
             // ---- staged rows of half h (node rows whose components sit in several MMA warps)
             if (!first[h] && xrows > 0 && st.half_active[h]) {
                 const int act_h = (st.act_word[h] >> (h * HS)) & 0xF;
-                const int nitems = xrows * HS * (FOLD ? 2 : 1);  // folded: each pair row and its mirror
-                for (int i = ft; i < nitems; i += FP_THREADS) {
-                    const int mir = FOLD ? i / (xrows * HS) : 0, ii = i - mir * xrows * HS;
-                    const int r = ii >> 2, s = ii & 3;
-                    const int j = mir ? N - 1 - (MAIN * MMA_WARPS * 8 + r) : MAIN * MMA_WARPS * 8 + r;
-                    const double* xs = xstage + (FOLD ? 2 * h + mir : h) * xrows * HC;
+                const double* xs = xstage + h * xrows * HC;  // (the folded plan stages no rows)
+                for (int i = ft; i < xrows * HS; i += FP_THREADS) {
+                    const int r = i >> 2, s = i & 3, j = MAIN * MMA_WARPS * 8 + r;
                     if (!((act_h >> s) & 1)) continue;
                     double yn[6], yo[6];
 #pragma unroll
@@ -804,11 +746,12 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
                     atomicMax(&st.slot_err[h * HS + s], static_cast<unsigned long long>(__double_as_longlong(sbn / sbd)));
                     if (snf != INT_MAX) atomicMin(&st.nf_key[h * HS + s], snf);
                 }
-                if (xrows * HS * (FOLD ? 2 : 1) > 32)
+                if (xrows * HS > 32)
                     bar_sync(BAR_FP, FP_THREADS);
                 else
                     __syncwarp();  // warp 0 staged every row and also takes the decisions
             }
+            WS_PHASE(10);
             // ---- decisions for half h (warp 0 of the FP group, lane = slot of the half)
             if (!first[h] && fw == 0) {
                 const int am = st.act_word[h];
@@ -1131,7 +1074,10 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
             }
             first[h] = false;
             WS_PHASE(8);
-            bar_arrive(BAR_F0 + h, WS_THREADS);  // F_h ready: the MMA group starts its DMMAs
+            // dense: F_h released before b0, which then overlaps the DMMAs of half h.  Folded:
+            // the halved DMMA stream leaves the MMA group slack, so b0 is formed first, while
+            // the FP64 pipe is free of DMMAs (it is ~3x slower issued into their gaps)
+            if constexpr (!FOLD) bar_arrive(BAR_F0 + h, WS_THREADS);  // F_h ready: the MMA group starts
             // ---- b0 = anchor_op.F + 2 y0 of half h (pc_matrices.hpp:138), overlapped with the
             //      DMMAs of half h: B0_PARTS strided partial dot products per column, summed in a
             //      fixed order; the MMA group waits for it (B_h) only before its epilogue
@@ -1170,6 +1116,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
                 }
             }
             WS_PHASE(9);
+            if constexpr (FOLD) bar_arrive(BAR_F0 + h, WS_THREADS);
             bar_arrive(BAR_B0 + h, WS_THREADS);
         }
     }
@@ -1196,20 +1143,26 @@ static cudaError_t launch_ws_t(const SegArgs& a, int grid, size_t smem, cudaStre
 
 /// Tiles of one half: m-tiles of node rows, or (folded) of row pairs.
 static int ws_mtiles(int N, bool fold) { return fold ? (N / 2 + 7) / 8 : (N + 7) / 8; }
-int ws_main_tiles(int N, bool fold) { return ws_mtiles(N, fold) / MMA_WARPS; }
+/// Dense: MAIN = floor(m-tiles / 8) full-width m-tiles per warp + extras.  Folded: every pair
+/// tile is full width, strided over the warps (ceil), no extras and no staged rows.
+int ws_main_tiles(int N, bool fold) {
+    return fold ? (ws_mtiles(N, true) + MMA_WARPS - 1) / MMA_WARPS : ws_mtiles(N, false) / MMA_WARPS;
+}
 /// Extra (m-tile, n-tile) tiles beyond the MAIN full-width m-tiles of every MMA warp.
-static int ws_extras(int N, bool fold) { return (ws_mtiles(N, fold) - ws_main_tiles(N, fold) * MMA_WARPS) * 3; }
+static int ws_extras(int N, bool fold) {
+    return fold ? 0 : (ws_mtiles(N, false) - ws_main_tiles(N, false) * MMA_WARPS) * 3;
+}
 
 int ws_extra_rows(int N, bool fold) {
-    const int rows = fold ? N / 2 : N;
-    const int r = rows - ws_main_tiles(N, fold) * MMA_WARPS * 8;
+    if (fold) return 0;
+    const int r = N - ws_main_tiles(N, false) * MMA_WARPS * 8;
     return r > 0 ? r : 0;
 }
 
 bool ws_supported(int N, bool fold) {
     const int main = ws_main_tiles(N, fold);
-    if (fold)  // even k-steps per part, 1-2 pair tiles per warp, <= 2 extra pair tiles
-        return N % 8 == 0 && main >= 1 && main <= 2 && ws_extras(N, true) <= 2 * MMA_WARPS;
+    if (fold)  // whole k-quads per part, 1-2 pair tiles per warp
+        return N % 8 == 0 && main >= 1 && main <= 2;
     return main >= 1 && main <= 4 && ws_extras(N, false) <= 3 * MMA_WARPS && (main < 4 || ws_extras(N, false) <= MMA_WARPS);
 }
 
@@ -1224,13 +1177,7 @@ cudaError_t launch_segment_ws(const SegArgs& a, int grid, cudaStream_t s) {
     const int xmw = std::max(1, (ws_extras(a.N, fold) + MMA_WARPS - 1) / MMA_WARPS);
     const size_t smem = ws_smem_bytes(a.N, a.nkp, a.xrows, a.fd.n_bodies, a.stage_eph, fold);
     if (fold) {
-        switch (main * 4 + xmw) {
-        case 5: return launch_ws_t<1, 1, true>(a, grid, smem, s);
-        case 6: return launch_ws_t<1, 2, true>(a, grid, smem, s);
-        case 9: return launch_ws_t<2, 1, true>(a, grid, smem, s);
-        case 10: return launch_ws_t<2, 2, true>(a, grid, smem, s);
-        default: return cudaErrorNotSupported;
-        }
+        return main == 1 ? launch_ws_t<1, 1, true>(a, grid, smem, s) : launch_ws_t<2, 1, true>(a, grid, smem, s);
     }
     switch (main * 4 + xmw) {
     case 5: return launch_ws_t<1, 1>(a, grid, smem, s);
