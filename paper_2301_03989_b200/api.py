@@ -360,6 +360,7 @@ class Context:
                    "decisions", "retire")
     WS_PHASE_NAMES = ("mma_wait_f", "mma_dmma", "mma_epilogue", "mma_wait_b0", "fp_wait_y", "fp_staged_decisions",
                       "fp_retire_claim", "fp_warm_start", "fp_force", "fp_b0", "fp_staged")
+    UNI_PHASE_NAMES = ("decisions", "retire_claim", "warm_start", "force", "sing_b0", "dmma_epilogue")
     N_PHASES = 12
 
     def phase_cycles(self) -> dict:
@@ -367,7 +368,9 @@ class Context:
         named after the solver kernel that ran."""
         buf = (C.c_uint64 * self.N_PHASES)()
         self.lib.pswarm_get_phase_cycles(self.ptr, buf, self.N_PHASES)
-        names = self.WS_PHASE_NAMES if self.kernel_name().startswith("k_pc_ws") else self.PHASE_NAMES
+        kn = self.kernel_name()
+        names = (self.UNI_PHASE_NAMES if kn == "k_pc_uni" else
+                 self.WS_PHASE_NAMES if kn.startswith("k_pc_ws") else self.PHASE_NAMES)
         d = {n: int(buf[k]) for k, n in enumerate(names)}
         d["ctas"] = int(buf[self.N_PHASES - 1])
         return d

@@ -231,6 +231,23 @@ __device__ __forceinline__ double rsqrt_newton(double x, double y) {
     return y * fma(-0.5 * x * y, y, 1.5);
 }
 
+/// mu / |d|^3 for a perturbing body from d2 = |d|^2, with the single Newton step of the
+/// planet terms folded into the cube: e = 3 - d2 y0^2, y1 = y0 e / 2 (the Newton iterate),
+/// mu y1^3 = (mu / 8) (y0 e)^3 — 2 DMUL + 1 DFMA for the step and 3 DMUL for the cube
+/// (mu8 = mu / 8, exact).  Same iterate as rsqrt_newton up to rounding.
+__device__ __forceinline__ double body_mu_ir3(double d2, double mu8) {
+    const double y0 = rsqrt_seed(d2);
+    const double y1h = y0 * fma(-d2 * y0, y0, 3.0);  // 2 / |d|
+    return (mu8 * y1h) * (y1h * y1h);
+}
+
+/// d2 < bound for non-negative doubles (d2 is a sum of squares, bound >= 0) as a 64-bit
+/// integer compare on the IEEE bits: the proximity pre-test stays off the FP64 pipe,
+/// which the force shares with the DMMA stream.  NaN d2 compares false, as with <.
+__device__ __forceinline__ bool below_bits(double d2, long long bound_bits) {
+    return __double_as_longlong(d2) < bound_bits;
+}
+
 __device__ __forceinline__ double rsqrt_nr(double x) {
     double y;
     asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
@@ -251,6 +268,7 @@ struct ForceData {
     double central_mu;
     double floor_km;
     double floor2_hi;  // floor^2 * (1 + 1e-9): cheap pre-test before the exact sqrt compare
+    long long floor2_hi_bits;  // its IEEE bits (integer pre-test, below_bits)
     int n_bodies;      // 0 for two-body
     int rel;           // 1: n_body_1pn (EXTENSION) -> add rel_correction()
     double ic2;        // 1 / c^2 (km^-2 s^2)

@@ -172,6 +172,8 @@ size_t ws_smem_bytes(int N, int nkp, int xrows, int B, int stage_eph, bool fold)
 int ws_main_tiles(int N, bool fold);
 int ws_extra_rows(int N, bool fold);
 bool ws_supported(int N, bool fold);
+bool uni_supported(int N);
+cudaError_t launch_segment_uni(const SegArgs& a, int grid, cudaStream_t s);
 cudaError_t launch_segment_ws(const SegArgs& a, int grid, cudaStream_t s);
 
 GemmPlan make_gemm_plan(int N);

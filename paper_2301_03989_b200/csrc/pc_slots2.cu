@@ -42,7 +42,7 @@ constexpr int YS2 = 2 * HC + 4;
 #endif
 constexpr int MMA_WARPS = PSWARM_MMA_WARPS, FP_WARPS = 8;
 constexpr int MMA_THREADS = 32 * MMA_WARPS, FP_THREADS = 32 * FP_WARPS, WS_THREADS = MMA_THREADS + FP_THREADS;
-constexpr int BAR_F0 = 1, BAR_Y0 = 3, BAR_FP = 6, BAR_B0 = 7;  // F_h = 1+h, Y_h = 3+h, B_h = 7+h
+constexpr int BAR_F0 = 1, BAR_Y0 = 3, BAR_MMA = 5, BAR_FP = 6, BAR_B0 = 7;  // F_h = 1+h, Y_h = 3+h, B_h = 7+h
 
 __device__ __forceinline__ int y2(int j, int h, int c, int s) {
     return j * YS2 + h * HC + c * HS + (s ^ ((j >> 2) & 3));
@@ -52,6 +52,10 @@ __device__ __forceinline__ int y2(int j, int h, int c, int s) {
 /// threads' stores (consecutive nodes j, bank set by j & 3 and the k-step) spread over
 /// all banks instead of 4.
 constexpr int FKS = 3 * 32 + 4;  // doubles per k-step
+#ifndef PSWARM_FP_UNROLL
+#define PSWARM_FP_UNROLL 2
+#endif
+constexpr int kForceUnroll = PSWARM_FP_UNROLL;  // body-loop unroll of force_pair (diagnostic knob)
 __device__ __forceinline__ int f2(int j, int c, int s) {
     return (j >> 2) * FKS + (c >> 1) * 32 + ((s * 2 + (c & 1)) * 4 + (j & 3));
 }
@@ -92,8 +96,8 @@ struct WsState {
     int act_word[2];     // active slots of half h (bits h*HS..h*HS+3); the MMA group reads
                          // act_word[h] while the FP group claims into act_word[h ^ 1]
     int new_mask[2];     // slots claimed at the last refill of each half
-    int free_mask;
-    int retire_mask;
+    int free_mask[2];    // per half: written by that half's decisions
+    int retire_mask[2];
     int half_active[2];  // MMA group skips an empty half
     int queue_done;
     int timeout;
@@ -127,7 +131,7 @@ __host__ __device__ inline WsLayout ws_layout(int N, int nkp, int xrows, int B, 
     L.xstage = L.fbuf1 + fb;  // [2 halves][xrows][HC]
     L.anchor = L.xstage + sizeof(double) * 2 * static_cast<size_t>(xrows) * HC;
     L.b0part = L.anchor + sizeof(double) * static_cast<size_t>(8 * nkp);
-    L.eph = L.b0part + sizeof(double) * B0_PARTS * HC;
+    L.eph = L.b0part + sizeof(double) * 2 * B0_PARTS * HC;  // [half][part][HC] (k_pc_uni forms both at once)
     L.state = L.eph + (stage_eph ? sizeof(double) * static_cast<size_t>(N) * (3 * B + 3) : 0);
     L.total = L.state + sizeof(WsState);
     return L;
@@ -455,7 +459,7 @@ __device__ __forceinline__ void force_half(const ForceData& fd, const double* yb
     const double* bp = pos_base + static_cast<size_t>(j) * psj;  // element (b, c) at bp[(3b + c) * psc]
 #pragma unroll 4
     for (int b = 0; b < B; ++b) {
-        const double mu_b = __ldg(fd.body_mu + b);
+        const double mu8 = 0.125 * __ldg(fd.body_mu + b);
         const double qx = bp[(3 * b) * psc], qy = bp[(3 * b + 1) * psc], qz = bp[(3 * b + 2) * psc];
         double dx[NS], dy[NS], dz[NS], d2[NS], y[NS];
 #pragma unroll
@@ -464,13 +468,13 @@ __device__ __forceinline__ void force_half(const ForceData& fd, const double* yb
             dy[s] = qy - ry[s];
             dz[s] = qz - rz[s];
             d2[s] = dx[s] * dx[s] + dy[s] * dy[s] + dz[s] * dz[s];
-            flag |= d2[s] < fd.floor2_hi;
+            flag |= below_bits(d2[s], fd.floor2_hi_bits);
         }
 #pragma unroll
-        for (int s = 0; s < NS; ++s) y[s] = rsqrt_newton(d2[s], rsqrt_seed(d2[s]));
+        for (int s = 0; s < NS; ++s) y[s] = body_mu_ir3(d2[s], mu8);
 #pragma unroll
         for (int s = 0; s < NS; ++s) {
-            const double kk = mu_b * (y[s] * y[s] * y[s]);
+            const double kk = y[s];
             ax[s] += kk * dx[s];
             ay[s] += kk * dy[s];
             az[s] += kk * dz[s];
@@ -510,8 +514,251 @@ __device__ __forceinline__ void force_half(const ForceData& fd, const double* yb
     }
 }
 
+/// Folded force (fold = 1, Newtonian): one thread evaluates the mirrored nodes j and
+/// N-1-j (j < N/2) for slots [s0, s0 + NS) — 2 NS independent chains — and writes the
+/// folded F directly: s = F_j + F_{N-1-j} at node j, a = F_j - F_{N-1-j} at node N-1-j
+/// (no separate fold pass).  Same arithmetic per node as force_half.
+template <int NS>
+__device__ __forceinline__ void force_pair(const ForceData& fd, const double* ybuf, double* fb, int* sing_key,
+                                           const double* pos_base, const double* ind_base, int psj, int psc,
+                                           int act_h, int h, int j, int N, int s0) {
+    constexpr int C = 2 * NS;  // chain k: node side k / NS (0: j, 1: N-1-j), slot s0 + k % NS
+    const int B = fd.n_bodies;
+    const int nd[2] = {j, N - 1 - j};
+    double rx[C], ry[C], rz[C], ax[C], ay[C], az[C], r2[C], ir[C];
+    bool on[C];
+    bool flag = false;
+#pragma unroll
+    for (int k = 0; k < C; ++k) {
+        const int n = nd[k / NS], sl = s0 + k % NS;
+        on[k] = (act_h >> sl) & 1;
+        rx[k] = on[k] ? ybuf[y2(n, h, 0, sl)] : 1.0e8;
+        ry[k] = on[k] ? ybuf[y2(n, h, 1, sl)] : 0.0;
+        rz[k] = on[k] ? ybuf[y2(n, h, 2, sl)] : 0.0;
+        r2[k] = rx[k] * rx[k] + ry[k] * ry[k] + rz[k] * rz[k];
+        flag |= !(r2[k] > 0.0);
+    }
+#pragma unroll
+    for (int k = 0; k < C; ++k) ir[k] = rsqrt_newton(r2[k], rsqrt_newton(r2[k], rsqrt_seed(r2[k])));
+#pragma unroll
+    for (int k = 0; k < C; ++k) {
+        const double sc = -fd.central_mu * (ir[k] * ir[k] * ir[k]);
+        ax[k] = sc * rx[k];
+        ay[k] = sc * ry[k];
+        az[k] = sc * rz[k];
+    }
+    const double* bp0 = pos_base + static_cast<size_t>(nd[0]) * psj;
+    const double* bp1 = pos_base + static_cast<size_t>(nd[1]) * psj;
+#pragma unroll(kForceUnroll)
+    for (int b = 0; b < B; ++b) {
+        const double mu8 = 0.125 * __ldg(fd.body_mu + b);
+        const double q0x = bp0[(3 * b) * psc], q0y = bp0[(3 * b + 1) * psc], q0z = bp0[(3 * b + 2) * psc];
+        const double q1x = bp1[(3 * b) * psc], q1y = bp1[(3 * b + 1) * psc], q1z = bp1[(3 * b + 2) * psc];
+        double dx[C], dy[C], dz[C], d2[C], y[C];
+#pragma unroll
+        for (int k = 0; k < C; ++k) {
+            dx[k] = (k < NS ? q0x : q1x) - rx[k];
+            dy[k] = (k < NS ? q0y : q1y) - ry[k];
+            dz[k] = (k < NS ? q0z : q1z) - rz[k];
+            d2[k] = dx[k] * dx[k] + dy[k] * dy[k] + dz[k] * dz[k];
+            flag |= below_bits(d2[k], fd.floor2_hi_bits);
+        }
+#pragma unroll
+        for (int k = 0; k < C; ++k) y[k] = body_mu_ir3(d2[k], mu8);
+#pragma unroll
+        for (int k = 0; k < C; ++k) {
+            const double kk = y[k];
+            ax[k] += kk * dx[k];
+            ay[k] += kk * dy[k];
+            az[k] += kk * dz[k];
+        }
+    }
+    if (B > 0) {
+#pragma unroll
+        for (int side = 0; side < 2; ++side) {
+            const int n = nd[side];
+            const int ij = psc == 1 ? 3 * n : n;  // [N][3] in global memory, [3][N] when staged
+            const double ix = ind_base[ij], iy = ind_base[ij + psc], iz = ind_base[ij + 2 * psc];
+#pragma unroll
+            for (int k = side * NS; k < (side + 1) * NS; ++k) {
+                ax[k] -= ix;
+                ay[k] -= iy;
+                az[k] -= iz;
+            }
+        }
+    }
+    if (flag) {  // rare: exact guard order of table_acceleration (force_model.hpp:57-69)
+#pragma unroll
+        for (int k = 0; k < C; ++k) {
+            if (!on[k]) continue;
+            const int n = nd[k / NS], sl = s0 + k % NS;
+            const double* bp = k < NS ? bp0 : bp1;
+            int fail = (rx[k] * rx[k] + ry[k] * ry[k] + rz[k] * rz[k] > 0.0) ? -1 : 0;
+            for (int b = 0; b < B && fail < 0; ++b) {
+                const double dx = bp[(3 * b) * psc] - rx[k], dy = bp[(3 * b + 1) * psc] - ry[k],
+                             dz = bp[(3 * b + 2) * psc] - rz[k];
+                if (sqrt(dx * dx + dy * dy + dz * dz) < fd.floor_km) fail = 1 + b;
+            }
+            if (fail >= 0) atomicMin(&sing_key[h * HS + sl], n * (B + 1) + fail);
+        }
+    }
+#pragma unroll
+    for (int t = 0; t < NS; ++t) {
+        const int sl = s0 + t, k0 = t, k1 = NS + t;
+        const bool o = on[k0];  // both sides of a slot share its activity
+        double lo[6], hi[6];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            lo[c] = o ? ybuf[y2(nd[0], h, 3 + c, sl)] : 0.0;
+            hi[c] = o ? ybuf[y2(nd[1], h, 3 + c, sl)] : 0.0;
+        }
+        lo[3] = o ? ax[k0] : 0.0;
+        lo[4] = o ? ay[k0] : 0.0;
+        lo[5] = o ? az[k0] : 0.0;
+        hi[3] = o ? ax[k1] : 0.0;
+        hi[4] = o ? ay[k1] : 0.0;
+        hi[5] = o ? az[k1] : 0.0;
+#pragma unroll
+        for (int c = 0; c < 6; ++c) {
+            fb[f2(nd[0], c, sl)] = lo[c] + hi[c];
+            fb[f2(nd[1], c, sl)] = lo[c] - hi[c];
+        }
+    }
+}
+
 }  // namespace
 
+
+/// Group decisions for half h after its epilogue (one warp, lane = slot of the half):
+/// pc_solve's stopping rule (err <= tol, it == max_it) and the fault order of the reference
+/// (warm-start failure, singularity, divergence); the leader of each group writes its report
+/// and frees / retires its slots (free_mask / retire_mask of the half).
+__device__ __forceinline__ void decide_half(const SegArgs& a, WsState& st, int h, int lane, int B) {
+    const int am = st.act_word[h];
+    const int s = lane, t = h * HS + s;
+    const bool act_t = s < HS && ((am >> t) & 1);
+    const int my_grp = act_t ? st.slot_grp[t] : -1;
+    const int my_mbr = act_t ? st.slot_member[t] : 0;
+    const double my_e2 = act_t ? __longlong_as_double(static_cast<long long>(st.slot_err[t])) : 0.0;
+    const int my_sk = act_t ? st.sing_key[t] : INT_MAX;
+    const int my_nk = act_t ? st.nf_key[t] : INT_MAX;
+    const int my_wk = (act_t && ((st.new_mask[h] >> t) & 1)) ? st.warm_key[t] : INT_MAX;
+    const int my_tr = act_t ? st.slot_traj[t] : INT_MAX;
+    const int lg = my_grp;
+    const int gid = act_t ? st.grp_id[lg] : -1;
+    const int size = act_t ? st.grp_size[lg] : 1;
+    int it = act_t ? st.grp_iter[lg] : 0;
+    bool leader = act_t;
+    double gerr2 = 0.0;
+    long long sing_s = LLONG_MAX, nf_best = LLONG_MAX;
+    int sing_t = -1, warm_t = -1, warm_tr = INT_MAX, members = 0;
+    if (a.gmax == 1 && act_t) {  // singleton groups (independent mode): no cross-lane scan
+        members = 1 << t;
+        gerr2 = my_e2;
+        if (my_wk != INT_MAX) warm_t = t;
+        if (my_sk != INT_MAX) {
+            sing_s = my_sk / (B + 1);
+            sing_t = t;
+        }
+        if (my_nk != INT_MAX) nf_best = static_cast<long long>(my_nk >> 3) * 6 + (my_nk & 7);
+    }
+#pragma unroll
+    for (int u = 0; u < (a.gmax == 1 ? 0 : HS); ++u) {
+        const int ug = __shfl_sync(0xffffffffu, my_grp, u);
+        const int um = __shfl_sync(0xffffffffu, my_mbr, u);
+        const double ue = __shfl_sync(0xffffffffu, my_e2, u);
+        const int usk = __shfl_sync(0xffffffffu, my_sk, u);
+        const int unk = __shfl_sync(0xffffffffu, my_nk, u);
+        const int uwk = __shfl_sync(0xffffffffu, my_wk, u);
+        const int utr = __shfl_sync(0xffffffffu, my_tr, u);
+        if (!act_t || ug != lg) continue;
+        const int ut = h * HS + u;
+        if (u < s) leader = false;
+        members |= 1 << ut;
+        gerr2 = fmax(gerr2, ue);
+        if (uwk != INT_MAX && utr < warm_tr) {
+            warm_tr = utr;
+            warm_t = ut;
+        }
+        if (usk != INT_MAX) {
+            const long long smp = static_cast<long long>(usk / (B + 1)) * size + um;
+            if (smp < sing_s) {
+                sing_s = smp;
+                sing_t = ut;
+            }
+        }
+        if (unk != INT_MAX) {
+            const long long key = static_cast<long long>(unk >> 3) * (6LL * size) +
+                                  static_cast<long long>(unk & 7) * size + um;
+            nf_best = min(nf_best, key);
+        }
+    }
+    __syncwarp();  // every lane has read the slot / group records the leader rewrites
+    int free_bits = 0, retire_bits = 0;
+    if (leader) {
+        // sqrt only where the value is needed (history, retire) or the squared test
+        // is within rounding of tol^2 (tol2_lo/hi carry a 1e-13 relative margin)
+        auto gerr_of = [&] { return sqrt(gerr2); };
+        GroupFault* fl = a.faults + gid;
+        bool retire = false, ok = false, conv = false;
+        if (warm_t >= 0) {
+            fl->status = st.warm_kind[warm_t] == CONIC_ZERO_RADIUS ? FAULT_WARM_ZERO_RADIUS : FAULT_WARM_SOLVER;
+            fl->iteration = 0;
+            fl->trajectory = st.slot_traj[warm_t];
+            fl->node = st.warm_key[warm_t] / 4;
+            fl->value = st.warm_val[warm_t][0];
+            fl->value2 = st.warm_val[warm_t][1];
+            retire = true;
+        } else {
+            it += 1;
+            st.grp_iter[lg] = it;
+            if (sing_t >= 0) {
+                const int key = st.sing_key[sing_t];
+                fl->status = FAULT_SINGULARITY;
+                fl->iteration = it;
+                fl->node = key / (B + 1);
+                fl->body = key % (B + 1) - 1;
+                fl->trajectory = st.slot_member[sing_t];
+                fl->value = st.sing_val[sing_t];
+                retire = true;
+            } else if (nf_best != LLONG_MAX) {
+                fl->status = FAULT_DIVERGENCE;
+                fl->iteration = it;
+                fl->node = nf_best / (6LL * size);
+                fl->column = nf_best % (6LL * size);
+                retire = true;
+            } else {
+                if (a.rep_hist) a.rep_hist[static_cast<size_t>(gid) * a.max_it + (it - 1)] = gerr_of();
+                const bool le_tol = PSWARM_ABLATE == 0 &&  // ablation builds: fixed max_it work
+                    (gerr2 <= a.tol2_lo ? true : (gerr2 > a.tol2_hi ? false : gerr_of() <= a.tol));
+                if (le_tol) {
+                    retire = ok = conv = true;
+                } else if (it >= a.max_it) {
+                    retire = ok = true;
+                }
+            }
+        }
+        if (retire) {
+            a.rep_iter[gid] = it;
+            a.rep_err[gid] = gerr_of();
+            a.rep_conv[gid] = conv ? 1 : 0;
+            free_bits = members;
+            retire_bits = ok ? members : 0;
+            st.grp_id[lg] = -1;
+        }
+    }
+    free_bits = __reduce_or_sync(0xffffffffu, static_cast<unsigned>(free_bits));
+    retire_bits = __reduce_or_sync(0xffffffffu, static_cast<unsigned>(retire_bits));
+    if (lane == 0) {
+        st.free_mask[h] = free_bits;
+        st.retire_mask[h] = retire_bits;
+    }
+    if (s < HS) {  // reset this half's accumulators for its next iteration
+        st.slot_err[t] = 0ull;
+        st.sing_key[t] = INT_MAX;
+        st.nf_key[t] = INT_MAX;
+    }
+}
 
 template <int MAIN, int XMW, bool STAGE, bool REL, bool FOLD>
 __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
@@ -640,6 +887,11 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
                         atomicMax(&st.slot_err[h * HS + q], static_cast<unsigned long long>(__double_as_longlong(e2)));
                         if (nf != INT_MAX) atomicMin(&st.nf_key[h * HS + q], nf);
                     }
+                    // decisions of half h here, not in the FP group: the MMA group has slack once
+                    // its DMMA stream is halved, and the FP group's warps issue ~3x slower while
+                    // DMMAs stream (the decisions sat on the FP group's critical chain)
+                    bar_sync(BAR_MMA, MMA_THREADS);  // every warp's slot_err / nf_key update is in
+                    if (warp == 0) decide_half(a, st, h, lane, B);
                 } else {
                 double acc[MAIN][3][2], xacc[XMW][2];
 #if PSWARM_ABLATE == 3  // diagnostic: no DMMA
@@ -713,6 +965,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
                 }
                 WS_PHASE(2);
             } else {
+                if (FOLD && tid == 0) st.free_mask[h] = st.retire_mask[h] = 0;  // no decisions ran
                 bar_sync(BAR_B0 + h, WS_THREADS);  // keep the B_h generations paired
             }
             bar_arrive(BAR_Y0 + h, WS_THREADS);  // bar.arrive/bar.sync order smem among participants
@@ -752,138 +1005,13 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
                     __syncwarp();  // warp 0 staged every row and also takes the decisions
             }
             WS_PHASE(10);
-            // ---- decisions for half h (warp 0 of the FP group, lane = slot of the half)
-            if (!first[h] && fw == 0) {
-                const int am = st.act_word[h];
-                const int s = lane, t = h * HS + s;
-                const bool act_t = s < HS && ((am >> t) & 1);
-                const int my_grp = act_t ? st.slot_grp[t] : -1;
-                const int my_mbr = act_t ? st.slot_member[t] : 0;
-                const double my_e2 = act_t ? __longlong_as_double(static_cast<long long>(st.slot_err[t])) : 0.0;
-                const int my_sk = act_t ? st.sing_key[t] : INT_MAX;
-                const int my_nk = act_t ? st.nf_key[t] : INT_MAX;
-                const int my_wk = (act_t && ((st.new_mask[h] >> t) & 1)) ? st.warm_key[t] : INT_MAX;
-                const int my_tr = act_t ? st.slot_traj[t] : INT_MAX;
-                const int lg = my_grp;
-                const int gid = act_t ? st.grp_id[lg] : -1;
-                const int size = act_t ? st.grp_size[lg] : 1;
-                int it = act_t ? st.grp_iter[lg] : 0;
-                bool leader = act_t;
-                double gerr2 = 0.0;
-                long long sing_s = LLONG_MAX, nf_best = LLONG_MAX;
-                int sing_t = -1, warm_t = -1, warm_tr = INT_MAX, members = 0;
-                if (a.gmax == 1 && act_t) {  // singleton groups (independent mode): no cross-lane scan
-                    members = 1 << t;
-                    gerr2 = my_e2;
-                    if (my_wk != INT_MAX) warm_t = t;
-                    if (my_sk != INT_MAX) {
-                        sing_s = my_sk / (B + 1);
-                        sing_t = t;
-                    }
-                    if (my_nk != INT_MAX) nf_best = static_cast<long long>(my_nk >> 3) * 6 + (my_nk & 7);
-                }
-#pragma unroll
-                for (int u = 0; u < (a.gmax == 1 ? 0 : HS); ++u) {
-                    const int ug = __shfl_sync(0xffffffffu, my_grp, u);
-                    const int um = __shfl_sync(0xffffffffu, my_mbr, u);
-                    const double ue = __shfl_sync(0xffffffffu, my_e2, u);
-                    const int usk = __shfl_sync(0xffffffffu, my_sk, u);
-                    const int unk = __shfl_sync(0xffffffffu, my_nk, u);
-                    const int uwk = __shfl_sync(0xffffffffu, my_wk, u);
-                    const int utr = __shfl_sync(0xffffffffu, my_tr, u);
-                    if (!act_t || ug != lg) continue;
-                    const int ut = h * HS + u;
-                    if (u < s) leader = false;
-                    members |= 1 << ut;
-                    gerr2 = fmax(gerr2, ue);
-                    if (uwk != INT_MAX && utr < warm_tr) {
-                        warm_tr = utr;
-                        warm_t = ut;
-                    }
-                    if (usk != INT_MAX) {
-                        const long long smp = static_cast<long long>(usk / (B + 1)) * size + um;
-                        if (smp < sing_s) {
-                            sing_s = smp;
-                            sing_t = ut;
-                        }
-                    }
-                    if (unk != INT_MAX) {
-                        const long long key = static_cast<long long>(unk >> 3) * (6LL * size) +
-                                              static_cast<long long>(unk & 7) * size + um;
-                        nf_best = min(nf_best, key);
-                    }
-                }
-                __syncwarp();  // every lane has read the slot / group records the leader rewrites
-                int free_bits = 0, retire_bits = 0;
-                if (leader) {
-                    // sqrt only where the value is needed (history, retire) or the squared test
-                    // is within rounding of tol^2 (tol2_lo/hi carry a 1e-13 relative margin)
-                    auto gerr_of = [&] { return sqrt(gerr2); };
-                    GroupFault* fl = a.faults + gid;
-                    bool retire = false, ok = false, conv = false;
-                    if (warm_t >= 0) {
-                        fl->status = st.warm_kind[warm_t] == CONIC_ZERO_RADIUS ? FAULT_WARM_ZERO_RADIUS : FAULT_WARM_SOLVER;
-                        fl->iteration = 0;
-                        fl->trajectory = st.slot_traj[warm_t];
-                        fl->node = st.warm_key[warm_t] / 4;
-                        fl->value = st.warm_val[warm_t][0];
-                        fl->value2 = st.warm_val[warm_t][1];
-                        retire = true;
-                    } else {
-                        it += 1;
-                        st.grp_iter[lg] = it;
-                        if (sing_t >= 0) {
-                            const int key = st.sing_key[sing_t];
-                            fl->status = FAULT_SINGULARITY;
-                            fl->iteration = it;
-                            fl->node = key / (B + 1);
-                            fl->body = key % (B + 1) - 1;
-                            fl->trajectory = st.slot_member[sing_t];
-                            fl->value = st.sing_val[sing_t];
-                            retire = true;
-                        } else if (nf_best != LLONG_MAX) {
-                            fl->status = FAULT_DIVERGENCE;
-                            fl->iteration = it;
-                            fl->node = nf_best / (6LL * size);
-                            fl->column = nf_best % (6LL * size);
-                            retire = true;
-                        } else {
-                            if (a.rep_hist) a.rep_hist[static_cast<size_t>(gid) * a.max_it + (it - 1)] = gerr_of();
-                            const bool le_tol = PSWARM_ABLATE == 0 &&  // ablation builds: fixed max_it work
-                                (gerr2 <= a.tol2_lo ? true : (gerr2 > a.tol2_hi ? false : gerr_of() <= a.tol));
-                            if (le_tol) {
-                                retire = ok = conv = true;
-                            } else if (it >= a.max_it) {
-                                retire = ok = true;
-                            }
-                        }
-                    }
-                    if (retire) {
-                        a.rep_iter[gid] = it;
-                        a.rep_err[gid] = gerr_of();
-                        a.rep_conv[gid] = conv ? 1 : 0;
-                        free_bits = members;
-                        retire_bits = ok ? members : 0;
-                        st.grp_id[lg] = -1;
-                    }
-                }
-                free_bits = __reduce_or_sync(0xffffffffu, static_cast<unsigned>(free_bits));
-                retire_bits = __reduce_or_sync(0xffffffffu, static_cast<unsigned>(retire_bits));
-                if (lane == 0) {
-                    st.free_mask = free_bits;
-                    st.retire_mask = retire_bits;
-                }
-                if (s < HS) {  // reset this half's accumulators for its next iteration
-                    st.slot_err[t] = 0ull;
-                    st.sing_key[t] = INT_MAX;
-                    st.nf_key[t] = INT_MAX;
-                }
-            }
+            // ---- decisions for half h (warp 0 of the FP group; folded: done by the MMA group)
+            if (!FOLD && !first[h] && fw == 0) decide_half(a, st, h, lane, B);
             bar_sync(BAR_FP, FP_THREADS);
             WS_PHASE(5);
             // ---- retire outputs of half h
-            if (!first[h] && st.retire_mask) {
-                const int retire = st.retire_mask;
+            if (!first[h] && st.retire_mask[h]) {
+                const int retire = st.retire_mask[h];
                 const int j_begin = a.seg == 0 ? 0 : 1;
                 for (int i = ft; i < N * HS; i += FP_THREADS) {
                     const int j = i >> 2, s = i & 3, t = h * HS + s;
@@ -907,7 +1035,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
             if (ft == 0) {
                 int am = st.act_word[0] | st.act_word[1];
                 if (!first[h]) {
-                    const int fm = st.free_mask;
+                    const int fm = st.free_mask[h];
                     am &= ~fm;
                     for (int t = 0; t < SLOTS; ++t)
                         if ((fm >> t) & 1) st.slot_traj[t] = -1;
@@ -921,7 +1049,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
                     const int g1 = min(g0 + k, a.P);
                     if (g0 + k >= a.P) st.queue_done = 1;
                     for (int gi = g0; gi < g1; ++gi) {
-                        int lg = 0;
+                        int lg = h * HS;  // group records of half h (a group never spans halves)
                         while (st.grp_id[lg] >= 0) ++lg;
                         const int off = static_cast<int>(a.group_off[gi]);
                         const int size = static_cast<int>(a.group_off[gi + 1]) - off;
@@ -1027,7 +1155,17 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
                 // slots per force thread: all FP warps stay busy down to N = 64 (the FP warps only
                 // issue in the DMMA stream's gaps, so their count sets the force throughput)
                 double* fbh = reinterpret_cast<double*>(smem_raw + L.fbuf0 + h * fb_bytes);
-                if (N > FP_THREADS / 2) {
+                if constexpr (FOLD && !REL) {  // mirrored node pairs, F folded as it is written
+                    if (half > FP_THREADS / 4) {
+                        for (int w = ft; w < 2 * half; w += FP_THREADS)
+                            force_pair<2>(a.fd, ybuf, fbh, st.sing_key, pos_base, ind_base, psj, psc, act_h, h,
+                                          w % half, N, (w / half) * 2);
+                    } else {
+                        for (int w = ft; w < 4 * half; w += FP_THREADS)
+                            force_pair<1>(a.fd, ybuf, fbh, st.sing_key, pos_base, ind_base, psj, psc, act_h, h,
+                                          w % half, N, w / half);
+                    }
+                } else if (N > FP_THREADS / 2) {
                     for (int j = ft; j < N; j += FP_THREADS) {
                         if constexpr (REL)
                             force_half_rel<4>(a.fd, ybuf, fbh, st.sing_key, act_h, h, j, 0);
@@ -1053,7 +1191,8 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
                 }
             }
             bar_sync(BAR_FP, FP_THREADS);
-            if constexpr (FOLD) {  // fold F in place: s_k at position k, a_k = F_k - F_{N-1-k} at N-1-k
+            WS_PHASE(8);
+            if constexpr (FOLD && REL) {  // fold F in place: s_k at position k, a_k = F_k - F_{N-1-k} at N-1-k
                 if (act_h) {
                     double* fbh = reinterpret_cast<double*>(smem_raw + L.fbuf0 + h * fb_bytes);
                     for (int i = ft; i < half * HC; i += FP_THREADS) {
@@ -1073,7 +1212,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
                     check_distance(ybuf[y2(j, h, 0, ft)], ybuf[y2(j, h, 1, ft)], ybuf[y2(j, h, 2, ft)], j, chk, a.fd);
             }
             first[h] = false;
-            WS_PHASE(8);
+            WS_PHASE(10);  // (diagnostic split: fold pass)
             // dense: F_h released before b0, which then overlaps the DMMAs of half h.  Folded:
             // the halved DMMA stream leaves the MMA group slack, so b0 is formed first, while
             // the FP64 pipe is free of DMMAs (it is ~3x slower issued into their gaps)
@@ -1130,6 +1269,433 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
     }
 }
 
+// =====================================================================================
+// k_pc_uni — unified (non-specialised) folded slot kernel, Newtonian forces.
+//
+// Same slots, state layout, operators and arithmetic as k_pc_ws<..., FOLD>, but every phase
+// runs on all 16 warps over both halves at once: decisions -> retire -> claim -> warm start
+// -> force -> b0 -> DMMA + epilogue.  Rationale: DMMA and DFMA share one FP64
+// pipe and the FP warps barely issue while a DMMA stream runs, so k_pc_ws's two groups do
+// not overlap their FP64 work; the tick is the DMMA phase plus the FP group's latency-bound
+// chain.  Here the force runs with twice the warps on an idle pipe, and the DMMA phase
+// spreads 2 x 13 pair tiles (N = 200) over 16 warps.
+// =====================================================================================
+
+/// The warp's NV pair-tile units (tile[i] of half hh[i]): folded GEMM of gemm_core_fold with
+/// a per-unit B-fragment buffer (the two halves have separate F buffers).
+template <int NV>
+__device__ __forceinline__ void gemm_units_fold(const double2* __restrict__ upf, int nkpf, int half,
+                                                const double* const (&fb)[NV], const int (&tile)[NV], int lane,
+                                                double (&acc)[NV][3][2][2]) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i)
+#pragma unroll
+        for (int p = 0; p < 3; ++p)
+#pragma unroll
+            for (int u = 0; u < 2; ++u) acc[i][p][u][0] = acc[i][p][u][1] = 0.0;
+    const double2* am[NV][2];
+#pragma unroll
+    for (int i = 0; i < NV; ++i)
+#pragma unroll
+        for (int u = 0; u < 2; ++u) am[i][u] = upf + (static_cast<size_t>(tile[i]) * 2 + (1 - u)) * nkpf * 32 + lane;
+    const int hi_off = (half >> 2) * FKS;  // part 1 (a) sits at positions >= N/2
+    struct Pair {
+        double2 m[NV][2];
+    };
+    auto load = [&](int kp, Pair& c) {
+#pragma unroll
+        for (int i = 0; i < NV; ++i)
+#pragma unroll
+            for (int u = 0; u < 2; ++u) c.m[i][u] = __ldg(am[i][u] + kp * 32);
+    };
+    auto compute = [&](int kp, const Pair& c) {
+#pragma unroll
+        for (int sub = 0; sub < 2; ++sub) {
+            const int ks = 2 * kp + sub;
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+#pragma unroll
+                for (int i = 0; i < NV; ++i) {
+                    const double* fk = fb[i] + lane + (u ? 0 : hi_off) + ks * FKS;
+                    const double bv[3] = {fk[0], fk[32], fk[64]};
+                    const double av = sub ? c.m[i][u].y : c.m[i][u].x;
+#pragma unroll
+                    for (int p = 0; p < 3; ++p) dmma(acc[i][p][u][0], acc[i][p][u][1], av, bv[p]);
+                }
+            }
+        }
+    };
+    Pair p0, p1;
+    load(0, p0);
+    int kp = 0;
+    for (; kp + 1 < nkpf; kp += 2) {
+        load(kp + 1, p1);
+        compute(kp, p0);
+        if (kp + 2 < nkpf) load(kp + 2, p0);
+        compute(kp + 1, p1);
+    }
+    if (kp < nkpf) compute(kp, p0);
+}
+
+/// Unfold + epilogue of one pair-tile unit of half h (rows j = 8 tile + g and N-1-j):
+/// identical arithmetic to k_pc_ws's folded epilogue.
+__device__ __forceinline__ void epilogue_unit_fold(const SegArgs& a, WsState& st, double* ybuf,
+                                                   const double (&acc)[3][2][2], int h, int tile, int half, int lane) {
+    const int g = lane >> 2, q = lane & 3, N = a.N;
+    const int act_h = (st.act_word[h] >> (h * HS)) & 0xF;
+    const double* b0 = st.b0h[h];
+    const double w2 = a.omega2;
+    double bn = 0.0, bd = 1.0;
+    int nf = INT_MAX;
+    const int j = tile * 8 + g, jm = N - 1 - j;
+    if (j < half && ((act_h >> q) & 1)) {
+        double ylo[6], yhi[6], olo[6], ohi[6];
+#pragma unroll
+        for (int p = 0; p < 3; ++p)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int c = 2 * p + e;
+                const double bb = b0[p * 8 + 2 * q + e];
+                ylo[c] = fma(w2, acc[p][0][e] + acc[p][1][e], bb);
+                yhi[c] = fma(w2, acc[p][0][e] - acc[p][1][e], bb);
+                olo[c] = ybuf[y2(j, h, c, q)];
+                ohi[c] = ybuf[y2(jm, h, c, q)];
+            }
+        update_sample(ylo, olo, j, a.error_mode, bn, bd, nf);
+        update_sample(yhi, ohi, jm, a.error_mode, bn, bd, nf);
+#pragma unroll
+        for (int c = 0; c < 6; ++c) {
+            ybuf[y2(j, h, c, q)] = ylo[c];
+            ybuf[y2(jm, h, c, q)] = yhi[c];
+        }
+    }
+    double e2 = bn / bd;
+#pragma unroll
+    for (int off = 4; off < 32; off <<= 1) {
+        e2 = fmax(e2, __shfl_xor_sync(0xffffffffu, e2, off));
+        nf = min(nf, __shfl_xor_sync(0xffffffffu, nf, off));
+    }
+    if (g == 0 && ((act_h >> q) & 1)) {
+        atomicMax(&st.slot_err[h * HS + q], static_cast<unsigned long long>(__double_as_longlong(e2)));
+        if (nf != INT_MAX) atomicMin(&st.nf_key[h * HS + q], nf);
+    }
+}
+
+#define UNI_PHASE(k)                                  \
+    do {                                              \
+        if (prof && tid == 0) {                       \
+            const long long now_ = clock64();         \
+            s_pc[(k)] += now_ - s_prev;               \
+            s_prev = now_;                            \
+        }                                             \
+    } while (0)
+
+template <int NV, bool STAGE>
+__global__ void __launch_bounds__(WS_THREADS, 1) k_pc_uni(const SegArgs a) {
+    constexpr int T = WS_THREADS, NW = WS_THREADS / 32;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int N = a.N, B = a.fd.n_bodies;
+    const int half = N / 2;
+    const WsLayout L = ws_layout(N, a.nkp, 0, B, STAGE ? 1 : 0, 1);
+    double* ybuf = reinterpret_cast<double*>(smem_raw + L.ybuf);
+    const size_t fb_bytes = L.fbuf1 - L.fbuf0;
+    double* fb0 = reinterpret_cast<double*>(smem_raw + L.fbuf0);
+    double* anc = reinterpret_cast<double*>(smem_raw + L.anchor);
+    double* b0part = reinterpret_cast<double*>(smem_raw + L.b0part);
+    double* eph = reinterpret_cast<double*>(smem_raw + L.eph);
+    WsState& st = *reinterpret_cast<WsState*>(smem_raw + L.state);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int KP = 8 * a.nkp;
+    const int mtiles = (half + 7) / 8;
+    const bool prof = a.phase_cycles != nullptr;
+    __shared__ long long s_pc[PHASES];
+    long long s_prev = 0;
+    if (tid < PHASES) s_pc[tid] = 0;
+    if (tid == 0) s_prev = clock64();
+
+    const int fb_doubles = ws_fold_ksteps(N, a.nkp) * FKS;
+    for (int i = tid; i < 2 * fb_doubles; i += T) fb0[i] = 0.0;
+    for (int k = tid; k < KP; k += T) anc[k] = k < N ? a.anc_fold[k] : 0.0;
+    if (STAGE && B > 0) {
+        for (int i = tid; i < N * 3 * B; i += T) {
+            const int r = i / N, j = i % N;
+            eph[i] = a.fd.body_pos[j * 3 * B + r];
+        }
+        for (int i = tid; i < N * 3; i += T) eph[N * 3 * B + i] = a.fd.indirect[(i % N) * 3 + i / N];
+    }
+    const double* pos_base = STAGE ? eph : a.fd.body_pos;
+    const double* ind_base = STAGE ? eph + N * 3 * B : a.fd.indirect;
+    const int psj = STAGE ? 1 : 3 * B, psc = STAGE ? N : 1;
+    if (tid == 0) {
+        for (int t = 0; t < SLOTS; ++t) {
+            st.slot_traj[t] = -1;
+            st.grp_id[t] = -1;
+            st.sing_key[t] = INT_MAX;
+            st.nf_key[t] = INT_MAX;
+            st.slot_err[t] = 0ull;
+        }
+        st.act_word[0] = st.act_word[1] = 0;
+        st.new_mask[0] = st.new_mask[1] = 0;
+        st.half_active[0] = st.half_active[1] = 0;
+        st.free_mask[0] = st.free_mask[1] = st.retire_mask[0] = st.retire_mask[1] = 0;
+        st.queue_done = 0;
+        st.timeout = 0;
+        st.exit_flag = 0;
+    }
+    __syncthreads();
+    bool first = true;
+    for (;;) {
+        // ---- decisions of both halves (warp h), after the previous iteration's epilogue
+        if (!first && warp < 2) decide_half(a, st, warp, lane, B);
+        __syncthreads();
+        UNI_PHASE(0);
+        // ---- retire outputs (both halves)
+        const int rm = st.retire_mask[0] | st.retire_mask[1];
+        if (!first && rm) {
+            const int j_begin = a.seg == 0 ? 0 : 1;
+            for (int i = tid; i < N * SLOTS; i += T) {
+                const int j = i >> 3, t = i & 7, h = t / HS, s = t % HS;
+                if (!((rm >> t) & 1)) continue;
+                const size_t tr = static_cast<size_t>(st.slot_traj[t]);
+                if (a.samples && j >= j_begin) {
+                    double* o = a.samples + (tr * a.R + a.row0 + j) * 6;
+#pragma unroll
+                    for (int c = 0; c < 6; ++c) o[c] = ybuf[y2(j, h, c, s)];
+                }
+                if (a.hot)
+                    for (int c = 0; c < 6; ++c) hot_retire_node(a.hot + (tr * N + j) * 6, c, ybuf[y2(j, h, c, s)]);
+                if (j == N - 1) {
+#pragma unroll
+                    for (int c = 0; c < 6; ++c) a.state_out[tr * 6 + c] = ybuf[y2(j, h, c, s)];
+                }
+            }
+            __syncthreads();  // slot_traj is rewritten by the claim below
+        }
+        // ---- free + claim into both halves (thread 0; the order of k_pc_ws: half 0, then 1)
+        if (tid == 0) {
+            for (int h = 0; h < 2; ++h) {
+                int am = st.act_word[0] | st.act_word[1];
+                if (!first) {
+                    const int fm = st.free_mask[h];
+                    am &= ~fm;
+                    for (int t = 0; t < SLOTS; ++t)
+                        if ((fm >> t) & 1) st.slot_traj[t] = -1;
+                }
+                int new_mask = 0;
+                const int hmask = 0xF << (h * HS);
+                const int free_h = HS - __popc(static_cast<unsigned>(am & hmask));
+                if (!st.queue_done && free_h >= a.gmax) {
+                    const int k = free_h / a.gmax;
+                    const int g0 = atomicAdd(a.queue, k);
+                    const int g1 = min(g0 + k, a.P);
+                    if (g0 + k >= a.P) st.queue_done = 1;
+                    for (int gi = g0; gi < g1; ++gi) {
+                        int lg = h * HS;
+                        while (st.grp_id[lg] >= 0) ++lg;
+                        const int off = static_cast<int>(a.group_off[gi]);
+                        const int size = static_cast<int>(a.group_off[gi + 1]) - off;
+                        st.grp_id[lg] = gi;
+                        st.grp_size[lg] = size;
+                        st.grp_iter[lg] = 0;
+                        int t = h * HS;
+                        for (int mbr = 0; mbr < size; ++mbr) {
+                            while ((am >> t) & 1) ++t;
+                            am |= 1 << t;
+                            new_mask |= 1 << t;
+                            st.slot_traj[t] = off + mbr;
+                            st.slot_grp[t] = lg;
+                            st.slot_member[t] = mbr;
+                            st.warm_key[t] = INT_MAX;
+                        }
+                    }
+                }
+                st.act_word[h] = am & hmask;
+                st.new_mask[h] = new_mask;
+                st.half_active[h] = (am & hmask) != 0;
+                st.free_mask[h] = st.retire_mask[h] = 0;
+            }
+            if (a.deadline_ns != 0ull && globaltimer_ns() > a.deadline_ns) st.timeout = 1;
+        }
+        __syncthreads();
+        UNI_PHASE(1);
+        const int am = st.act_word[0] | st.act_word[1];
+        if (st.timeout || (am == 0 && st.queue_done)) {
+            if (tid == 0 && st.timeout)
+                for (int lg = 0; lg < SLOTS; ++lg) {
+                    const int gi = st.grp_id[lg];
+                    if (gi < 0) continue;
+                    a.faults[gi].status = FAULT_TIMEOUT;
+                    a.faults[gi].iteration = st.grp_iter[lg];
+                    a.rep_iter[gi] = st.grp_iter[lg];
+                    a.rep_conv[gi] = 0;
+                }
+            break;
+        }
+        // ---- load + warm start of new slots (both halves)
+        const int new_mask = st.new_mask[0] | st.new_mask[1];
+        if (new_mask) {
+            for (int i = tid; i < SLOTS * 6; i += T) {
+                const int s = i / 6, c = i % 6;
+                if ((new_mask >> s) & 1) st.y0[s][c] = a.state_in[static_cast<size_t>(st.slot_traj[s]) * 6 + c];
+            }
+            __syncthreads();
+            for (int i = tid; i < N * SLOTS; i += T) {
+                const int j = i >> 3, t = i & 7, h = t / HS, s = t % HS;
+                if (!((new_mask >> t) & 1)) continue;
+                const double r[3] = {st.y0[t][0], st.y0[t][1], st.y0[t][2]};
+                const double v[3] = {st.y0[t][3], st.y0[t][4], st.y0[t][5]};
+                double ro[3] = {r[0], r[1], r[2]}, vo[3] = {v[0], v[1], v[2]};
+                if (!a.cold_start) {
+                    const int chk = conic_check(r, v, a.fd.central_mu);
+                    if (chk == CONIC_ZERO_RADIUS) {
+                        atomicMin(&st.warm_key[t], j * 4 + CONIC_ZERO_RADIUS);
+                    } else if (chk == CONIC_OK) {
+                        double mf, ef;
+                        if (kepler_propagate(r, v, a.fd.central_mu, a.times[j] - a.epoch, ro, vo, &mf, &ef) != CONIC_OK)
+                            atomicMin(&st.warm_key[t], j * 4 + CONIC_SOLVER);
+                    }
+                    if (j == 0 && a.cold_fallback) a.cold_fallback[st.slot_traj[t]] = (chk == CONIC_NON_ELLIPTIC) ? 1 : 0;
+                }
+                if (a.hot) hot_start_node(a.hot + (static_cast<size_t>(st.slot_traj[t]) * N + j) * 6, a.hot_apply, ro, vo);
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    ybuf[y2(j, h, c, s)] = ro[c];
+                    ybuf[y2(j, h, c + 3, s)] = vo[c];
+                }
+            }
+            __syncthreads();
+            if (tid < SLOTS && ((new_mask >> tid) & 1) && st.warm_key[tid] != INT_MAX) {
+                const int t = tid, j = st.warm_key[t] / 4;
+                st.warm_kind[t] = st.warm_key[t] % 4;
+                const double r[3] = {st.y0[t][0], st.y0[t][1], st.y0[t][2]};
+                const double v[3] = {st.y0[t][3], st.y0[t][4], st.y0[t][5]};
+                double ro[3], vo[3], mf = 0.0, ef = 0.0;
+                if (st.warm_kind[t] == CONIC_SOLVER)
+                    kepler_propagate(r, v, a.fd.central_mu, a.times[j] - a.epoch, ro, vo, &mf, &ef);
+                st.warm_val[t][0] = mf;
+                st.warm_val[t][1] = ef;
+            }
+        }
+        UNI_PHASE(2);
+        // ---- force of both halves, folded as written (mirrored node pairs)
+        {
+            const int npw = half > T / 8 ? 2 : 4;  // work items per (half, node pair): slot pairs or slots
+            for (int w = tid; w < 2 * npw * half; w += T) {
+                const int h = w / (npw * half), r = w % (npw * half);
+                const int act_h = (am >> (h * HS)) & 0xF;
+                if (!act_h) continue;
+                double* fbh = fb0 + h * (fb_bytes / sizeof(double));
+                if (npw == 2)
+                    force_pair<2>(a.fd, ybuf, fbh, st.sing_key, pos_base, ind_base, psj, psc, act_h, h, r % half, N,
+                                  (r / half) * 2);
+                else
+                    force_pair<1>(a.fd, ybuf, fbh, st.sing_key, pos_base, ind_base, psj, psc, act_h, h, r % half, N,
+                                  r / half);
+            }
+        }
+        __syncthreads();
+        UNI_PHASE(3);
+        if (tid < SLOTS && st.sing_key[tid] != INT_MAX) {
+            const int t = tid, h = t / HS, s = t % HS, key = st.sing_key[t], j = key / (B + 1), chk = key % (B + 1);
+            st.sing_val[t] = check_distance(ybuf[y2(j, h, 0, s)], ybuf[y2(j, h, 1, s)], ybuf[y2(j, h, 2, s)], j, chk, a.fd);
+        }
+        // ---- b0 = anchor.F + 2 y0 of both halves (warps 0-7: half 0, 8-15: half 1; fixed order)
+        {
+            const int h = warp >> 3, fw = warp & 7;
+            if ((am >> (h * HS)) & 0xF) {
+                const double* fbh = fb0 + h * (fb_bytes / sizeof(double));
+                double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+                const int jl = lane & 3;
+                for (int kq = fw; kq < a.nkp * 2; kq += 8) {
+                    const double w = anc[4 * kq + jl];
+                    const double* fq = fbh + kq * FKS + lane;
+                    s0 = fma(w, fq[0], s0);
+                    s1 = fma(w, fq[32], s1);
+                    s2 = fma(w, fq[64], s2);
+                }
+#pragma unroll
+                for (int off = 1; off < 4; off <<= 1) {
+                    s0 += __shfl_xor_sync(0xffffffffu, s0, off);
+                    s1 += __shfl_xor_sync(0xffffffffu, s1, off);
+                    s2 += __shfl_xor_sync(0xffffffffu, s2, off);
+                }
+                if (jl == 0) {
+                    double* bp = b0part + (h * B0_PARTS + fw) * HC;
+                    const int c8 = lane >> 2;
+                    bp[c8] = s0;
+                    bp[8 + c8] = s1;
+                    bp[16 + c8] = s2;
+                }
+            }
+        }
+        __syncthreads();
+        if (tid < 2 * HC) {
+            const int h = tid / HC, ft = tid % HC;
+            if ((am >> (h * HS)) & 0xF) {
+                const int c = 2 * (ft >> 3) + (ft & 1), s = (ft & 7) >> 1;
+                double sum = 0.0;
+#pragma unroll
+                for (int part = 0; part < B0_PARTS; ++part) sum += b0part[(h * B0_PARTS + part) * HC + ft];
+                st.b0h[h][ft] = 0.5 * fma(a.omega2, sum, 2.0 * st.y0[h * HS + s][c]);
+            }
+        }
+        __syncthreads();
+        UNI_PHASE(4);
+        // ---- DMMA + epilogue: units (pair tile, half), unit u = warp + 16 i
+        {
+            const int nunits = 2 * mtiles;
+            int tl[NV], hh[NV];
+            const double* fbu[NV];
+            int nv = 0;
+#pragma unroll
+            for (int i = 0; i < NV; ++i) {
+                const int u = warp + i * NW;
+                hh[i] = u < nunits ? u / mtiles : 0;
+                tl[i] = u < nunits ? u % mtiles : 0;
+                fbu[i] = fb0 + hh[i] * (fb_bytes / sizeof(double));
+                if (u < nunits && st.half_active[hh[i]]) nv = i + 1;
+            }
+            double acc[NV][3][2][2];
+            if (nv == NV) {
+                gemm_units_fold<NV>(a.upack_fold, a.nkp_fold, half, fbu, tl, lane, acc);
+#pragma unroll
+                for (int i = 0; i < NV; ++i)
+                    if (st.half_active[hh[i]]) epilogue_unit_fold(a, st, ybuf, acc[i], hh[i], tl[i], half, lane);
+            } else if (nv > 0) {  // NV == 2, the warp's second unit is out of range or idle
+                if constexpr (NV == 2) {
+                    const double* f1[1] = {fbu[0]};
+                    const int t1[1] = {tl[0]};
+                    double a1[1][3][2][2];
+                    if (st.half_active[hh[0]]) {
+                        gemm_units_fold<1>(a.upack_fold, a.nkp_fold, half, f1, t1, lane, a1);
+                        epilogue_unit_fold(a, st, ybuf, a1[0], hh[0], tl[0], half, lane);
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        UNI_PHASE(5);
+        first = false;
+    }
+    if (prof) {
+        __syncthreads();
+        if (tid == 0) {
+            s_pc[PHASES - 1] = 1;
+            for (int k = 0; k < PHASES; ++k)
+                if (s_pc[k]) atomicAdd(a.phase_cycles + k, static_cast<unsigned long long>(s_pc[k]));
+        }
+    }
+}
+
+template <int NV, bool STAGE>
+static cudaError_t launch_uni_t(const SegArgs& a, int grid, size_t smem, cudaStream_t s) {
+    auto kern = k_pc_uni<NV, STAGE>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    kern<<<grid, WS_THREADS, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
 template <int MAIN, int XMW, bool FOLD = false>
 static cudaError_t launch_ws_t(const SegArgs& a, int grid, size_t smem, cudaStream_t s) {
     // relativistic launches never stage the ephemeris (the host clears stage_eph)
@@ -1168,6 +1734,18 @@ bool ws_supported(int N, bool fold) {
 
 size_t ws_smem_bytes(int N, int nkp, int xrows, int B, int stage_eph, bool fold) {
     return ws_layout(N, nkp, xrows, B, stage_eph, fold ? 1 : 0).total;
+}
+
+/// Unified folded kernel (Newtonian, N % 8 == 0): units of 2 x ceil(N/16) pair tiles over 16 warps.
+bool uni_supported(int N) { return N % 8 == 0 && (2 * ws_mtiles(N, true) + 15) / 16 <= 2; }
+
+cudaError_t launch_segment_uni(const SegArgs& a, int grid, cudaStream_t s) {
+    if (!uni_supported(a.N) || a.fd.rel || a.upack_fold == nullptr) return cudaErrorNotSupported;
+    const int nv = (2 * ws_mtiles(a.N, true) + 15) / 16;
+    const size_t smem = ws_smem_bytes(a.N, a.nkp, 0, a.fd.n_bodies, a.stage_eph, true);
+    if (a.stage_eph)
+        return nv == 1 ? launch_uni_t<1, true>(a, grid, smem, s) : launch_uni_t<2, true>(a, grid, smem, s);
+    return nv == 1 ? launch_uni_t<1, false>(a, grid, smem, s) : launch_uni_t<2, false>(a, grid, smem, s);
 }
 
 cudaError_t launch_segment_ws(const SegArgs& a, int grid, cudaStream_t s) {

@@ -206,6 +206,7 @@ struct pswarm_ctx {
     int slot_kernel = 0;  // 0 auto, 1 generic k_pc_segment, 2 warp-specialised k_pc_ws
     int poison_outputs = 0;  // 1: NaN-fill device outputs before each solve (tests)
     int fold = 1;            // 1: mirror-folded update when N % 8 == 0 (k_pc_ws_fold)
+    int unified = 1;         // 1: the folded Newtonian solve runs k_pc_uni (all warps per phase)
     unsigned long long phase_host[pswarm_dev::PHASES] = {};
     PinnedBuf pin_in, pin_rep, pin_term;
     // wide-group path
@@ -333,6 +334,7 @@ ForceData make_force_data(const double* pos, const double* mus, const double* in
     fd.central_mu = central_mu;
     fd.floor_km = floor_km;
     fd.floor2_hi = floor_km * floor_km * (1.0 + 1e-9);
+    std::memcpy(&fd.floor2_hi_bits, &fd.floor2_hi, sizeof(double));
     fd.n_bodies = n_bodies;
     return fd;
 }
@@ -596,7 +598,8 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
     const bool use_ws = fold || (!wide && gmax <= 4 && ws_supported(Ni, false) && ctx->slot_kernel != 1 &&
                                  ws_smem_bytes(Ni, op.nkp, ws_extra_rows(Ni, false), nb, 0, false) <= SMEM_MAX);
     const int xrows = use_ws ? ws_extra_rows(Ni, fold) : extra_rows(Ni, op.gp);
-    ctx->last_kernel = wide ? "k_wide_iter" : fold ? "k_pc_ws_fold" : use_ws ? "k_pc_ws" : "k_pc_segment";
+    const bool uni = fold && !rel && ctx->unified && uni_supported(Ni);
+    ctx->last_kernel = wide ? "k_wide_iter" : uni ? "k_pc_uni" : fold ? "k_pc_ws_fold" : use_ws ? "k_pc_ws" : "k_pc_segment";
     // stage the frozen ephemeris in shared memory when it fits next to the state blocks
     const int stage_eph = nb > 0 && !rel &&
                                   (use_ws ? ws_smem_bytes(Ni, op.nkp, xrows, nb, 1, fold)
@@ -738,7 +741,9 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
         a.anc_fold = fold ? reinterpret_cast<const double*>(op.anc_fold.p) : nullptr;
         if (max_it > 0 && !wide) {
             cuda_check(cudaEventRecord(ctx->evk0, st), "event");
-            cuda_check(use_ws ? launch_segment_ws(a, grid, st) : launch_segment(a, grid, st), "slot kernel launch");
+            cuda_check(uni ? launch_segment_uni(a, grid, st)
+                           : use_ws ? launch_segment_ws(a, grid, st) : launch_segment(a, grid, st),
+                       "slot kernel launch");
             cuda_check(cudaEventRecord(ctx->evk1, st), "event");
             ++ctx->launches;
         } else if (max_it > 0) {
@@ -1075,6 +1080,7 @@ pswarm_status pswarm_set_option(pswarm_ctx* ctx, const char* key, int64_t value)
         else if (k == "slot_kernel") ctx->slot_kernel = static_cast<int>(value);
         else if (k == "poison_outputs") ctx->poison_outputs = value != 0;
         else if (k == "fold") ctx->fold = value != 0;
+        else if (k == "unified") ctx->unified = value != 0;
         else raise(PSWARM_ERR_GENERIC, "pswarm_set_option: unknown key '" + k + "'");
     });
 }

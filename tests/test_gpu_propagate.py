@@ -262,20 +262,40 @@ def test_pinned_samples_overlapped_copy_identical(ctx):
     assert np.array_equal(a.terminal_states, b.terminal_states)
 
 
-@pytest.mark.parametrize("n", [128, 200, 256])
-@pytest.mark.parametrize("fold", [1, 0])
-def test_mirror_folded_and_dense_updates(ctx, oracle, n, fold):
-    """The slot kernel's Picard update folded over the Chebyshev mirror symmetry
-    (half the DMMAs, default where N % 8 == 0) and the dense update both match the
-    oracle; the kernel that ran is the one selected."""
+@pytest.mark.parametrize("n", [64, 128, 200, 256])
+@pytest.mark.parametrize("fold,unified,kernel", [(1, 1, "k_pc_uni"), (1, 0, "k_pc_ws_fold"), (0, 0, "k_pc_ws")])
+def test_mirror_folded_and_dense_updates(ctx, oracle, n, fold, unified, kernel):
+    """The Picard update folded over the Chebyshev mirror symmetry (half the DMMAs,
+    default where N % 8 == 0) in the unified kernel and in the warp-specialised one, and
+    the dense update, all match the oracle; the kernel that ran is the one selected."""
     states, plan, cfg = _setup(24, n, 0.87, "planets8")
     ctx.set_option("fold", fold)
+    ctx.set_option("unified", unified)
     try:
         got = ctx.run_batch(states, cfg, plan, "independent")
         name = ctx.kernel_name()
     finally:
         ctx.set_option("fold", 1)
-    assert name == ("k_pc_ws_fold" if fold else "k_pc_ws")
+        ctx.set_option("unified", 1)
+    assert name == kernel
     want = oracle.run_batch(states, cfg, plan, "independent", 8)
     _parity(got, want)
     assert got.converged.all()
+
+
+def test_unified_kernel_refill_and_multisegment(ctx, oracle):
+    """k_pc_uni with few CTAs (slots refilled many times, heterogeneous iteration counts)
+    over a multi-segment per-orbit plan: every trajectory matches its own oracle solve."""
+    base = ps.reference_state()
+    states = np.concatenate([ps.make_clone_batch(base, 30, sp) for sp in (1e-7, 1e-4, 1e-2)])
+    period = ps.osculating_period(base, ps.MU_SUN)
+    plan = ps.plan_segments(base, 0.0, 2.3 * period, ps.MU_SUN, "per_orbit", 200)
+    cfg = ps.reference_force_config("n_body", bodies=ps.planets8(), n_nodes=200)
+    ctx.set_option("max_ctas", 2)
+    try:
+        got = ctx.run_batch(states, cfg, plan, "independent")
+        assert ctx.kernel_name() == "k_pc_uni"
+    finally:
+        ctx.set_option("max_ctas", 0)
+    want = oracle.run_batch(states, cfg, plan, "independent", 8)
+    _parity(got, want)

@@ -1,5 +1,5 @@
-"""Attribute ncu SASS-level warp-stall samples of k_pc_ws<3,1,1,0> to CUDA source lines
-(diagnostics).  usage: python tools/ncu_lines.py <source.csv> <nvdisasm -g -c output> [lo hi]"""
+"""Attribute ncu SASS-level warp-stall samples of one kernel to CUDA source lines
+(diagnostics).  usage: python tools/ncu_lines.py <source.csv> <nvdisasm -g -c output> [mangled name]"""
 import csv
 import re
 import sys
@@ -7,7 +7,7 @@ from collections import Counter, defaultdict
 
 src, sass = sys.argv[1], sys.argv[2]
 lines = open(sass).read().split('\n')
-name = '.text._ZN10pswarm_dev7k_pc_wsILi3ELi1ELb1ELb0EEEvNS_7SegArgsE:'
+name = '.text.' + (sys.argv[3] if len(sys.argv) > 3 else '_ZN10pswarm_dev7k_pc_wsILi2ELi1ELb1ELb0ELb1EEEvNS_7SegArgsE') + ':'
 start = [i for i, l in enumerate(lines) if l.startswith(name)][0]
 end = next((i for i in range(start + 1, len(lines)) if lines[i].startswith('//-----')), len(lines))
 cur, a2l = None, {}

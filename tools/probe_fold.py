@@ -15,19 +15,22 @@ for n in (128, 160, 200, 256):
     plan = ps.plan_segments(base, 0.0, 0.87 * period, ps.MU_SUN, "single", n)
     cfg = ps.reference_force_config("n_body", bodies=ps.planets8(), n_nodes=n)
     want = orc.run_batch(states, cfg, plan, "independent", 8)
-    for fold in (1, 0):
+    for fold, uni in ((1, 1), (1, 0), (0, 0)):
         ctx.set_option("fold", fold)
+        ctx.set_option("unified", uni)
         got = ctx.run_batch(states, cfg, plan, "independent")
         d = ps.max_state_discrepancy(got.trajectories, want.trajectories)
         di = int(np.abs(got.iterations.astype(int) - want.iterations.astype(int)).max())
         print(n, ctx.kernel_name(), f"disc {d:.3e} diter {di}", flush=True)
 ctx.set_option("fold", 1)
+ctx.set_option("unified", 1)
 for M in (1000, 100000):
     states = ps.make_clone_batch(base, M, 1e-5)
     plan = ps.plan_segments(base, 0.0, 0.87 * period, ps.MU_SUN, "single", 200)
     cfg = ps.reference_force_config("n_body", bodies=ps.planets8(), n_nodes=200)
-    for fold in (1, 0):
+    for fold, uni in ((1, 1), (1, 0), (0, 0)):
         ctx.set_option("fold", fold)
+        ctx.set_option("unified", uni)
         for rep in range(3):
             r = ctx.run_batch(states, cfg, plan, "independent", samples=False, history=False)
         fit = 12 * 200 * 200 + (75 + 160) * 200 + 12

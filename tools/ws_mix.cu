@@ -7,7 +7,7 @@
 #include "../paper_2301_03989_b200/csrc/pc_slots2.cu"
 using namespace pswarm_dev;
 
-template <int FPW>
+template <int FPW, int MODE>
 __global__ void __launch_bounds__(256 + 32 * FPW, 1) k_mix(const double2* upack, int nkp, int N, int reps,
                                                           double* sink, long long* cycles, unsigned long long* fp_iters) {
     extern __shared__ __align__(16) double fbuf[];
@@ -41,32 +41,46 @@ __global__ void __launch_bounds__(256 + 32 * FPW, 1) k_mix(const double2* upack,
     } else {
         if constexpr (FPW > 8) asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
         double x[4] = {1.1 + tid, 2.2 + tid, 3.3 + tid, 4.4 + tid}, y[4] = {0, 0, 0, 0};
+        unsigned u[4] = {1u + tid, 2u + tid, 3u + tid, 4u + tid};
+        const volatile unsigned* sidx = reinterpret_cast<const volatile unsigned*>(fbuf);
         unsigned long long it = 0;
         while (!done) {
+            if constexpr (MODE == 0) {
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {  // 6 FP64 instructions per chain step
-                const double q = rsqrt_newton(x[k], rsqrt_seed(x[k]));
-                y[k] = fma(q * q, q, y[k]);
-                x[k] = fma(x[k], 1.0000001, 1e-9);
+                for (int k = 0; k < 4; ++k) {  // 6 FP64 instructions per chain step
+                    const double q = rsqrt_newton(x[k], rsqrt_seed(x[k]));
+                    y[k] = fma(q * q, q, y[k]);
+                    x[k] = fma(x[k], 1.0000001, 1e-9);
+                }
+            } else if constexpr (MODE == 1) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k)  // 6 integer ALU instructions per chain step
+#pragma unroll
+                    for (int r = 0; r < 3; ++r) u[k] = (u[k] * 2654435761u + 12345u) ^ (u[k] >> 7);
+            } else {
+#pragma unroll
+                for (int k = 0; k < 4; ++k)  // dependent shared loads (+ index arithmetic)
+#pragma unroll
+                    for (int r = 0; r < 6; ++r) u[k] = sidx[(u[k] + lane) & 1023] & 1023;
             }
             ++it;
         }
         if (lane == 0) atomicAdd(fp_iters, it);
-        sink[blockIdx.x * blockDim.x + tid] = y[0] + y[1] + y[2] + y[3];
+        sink[blockIdx.x * blockDim.x + tid] = y[0] + y[1] + y[2] + y[3] + u[0] + u[1] + u[2] + u[3];
     }
 }
 
-template <int FPW>
+template <int FPW, int MODE>
 void run(const double2* du, int nkp, int N) {
     double* sink; cudaMalloc(&sink, 148 * 1024 * 8);
     long long* cyc; cudaMalloc(&cyc, 148 * 8);
     unsigned long long* it; cudaMalloc(&it, 8); cudaMemset(it, 0, 8);
     const size_t smem = 2 * nkp * FKS * 8;
-    cudaFuncSetAttribute(k_mix<FPW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_mix<FPW, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int reps = 200;
-    k_mix<FPW><<<148, 256 + 32 * FPW, smem>>>(du, nkp, N, reps, sink, cyc, it);
+    k_mix<FPW, MODE><<<148, 256 + 32 * FPW, smem>>>(du, nkp, N, reps, sink, cyc, it);
     cudaMemset(it, 0, 8);
-    k_mix<FPW><<<148, 256 + 32 * FPW, smem>>>(du, nkp, N, reps, sink, cyc, it);
+    k_mix<FPW, MODE><<<148, 256 + 32 * FPW, smem>>>(du, nkp, N, reps, sink, cyc, it);
     cudaDeviceSynchronize();
     std::vector<long long> hc(148); cudaMemcpy(hc.data(), cyc, 148 * 8, cudaMemcpyDeviceToHost);
     unsigned long long hi; cudaMemcpy(&hi, it, 8, cudaMemcpyDeviceToHost);
@@ -74,8 +88,9 @@ void run(const double2* du, int nkp, int N) {
     // FP64 warp instructions issued by the FP warps per SM-cycle (24 per loop iteration)
     const double fp_rate = hi * 24.0 / 148.0 / avg;
     std::fflush(stdout);
-    std::printf("{\"fp_warps\": %d, \"gemm_cycles_per_half\": %.0f, \"fp64_warp_instr_per_cycle_per_sm\": %.3f, \"err\": \"%s\"}\n",
-                FPW, avg / reps, fp_rate, cudaGetErrorString(cudaGetLastError()));
+    std::printf("{\"mode\": \"%s\", \"fp_warps\": %d, \"gemm_cycles_per_half\": %.0f, \"warp_instr_per_cycle_per_sm\": %.3f, \"err\": \"%s\"}\n",
+                MODE == 0 ? "fp64" : (MODE == 1 ? "int" : "lds"), FPW, avg / reps, fp_rate,
+                cudaGetErrorString(cudaGetLastError()));
     std::fflush(stdout);
 }
 
@@ -84,9 +99,9 @@ int main() {
     std::vector<double> hu(static_cast<size_t>(mt) * nkp * 64);
     for (size_t i = 0; i < hu.size(); ++i) hu[i] = 1e-4 * ((i * 2654435761u) % 1000);
     double2* du; cudaMalloc(&du, hu.size() * 8); cudaMemcpy(du, hu.data(), hu.size() * 8, cudaMemcpyHostToDevice);
-    run<0>(du, nkp, N);
-    run<4>(du, nkp, N);
-    run<8>(du, nkp, N);
-    run<16>(du, nkp, N);
+    run<0, 0>(du, nkp, N);
+    run<8, 0>(du, nkp, N);
+    run<8, 1>(du, nkp, N);
+    run<8, 2>(du, nkp, N);
     return 0;
 }
