@@ -360,7 +360,7 @@ class Context:
                    "decisions", "retire")
     WS_PHASE_NAMES = ("mma_wait_f", "mma_dmma", "mma_epilogue", "mma_wait_b0", "fp_wait_y", "fp_staged_decisions",
                       "fp_retire_claim", "fp_warm_start", "fp_force", "fp_b0", "fp_staged")
-    UNI_PHASE_NAMES = ("decisions", "retire_claim", "warm_start", "force", "sing_b0", "dmma_epilogue")
+    UNI_PHASE_NAMES = ("decisions", "retire_claim", "warm_start", "force", "sing_b0", "dmma", "epilogue")
     N_PHASES = 12
 
     def phase_cycles(self) -> dict:

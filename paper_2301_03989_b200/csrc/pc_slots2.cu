@@ -128,8 +128,8 @@ __host__ __device__ inline WsLayout ws_layout(int N, int nkp, int xrows, int B, 
     L.fbuf0 = L.ybuf + sizeof(double) * static_cast<size_t>(N) * YS2;
     const size_t fb = sizeof(double) * static_cast<size_t>(fold ? ws_fold_ksteps(N, nkp) : 2 * nkp) * FKS;
     L.fbuf1 = L.fbuf0 + fb;
-    L.xstage = L.fbuf1 + fb;  // [2 halves][xrows][HC]
-    L.anchor = L.xstage + sizeof(double) * 2 * static_cast<size_t>(xrows) * HC;
+    L.xstage = L.fbuf1 + fb;  // [2 halves][fold ? lo, hi : 1][xrows][HC]
+    L.anchor = L.xstage + sizeof(double) * (fold ? 4 : 2) * static_cast<size_t>(xrows) * HC;
     L.b0part = L.anchor + sizeof(double) * static_cast<size_t>(8 * nkp);
     L.eph = L.b0part + sizeof(double) * 2 * B0_PARTS * HC;  // [half][part][HC] (k_pc_uni forms both at once)
     L.state = L.eph + (stage_eph ? sizeof(double) * static_cast<size_t>(N) * (3 * B + 3) : 0);
@@ -259,27 +259,31 @@ __device__ __forceinline__ void gemm_half(const double2* __restrict__ upack, int
 }
 
 /// Folded counterpart of gemm_core: each of the warp's NV tiles is a pair tile (rows
-/// 8mt..8mt+7 of both half-size operators), mt = warp + i * MMA_WARPS (strided, so the four
-/// SMSPs carry equal DMMA streams to within one tile): acc[.][.][0] = Y_j + Y_{N-1-j} part
-/// (upf part 1, Fbuf positions >= N/2), acc[.][.][1] = Y_j - Y_{N-1-j} part (upf part 0,
-/// positions < N/2).  upf layout: [pair mt][part][k-pair][lane] double2, nkpf k-pairs per part.
-template <int NV, int MAIN>
+/// 8mt..8mt+7 of both half-size operators), mt = warp + i * MMA_WARPS (strided), plus NX
+/// (0/1) single-n-tile unit of a leftover pair tile (xt, n-tile xp) that balances the four
+/// SMSPs' DMMA streams: acc[.][.][0] = Y_j + Y_{N-1-j} part (upf part 1, Fbuf positions
+/// >= N/2), acc[.][.][1] = Y_j - Y_{N-1-j} part (upf part 0, positions < N/2).
+/// upf layout: [pair mt][part][k-pair][lane] double2, nkpf k-pairs per part.
+template <int NV, int NX, int MAIN>
 __device__ __forceinline__ void gemm_core_fold(const double2* __restrict__ upf, int nkpf, int half, const double* fb,
-                                               int warp, int lane, double (&acc)[MAIN][3][2][2]) {
-    const double2* am[NV][2];
+                                               int warp, int lane, int xt, int xp, double (&acc)[MAIN][3][2][2],
+                                               double (&xacc)[2][2]) {
+    constexpr int NA = NV + NX;
+    const double2* am[NA][2];
 #pragma unroll
-    for (int i = 0; i < NV; ++i)
+    for (int i = 0; i < NA; ++i) {
+        const int t = i < NV ? warp + i * MMA_WARPS : xt;
 #pragma unroll
-        for (int u = 0; u < 2; ++u)
-            am[i][u] = upf + (static_cast<size_t>(warp + i * MMA_WARPS) * 2 + (1 - u)) * nkpf * 32 + lane;
+        for (int u = 0; u < 2; ++u) am[i][u] = upf + (static_cast<size_t>(t) * 2 + (1 - u)) * nkpf * 32 + lane;
+    }
     const double* fb_lo = fb + lane;                          // part 0: s at positions < N/2
     const double* fb_hi = fb + (half >> 2) * FKS + lane;      // part 1: a at positions >= N/2
     struct Pair {
-        double2 m[NV][2];
+        double2 m[NA][2];
     };
     auto load = [&](int kp, Pair& c) {
 #pragma unroll
-        for (int i = 0; i < NV; ++i)
+        for (int i = 0; i < NA; ++i)
 #pragma unroll
             for (int u = 0; u < 2; ++u) c.m[i][u] = __ldg(am[i][u] + kp * 32);
     };
@@ -297,6 +301,10 @@ __device__ __forceinline__ void gemm_core_fold(const double2* __restrict__ upf, 
 #pragma unroll
                     for (int p = 0; p < 3; ++p) dmma(acc[i][p][u][0], acc[i][p][u][1], av, bv[p]);
                 }
+                if constexpr (NX > 0) {
+                    const double bx = xp == 0 ? bv[0] : (xp == 1 ? bv[1] : bv[2]);
+                    dmma(xacc[u][0], xacc[u][1], sub ? c.m[NV][u].y : c.m[NV][u].x, bx);
+                }
             }
         }
     };
@@ -312,21 +320,29 @@ __device__ __forceinline__ void gemm_core_fold(const double2* __restrict__ upf, 
     if (kp < nkpf) compute(kp, p0);
 }
 
-/// gemm_core_fold for this warp's number of valid pair tiles (0..MAIN).
+/// The warp's folded share of half h: its full pair tiles (0..MAIN of tiles < nfull) and
+/// its extra unit (xt >= 0) — compile-time counts (a predicated-off DMMA costs a pipe slot).
 template <int MAIN>
 __device__ __forceinline__ void gemm_half_fold(const double2* __restrict__ upf, int nkpf, int half, const double* fb,
-                                               int mtiles, int warp, int lane, double (&acc)[MAIN][3][2][2]) {
+                                               int nfull, int warp, int lane, int xt, int xp,
+                                               double (&acc)[MAIN][3][2][2], double (&xacc)[2][2]) {
 #pragma unroll
     for (int i = 0; i < MAIN; ++i)
 #pragma unroll
         for (int p = 0; p < 3; ++p)
 #pragma unroll
             for (int u = 0; u < 2; ++u) acc[i][p][u][0] = acc[i][p][u][1] = 0.0;
+    xacc[0][0] = xacc[0][1] = xacc[1][0] = xacc[1][1] = 0.0;
     if (PSWARM_ABLATE == 3) return;  // diagnostic: no DMMA
-    if (warp + (MAIN - 1) * MMA_WARPS < mtiles)
-        gemm_core_fold<MAIN, MAIN>(upf, nkpf, half, fb, warp, lane, acc);
-    else if constexpr (MAIN >= 2) {
-        if (warp < mtiles) gemm_core_fold<1, MAIN>(upf, nkpf, half, fb, warp, lane, acc);
+    const int nv = warp + (MAIN - 1) * MMA_WARPS < nfull ? MAIN : (warp < nfull ? 1 : 0);
+    if (xt >= 0) {  // extra units go to warps with fewer than MAIN full tiles (host plan)
+        if (nv >= 1) gemm_core_fold<1, 1, MAIN>(upf, nkpf, half, fb, warp, lane, xt, xp, acc, xacc);
+        else gemm_core_fold<0, 1, MAIN>(upf, nkpf, half, fb, warp, lane, xt, xp, acc, xacc);
+    } else {
+        if (nv == MAIN) gemm_core_fold<MAIN, 0, MAIN>(upf, nkpf, half, fb, warp, lane, xt, xp, acc, xacc);
+        else if constexpr (MAIN >= 2) {
+            if (nv == 1) gemm_core_fold<1, 0, MAIN>(upf, nkpf, half, fb, warp, lane, xt, xp, acc, xacc);
+        }
     }
 }
 
@@ -839,10 +855,15 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
             if (st.exit_flag) break;
             if (st.half_active[h]) {
                 if constexpr (FOLD) {
-                    double facc[MAIN][3][2][2];
+                    // full pair tiles < nfull strided over the warps; the leftover tiles' 3 n-tiles
+                    // each go to the warps that hold one full tile fewer (rows staged, below)
+                    const int nxt = xrows >> 3, nfull = mtiles - nxt;
+                    const int xk = (warp - nfull % MMA_WARPS + MMA_WARPS) % MMA_WARPS;
+                    const int xt = (XMW > 0 && xk < 3 * nxt) ? nfull + xk / 3 : -1, xp = xk % 3;  // XMW: extras
+                    double facc[MAIN][3][2][2], fxacc[2][2];
                     gemm_half_fold<MAIN>(a.upack_fold, a.nkp_fold, half,
-                                         reinterpret_cast<const double*>(smem_raw + L.fbuf0 + h * fb_bytes), mtiles,
-                                         warp, lane, facc);
+                                         reinterpret_cast<const double*>(smem_raw + L.fbuf0 + h * fb_bytes), nfull,
+                                         warp, lane, xt, xp, facc, fxacc);
                     WS_PHASE(1);
                     bar_sync(BAR_B0 + h, WS_THREADS);  // b0 of half h (FP group, formed before F_h)
                     WS_PHASE(3);
@@ -856,7 +877,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
 #pragma unroll
                     for (int i = 0; i < MAIN; ++i) {
                         const int j = (warp + i * MMA_WARPS) * 8 + g, jm = N - 1 - j;
-                        if (j >= half || !((act_h >> q) & 1)) continue;
+                        if (warp + i * MMA_WARPS >= nfull || j >= half || !((act_h >> q) & 1)) continue;
                         double ylo[6], yhi[6], olo[6], ohi[6];
 #pragma unroll
                         for (int p = 0; p < 3; ++p)
@@ -887,10 +908,48 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
                         atomicMax(&st.slot_err[h * HS + q], static_cast<unsigned long long>(__double_as_longlong(e2)));
                         if (nf != INT_MAX) atomicMin(&st.nf_key[h * HS + q], nf);
                     }
+                    double* xs_lo = xstage + (2 * h) * xrows * HC;
+                    double* xs_hi = xs_lo + xrows * HC;
+                    if (xt >= 0) {  // extra unit -> stage (both mirrored rows; finalised below)
+                        const int j = xt * 8 + g;
+                        if (j < half) {
+#pragma unroll
+                            for (int e = 0; e < 2; ++e) {
+                                const double bb = b0[xp * 8 + 2 * q + e];
+                                const int o = (j - nfull * 8) * HC + q * 6 + 2 * xp + e;
+                                xs_lo[o] = fma(w2, fxacc[0][e] + fxacc[1][e], bb);
+                                xs_hi[o] = fma(w2, fxacc[0][e] - fxacc[1][e], bb);
+                            }
+                        }
+                    }
                     // decisions of half h here, not in the FP group: the MMA group has slack once
                     // its DMMA stream is halved, and the FP group's warps issue ~3x slower while
                     // DMMAs stream (the decisions sat on the FP group's critical chain)
                     bar_sync(BAR_MMA, MMA_THREADS);  // every warp's slot_err / nf_key update is in
+                    if (nxt > 0) {  // staged rows: pair rows of the leftover tiles and their mirrors
+                        const int xv = min(xrows, half - nfull * 8);  // valid pair rows
+                        for (int i = tid; i < xv * HS * 2; i += MMA_THREADS) {
+                            const int mir = i / (xv * HS), ii = i - mir * xv * HS;
+                            const int r = ii >> 2, s = ii & 3;
+                            const int jp = nfull * 8 + r, j = mir ? N - 1 - jp : jp;
+                            if (!((act_h >> s) & 1)) continue;
+                            const double* xs = mir ? xs_hi : xs_lo;
+                            double yn[6], yo[6];
+#pragma unroll
+                            for (int c = 0; c < 6; ++c) {
+                                yn[c] = xs[r * HC + s * 6 + c];
+                                yo[c] = ybuf[y2(j, h, c, s)];
+                            }
+                            double sbn = 0.0, sbd = 1.0;
+                            int snf = INT_MAX;
+                            update_sample(yn, yo, j, a.error_mode, sbn, sbd, snf);
+#pragma unroll
+                            for (int c = 0; c < 6; ++c) ybuf[y2(j, h, c, s)] = yn[c];
+                            atomicMax(&st.slot_err[h * HS + s], static_cast<unsigned long long>(__double_as_longlong(sbn / sbd)));
+                            if (snf != INT_MAX) atomicMin(&st.nf_key[h * HS + s], snf);
+                        }
+                        bar_sync(BAR_MMA, MMA_THREADS);
+                    }
                     if (warp == 0) decide_half(a, st, h, lane, B);
                 } else {
                 double acc[MAIN][3][2], xacc[XMW][2];
@@ -979,9 +1038,9 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
             if (!first[h]) bar_sync(BAR_Y0 + h, WS_THREADS);  // epilogue of half h done
             WS_PHASE(4);
             // ---- staged rows of half h (node rows whose components sit in several MMA warps)
-            if (!first[h] && xrows > 0 && st.half_active[h]) {
+            if (!FOLD && !first[h] && xrows > 0 && st.half_active[h]) {  // (folded: the MMA group's)
                 const int act_h = (st.act_word[h] >> (h * HS)) & 0xF;
-                const double* xs = xstage + h * xrows * HC;  // (the folded plan stages no rows)
+                const double* xs = xstage + h * xrows * HC;
                 for (int i = ft; i < xrows * HS; i += FP_THREADS) {
                     const int r = i >> 2, s = i & 3, j = MAIN * MMA_WARPS * 8 + r;
                     if (!((act_h >> s) & 1)) continue;
@@ -1658,6 +1717,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_uni(const SegArgs a) {
             double acc[NV][3][2][2];
             if (nv == NV) {
                 gemm_units_fold<NV>(a.upack_fold, a.nkp_fold, half, fbu, tl, lane, acc);
+                UNI_PHASE(5);
 #pragma unroll
                 for (int i = 0; i < NV; ++i)
                     if (st.half_active[hh[i]]) epilogue_unit_fold(a, st, ybuf, acc[i], hh[i], tl[i], half, lane);
@@ -1674,7 +1734,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_uni(const SegArgs a) {
             }
         }
         __syncthreads();
-        UNI_PHASE(5);
+        UNI_PHASE(6);
         first = false;
     }
     if (prof) {
@@ -1709,10 +1769,20 @@ static cudaError_t launch_ws_t(const SegArgs& a, int grid, size_t smem, cudaStre
 
 /// Tiles of one half: m-tiles of node rows, or (folded) of row pairs.
 static int ws_mtiles(int N, bool fold) { return fold ? (N / 2 + 7) / 8 : (N + 7) / 8; }
-/// Dense: MAIN = floor(m-tiles / 8) full-width m-tiles per warp + extras.  Folded: every pair
-/// tile is full width, strided over the warps (ceil), no extras and no staged rows.
+/// Folded: pair tiles beyond the largest multiple of 4 (one per SMSP) when 1 or 2 are left
+/// over become single-n-tile units on the warps with one full tile fewer (3 or 6 units; with
+/// 3 left over the strided plan is already as balanced; below 9 pair tiles the staged rows
+/// cost more than the balance gains).  N = 200: 13 pair tiles -> 12 full
+/// + 3 units, the busiest SMSP issues 10 instead of 12 n-tile streams per half.
+static int ws_fold_extra_tiles(int N) {
+    const int r = ws_mtiles(N, true) % 4;
+    return (r == 1 || r == 2) && ws_mtiles(N, true) > 8 ? r : 0;  // N = 96: staging costs more (measured)
+}
+/// Dense: MAIN = floor(m-tiles / 8) full-width m-tiles per warp + extras.  Folded: full pair
+/// tiles strided over the warps (ceil) + the extra units above.
 int ws_main_tiles(int N, bool fold) {
-    return fold ? (ws_mtiles(N, true) + MMA_WARPS - 1) / MMA_WARPS : ws_mtiles(N, false) / MMA_WARPS;
+    return fold ? (ws_mtiles(N, true) - ws_fold_extra_tiles(N) + MMA_WARPS - 1) / MMA_WARPS
+                : ws_mtiles(N, false) / MMA_WARPS;
 }
 /// Extra (m-tile, n-tile) tiles beyond the MAIN full-width m-tiles of every MMA warp.
 static int ws_extras(int N, bool fold) {
@@ -1720,7 +1790,7 @@ static int ws_extras(int N, bool fold) {
 }
 
 int ws_extra_rows(int N, bool fold) {
-    if (fold) return 0;
+    if (fold) return 8 * ws_fold_extra_tiles(N);  // staged pair rows
     const int r = N - ws_main_tiles(N, false) * MMA_WARPS * 8;
     return r > 0 ? r : 0;
 }
@@ -1755,7 +1825,9 @@ cudaError_t launch_segment_ws(const SegArgs& a, int grid, cudaStream_t s) {
     const int xmw = std::max(1, (ws_extras(a.N, fold) + MMA_WARPS - 1) / MMA_WARPS);
     const size_t smem = ws_smem_bytes(a.N, a.nkp, a.xrows, a.fd.n_bodies, a.stage_eph, fold);
     if (fold) {
-        return main == 1 ? launch_ws_t<1, 1, true>(a, grid, smem, s) : launch_ws_t<2, 1, true>(a, grid, smem, s);
+        if (ws_fold_extra_tiles(a.N) > 0)  // XMW = 1: leftover pair tiles as single-n-tile units
+            return main == 1 ? launch_ws_t<1, 1, true>(a, grid, smem, s) : launch_ws_t<2, 1, true>(a, grid, smem, s);
+        return main == 1 ? launch_ws_t<1, 0, true>(a, grid, smem, s) : launch_ws_t<2, 0, true>(a, grid, smem, s);
     }
     switch (main * 4 + xmw) {
     case 5: return launch_ws_t<1, 1>(a, grid, smem, s);

@@ -206,7 +206,8 @@ struct pswarm_ctx {
     int slot_kernel = 0;  // 0 auto, 1 generic k_pc_segment, 2 warp-specialised k_pc_ws
     int poison_outputs = 0;  // 1: NaN-fill device outputs before each solve (tests)
     int fold = 1;            // 1: mirror-folded update when N % 8 == 0 (k_pc_ws_fold)
-    int unified = 1;         // 1: the folded Newtonian solve runs k_pc_uni (all warps per phase)
+    int unified = 0;         // 1: the folded Newtonian solve runs k_pc_uni (all warps per phase; measured
+                             //    equal at N = 200 and slower elsewhere, tools/probe_uni.py)
     unsigned long long phase_host[pswarm_dev::PHASES] = {};
     PinnedBuf pin_in, pin_rep, pin_term;
     // wide-group path

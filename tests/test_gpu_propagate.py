@@ -276,7 +276,7 @@ def test_mirror_folded_and_dense_updates(ctx, oracle, n, fold, unified, kernel):
         name = ctx.kernel_name()
     finally:
         ctx.set_option("fold", 1)
-        ctx.set_option("unified", 1)
+        ctx.set_option("unified", 0)
     assert name == kernel
     want = oracle.run_batch(states, cfg, plan, "independent", 8)
     _parity(got, want)
@@ -292,10 +292,12 @@ def test_unified_kernel_refill_and_multisegment(ctx, oracle):
     plan = ps.plan_segments(base, 0.0, 2.3 * period, ps.MU_SUN, "per_orbit", 200)
     cfg = ps.reference_force_config("n_body", bodies=ps.planets8(), n_nodes=200)
     ctx.set_option("max_ctas", 2)
+    ctx.set_option("unified", 1)
     try:
         got = ctx.run_batch(states, cfg, plan, "independent")
         assert ctx.kernel_name() == "k_pc_uni"
     finally:
         ctx.set_option("max_ctas", 0)
+        ctx.set_option("unified", 0)
     want = oracle.run_batch(states, cfg, plan, "independent", 8)
     _parity(got, want)
