@@ -147,7 +147,8 @@ void pswarm_destroy(pswarm_ctx* ctx);
  * before every solve, so an unwritten sample can never read back as a stale value). */
 pswarm_status pswarm_set_option(pswarm_ctx* ctx, const char* key, int64_t value);
 
-/* Diagnostics: SM cycles summed over CTAs per kernel phase of the last call (12 slots).
+/* Diagnostics: SM cycles summed over CTAs per kernel phase of the last call (16 slots,
+ * the last one = number of CTAs).
  * Generic slot kernel: 0 claim, 1 warm start, 2 force, 3 DMMA, 4 anchor barrier,
  * 5 epilogue, 6 staged epilogue, 7 decisions, 8 retire.  Warp-specialised kernel
  * (MMA group / FP group leaders): 0 wait for F, 1 DMMA, 2 epilogue, 3 wait for b0,

@@ -1,3 +1,4 @@
+#include <algorithm>
 // CUDA kernels of the B200-native augmented Picard–Chebyshev propagator (sm_100a).
 //
 // k_pc_segment   persistent slot kernel: one CTA per SM owns SLOTS = 8 trajectory
@@ -694,6 +695,22 @@ __global__ void k_ephemeris(int N, const double* __restrict__ times, double cent
         row[10] = ic2 * (2.0 * (v[0] * v[0] + v[1] * v[1] + v[2] * v[2]) - phi);
         row[11] = 0.0;
     }
+}
+
+/// Batch states [M][7] = (epoch, r, v) as the caller passed them -> the solver's [M][6]:
+/// the host copies the caller's buffer as is (one DMA, no host repacking pass).
+__global__ void k_repack_states(const double* __restrict__ s7, double* __restrict__ s6, long long M) {
+    const long long n = M * 6;
+    for (long long k = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; k < n;
+         k += static_cast<long long>(gridDim.x) * blockDim.x)
+        s6[k] = s7[(k / 6) * 7 + 1 + k % 6];
+}
+
+cudaError_t launch_repack_states(const double* s7, double* s6, long long M, cudaStream_t s) {
+    const long long n = M * 6;
+    const int grid = static_cast<int>(std::min<long long>((n + 255) / 256, 148 * 16));
+    k_repack_states<<<grid, 256, 0, s>>>(s7, s6, M);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_ephemeris(int N, const double* times, double central_mu, const BodyTable& bt, double* pos,

@@ -35,7 +35,7 @@ struct GroupFault {
 /// Phase accounting slots (generic kernel): 0 claim, 1 warm start, 2 force, 3 DMMA,
 /// 4 anchor/b0 barrier, 5 epilogue (main rows), 6 epilogue (staged rows), 7 decisions,
 /// 8 retire; warp-specialised kernel: see pc_slots2.cu.  Slot PHASES-1 = CTA count.
-constexpr int PHASES = 12;
+constexpr int PHASES = 16;
 
 /// Arguments of one segment launch of the persistent slot kernel.
 struct SegArgs {
@@ -101,6 +101,7 @@ struct BodyTable {
 /// fault_key = min over (body, node) of (b*N + j)*4 + kind (1 coverage, 3 solver).
 /// Relativistic model (EXTENSION, rel_tab != nullptr): also body velocities vel [N][B][3]
 /// and the node table rel_tab [N][B+1][REL_W] (Sun row first).
+cudaError_t launch_repack_states(const double* s7, double* s6, long long M, cudaStream_t s);
 cudaError_t launch_ephemeris(int N, const double* times, double central_mu, const BodyTable& bt, double* pos,
                              double* indirect, unsigned long long* fault_key, double* vel, double* rel_tab, double ic2,
                              cudaStream_t s);

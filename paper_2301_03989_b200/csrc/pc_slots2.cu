@@ -925,7 +925,9 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
                     // decisions of half h here, not in the FP group: the MMA group has slack once
                     // its DMMA stream is halved, and the FP group's warps issue ~3x slower while
                     // DMMAs stream (the decisions sat on the FP group's critical chain)
+                    WS_PHASE(2);
                     bar_sync(BAR_MMA, MMA_THREADS);  // every warp's slot_err / nf_key update is in
+                    WS_PHASE(11);
                     if (nxt > 0) {  // staged rows: pair rows of the leftover tiles and their mirrors
                         const int xv = min(xrows, half - nfull * 8);  // valid pair rows
                         for (int i = tid; i < xv * HS * 2; i += MMA_THREADS) {
@@ -950,7 +952,9 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
                         }
                         bar_sync(BAR_MMA, MMA_THREADS);
                     }
+                    WS_PHASE(12);
                     if (warp == 0) decide_half(a, st, h, lane, B);
+                    WS_PHASE(13);
                 } else {
                 double acc[MAIN][3][2], xacc[XMW][2];
 #if PSWARM_ABLATE == 3  // diagnostic: no DMMA

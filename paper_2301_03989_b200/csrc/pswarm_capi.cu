@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -152,7 +153,7 @@ enum BufId {
     B_OP_IN, B_OP_IN2, B_OP_OUT, B_OP_AUX, B_OP_KEY,
     B_BT_KIND, B_BT_SOFF, B_BT_NC, B_BT_EL, B_BT_BND, B_BT_COFF, B_BT_CF, B_PHASES,
     B_W_TG, B_W_Y, B_W_ACT, B_W_ITER, B_W_ERR, B_W_NF, B_W_SING, B_W_TSK, B_W_TSV, B_W_WK, B_W_CNT,
-    B_IN_PACK, B_REPORT, B_BODY_VEL, B_REL_TAB, B_HOT, B_COUNT
+    B_IN_PACK, B_REPORT, B_BODY_VEL, B_REL_TAB, B_HOT, B_STATES7, B_COUNT
 };
 
 /// Page-locked host staging (grow-only): every host<->device transfer of a solve goes
@@ -449,10 +450,23 @@ struct RunSpec {
     bool independent = false;  // run_batch independent mode: reference error order is per trajectory
 };
 
+/// PSWARM_TRACE=1: host-side stage times of propagate (diagnostics, stderr).
+struct StageTrace {
+    bool on = std::getenv("PSWARM_TRACE") != nullptr;
+    std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+    void mark(const char* what) {
+        if (!on) return;
+        const auto now = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[pswarm] %-22s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(now - t).count());
+        t = now;
+    }
+};
+
 void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P, const int64_t* group_sizes,
                     int64_t n_boundaries, const double* boundaries, int64_t N, const pswarm_config* cfg,
                     pswarm_outputs* out, const RunSpec& spec) {
     const auto wall0 = std::chrono::steady_clock::now();
+    StageTrace trace;
     if (!cfg) raise(PSWARM_ERR_GENERIC, "propagate: null config");
     // ---- validation, same order and wording as propagator.hpp:196-216
     if (M <= 0) throw pswarm::InvalidPlanError("propagate: empty batch");
@@ -510,18 +524,16 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
     }
     // ---- one packed host->device transfer: states, group offsets, grids, body table
     Pack in;
-    const size_t o_s6 = in.add(sizeof(double) * M * 6), o_off = in.add(sizeof(int64_t) * (P + 1)),
+    const size_t o_off = in.add(sizeof(int64_t) * (P + 1)),
                  o_times = in.add(sizeof(double) * S * N), o_kind = in.add(sizeof(int) * bu.kind.size()),
                  o_soff = in.add(sizeof(int) * bu.seg_off.size()), o_nc = in.add(sizeof(int) * bu.ncoef.size()),
                  o_el = in.add(sizeof(double) * bu.elements.size()), o_mu = in.add(sizeof(double) * bu.mu.size()),
                  o_bnd = in.add(sizeof(double) * bu.bounds.size()),
                  o_coff = in.add(sizeof(long long) * bu.coeff_off.size()),
                  o_cf = in.add(sizeof(double) * bu.coeffs.size());
-    char* hin = ctx->pin_in.get<char>(in.total);
+    const size_t o_s6 = in.add(sizeof(double) * M * 6);  // filled on the device (k_repack_states)
+    char* hin = ctx->pin_in.get<char>(o_s6);
     {
-        double* s6 = reinterpret_cast<double*>(hin + o_s6);
-        for (int64_t i = 0; i < M; ++i)
-            for (int c = 0; c < 6; ++c) s6[i * 6 + c] = states[7 * i + 1 + c];
         int64_t* off = reinterpret_cast<int64_t*>(hin + o_off);
         off[0] = 0;
         for (int64_t g = 0; g < P; ++g) off[g + 1] = off[g] + group_sizes[g];
@@ -538,8 +550,15 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
         put(o_coff, bu.coeff_off);
         put(o_cf, bu.coeffs);
     }
+    trace.mark("validate+grids+pack");
     char* din = ctx->buf[B_IN_PACK].get<char>(in.total);
-    cuda_check(cudaMemcpyAsync(din, hin, in.total, cudaMemcpyHostToDevice, st), "H2D inputs");
+    cuda_check(cudaMemcpyAsync(din, hin, o_s6, cudaMemcpyHostToDevice, st), "H2D inputs");
+    {  // the caller's [M][7] states as they are; repacked to [M][6] on the device
+        double* d7 = ctx->buf[B_STATES7].get<double>(static_cast<size_t>(M) * 7);
+        cuda_check(cudaMemcpyAsync(d7, states, sizeof(double) * M * 7, cudaMemcpyHostToDevice, st), "H2D states");
+        cuda_check(launch_repack_states(d7, reinterpret_cast<double*>(din + o_s6), M, st), "k_repack_states");
+        ++ctx->launches;
+    }
     std::vector<int64_t> h_off(reinterpret_cast<int64_t*>(hin + o_off), reinterpret_cast<int64_t*>(hin + o_off) + P + 1);
     double* d_in = reinterpret_cast<double*>(din + o_s6);
     const int64_t* d_off = reinterpret_cast<const int64_t*>(din + o_off);
@@ -555,9 +574,10 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
     if (d_hist) cuda_check(cudaMemsetAsync(d_hist, 0xff, sizeof(double) * S * P * max_it, st), "memset");
     // ---- per-segment report block: zeroed with one memset, read back with one copy
     Pack rp;
+    // fault records last: they are read back only when some group did not converge
     const size_t r_queue = rp.add(16), r_iter = rp.add(sizeof(int32_t) * P), r_conv = rp.add(P), r_fb = rp.add(M),
-                 r_faults = rp.add(sizeof(GroupFault) * P), r_err = rp.add(sizeof(double) * P), r_zero = rp.total,
-                 r_ekey = rp.add(sizeof(unsigned long long));
+                 r_err = rp.add(sizeof(double) * P), r_zero = rp.total, r_ekey = rp.add(sizeof(unsigned long long)),
+                 r_faults = rp.add(sizeof(GroupFault) * P);
     char* drep = ctx->buf[B_REPORT].get<char>(rp.total);
     char* hrep = ctx->pin_rep.get<char>(rp.total);
     int* d_queue = reinterpret_cast<int*>(drep + r_queue);
@@ -573,7 +593,7 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
     std::vector<int32_t> h_iter(static_cast<size_t>(S * P), 0);
     std::vector<double> h_err(static_cast<size_t>(S * P), 0.0);
     std::vector<uint8_t> h_conv(static_cast<size_t>(S * P), 0), h_fb(static_cast<size_t>(S * M), 0);
-    std::vector<GroupFault> h_faults(static_cast<size_t>(P));
+    std::vector<GroupFault> h_faults;  // sized on the first segment that needs fault records
 
     // device deadline in %globaltimer units
     unsigned long long gpu_deadline = 0;
@@ -684,6 +704,7 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
         const double* d_times = reinterpret_cast<const double*>(din + o_times) + seg * N;
         cuda_check(cudaMemsetAsync(drep, 0, r_zero, st), "memset reports");
         cuda_check(cudaMemsetAsync(d_ekey, 0xff, sizeof(unsigned long long), st), "memset");
+        cuda_check(cudaMemsetAsync(d_faults, 0, sizeof(GroupFault) * P, st), "memset faults");
         if (nb > 0 || rel) {  // frozen per-node ephemeris of this segment, evaluated on the device
             cuda_check(launch_ephemeris(static_cast<int>(N), d_times, cfg->central_mu, bt, d_pos, d_ind, d_ekey, d_vel,
                                         d_rel, 1.0 / (c_light * c_light), st),
@@ -759,17 +780,30 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
                                          sizeof(double) * 6 * nrows, M, cudaMemcpyDeviceToHost, ctx->copy_stream),
                        "D2H segment samples");
         }
-        cuda_check(cudaMemcpyAsync(hrep, drep, rp.total, cudaMemcpyDeviceToHost, st), "D2H reports");
+        cuda_check(cudaMemcpyAsync(hrep, drep, r_faults, cudaMemcpyDeviceToHost, st), "D2H reports");
         if (h_term && seg == S - 1) {  // terminal states ride along with the last segment's reports
             cuda_check(cudaMemcpyAsync(h_term, d_out, sizeof(double) * M * 6, cudaMemcpyDeviceToHost, st), "D2H terminal");
             term_ready = true;
         }
         cuda_check(cudaStreamSynchronize(st), "segment solve");
+        trace.mark("segment sync");
         std::memcpy(h_iter.data() + seg * P, hrep + r_iter, sizeof(int32_t) * P);
         std::memcpy(h_err.data() + seg * P, hrep + r_err, sizeof(double) * P);
         std::memcpy(h_conv.data() + seg * P, hrep + r_conv, P);
-        std::memcpy(h_faults.data(), hrep + r_faults, sizeof(GroupFault) * P);
         std::memcpy(h_fb.data() + seg * M, hrep + r_fb, M);
+        // fault records (48 B per group) only when some group stopped unconverged: every fault
+        // retires its group with converged = 0; the wide path adds host-side records below
+        bool any_unconverged = false;
+        for (int64_t gi = 0; gi < P && !any_unconverged; ++gi) any_unconverged = !h_conv[seg * P + gi];
+        const bool need_faults =
+            any_unconverged || (wide && (ctx->wide_timeout || ctx->wide_warm_key != ~0ull));
+        if (need_faults) {
+            h_faults.resize(static_cast<size_t>(P));
+            cuda_check(cudaMemcpyAsync(h_faults.data(), drep + r_faults, sizeof(GroupFault) * P, cudaMemcpyDeviceToHost,
+                                       st),
+                       "D2H faults");
+            cuda_check(cudaStreamSynchronize(st), "faults");
+        }
         unsigned long long ekey;
         std::memcpy(&ekey, hrep + r_ekey, sizeof ekey);
         // ---- ephemeris faults come first: build_ephemeris_cache precedes the solve
@@ -826,7 +860,7 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
 
         // ---- faults, in the order the serial reference would raise them
         int64_t warm_traj = -1, warm_g = -1, first_g = -1;
-        for (int64_t gi = 0; gi < P; ++gi) {
+        for (int64_t gi = 0; gi < (need_faults ? P : 0); ++gi) {
             const GroupFault& f = h_faults[gi];
             if (f.status == FAULT_WARM_ZERO_RADIUS || f.status == FAULT_WARM_SOLVER) {
                 if (warm_traj < 0 || f.trajectory < warm_traj) {
@@ -844,7 +878,7 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
             // segment of every trajectory at the same time only if no lower index fails later;
             // report the lowest index of this segment.
             int64_t best = -1;
-            for (int64_t gi = 0; gi < P; ++gi)
+            for (int64_t gi = 0; gi < P; ++gi)  // (reached only with fault records read back)
                 if (h_faults[gi].status != FAULT_NONE) {
                     best = gi;
                     break;
@@ -934,6 +968,7 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
         if (out) out->segments_reported = seg + 1;
     }
     cuda_check(cudaEventRecord(ctx->ev1, st), "event");
+    trace.mark("segments (device+host)");
 
     // ---- outputs
     if (out) {
@@ -941,11 +976,9 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
         if (fail_status != PSWARM_OK && fail_status != PSWARM_ERR_INCOMPLETE) out->segments_reported = seg_done;
         if (out->times) std::memcpy(out->times, h_times.data(), sizeof(double) * R);
         const int64_t rep = out->segments_reported;
-        for (int64_t k = 0; k < rep * P; ++k) {
-            if (out->iterations) out->iterations[k] = h_iter[k];
-            if (out->final_error) out->final_error[k] = h_err[k];
-            if (out->converged) out->converged[k] = h_conv[k];
-        }
+        if (out->iterations) std::memcpy(out->iterations, h_iter.data(), sizeof(int32_t) * rep * P);
+        if (out->final_error) std::memcpy(out->final_error, h_err.data(), sizeof(double) * rep * P);
+        if (out->converged) std::memcpy(out->converged, h_conv.data(), static_cast<size_t>(rep * P));
         if (out->cold_fallback) std::memcpy(out->cold_fallback, h_fb.data(), static_cast<size_t>(rep * M));
         if (out->error_history && max_it > 0 && rep > 0)
             cuda_check(cudaMemcpyAsync(out->error_history, d_hist, sizeof(double) * rep * P * max_it,
@@ -976,6 +1009,7 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
         out->trajectory_iterations = traj_iters;
         out->gpu_launches = ctx->launches;
         out->wall_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
+        trace.mark("outputs");
     }
     if (fail_status != PSWARM_OK) {
         CapiFault f;
@@ -1110,16 +1144,21 @@ pswarm_status pswarm_run_batch(pswarm_ctx* ctx, int64_t n_states, const double* 
                                int32_t workers, pswarm_outputs* out, pswarm_error* err) {
     return guarded(err, [&] {
         if (workers < 1) throw pswarm::InvalidPlanError("run_batch: need at least one worker");
-        pswarm::GroupingPlan plan;
         if (n_states < 1) throw pswarm::InvalidPlanError("propagate: empty batch");
-        if (mode == 0) plan = pswarm::split_groups(n_states, n_states);
-        else if (mode == 1 || mode == 2) plan = pswarm::split_groups(n_states, 1);
-        else if (mode == 3) plan = pswarm::split_groups(n_states, std::clamp<int64_t>(config->p_groups, 1, n_states));
+        int64_t p_groups;  // grouping_for_mode (runner.hpp:47-55)
+        if (mode == 0) p_groups = n_states;
+        else if (mode == 1 || mode == 2) p_groups = 1;
+        else if (mode == 3) p_groups = std::clamp<int64_t>(config->p_groups, 1, n_states);
         else throw pswarm::InvalidPlanError("grouping_for_mode: invalid mode");
+        // the sizes of split_groups (block.hpp: larger groups first); the device path needs no
+        // per-trajectory assignment tables (24 MB at 1M trajectories)
+        const int64_t base = n_states / p_groups, rem = n_states % p_groups;
+        std::vector<int64_t> sizes(static_cast<size_t>(p_groups), base);
+        for (int64_t g = 0; g < rem; ++g) sizes[g] = base + 1;
         RunSpec spec;
         spec.independent = mode == 0;
-        propagate_impl(ctx, n_states, states, plan.groups(), plan.group_sizes.data(), n_boundaries, boundaries, n_nodes,
-                       config, out, spec);
+        propagate_impl(ctx, n_states, states, p_groups, sizes.data(), n_boundaries, boundaries, n_nodes, config, out,
+                       spec);
     });
 }
 

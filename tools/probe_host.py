@@ -1,27 +1,29 @@
-"""Host-side overhead breakdown of one bench step (diagnostics)."""
-import cProfile, pstats, sys, os, time, statistics
+"""Host-side overhead of run_batch at C4 size (diagnostics): Python wall vs C-ABI wall vs
+device time, plus a cProfile of the Python wrapper."""
+import sys, os, time, cProfile, pstats, io
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
 import paper_2301_03989_b200 as ps
+
+M = int(sys.argv[1]) if len(sys.argv) > 1 else 1000000
 ctx = ps.Context(0)
 base = ps.reference_state()
 period = ps.osculating_period(base, ps.MU_SUN)
-states = ps.make_clone_batch(base, 1000, 1e-5)
+states = ps.make_clone_batch(base, M, 1e-5)
+shard = torch.from_numpy(states.copy()).pin_memory().numpy()
 plan = ps.plan_segments(base, 0.0, 0.87 * period, ps.MU_SUN, "single", 200)
-cfg = ps.reference_force_config("n_body", bodies=ps.planets8())
-for _ in range(5):
-    ctx.run_batch(states, cfg, plan, "independent", samples=False, history=False)
-py, cw, dm = [], [], []
-for _ in range(50):
+cfg = ps.reference_force_config("n_body", bodies=ps.planets8(), n_nodes=200)
+for rep in range(3):
     t0 = time.perf_counter()
-    r = ctx.run_batch(states, cfg, plan, "independent", samples=False, history=False)
-    py.append(time.perf_counter() - t0)
-    cw.append(r.wall_s)
-    dm.append(r.device_ms)
-print("python_ms", 1e3 * statistics.median(py), "capi_wall_ms", 1e3 * statistics.median(cw), "device_ms",
-      statistics.median(dm), "kernel_ms", r.kernel_ms)
+    r = ctx.run_batch(shard, cfg, plan, "independent", samples=False, history=False)
+    t1 = time.perf_counter()
+    print(f"py wall {1e3 * (t1 - t0):.1f} ms  C wall {1e3 * r.wall_s:.1f} ms  device {r.device_ms:.1f} ms  kernel {r.kernel_ms:.1f} ms",
+          flush=True)
 pr = cProfile.Profile()
 pr.enable()
-for _ in range(20):
-    ctx.run_batch(states, cfg, plan, "independent", samples=False, history=False)
+r = ctx.run_batch(shard, cfg, plan, "independent", samples=False, history=False)
 pr.disable()
-pstats.Stats(pr).sort_stats("cumulative").print_stats(25)
+s = io.StringIO()
+pstats.Stats(pr, stream=s).sort_stats("cumulative").print_stats(14)
+print(s.getvalue())
