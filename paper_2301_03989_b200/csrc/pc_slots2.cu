@@ -1453,7 +1453,7 @@ __device__ __forceinline__ void epilogue_unit_fold(const SegArgs& a, WsState& st
         }                                             \
     } while (0)
 
-template <int NV, bool STAGE>
+template <int NV, bool STAGE, bool REL>
 __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_uni(const SegArgs a) {
     constexpr int T = WS_THREADS, NW = WS_THREADS / 32;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1640,8 +1640,34 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_uni(const SegArgs a) {
             }
         }
         UNI_PHASE(2);
-        // ---- force of both halves, folded as written (mirrored node pairs)
-        {
+        // ---- force of both halves, folded as written (mirrored node pairs); relativistic: per
+        //      node with the fused 1PN pass, then folded in place
+        if constexpr (REL) {
+            const int ns = 2 * N > T / 2 ? 4 : (4 * N > T / 2 ? 2 : 1);  // slots per item
+            const int per_h = N * (4 / ns);
+            for (int w = tid; w < 2 * per_h; w += T) {
+                const int h = w / per_h, r = w % per_h;
+                const int act_h = (am >> (h * HS)) & 0xF;
+                if (!act_h) continue;
+                double* fbh = fb0 + h * (fb_bytes / sizeof(double));
+                const int j = r % N, s0 = (r / N) * ns;
+                if (ns == 4) force_half_rel<4>(a.fd, ybuf, fbh, st.sing_key, act_h, h, j, s0);
+                else if (ns == 2) force_half_rel<2>(a.fd, ybuf, fbh, st.sing_key, act_h, h, j, s0);
+                else force_half_rel<1>(a.fd, ybuf, fbh, st.sing_key, act_h, h, j, s0);
+            }
+            __syncthreads();
+            for (int i = tid; i < 2 * half * HC; i += T) {  // fold: s_k at k, a_k = F_k - F_{N-1-k} at N-1-k
+                const int h = i / (half * HC), ii = i % (half * HC);
+                if (!((am >> (h * HS)) & 0xF)) continue;
+                double* fbh = fb0 + h * (fb_bytes / sizeof(double));
+                const int k = ii % half, col = ii / half;
+                const int c = 2 * (col >> 3) + (col & 1), sl = (col & 7) >> 1;
+                const int lo = f2(k, c, sl), hi = f2(N - 1 - k, c, sl);
+                const double flo = fbh[lo], fhi = fbh[hi];
+                fbh[lo] = flo + fhi;
+                fbh[hi] = flo - fhi;
+            }
+        } else {
             const int npw = half > T / 8 ? 2 : 4;  // work items per (half, node pair): slot pairs or slots
             for (int w = tid; w < 2 * npw * half; w += T) {
                 const int h = w / (npw * half), r = w % (npw * half);
@@ -1751,9 +1777,9 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_uni(const SegArgs a) {
     }
 }
 
-template <int NV, bool STAGE>
+template <int NV, bool STAGE, bool REL = false>
 static cudaError_t launch_uni_t(const SegArgs& a, int grid, size_t smem, cudaStream_t s) {
-    auto kern = k_pc_uni<NV, STAGE>;
+    auto kern = k_pc_uni<NV, STAGE, REL>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     kern<<<grid, WS_THREADS, smem, s>>>(a);
@@ -1810,13 +1836,15 @@ size_t ws_smem_bytes(int N, int nkp, int xrows, int B, int stage_eph, bool fold)
     return ws_layout(N, nkp, xrows, B, stage_eph, fold ? 1 : 0).total;
 }
 
-/// Unified folded kernel (Newtonian, N % 8 == 0): units of 2 x ceil(N/16) pair tiles over 16 warps.
+/// Unified folded kernel (N % 8 == 0): units of 2 x ceil(N/16) pair tiles over 16 warps.
 bool uni_supported(int N) { return N % 8 == 0 && (2 * ws_mtiles(N, true) + 15) / 16 <= 2; }
 
 cudaError_t launch_segment_uni(const SegArgs& a, int grid, cudaStream_t s) {
-    if (!uni_supported(a.N) || a.fd.rel || a.upack_fold == nullptr) return cudaErrorNotSupported;
+    if (!uni_supported(a.N) || a.upack_fold == nullptr) return cudaErrorNotSupported;
     const int nv = (2 * ws_mtiles(a.N, true) + 15) / 16;
     const size_t smem = ws_smem_bytes(a.N, a.nkp, 0, a.fd.n_bodies, a.stage_eph, true);
+    if (a.fd.rel)  // relativistic launches never stage the ephemeris (the host clears stage_eph)
+        return nv == 1 ? launch_uni_t<1, false, true>(a, grid, smem, s) : launch_uni_t<2, false, true>(a, grid, smem, s);
     if (a.stage_eph)
         return nv == 1 ? launch_uni_t<1, true>(a, grid, smem, s) : launch_uni_t<2, true>(a, grid, smem, s);
     return nv == 1 ? launch_uni_t<1, false>(a, grid, smem, s) : launch_uni_t<2, false>(a, grid, smem, s);

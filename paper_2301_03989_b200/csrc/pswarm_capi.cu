@@ -207,8 +207,9 @@ struct pswarm_ctx {
     int slot_kernel = 0;  // 0 auto, 1 generic k_pc_segment, 2 warp-specialised k_pc_ws
     int poison_outputs = 0;  // 1: NaN-fill device outputs before each solve (tests)
     int fold = 1;            // 1: mirror-folded update when N % 8 == 0 (k_pc_ws_fold)
-    int unified = 0;         // 1: the folded Newtonian solve runs k_pc_uni (all warps per phase; measured
-                             //    equal at N = 200 and slower elsewhere, tools/probe_uni.py)
+    int unified = 2;         // folded solves: 1 k_pc_uni (all warps per phase), 0 k_pc_ws_fold, 2 auto =
+                             // k_pc_uni for the force-bound 1PN model, k_pc_ws_fold for Newtonian forces
+                             // (measured, tools/probe_uni.py)
     unsigned long long phase_host[pswarm_dev::PHASES] = {};
     PinnedBuf pin_in, pin_rep, pin_term;
     // wide-group path
@@ -619,7 +620,7 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
     const bool use_ws = fold || (!wide && gmax <= 4 && ws_supported(Ni, false) && ctx->slot_kernel != 1 &&
                                  ws_smem_bytes(Ni, op.nkp, ws_extra_rows(Ni, false), nb, 0, false) <= SMEM_MAX);
     const int xrows = use_ws ? ws_extra_rows(Ni, fold) : extra_rows(Ni, op.gp);
-    const bool uni = fold && !rel && ctx->unified && uni_supported(Ni);
+    const bool uni = fold && (ctx->unified == 1 || (ctx->unified == 2 && rel)) && uni_supported(Ni);
     ctx->last_kernel = wide ? "k_wide_iter" : uni ? "k_pc_uni" : fold ? "k_pc_ws_fold" : use_ws ? "k_pc_ws" : "k_pc_segment";
     // stage the frozen ephemeris in shared memory when it fits next to the state blocks
     const int stage_eph = nb > 0 && !rel &&
@@ -1115,7 +1116,7 @@ pswarm_status pswarm_set_option(pswarm_ctx* ctx, const char* key, int64_t value)
         else if (k == "slot_kernel") ctx->slot_kernel = static_cast<int>(value);
         else if (k == "poison_outputs") ctx->poison_outputs = value != 0;
         else if (k == "fold") ctx->fold = value != 0;
-        else if (k == "unified") ctx->unified = value != 0;
+        else if (k == "unified") ctx->unified = static_cast<int>(std::clamp<int64_t>(value, 0, 2));
         else raise(PSWARM_ERR_GENERIC, "pswarm_set_option: unknown key '" + k + "'");
     });
 }

@@ -33,10 +33,17 @@ def _rel_setup(m, n, frac, bodies="planets8", spread=1e-5, policy="single"):
 
 
 @pytest.mark.parametrize("n", [64, 128, 200, 256])
-def test_c5_relativistic_node_sweep(ctx, oracle, n):
-    """C5: Sun + 8 planets with the EIH 1PN correction, node sweep, warp-specialised kernel."""
+@pytest.mark.parametrize("unified,kernel", [(2, "k_pc_uni"), (0, "k_pc_ws_fold")])
+def test_c5_relativistic_node_sweep(ctx, oracle, n, unified, kernel):
+    """C5: Sun + 8 planets with the EIH 1PN correction, node sweep: the unified folded kernel
+    (auto choice for this force-bound model) and the warp-specialised folded kernel."""
     states, plan, cfg = _rel_setup(24, n, 0.87)
-    got = ctx.run_batch(states, cfg, plan, "independent")
+    ctx.set_option("unified", unified)
+    try:
+        got = ctx.run_batch(states, cfg, plan, "independent")
+        assert ctx.kernel_name() == kernel
+    finally:
+        ctx.set_option("unified", 2)
     want = oracle.run_batch(states, cfg, plan, "independent", 8)
     _parity(got, want)
     assert got.converged.all()

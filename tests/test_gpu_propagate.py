@@ -276,7 +276,7 @@ def test_mirror_folded_and_dense_updates(ctx, oracle, n, fold, unified, kernel):
         name = ctx.kernel_name()
     finally:
         ctx.set_option("fold", 1)
-        ctx.set_option("unified", 0)
+        ctx.set_option("unified", 2)
     assert name == kernel
     want = oracle.run_batch(states, cfg, plan, "independent", 8)
     _parity(got, want)
@@ -298,6 +298,6 @@ def test_unified_kernel_refill_and_multisegment(ctx, oracle):
         assert ctx.kernel_name() == "k_pc_uni"
     finally:
         ctx.set_option("max_ctas", 0)
-        ctx.set_option("unified", 0)
+        ctx.set_option("unified", 2)
     want = oracle.run_batch(states, cfg, plan, "independent", 8)
     _parity(got, want)

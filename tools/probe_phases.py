@@ -12,7 +12,8 @@ base = ps.reference_state()
 period = ps.osculating_period(base, ps.MU_SUN)
 states = ps.make_clone_batch(base, M, 1e-5)
 plan = ps.plan_segments(base, 0.0, 0.87 * period, ps.MU_SUN, "single", N)
-cfg = ps.reference_force_config("n_body", bodies=ps.planets8() if bodies == "planets8" else ps.reference_bodies(),
+kind = sys.argv[5] if len(sys.argv) > 5 else "n_body"
+cfg = ps.reference_force_config(kind, bodies=ps.planets8() if bodies == "planets8" else ps.reference_bodies(),
                                 n_nodes=N)
 def run():
     try:
