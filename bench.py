@@ -124,6 +124,7 @@ class Clocks:
     """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
 
     def __init__(self, index):
+        self.index = str(index)
         self.path = f"/tmp/bench_clocks_{os.getpid()}.csv"
         q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -154,9 +155,23 @@ class Clocks:
                 if v.lower().startswith("active"):
                     reasons.add(n)
         os.unlink(self.path)
+        post = False
+        if not sm:  # timed region shorter than the 20 ms sampling period: one query right after it
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", self.index, "--query-gpu=clocks.sm,clocks.max.sm",
+                                      "--format=csv,noheader"], capture_output=True, text=True, timeout=10).stdout
+                f = [x.strip() for x in out.split(",")]
+                sm.append(float(f[0].split()[0]))
+                mx.append(float(f[1].split()[0]))
+                post = True
+            except (OSError, ValueError, IndexError, subprocess.SubprocessError):
+                pass
         under = [s for s in sm if s > 0.5 * max(sm)] if sm else []
-        return {"sm_mhz": statistics.median(under) if under else None, "sm_max_mhz": max(mx) if mx else None,
-                "samples": len(sm), "reasons": sorted(reasons)}
+        res = {"sm_mhz": statistics.median(under) if under else None, "sm_max_mhz": max(mx) if mx else None,
+               "samples": len(sm), "reasons": sorted(reasons)}
+        if post:
+            res["sampled_after_region"] = True
+        return res
 
 
 def fp64_peak():

@@ -1575,7 +1575,8 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_uni(const SegArgs a) {
                 st.act_word[h] = am & hmask;
                 st.new_mask[h] = new_mask;
                 st.half_active[h] = (am & hmask) != 0;
-                st.free_mask[h] = st.retire_mask[h] = 0;
+                // (free / retire masks: rewritten by decide_half every iteration; every thread read
+                //  retire_mask above without a barrier when nothing retired)
             }
             if (a.deadline_ns != 0ull && globaltimer_ns() > a.deadline_ns) st.timeout = 1;
         }

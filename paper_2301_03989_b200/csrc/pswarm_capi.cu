@@ -208,7 +208,7 @@ struct pswarm_ctx {
     int poison_outputs = 0;  // 1: NaN-fill device outputs before each solve (tests)
     int fold = 1;            // 1: mirror-folded update when N % 8 == 0 (k_pc_ws_fold)
     int unified = 2;         // folded solves: 1 k_pc_uni (all warps per phase), 0 k_pc_ws_fold, 2 auto =
-                             // k_pc_uni for the force-bound 1PN model, k_pc_ws_fold for Newtonian forces
+                             // k_pc_uni for the force-bound 1PN model (N <= 200), else k_pc_ws_fold
                              // (measured, tools/probe_uni.py)
     unsigned long long phase_host[pswarm_dev::PHASES] = {};
     PinnedBuf pin_in, pin_rep, pin_term;
@@ -620,7 +620,9 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
     const bool use_ws = fold || (!wide && gmax <= 4 && ws_supported(Ni, false) && ctx->slot_kernel != 1 &&
                                  ws_smem_bytes(Ni, op.nkp, ws_extra_rows(Ni, false), nb, 0, false) <= SMEM_MAX);
     const int xrows = use_ws ? ws_extra_rows(Ni, fold) : extra_rows(Ni, op.gp);
-    const bool uni = fold && (ctx->unified == 1 || (ctx->unified == 2 && rel)) && uni_supported(Ni);
+    // auto: the unified kernel for the force-bound 1PN model up to N = 200 (at N = 256 the
+    // warp-specialised one is faster, profiles/bench_r01_c5_n*.json)
+    const bool uni = fold && (ctx->unified == 1 || (ctx->unified == 2 && rel && Ni <= 200)) && uni_supported(Ni);
     ctx->last_kernel = wide ? "k_wide_iter" : uni ? "k_pc_uni" : fold ? "k_pc_ws_fold" : use_ws ? "k_pc_ws" : "k_pc_segment";
     // stage the frozen ephemeris in shared memory when it fits next to the state blocks
     const int stage_eph = nb > 0 && !rel &&

@@ -7,12 +7,26 @@ ctx = ps.Context(0)
 base = ps.reference_state()
 period = ps.osculating_period(base, ps.MU_SUN)
 states = ps.make_clone_batch(base, 24, 1e-5)
-for n, mode, p, kind, start in [(200, "independent", 1, "n_body", "warm"), (96, "independent", 1, "n_body_1pn", "warm"),
-                                (64, "grouped", 4, "n_body", "warm"), (64, "augmented", 1, "n_body", "warm"),
-                                (64, "independent", 1, "n_body", "hot")]:
+# (N, mode, p_groups, force kind, start, options)
+CASES = [(200, "independent", 1, "n_body", "warm", {}),                      # k_pc_ws_fold, extra units
+         (160, "independent", 1, "n_body", "warm", {}),                      # k_pc_ws_fold, 6 extra units
+         (256, "independent", 1, "n_body", "warm", {}),                      # k_pc_ws_fold, no extras
+         (200, "independent", 1, "n_body", "warm", {"fold": 0}),             # dense k_pc_ws
+         (200, "independent", 1, "n_body", "warm", {"unified": 1}),          # k_pc_uni Newtonian
+         (96, "independent", 1, "n_body_1pn", "warm", {}),                   # k_pc_uni 1PN (auto)
+         (256, "independent", 1, "n_body_1pn", "warm", {}),                  # k_pc_ws_fold 1PN (auto)
+         (64, "grouped", 4, "n_body", "warm", {}),                           # grouped, folded kernels
+         (72, "grouped", 4, "n_body", "warm", {}),                           # N % 8 != 0 ... generic path
+         (64, "augmented", 1, "n_body", "warm", {}),                         # k_wide_iter
+         (64, "independent", 1, "n_body", "hot", {})]                        # hot start, multi-segment
+for n, mode, p, kind, start, opts in CASES:
     plan = ps.plan_segments(base, 0.0, (2.2 if start == "hot" else 0.4) * period, ps.MU_SUN,
                             "per_orbit" if start == "hot" else "single", n)
     cfg = ps.reference_force_config(kind, bodies=ps.planets8(), n_nodes=n, start_mode=start)
     cfg.p_groups = p
+    for k, v in opts.items():
+        ctx.set_option(k, v)
     r = ctx.run_batch(states, cfg, plan, mode)
-    print(n, mode, kind, start, ctx.kernel_name(), int(r.iterations.sum()), flush=True)
+    print(n, mode, kind, start, opts, ctx.kernel_name(), int(r.iterations.sum()), flush=True)
+    ctx.set_option("fold", 1)
+    ctx.set_option("unified", 2)
