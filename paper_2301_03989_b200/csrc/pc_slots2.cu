@@ -795,6 +795,9 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
     const int KP = 8 * a.nkp;
     // node rows only (b0 comes from the FP group's anchor GEMV); folded: row pairs
     const int mtiles = FOLD ? (half + 7) / 8 : (N + 7) / 8;
+    // folded with a spare pair row (N/2 % 8 != 0): pair row N/2 of the packed operator is the
+    // anchor row, so the DMMA stream forms b0 and the FP group's GEMV + B_h barrier drop out
+    const bool b0mma = FOLD && (half & 7) != 0 && a.b0_mma;
     const bool prof = a.phase_cycles != nullptr;
     const bool stamp = tid == 0 || tid == MMA_THREADS;
     // phase counters live in shared memory (no registers / local memory on the hot path)
@@ -865,7 +868,30 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
                                          reinterpret_cast<const double*>(smem_raw + L.fbuf0 + h * fb_bytes), nfull,
                                          warp, lane, xt, xp, facc, fxacc);
                     WS_PHASE(1);
-                    bar_sync(BAR_B0 + h, WS_THREADS);  // b0 of half h (FP group, formed before F_h)
+                    if (b0mma) {  // b0 = (omega2 anchor.F + 2 y0) / 2 from the anchor pair row
+                        const int at = half >> 3;
+                        if (g == (half & 7)) {
+                            const double w2a = a.omega2;
+#pragma unroll
+                            for (int i = 0; i < MAIN; ++i)
+                                if (warp + i * MMA_WARPS == at && at < nfull)
+#pragma unroll
+                                    for (int p = 0; p < 3; ++p)
+#pragma unroll
+                                        for (int e = 0; e < 2; ++e)
+                                            st.b0h[h][p * 8 + 2 * q + e] =
+                                                0.5 * fma(w2a, facc[i][p][0][e] + facc[i][p][1][e],
+                                                          2.0 * st.y0[h * HS + q][2 * p + e]);
+                            if (xt == at)
+#pragma unroll
+                                for (int e = 0; e < 2; ++e)
+                                    st.b0h[h][xp * 8 + 2 * q + e] = 0.5 * fma(w2a, fxacc[0][e] + fxacc[1][e],
+                                                                               2.0 * st.y0[h * HS + q][2 * xp + e]);
+                        }
+                        bar_sync(BAR_MMA, MMA_THREADS);
+                    } else {
+                        bar_sync(BAR_B0 + h, WS_THREADS);  // b0 of half h (FP group, formed before F_h)
+                    }
                     WS_PHASE(3);
                     // unfold: Y_j = acc_sum + acc_diff, Y_{N-1-j} = acc_sum - acc_diff (the 1/2 sits in
                     // the packed operators), then the same epilogue as the dense path for both rows
@@ -1029,7 +1055,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
                 WS_PHASE(2);
             } else {
                 if (FOLD && tid == 0) st.free_mask[h] = st.retire_mask[h] = 0;  // no decisions ran
-                bar_sync(BAR_B0 + h, WS_THREADS);  // keep the B_h generations paired
+                if (!b0mma) bar_sync(BAR_B0 + h, WS_THREADS);  // keep the B_h generations paired
             }
             bar_arrive(BAR_Y0 + h, WS_THREADS);  // bar.arrive/bar.sync order smem among participants
         }
@@ -1283,7 +1309,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
             // ---- b0 = anchor_op.F + 2 y0 of half h (pc_matrices.hpp:138), overlapped with the
             //      DMMAs of half h: B0_PARTS strided partial dot products per column, summed in a
             //      fixed order; the MMA group waits for it (B_h) only before its epilogue
-            if (act_h && PSWARM_ABLATE != 4) {  // 4: diagnostic, no b0
+            if (act_h && !b0mma && PSWARM_ABLATE != 4) {  // 4: diagnostic, no b0
                 const double* fbh = reinterpret_cast<const double*>(smem_raw + L.fbuf0 + h * fb_bytes);
                 {  // warp fw reads whole 32-double fragments (conflict-free): lane = (col & 7) * 4 + (j & 3)
                     double s0 = 0.0, s1 = 0.0, s2 = 0.0;
@@ -1319,7 +1345,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
             }
             WS_PHASE(9);
             if constexpr (FOLD) bar_arrive(BAR_F0 + h, WS_THREADS);
-            bar_arrive(BAR_B0 + h, WS_THREADS);
+            if (!b0mma) bar_arrive(BAR_B0 + h, WS_THREADS);
         }
     }
     if (prof) {

@@ -207,6 +207,7 @@ struct pswarm_ctx {
     int slot_kernel = 0;  // 0 auto, 1 generic k_pc_segment, 2 warp-specialised k_pc_ws
     int poison_outputs = 0;  // 1: NaN-fill device outputs before each solve (tests)
     int fold = 1;            // 1: mirror-folded update when N % 8 == 0 (k_pc_ws_fold)
+    int b0_mma = 1;          // folded: b0 from the anchor pair row (spare row, N/2 % 8 != 0)
     int unified = 2;         // folded solves: 1 k_pc_uni (all warps per phase), 0 k_pc_ws_fold, 2 auto =
                              // k_pc_uni for the force-bound 1PN model (N <= 200), else k_pc_ws_fold
                              // (measured, tools/probe_uni.py)
@@ -255,7 +256,14 @@ const OpPack& operators(pswarm_ctx* ctx, Index n) {
     cuda_check(cudaMemcpy(d, host.data(), host.size() * sizeof(double), cudaMemcpyHostToDevice), "upload operators");
     if (n % 8 == 0) {  // U anticommutes with the node reversal: two half-size operators
         const int half = static_cast<int>(n / 2), np = (half + 7) / 8, nkpf = (half + 7) / 8;
+        std::vector<double> af(static_cast<size_t>(8 * nkp), 0.0);
+        for (int k = 0; k < n; ++k)
+            af[k] = k < half ? 0.5 * (mats->anchor_op[k] + mats->anchor_op[n - 1 - k])
+                             : 0.5 * (mats->anchor_op[n - 1 - k] - mats->anchor_op[k]);
         auto G = [&](int part, int r, int k) -> double {  // 1/2 folded into the operator
+            // pair row N/2 (a spare row of the last pair tile when N/2 % 8 != 0) carries the
+            // anchor row: its unfolded sum is anchor_op.F (the DMMA stream forms b0)
+            if (r == half && k < half) return part == 0 ? af[k] : af[half + k];
             if (r >= half || k >= half) return 0.0;
             if (part == 0) return 0.5 * (mats->update_op(r, k) + mats->update_op(r, n - 1 - k));  // -> Y_r - Y_{N-1-r}
             const int pos = half + k;                                                           // a at pos >= N/2
@@ -271,10 +279,6 @@ const OpPack& operators(pswarm_ctx* ctx, Index n) {
                         hf[2 * idx] = G(part, m * 8 + g, kp * 8 + q);
                         hf[2 * idx + 1] = G(part, m * 8 + g, kp * 8 + 4 + q);
                     }
-        std::vector<double> af(static_cast<size_t>(8 * nkp), 0.0);
-        for (int k = 0; k < n; ++k)
-            af[k] = k < half ? 0.5 * (mats->anchor_op[k] + mats->anchor_op[n - 1 - k])
-                             : 0.5 * (mats->anchor_op[n - 1 - k] - mats->anchor_op[k]);
         p->nkp_fold = nkpf;
         cuda_check(cudaMemcpy(p->fold.get<double>(hf.size()), hf.data(), hf.size() * sizeof(double),
                               cudaMemcpyHostToDevice),
@@ -763,6 +767,7 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
         a.phase_cycles = d_phase;
         a.upack_fold = fold ? reinterpret_cast<const double2*>(op.fold.p) : nullptr;
         a.nkp_fold = op.nkp_fold;
+        a.b0_mma = ctx->b0_mma;
         a.anc_fold = fold ? reinterpret_cast<const double*>(op.anc_fold.p) : nullptr;
         if (max_it > 0 && !wide) {
             cuda_check(cudaEventRecord(ctx->evk0, st), "event");
@@ -1118,6 +1123,7 @@ pswarm_status pswarm_set_option(pswarm_ctx* ctx, const char* key, int64_t value)
         else if (k == "slot_kernel") ctx->slot_kernel = static_cast<int>(value);
         else if (k == "poison_outputs") ctx->poison_outputs = value != 0;
         else if (k == "fold") ctx->fold = value != 0;
+        else if (k == "b0_mma") ctx->b0_mma = value != 0;
         else if (k == "unified") ctx->unified = static_cast<int>(std::clamp<int64_t>(value, 0, 2));
         else raise(PSWARM_ERR_GENERIC, "pswarm_set_option: unknown key '" + k + "'");
     });
