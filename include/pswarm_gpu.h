@@ -150,14 +150,17 @@ pswarm_status pswarm_set_option(pswarm_ctx* ctx, const char* key, int64_t value)
 /* Diagnostics: SM cycles summed over CTAs per kernel phase of the last call (16 slots,
  * the last one = number of CTAs).
  * Generic slot kernel: 0 claim, 1 warm start, 2 force, 3 DMMA, 4 anchor barrier,
- * 5 epilogue, 6 staged epilogue, 7 decisions, 8 retire.  Warp-specialised kernel
+ * 5 epilogue, 6 staged epilogue, 7 decisions, 8 retire.  Warp-specialised kernels
  * (MMA group / FP group leaders): 0 wait for F, 1 DMMA, 2 epilogue, 3 wait for b0,
  * 4 wait for Y, 5 staged rows + decisions, 6 retire + claim, 7 warm start, 8 force,
- * 9 b0.  Slot 11 = CTA count. */
+ * 9 b0, 10 force tail (singularity check / fold pass), 11 MMA barrier, 12 MMA staged
+ * rows, 13 MMA decisions (folded).  Unified kernel: 0 decisions, 1 retire + claim,
+ * 2 warm start, 3 force, 4 b0, 5 DMMA, 6 epilogue. */
 pswarm_status pswarm_get_phase_cycles(pswarm_ctx* ctx, uint64_t* out, int32_t n);
 
 /* Diagnostics: name of the solver kernel the last propagate/run_batch call used
- * ("k_pc_ws", "k_pc_segment", "k_wide_iter" or "" before the first call). */
+ * ("k_pc_ws_fold", "k_pc_uni", "k_pc_ws", "k_pc_segment", "k_wide_iter" or "" before the
+ * first call). */
 const char* pswarm_last_kernel(pswarm_ctx* ctx);
 
 /* ---- batch API (the drop-in boundary) ---------------------------------- */
