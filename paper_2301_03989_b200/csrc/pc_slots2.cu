@@ -1832,8 +1832,13 @@ static int ws_mtiles(int N, bool fold) { return fold ? (N / 2 + 7) / 8 : (N + 7)
 /// cost more than the balance gains).  N = 200: 13 pair tiles -> 12 full
 /// + 3 units, the busiest SMSP issues 10 instead of 12 n-tile streams per half.
 static int ws_fold_extra_tiles(int N) {
-    const int r = ws_mtiles(N, true) % 4;
-    return (r == 1 || r == 2) && ws_mtiles(N, true) > 8 ? r : 0;  // N = 96: staging costs more (measured)
+    const int mt = ws_mtiles(N, true), r = mt % 4, nfull = mt - r;
+    if (!(r == 1 || r == 2) || mt <= 8) return 0;  // N = 96: staging costs more (measured)
+    // every extra unit must land on a warp with fewer than MAIN full tiles (gemm_half_fold runs
+    // one full tile + the unit there): with MAIN = 2 only 16 - nfull warps qualify
+    const int main = (nfull + MMA_WARPS - 1) / MMA_WARPS;
+    if (main > 1 && 3 * r > 2 * MMA_WARPS - nfull) return 0;  // N = 216: 6 units, 4 such warps
+    return r;
 }
 /// Dense: MAIN = floor(m-tiles / 8) full-width m-tiles per warp + extras.  Folded: full pair
 /// tiles strided over the warps (ceil) + the extra units above.

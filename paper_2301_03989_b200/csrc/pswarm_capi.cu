@@ -615,7 +615,7 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
 
     // kernel choice: warp-specialised slot kernel (groups <= 4, N in its tile range),
     // the generic slot kernel (groups <= 8), or the wide-group path
-    constexpr size_t SMEM_MAX = 227 * 1024;
+    constexpr size_t SMEM_MAX = 227 * 1024 - 1024;  // opt-in limit minus the kernels' static __shared__ (< 1 KB)
     const int Ni = static_cast<int>(N);
     // mirror-folded update when N allows it (half the DMMAs); "fold" option 0 forces the dense one
     const bool fold = !wide && gmax <= 4 && ctx->fold && op.nkp_fold > 0 && ws_supported(Ni, true) &&

@@ -301,3 +301,15 @@ def test_unified_kernel_refill_and_multisegment(ctx, oracle):
         ctx.set_option("unified", 2)
     want = oracle.run_batch(states, cfg, plan, "independent", 8)
     _parity(got, want)
+
+
+@pytest.mark.parametrize("n", [8, 16, 24, 40, 56, 72, 88, 104, 120, 136, 144, 168, 184, 216, 248])
+def test_folded_tile_plans(ctx, oracle, n):
+    """Every folded tile plan against the oracle: pair-tile counts 1..16, with and without
+    leftover tiles as single-n-tile units (staged rows), with and without the anchor row in
+    a spare pair row (b0 from the DMMA stream), Sun + 8 planets, 0.5 period."""
+    states, plan, cfg = _setup(12, n, 0.5, "planets8")
+    got = ctx.run_batch(states, cfg, plan, "independent")
+    assert ctx.kernel_name() == "k_pc_ws_fold"
+    want = oracle.run_batch(states, cfg, plan, "independent", 8)
+    _parity(got, want)
