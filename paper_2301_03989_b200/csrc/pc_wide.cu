@@ -229,8 +229,9 @@ __global__ void __launch_bounds__(MAXT, 1) k_wide_iter(WideArgs a) {
             }
         }
         __syncthreads();
-        if (tid < a.xrows * SLOTS) {  // epilogue: staged rows
-            const int r = tid >> 3, t = tid & 7, j = gp.mb * 8 + r;
+        // every staged row (up to 31 x 8 items on the 128-thread small-N plan)
+        for (int i = tid; i < a.xrows * SLOTS; i += blockDim.x) {  // epilogue: staged rows
+            const int r = i >> 3, t = i & 7, j = gp.mb * 8 + r;
             if ((act >> t) & 1) {
                 double yn[6], yo[6];
 #pragma unroll

@@ -313,3 +313,47 @@ def test_folded_tile_plans(ctx, oracle, n):
     assert ctx.kernel_name() == "k_pc_ws_fold"
     want = oracle.run_batch(states, cfg, plan, "independent", 8)
     _parity(got, want)
+
+
+@pytest.mark.parametrize("n", [5, 13, 33, 50, 67, 99, 130, 201, 255])
+def test_dense_node_counts(ctx, oracle, n):
+    """N % 8 != 0 (no mirror fold): the dense warp-specialised or generic slot kernels
+    against the oracle, Sun + 8 planets, 0.5 period."""
+    states, plan, cfg = _setup(12, n, 0.5, "planets8")
+    got = ctx.run_batch(states, cfg, plan, "independent")
+    assert ctx.kernel_name() in ("k_pc_ws", "k_pc_segment")
+    want = oracle.run_batch(states, cfg, plan, "independent", 8)
+    _parity(got, want)
+
+
+@pytest.mark.parametrize("n", [8, 24, 56, 104, 136, 184, 216, 248])
+@pytest.mark.parametrize("kind", ["n_body", "n_body_1pn"])
+def test_unified_tile_plans(ctx, oracle, n, kind):
+    """k_pc_uni over its unit plans (2 x pair tiles over 16 warps) for both force models."""
+    states, plan, cfg = _setup(12, n, 0.5, "planets8")
+    cfg.force_kind = kind
+    ctx.set_option("unified", 1)
+    try:
+        got = ctx.run_batch(states, cfg, plan, "independent")
+        assert ctx.kernel_name() == "k_pc_uni"
+    finally:
+        ctx.set_option("unified", 2)
+    want = oracle.run_batch(states, cfg, plan, "independent", 8)
+    _parity(got, want)
+
+
+@pytest.mark.parametrize("n", [17, 23, 31, 49, 55, 63])
+@pytest.mark.parametrize("mode,p", [("independent", 1), ("grouped", 3), ("augmented", 1)])
+def test_small_n_staged_rows(ctx, oracle, n, mode, p):
+    """The 128-thread small-N plan of the generic and wide-group kernels stages up to 31
+    rows x 8 slots (more items than threads): every staged row must be finalised."""
+    states, plan, cfg = _setup(12, n, 0.4, "planets8")
+    cfg.p_groups = p
+    ctx.set_option("slot_kernel", 1)  # the generic slot kernel where the mode allows it
+    try:
+        got = ctx.run_batch(states, cfg, plan, mode)
+        assert ctx.kernel_name() in ("k_pc_segment", "k_wide_iter")
+    finally:
+        ctx.set_option("slot_kernel", 0)
+    want = oracle.run_batch(states, cfg, plan, mode, 8)
+    _parity(got, want)
