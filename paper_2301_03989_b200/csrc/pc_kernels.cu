@@ -94,7 +94,7 @@ GemmPlan make_gemm_plan(int N) {
         gp.xmax = XMAX_SMALL;
         return gp;
     }
-    for (int w = 4 * (gp.mtiles / 8);; w += 4) {
+    for (int w = 4 * (gp.mtiles / 8); w <= 16; w += 4) {  // the kernels launch at most 16 warps
         const int main = gp.mtiles / w < 2 ? gp.mtiles / w : 2;
         const int extras = (gp.mtiles - main * w) * 6;
         if ((extras + w - 1) / w <= XMAX) {
@@ -103,9 +103,21 @@ GemmPlan make_gemm_plan(int N) {
             gp.mb = main * w;
             gp.extras = extras;
             gp.xmax = XMAX;
-            break;
+            return gp;
         }
     }
+    // 29-31 m-tiles (N = 225..247): no 16-warp plan with <= XMAX extras per warp; pad the
+    // operator to 32 m-tiles (zero rows past N, never written back): 16 warps x 2 full tiles
+    if (gp.mtiles <= 32) {
+        gp.mtiles = 32;
+        gp.warps = 16;
+        gp.main = 2;
+        gp.mb = 32;
+        gp.extras = 0;
+        gp.xmax = XMAX;
+        return gp;
+    }
+    gp.warps = 0;  // no plan: N beyond the device path (rejected by the host)
     return gp;
 }
 

@@ -15,8 +15,9 @@ import paper_2301_03989_b200 as ps
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("n,cols", [(3, 1), (8, 6), (16, 50), (24, 6), (64, 96), (101, 47), (200, 6 * 37),
-                                    (200, 48), (256, 6 * 9)])
+@pytest.mark.parametrize("n,cols", [(3, 1), (8, 6), (16, 50), (24, 6), (31, 13), (49, 48), (55, 7), (63, 100),
+                                    (64, 96), (101, 47), (130, 49), (200, 6 * 37), (200, 48), (223, 5),
+                                    (241, 60), (256, 6 * 9)])
 def test_picard_update_matches_oracle(ctx, oracle, n, cols):
     rng = np.random.default_rng(n * 1000 + cols)
     f = rng.uniform(-3, 3, size=(n, cols))

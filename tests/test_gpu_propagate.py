@@ -315,7 +315,7 @@ def test_folded_tile_plans(ctx, oracle, n):
     _parity(got, want)
 
 
-@pytest.mark.parametrize("n", [5, 13, 33, 50, 67, 99, 130, 201, 255])
+@pytest.mark.parametrize("n", [5, 13, 33, 50, 67, 99, 130, 201, 225, 241, 247, 255, 257, 263])
 def test_dense_node_counts(ctx, oracle, n):
     """N % 8 != 0 (no mirror fold): the dense warp-specialised or generic slot kernels
     against the oracle, Sun + 8 planets, 0.5 period."""
@@ -342,7 +342,7 @@ def test_unified_tile_plans(ctx, oracle, n, kind):
     _parity(got, want)
 
 
-@pytest.mark.parametrize("n", [17, 23, 31, 49, 55, 63])
+@pytest.mark.parametrize("n", [17, 23, 31, 49, 55, 63, 225, 241])
 @pytest.mark.parametrize("mode,p", [("independent", 1), ("grouped", 3), ("augmented", 1)])
 def test_small_n_staged_rows(ctx, oracle, n, mode, p):
     """The 128-thread small-N plan of the generic and wide-group kernels stages up to 31
