@@ -146,3 +146,24 @@ def test_hot_start_group_modes(ctx, oracle, mode, p, m):
     got = ctx.run_batch(states, cfg, plan, mode)
     want = oracle.run_batch(states, cfg, plan, mode, 4)
     _parity(got, want)
+
+
+@pytest.mark.parametrize("n", [33, 50, 99, 201])
+def test_relativistic_dense_node_counts(ctx, oracle, n):
+    """1PN at N % 8 != 0 (dense warp-specialised / generic kernels) against the oracle."""
+    states, plan, cfg = _rel_setup(12, n, 0.5)
+    got = ctx.run_batch(states, cfg, plan, "independent")
+    assert ctx.kernel_name() in ("k_pc_ws", "k_pc_segment")
+    want = oracle.run_batch(states, cfg, plan, "independent", 8)
+    _parity(got, want)
+
+
+@pytest.mark.parametrize("n", [136, 216, 232])
+@pytest.mark.parametrize("kind", ["n_body", "n_body_1pn"])
+def test_hot_start_folded_tile_plans(ctx, oracle, n, kind):
+    """Hot start (EXTENSION) over per-orbit segments with the folded tile plans that use
+    extra units (136), none (216) and b0 from the DMMA stream (136, 232)."""
+    states, plan, cfg = _hot_setup(12, 2.2, kind=kind, n=n)
+    got = ctx.run_batch(states, cfg, plan, "independent")
+    want = oracle.run_batch(states, cfg, plan, "independent", 8)
+    _parity(got, want)

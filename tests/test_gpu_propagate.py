@@ -357,3 +357,16 @@ def test_small_n_staged_rows(ctx, oracle, n, mode, p):
         ctx.set_option("slot_kernel", 0)
     want = oracle.run_batch(states, cfg, plan, mode, 8)
     _parity(got, want)
+
+
+@pytest.mark.parametrize("n", [64, 136, 200, 216])
+@pytest.mark.parametrize("p", [6, 4, 3])  # 12 ICs -> groups of 2, 3, 4 members
+def test_grouped_folded_kernels(ctx, oracle, n, p):
+    """Grouped mode (group members share one convergence decision) through the folded
+    kernels: groups of 2-4 members inside a 4-slot half, every tile plan."""
+    states, plan, cfg = _setup(12, n, 0.5, "planets8")
+    cfg.p_groups = p
+    got = ctx.run_batch(states, cfg, plan, "grouped")
+    assert ctx.kernel_name() == "k_pc_ws_fold"
+    want = oracle.run_batch(states, cfg, plan, "grouped", 8)
+    _parity(got, want)
