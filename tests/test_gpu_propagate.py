@@ -370,3 +370,34 @@ def test_grouped_folded_kernels(ctx, oracle, n, p):
     assert ctx.kernel_name() == "k_pc_ws_fold"
     want = oracle.run_batch(states, cfg, plan, "grouped", 8)
     _parity(got, want)
+
+
+def test_non_elliptic_cold_fallback_and_warnings(ctx, oracle):
+    """Non-elliptic ICs in a warm-start batch fall back to cold rows with a per-trajectory
+    warning (propagator.hpp:94-99); results and warnings match the oracle."""
+    base = ps.reference_state()
+    states = ps.make_clone_batch(base, 8, 1e-5)
+    states[[2, 5], 4:7] *= 1.5  # hyperbolic: beyond escape speed
+    period = ps.osculating_period(base, ps.MU_SUN)
+    plan = ps.plan_segments(base, 0.0, 0.05 * period, ps.MU_SUN, "single", 200)
+    cfg = ps.reference_force_config("n_body", bodies=ps.planets8(), n_nodes=200)
+    got = ctx.run_batch(states, cfg, plan, "independent")
+    want = oracle.run_batch(states, cfg, plan, "independent", 8)
+    _parity(got, want)
+    assert got.warnings == want.warnings
+    assert len(got.warnings) == 2 and "trajectory 2" in got.warnings[0] and "trajectory 5" in got.warnings[1]
+
+
+def test_backward_and_single_ic_match_oracle(ctx, oracle):
+    """Backward propagation (descending boundaries, omega2 < 0) and a one-IC batch."""
+    base = ps.reference_state()
+    period = ps.osculating_period(base, ps.MU_SUN)
+    cfg = ps.reference_force_config("n_body", bodies=ps.planets8(), n_nodes=200)
+    states = ps.make_clone_batch(base, 10, 1e-5)
+    plan = ps.plan_segments(base, 0.0, -1.3 * period, ps.MU_SUN, "per_orbit", 200)
+    got = ctx.run_batch(states, cfg, plan, "independent")
+    want = oracle.run_batch(states, cfg, plan, "independent", 8)
+    _parity(got, want)
+    one = states[:1]
+    plan1 = ps.plan_segments(base, 0.0, 0.7 * period, ps.MU_SUN, "single", 200)
+    _parity(ctx.run_batch(one, cfg, plan1, "independent"), oracle.run_batch(one, cfg, plan1, "independent", 8))
