@@ -16,8 +16,8 @@ namespace pswarm_dev {
 __device__ __forceinline__ void update_sample(const double (&yn)[6], const double (&yo)[6], int j, int error_mode,
                                               double& bn, double& bd, int& nf) {
 #pragma unroll
-    for (int c = 5; c >= 0; --c)
-        if (!isfinite(yn[c])) nf = min(nf, j * 8 + c);
+    for (int c = 5; c >= 0; --c)  // finite <=> exponent field != 0x7ff: integer test, off the FP64 pipe
+        if ((__double2hiint(yn[c]) & 0x7ff00000) == 0x7ff00000) nf = min(nf, j * 8 + c);
     double dr2 = 0.0, r2 = 0.0, dv2 = 0.0, v2 = 0.0;
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
