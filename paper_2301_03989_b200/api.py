@@ -11,6 +11,7 @@ use and run without a device.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 from dataclasses import dataclass, field
 from typing import List, Optional, Sequence
@@ -605,3 +606,65 @@ def max_state_discrepancy(a: np.ndarray, b: np.ndarray) -> float:
     rn = np.maximum(np.linalg.norm(b[..., :3], axis=-1), 1e-30)
     vn = np.maximum(np.linalg.norm(b[..., 3:], axis=-1), 1e-30)
     return float(max((dr / rn).max(initial=0.0), (dv / vn).max(initial=0.0)))
+
+
+@dataclass
+class BenchmarkRow:  # runner.hpp:160-169
+    mode: str = "independent"
+    threads: int = 1
+    groups: int = 1
+    wall_time_s: float = 0.0
+    speedup: float = 1.0
+    max_iterations: int = 0
+    max_discrepancy: float = 0.0
+    group_iterations: list = field(default_factory=list)
+
+
+@dataclass
+class BenchmarkReport:
+    machine: str = ""
+    repeat: int = 1
+    rows: list = field(default_factory=list)
+
+
+def run_benchmark(ctx: "Context", states, config: PropagationConfig, plan: SegmentPlan, thread_counts=(1,),
+                  modes=("independent", "augmented_parallel"), repeat: int = 5) -> BenchmarkReport:
+    """run_benchmark (runner.hpp:186-253): every (mode, workers) combination `repeat` times,
+    median wall time of the C-ABI call, speed-up against the independent single-worker
+    baseline and the cross-mode state discrepancy.  `workers` only labels a row on the
+    device (one context runs the whole batch); numerical outputs never depend on it."""
+    import statistics
+    if repeat < 1:
+        raise InvalidPlanError("run_benchmark: repeat must be positive")
+    rep = BenchmarkReport(machine=f"{os.cpu_count()} hardware threads + B200 (device path)", repeat=repeat)
+
+    def iters_of(r):
+        return [int(x) for x in np.asarray(r.iterations).ravel()]
+
+    base_t, base = [], None
+    for _ in range(repeat):
+        base = ctx.run_batch(states, config, plan, "independent", 1)
+        base_t.append(base.wall_s)
+    base_med = statistics.median(base_t)
+    for mode in modes:
+        mode = parse_run_mode(mode)
+        for threads in thread_counts:
+            row = BenchmarkRow(mode=mode, threads=int(threads))
+            if mode == "independent" and threads == 1:
+                row.wall_time_s, row.groups = base_med, len(base.group_sizes)
+                row.max_iterations = base.max_iterations_used()
+                row.group_iterations = iters_of(base)
+                rep.rows.append(row)
+                continue
+            ts, out = [], None
+            for _ in range(repeat):
+                out = ctx.run_batch(states, config, plan, mode, int(threads))
+                ts.append(out.wall_s)
+            row.wall_time_s = statistics.median(ts)
+            row.groups = len(out.group_sizes)
+            row.speedup = base_med / row.wall_time_s
+            row.max_iterations = out.max_iterations_used()
+            row.max_discrepancy = max_state_discrepancy(out.trajectories, base.trajectories)
+            row.group_iterations = iters_of(out)
+            rep.rows.append(row)
+    return rep

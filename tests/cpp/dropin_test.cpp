@@ -312,6 +312,35 @@ int main() {
         expect(per_node.rows() == static_cast<ps::Index>(out.result.times.size()) && per_node.cols() == 16,
                "per-node shape");
     });
+    run("run_benchmark_rows", [] {  // runner.hpp:186-253: rows, baseline, cross-mode discrepancy
+        ps::PropagationConfig cfg;
+        cfg.force = ps::make_reference_force_model();
+        cfg.p_groups = 4;
+        const auto st = ps::make_clone_batch(ps::make_reference_state(), 16, 1e-5);
+        const double period = ps::osculating_period(st[0], ps::mu_sun_km3s2);
+        const auto sp = ps::plan_segments(st[0], 0.0, 0.5 * period, ps::mu_sun_km3s2, ps::SegmentPolicy::single, 64);
+        const auto rep = ps::run_benchmark(st, cfg, sp, {1, 4},
+                                           {ps::RunMode::independent, ps::RunMode::augmented_parallel,
+                                            ps::RunMode::grouped},
+                                           2);
+        expect(rep.repeat == 2 && rep.rows.size() == 6, "rows " + std::to_string(rep.rows.size()));
+        expect(rep.rows[0].speedup == 1.0 && rep.rows[0].max_discrepancy == 0.0 && rep.rows[0].groups == 16,
+               "baseline row");
+        double worst = 0.0;
+        for (const auto& r : rep.rows) {
+            expect(r.wall_time_s > 0.0 && r.max_iterations > 0, "row timing");
+            worst = std::max(worst, r.max_discrepancy);
+        }
+        expect(rep.rows[2].groups == 1 && rep.rows[4].groups == 4, "group counts");
+        expect(worst <= 1e-9, "cross-mode discrepancy " + sci(worst));  // test_runner.cpp:45-59 (mode invariance)
+        bool threw = false;
+        try {
+            ps::run_benchmark(st, cfg, sp, {1}, {ps::RunMode::independent}, 0);
+        } catch (const ps::InvalidPlanError&) {
+            threw = true;
+        }
+        expect(threw, "repeat 0 must throw");
+    });
     std::printf("SUMMARY %d %d\n", n_pass, n_fail);
     return n_fail == 0 ? 0 : 1;
 }

@@ -401,3 +401,16 @@ def test_backward_and_single_ic_match_oracle(ctx, oracle):
     one = states[:1]
     plan1 = ps.plan_segments(base, 0.0, 0.7 * period, ps.MU_SUN, "single", 200)
     _parity(ctx.run_batch(one, cfg, plan1, "independent"), oracle.run_batch(one, cfg, plan1, "independent", 8))
+
+
+def test_run_benchmark_harness(ctx):
+    """api.run_benchmark (runner.hpp:186-253) on the device: rows per (mode, workers), the
+    independent single-worker baseline, cross-mode discrepancy within the mode-invariance bar."""
+    states, plan, cfg = _setup(16, 64, 0.5, "planets8")
+    cfg.p_groups = 4
+    rep = ps.run_benchmark(ctx, states, cfg, plan, thread_counts=(1, 8),
+                           modes=("independent", "augmented_parallel", "grouped"), repeat=2)
+    assert len(rep.rows) == 6 and rep.rows[0].speedup == 1.0 and rep.rows[0].groups == 16
+    assert [r.groups for r in rep.rows] == [16, 16, 1, 1, 4, 4]
+    assert all(r.wall_time_s > 0 and r.max_iterations > 0 for r in rep.rows)
+    assert max(r.max_discrepancy for r in rep.rows) <= 1e-9  # test_runner.cpp:45-59
