@@ -16,6 +16,9 @@ CASES = [(200, "independent", 1, "n_body", "warm", {}),                      # k
          (96, "independent", 1, "n_body_1pn", "warm", {}),                   # k_pc_uni 1PN (auto)
          (256, "independent", 1, "n_body_1pn", "warm", {}),                  # k_pc_ws_fold 1PN (auto)
          (64, "grouped", 4, "n_body", "warm", {}),                           # grouped, folded kernels
+         (216, "independent", 1, "n_body", "warm", {}),                      # k_pc_ws_fold, no extras, b0 from DMMA
+         (55, "independent", 1, "n_body", "warm", {"slot_kernel": 1}),       # generic small-N, 23 staged rows
+         (241, "augmented", 1, "n_body", "warm", {}),                        # wide path, padded 32 m-tiles
          (72, "grouped", 4, "n_body", "warm", {}),                           # N % 8 != 0 ... generic path
          (64, "augmented", 1, "n_body", "warm", {}),                         # k_wide_iter
          (64, "independent", 1, "n_body", "hot", {})]                        # hot start, multi-segment
@@ -30,3 +33,4 @@ for n, mode, p, kind, start, opts in CASES:
     print(n, mode, kind, start, opts, ctx.kernel_name(), int(r.iterations.sum()), flush=True)
     ctx.set_option("fold", 1)
     ctx.set_option("unified", 2)
+    ctx.set_option("slot_kernel", 0)
