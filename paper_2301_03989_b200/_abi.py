@@ -87,15 +87,17 @@ class PswarmConfig(C.Structure):
 
 
 class PswarmOutputs(C.Structure):
+    # caller-owned output arrays as raw addresses (double*, int32_t*, uint8_t* in the
+    # header): set from numpy's data pointer without building ctypes pointer objects
     _fields_ = [
-        ("terminal_states", C.POINTER(C.c_double)),
-        ("samples", C.POINTER(C.c_double)),
-        ("times", C.POINTER(C.c_double)),
-        ("iterations", C.POINTER(C.c_int32)),
-        ("final_error", C.POINTER(C.c_double)),
-        ("converged", C.POINTER(C.c_uint8)),
-        ("error_history", C.POINTER(C.c_double)),
-        ("cold_fallback", C.POINTER(C.c_uint8)),
+        ("terminal_states", C.c_void_p),
+        ("samples", C.c_void_p),
+        ("times", C.c_void_p),
+        ("iterations", C.c_void_p),
+        ("final_error", C.c_void_p),
+        ("converged", C.c_void_p),
+        ("error_history", C.c_void_p),
+        ("cold_fallback", C.c_void_p),
         ("segments_reported", C.c_int64),
         ("segments_completed", C.c_int64),
         ("device_ms", C.c_double),
@@ -167,3 +169,8 @@ def load(path: str = LIB_PATH) -> C.CDLL:
 def dptr(a):
     """double* of a C-contiguous float64 numpy array (or None)."""
     return None if a is None else a.ctypes.data_as(_dp)
+
+
+def addr(a):
+    """Raw address of a C-contiguous numpy array (or None) for c_void_p fields."""
+    return None if a is None else a.__array_interface__["data"][0]
