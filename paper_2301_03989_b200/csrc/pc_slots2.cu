@@ -745,8 +745,13 @@ __device__ __forceinline__ void decide_half(const SegArgs& a, WsState& st, int h
                 retire = true;
             } else {
                 if (a.rep_hist) a.rep_hist[static_cast<size_t>(gid) * a.max_it + (it - 1)] = gerr_of();
+                // squared-error bands as integer compares of the IEEE bits (non-negative doubles
+                // order like integers; NaN sorts above every finite band): off the FP64 pipe
+                const long long e2b = __double_as_longlong(gerr2);
                 const bool le_tol = PSWARM_ABLATE == 0 &&  // ablation builds: fixed max_it work
-                    (gerr2 <= a.tol2_lo ? true : (gerr2 > a.tol2_hi ? false : gerr_of() <= a.tol));
+                    (e2b <= __double_as_longlong(a.tol2_lo)
+                         ? true
+                         : (e2b > __double_as_longlong(a.tol2_hi) ? false : gerr_of() <= a.tol));
                 if (le_tol) {
                     retire = ok = conv = true;
                 } else if (it >= a.max_it) {
