@@ -78,8 +78,9 @@ struct SegArgs {
     double* hot;                // [M][N][6] hot-start corrections (EXTENSION) or nullptr
     int hot_apply;              // 1: this segment starts from base + correction
     const double2* upack_fold;  // mirror-folded operator pairs [pair][part][k-pair][lane] or nullptr
-    int nkp_fold;
-    int b0_mma;                  // 1: folded b0 from the anchor pair row when N/2 % 8 != 0               // k-pairs per folded part
+    int nkp_fold;               // k-pairs per folded part
+    int b0_mma;                 // 1: folded b0 from the anchor pair row when N/2 % 8 != 0
+    int fast_decide;            // 1: singleton-group decisions fast path (gmax == 1)
     const double* anc_fold;     // [8 nkp] anchor weights of the folded F layout
 };
 

@@ -649,7 +649,85 @@ __device__ __forceinline__ void force_pair(const ForceData& fd, const double* yb
 /// pc_solve's stopping rule (err <= tol, it == max_it) and the fault order of the reference
 /// (warm-start failure, singularity, divergence); the leader of each group writes its report
 /// and frees / retires its slots (free_mask / retire_mask of the half).
+/// decide_half for singleton groups (independent mode, gmax == 1): each lane decides its
+/// own slot — no cross-lane scan or warp sync (a lane rewrites only its own group record),
+/// one combined mask reduction; same stopping rule, fault order and reports.
+__device__ __forceinline__ void decide_single(const SegArgs& a, WsState& st, int h, int lane, int B) {
+    const int s = lane, t = h * HS + s;
+    unsigned bits = 0;  // bit t: slot freed; bit 8 + t: outputs to retire
+    if (s < HS && ((st.act_word[h] >> t) & 1)) {
+        const int lg = st.slot_grp[t];
+        const int gid = st.grp_id[lg];
+        const long long e2b = static_cast<long long>(st.slot_err[t]);
+        const double gerr2 = __longlong_as_double(e2b);
+        const int sk = st.sing_key[t], nk = st.nf_key[t];
+        GroupFault* fl = a.faults + gid;
+        bool retire = false, ok = false, conv = false;
+        int it = st.grp_iter[lg];
+        if (((st.new_mask[h] >> t) & 1) && st.warm_key[t] != INT_MAX) {
+            fl->status = st.warm_kind[t] == CONIC_ZERO_RADIUS ? FAULT_WARM_ZERO_RADIUS : FAULT_WARM_SOLVER;
+            fl->iteration = 0;
+            fl->trajectory = st.slot_traj[t];
+            fl->node = st.warm_key[t] / 4;
+            fl->value = st.warm_val[t][0];
+            fl->value2 = st.warm_val[t][1];
+            retire = true;
+        } else {
+            it += 1;
+            st.grp_iter[lg] = it;
+            if (sk != INT_MAX) {
+                fl->status = FAULT_SINGULARITY;
+                fl->iteration = it;
+                fl->node = sk / (B + 1);
+                fl->body = sk % (B + 1) - 1;
+                fl->trajectory = st.slot_member[t];
+                fl->value = st.sing_val[t];
+                retire = true;
+            } else if (nk != INT_MAX) {
+                const long long key = static_cast<long long>(nk >> 3) * 6 + (nk & 7);
+                fl->status = FAULT_DIVERGENCE;
+                fl->iteration = it;
+                fl->node = key / 6;
+                fl->column = key % 6;
+                retire = true;
+            } else {
+                if (a.rep_hist) a.rep_hist[static_cast<size_t>(gid) * a.max_it + (it - 1)] = sqrt(gerr2);
+                const bool le_tol = PSWARM_ABLATE == 0 &&
+                    (e2b <= __double_as_longlong(a.tol2_lo)
+                         ? true
+                         : (e2b > __double_as_longlong(a.tol2_hi) ? false : sqrt(gerr2) <= a.tol));
+                if (le_tol) {
+                    retire = ok = conv = true;
+                } else if (it >= a.max_it) {
+                    retire = ok = true;
+                }
+            }
+        }
+        if (retire) {
+            a.rep_iter[gid] = it;
+            a.rep_err[gid] = sqrt(gerr2);
+            a.rep_conv[gid] = conv ? 1 : 0;
+            bits = (1u << t) | (ok ? (1u << (8 + t)) : 0u);
+            st.grp_id[lg] = -1;
+        }
+    }
+    bits = __reduce_or_sync(0xffffffffu, bits);
+    if (lane == 0) {
+        st.free_mask[h] = static_cast<int>(bits & 0xffu);
+        st.retire_mask[h] = static_cast<int>(bits >> 8);
+    }
+    if (s < HS) {  // reset this half's accumulators for its next iteration
+        st.slot_err[t] = 0ull;
+        st.sing_key[t] = INT_MAX;
+        st.nf_key[t] = INT_MAX;
+    }
+}
+
 __device__ __forceinline__ void decide_half(const SegArgs& a, WsState& st, int h, int lane, int B) {
+    if (a.gmax == 1 && a.fast_decide) {
+        decide_single(a, st, h, lane, B);
+        return;
+    }
     const int am = st.act_word[h];
     const int s = lane, t = h * HS + s;
     const bool act_t = s < HS && ((am >> t) & 1);
