@@ -951,6 +951,22 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
                                          reinterpret_cast<const double*>(smem_raw + L.fbuf0 + h * fb_bytes), nfull,
                                          warp, lane, xt, xp, facc, fxacc);
                     WS_PHASE(1);
+                    // extra unit -> stage its unfolded raw sums now (both mirrored rows); the light
+                    // warps add omega2 / b0 and finalise them after the b0 barrier, concurrently
+                    // with the other warps' main epilogue
+                    double* xs_lo = xstage + (2 * h) * xrows * HC;
+                    double* xs_hi = xs_lo + xrows * HC;
+                    if (xt >= 0) {
+                        const int j = xt * 8 + g;
+                        if (j < half) {
+#pragma unroll
+                            for (int e = 0; e < 2; ++e) {
+                                const int o = (j - nfull * 8) * HC + q * 6 + 2 * xp + e;
+                                xs_lo[o] = fxacc[0][e] + fxacc[1][e];
+                                xs_hi[o] = fxacc[0][e] - fxacc[1][e];
+                            }
+                        }
+                    }
                     if (b0mma) {  // b0 = (omega2 anchor.F + 2 y0) / 2 from the anchor pair row
                         const int at = half >> 3;
                         if (g == (half & 7)) {
@@ -1017,17 +1033,31 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
                         atomicMax(&st.slot_err[h * HS + q], static_cast<unsigned long long>(__double_as_longlong(e2)));
                         if (nf != INT_MAX) atomicMin(&st.nf_key[h * HS + q], nf);
                     }
-                    double* xs_lo = xstage + (2 * h) * xrows * HC;
-                    double* xs_hi = xs_lo + xrows * HC;
-                    if (xt >= 0) {  // extra unit -> stage (both mirrored rows; finalised below)
-                        const int j = xt * 8 + g;
-                        if (j < half) {
+                    if (nxt > 0) {  // staged rows (pair rows of the leftover tiles and mirrors): light warps
+                        const int light = MMA_WARPS - (nfull % MMA_WARPS + 3 * nxt);  // warps without extras
+                        const int lt = tid - (MMA_WARPS - light) * 32;
+                        if (lt >= 0) {
+                            const int xv = min(xrows, half - nfull * 8);  // valid pair rows
+                            for (int i = lt; i < xv * HS * 2; i += light * 32) {
+                                const int mir = i / (xv * HS), ii = i - mir * xv * HS;
+                                const int r = ii >> 2, s = ii & 3;
+                                const int jp = nfull * 8 + r, j = mir ? N - 1 - jp : jp;
+                                if (!((act_h >> s) & 1)) continue;
+                                const double* xs = mir ? xs_hi : xs_lo;
+                                double yn[6], yo[6];
 #pragma unroll
-                            for (int e = 0; e < 2; ++e) {
-                                const double bb = b0[xp * 8 + 2 * q + e];
-                                const int o = (j - nfull * 8) * HC + q * 6 + 2 * xp + e;
-                                xs_lo[o] = fma(w2, fxacc[0][e] + fxacc[1][e], bb);
-                                xs_hi[o] = fma(w2, fxacc[0][e] - fxacc[1][e], bb);
+                                for (int c = 0; c < 6; ++c) {
+                                    yn[c] = fma(w2, xs[r * HC + s * 6 + c], b0[(c >> 1) * 8 + 2 * s + (c & 1)]);
+                                    yo[c] = ybuf[y2(j, h, c, s)];
+                                }
+                                double sbn = 0.0, sbd = 1.0;
+                                int snf = INT_MAX;
+                                update_sample(yn, yo, j, a.error_mode, sbn, sbd, snf);
+#pragma unroll
+                                for (int c = 0; c < 6; ++c) ybuf[y2(j, h, c, s)] = yn[c];
+                                atomicMax(&st.slot_err[h * HS + s],
+                                          static_cast<unsigned long long>(__double_as_longlong(sbn / sbd)));
+                                if (snf != INT_MAX) atomicMin(&st.nf_key[h * HS + s], snf);
                             }
                         }
                     }
@@ -1037,30 +1067,6 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
                     WS_PHASE(2);
                     bar_sync(BAR_MMA, MMA_THREADS);  // every warp's slot_err / nf_key update is in
                     WS_PHASE(11);
-                    if (nxt > 0) {  // staged rows: pair rows of the leftover tiles and their mirrors
-                        const int xv = min(xrows, half - nfull * 8);  // valid pair rows
-                        for (int i = tid; i < xv * HS * 2; i += MMA_THREADS) {
-                            const int mir = i / (xv * HS), ii = i - mir * xv * HS;
-                            const int r = ii >> 2, s = ii & 3;
-                            const int jp = nfull * 8 + r, j = mir ? N - 1 - jp : jp;
-                            if (!((act_h >> s) & 1)) continue;
-                            const double* xs = mir ? xs_hi : xs_lo;
-                            double yn[6], yo[6];
-#pragma unroll
-                            for (int c = 0; c < 6; ++c) {
-                                yn[c] = xs[r * HC + s * 6 + c];
-                                yo[c] = ybuf[y2(j, h, c, s)];
-                            }
-                            double sbn = 0.0, sbd = 1.0;
-                            int snf = INT_MAX;
-                            update_sample(yn, yo, j, a.error_mode, sbn, sbd, snf);
-#pragma unroll
-                            for (int c = 0; c < 6; ++c) ybuf[y2(j, h, c, s)] = yn[c];
-                            atomicMax(&st.slot_err[h * HS + s], static_cast<unsigned long long>(__double_as_longlong(sbn / sbd)));
-                            if (snf != INT_MAX) atomicMin(&st.nf_key[h * HS + s], snf);
-                        }
-                        bar_sync(BAR_MMA, MMA_THREADS);
-                    }
                     WS_PHASE(12);
                     if (warp == 0) decide_half(a, st, h, lane, B);
                     WS_PHASE(13);
