@@ -988,8 +988,10 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
                                                                                2.0 * st.y0[h * HS + q][2 * xp + e]);
                         }
                         bar_sync(BAR_MMA, MMA_THREADS);
-                    } else {
-                        bar_sync(BAR_B0 + h, WS_THREADS);  // b0 of half h (FP group, formed before F_h)
+                    } else if (nxt > 0) {
+                        // the FP group formed b0 before releasing F_h (ordered by the F barrier);
+                        // the barrier orders the raw staging writes before the light warps' reads
+                        bar_sync(BAR_MMA, MMA_THREADS);
                     }
                     WS_PHASE(3);
                     // unfold: Y_j = acc_sum + acc_diff, Y_{N-1-j} = acc_sum - acc_diff (the 1/2 sits in
@@ -1144,7 +1146,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
                 WS_PHASE(2);
             } else {
                 if (FOLD && tid == 0) st.free_mask[h] = st.retire_mask[h] = 0;  // no decisions ran
-                if (!b0mma) bar_sync(BAR_B0 + h, WS_THREADS);  // keep the B_h generations paired
+                if (!FOLD) bar_sync(BAR_B0 + h, WS_THREADS);  // keep the B_h generations paired
             }
             bar_arrive(BAR_Y0 + h, WS_THREADS);  // bar.arrive/bar.sync order smem among participants
         }
@@ -1434,7 +1436,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
             }
             WS_PHASE(9);
             if constexpr (FOLD) bar_arrive(BAR_F0 + h, WS_THREADS);
-            if (!b0mma) bar_arrive(BAR_B0 + h, WS_THREADS);
+            if (!FOLD) bar_arrive(BAR_B0 + h, WS_THREADS);  // folded: b0 precedes F_h
         }
     }
     if (prof) {
