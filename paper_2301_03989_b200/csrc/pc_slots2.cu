@@ -1,16 +1,19 @@
-// Warp-specialised slot kernel (k_pc_ws): the fast path of the persistent solve for
-// groups of at most 4 trajectories (independent mode = singleton groups).
+// Slot kernels of the persistent solve for groups of at most 4 trajectories
+// (independent mode = singleton groups): the warp-specialised k_pc_ws (dense update, or
+// mirror-folded when N % 8 == 0 — the default path) and the unified k_pc_uni.
 //
-// The 8 trajectory slots of a CTA are split into two halves of 4.  Sixteen warps
+// k_pc_ws: the 8 trajectory slots of a CTA are split into two halves of 4.  Sixteen warps
 // form two groups that run the halves out of phase:
 //   MMA group (warps 0-7):  [DMMA update of half h] -> [epilogue of half h: + b0/2,
-//                           finite check, error] -> signal "Y_h ready"
-//   FP group  (warps 8-15): [decisions / retire / refill / warm start of half h]
-//                           -> [force of half h] -> signal "F_h ready"
-// so the FP64-vector work of one half (force, conics) overlaps the DMMA work of the
-// other half instead of idling the shared FP64 pipe between phases (on B200 the DMMA
-// and DFMA paths share one FP64 datapath, tools/fp64_peak.cu).  Hand-off is through
-// named barriers (bar.arrive / bar.sync, 512 threads).  Semantics are identical to
+//                           finite check, error] -> (folded) [staged rows, decisions]
+//                           -> signal "Y_h ready"
+//   FP group  (warps 8-15): [(dense) decisions / retire / refill / warm start of half h]
+//                           -> [force of half h (folded: mirrored node pairs)] -> b0
+//                           -> signal "F_h ready"
+// On B200 the DMMA and DFMA paths share one FP64 datapath (tools/fp64_peak.cu,
+// tools/ws_mix.cu), so the two groups' FP64 work largely serialises; the split still
+// hides the integer / shared-memory latency of one phase under the other.
+// Hand-off is through named barriers (bar.arrive / bar.sync).  Semantics are identical to
 // k_pc_segment (pc_kernels.cu): pc_solve's loop (picard.hpp:66-81) per group with
 // per-trajectory masking and refill.
 //
