@@ -1378,13 +1378,14 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
             if constexpr (FOLD && REL) {  // fold F in place: s_k at position k, a_k = F_k - F_{N-1-k} at N-1-k
                 if (act_h) {
                     double* fbh = reinterpret_cast<double*>(smem_raw + L.fbuf0 + h * fb_bytes);
-                    for (int i = ft; i < half * HC; i += FP_THREADS) {
-                        const int k = i % half, col = i / half;
+                    for (int col = fw; col < HC; col += FP_WARPS) {  // warp per column, lane per node
                         const int c = 2 * (col >> 3) + (col & 1), sl = (col & 7) >> 1;
-                        const int lo = f2(k, c, sl), hi = f2(N - 1 - k, c, sl);
-                        const double flo = fbh[lo], fhi = fbh[hi];
-                        fbh[lo] = flo + fhi;
-                        fbh[hi] = flo - fhi;
+                        for (int k = lane; k < half; k += 32) {
+                            const int lo = f2(k, c, sl), hi = f2(N - 1 - k, c, sl);
+                            const double flo = fbh[lo], fhi = fbh[hi];
+                            fbh[lo] = flo + fhi;
+                            fbh[hi] = flo - fhi;
+                        }
                     }
                 }
                 bar_sync(BAR_FP, FP_THREADS);
@@ -1777,16 +1778,17 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_uni(const SegArgs a) {
                 else force_half_rel<1>(a.fd, ybuf, fbh, st.sing_key, act_h, h, j, s0);
             }
             __syncthreads();
-            for (int i = tid; i < 2 * half * HC; i += T) {  // fold: s_k at k, a_k = F_k - F_{N-1-k} at N-1-k
-                const int h = i / (half * HC), ii = i % (half * HC);
+            for (int hc = warp; hc < 2 * HC; hc += NW) {  // fold: s_k at k, a_k = F_k - F_{N-1-k} at N-1-k
+                const int h = hc / HC, col = hc % HC;       // warp per (half, column), lane per node
                 if (!((am >> (h * HS)) & 0xF)) continue;
                 double* fbh = fb0 + h * (fb_bytes / sizeof(double));
-                const int k = ii % half, col = ii / half;
                 const int c = 2 * (col >> 3) + (col & 1), sl = (col & 7) >> 1;
-                const int lo = f2(k, c, sl), hi = f2(N - 1 - k, c, sl);
-                const double flo = fbh[lo], fhi = fbh[hi];
-                fbh[lo] = flo + fhi;
-                fbh[hi] = flo - fhi;
+                for (int k = lane; k < half; k += 32) {
+                    const int lo = f2(k, c, sl), hi = f2(N - 1 - k, c, sl);
+                    const double flo = fbh[lo], fhi = fbh[hi];
+                    fbh[lo] = flo + fhi;
+                    fbh[hi] = flo - fhi;
+                }
             }
         } else {
             const int npw = half > T / 8 ? 2 : 4;  // work items per (half, node pair): slot pairs or slots
