@@ -1765,7 +1765,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_uni(const SegArgs a) {
         // ---- force of both halves, folded as written (mirrored node pairs); relativistic: per
         //      node with the fused 1PN pass, then folded in place
         if constexpr (REL) {
-            const int ns = 2 * N > T / 2 ? 4 : (4 * N > T / 2 ? 2 : 1);  // slots per item
+            const int ns = N > 64 ? 2 : 1;  // slots per item (2 fused chains; N = 200: 800 items, all warps)
             const int per_h = N * (4 / ns);
             for (int w = tid; w < 2 * per_h; w += T) {
                 const int h = w / per_h, r = w % per_h;
