@@ -21,6 +21,10 @@ from paper_2301_03989_b200.api import (PropagationIncompleteError, _ConfigMarsha
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB = os.path.join(HERE, "liboracle.so")
 KAT = os.path.join(HERE, "kat_tests")
+# the reference's OWN sources compiled here (oracle/Makefile.ref; needs /root/reference
+# at build time, the built .so travels to the GPU box)
+REF_LIB = os.path.join(HERE, "_ref", "libpswarm_refsrc.so")
+REF_SRC = "/root/reference/proj/include/pswarm"
 
 _dp = C.POINTER(C.c_double)
 _ep = C.POINTER(_abi.PswarmError)
@@ -32,10 +36,33 @@ def build(force: bool = False) -> None:
         subprocess.run(["make", "-s", "-C", HERE], check=True)
 
 
+def build_reference(force: bool = False) -> bool:
+    """Compile oracle/_ref from the reference's own sources when they are present
+    (this container); returns whether oracle/_ref/libpswarm_refsrc.so exists."""
+    if os.path.isdir(REF_SRC) and (force or not os.path.exists(REF_LIB)):
+        subprocess.run(["make", "-s", "-C", HERE, "-f", "Makefile.ref"], check=True)
+    return os.path.exists(REF_LIB)
+
+
+def reference_available() -> bool:
+    return os.path.exists(REF_LIB)
+
+
 class Oracle:
-    def __init__(self):
-        build()
-        lib = C.CDLL(LIB)
+    """CPU checker.  Default: the Eigen-free restatement (oracle/pswarm_ref.hpp,
+    liboracle.so).  Oracle(reference=True): the reference's own sources
+    (oracle/_ref/libpswarm_refsrc.so) behind the same entry points (batch
+    propagation, run_batch, operators, Picard update, clone batches)."""
+
+    def __init__(self, reference: bool = False):
+        self.is_reference = reference
+        if reference:
+            if not reference_available():
+                raise FileNotFoundError(f"{REF_LIB} not built (oracle/Makefile.ref needs /root/reference)")
+            lib = C.CDLL(REF_LIB)
+        else:
+            build()
+            lib = C.CDLL(LIB)
         sig = {
             "ref_propagate": [C.c_int64, _dp, C.c_int64, C.POINTER(C.c_int64), C.c_int64, _dp, C.c_int64,
                               C.POINTER(_abi.PswarmConfig), C.c_int32, C.c_int32, C.POINTER(_abi.PswarmOutputs), _ep],
@@ -57,6 +84,8 @@ class Oracle:
             "ref_rk_sample": [_dp, C.POINTER(_abi.PswarmConfig), C.c_int64, _dp, _dp, _ep],
         }
         for name, args in sig.items():
+            if not hasattr(lib, name):  # the reference-source library exports the batch subset
+                continue
             fn = getattr(lib, name)
             fn.restype = C.c_int32
             fn.argtypes = args

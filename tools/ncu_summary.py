@@ -21,6 +21,11 @@ KEYS = {
     "launch__block_size": "block",
     "sm__throughput.avg.pct_of_peak_sustained_elapsed": "sm_throughput_pct",
     "smsp__cycles_active.avg": "smsp_cycles_active",
+    "sm__sass_thread_inst_executed_op_dfma_pred_on.sum": "dfma_thread_inst",
+    "sm__sass_thread_inst_executed_op_dadd_pred_on.sum": "dadd_thread_inst",
+    "sm__sass_thread_inst_executed_op_dmul_pred_on.sum": "dmul_thread_inst",
+    "sm__cycles_elapsed.avg.per_second": "sm_hz",
+    "launch__waves_per_multiprocessor": "waves_per_sm",
 }
 UNITS = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "msecond": 1, "ms": 1, "usecond": 1e-3, "us": 1e-3, "nsecond": 1e-6, "ns": 1e-6}
 
