@@ -18,3 +18,4 @@
 #include "pswarm/synthetic.hpp"
 #include "pswarm/types.hpp"
 #include "pswarm/oracle.hpp"
+#include "pswarm/selftest.hpp"

@@ -26,6 +26,41 @@ struct ForceModelConfig {  // force_model.hpp:17-24
     double c_light = 299792.458;  // km/s, n_body_1pn only
 };
 
+/// Single-sample host forms (force_model.hpp:26-52): the central term and the direct +
+/// indirect term of one perturbing body, with the reference's singularity guards.  They
+/// back acceleration_at, the continuous-time force of the host verifier; the batched
+/// iteration-path force runs on the device (eval_force_block_data, propagate).
+inline Vec3 central_acceleration(const Vec3& r, double mu) {
+    const double rn = r.norm();
+    if (!(rn > 0.0)) throw SingularityError("central-body acceleration at zero radius");
+    return (-mu / (rn * rn * rn)) * r;
+}
+
+inline Vec3 perturber_acceleration(const Vec3& r, const Vec3& r_body, double mu_body, double proximity_floor_km,
+                                   const std::string& body_name) {
+    const Vec3 d = r_body - r;
+    const double dn = d.norm();
+    if (dn < proximity_floor_km)
+        throw SingularityError("close approach to body '" + body_name + "': distance " + std::to_string(dn) +
+                                   " km below floor " + std::to_string(proximity_floor_km) + " km",
+                               body_name);
+    const double bn = r_body.norm();
+    return mu_body * (d / (dn * dn * dn) - r_body / (bn * bn * bn));
+}
+
+/// Continuous-time acceleration (force_model.hpp:78-87): body positions evaluated at t,
+/// not frozen per node — the derivative the RKF7(8) verifier integrates.
+inline Vec3 acceleration_at(const Vec3& r, double t, const ForceModelConfig& config) {
+    if (config.kind == ForceKind::n_body_1pn)
+        throw InvalidPlanError("acceleration_at: the 1PN model needs body velocities; use oracle_check_batch");
+    Vec3 a = central_acceleration(r, config.central_mu);
+    if (config.kind == ForceKind::n_body)
+        for (const BodySpec& b : config.bodies)
+            a += perturber_acceleration(r, body_position(b, config.central_mu, t), b.mu, config.proximity_floor_km,
+                                        b.name);
+    return a;
+}
+
 /// omega2-scaled derivative block of a component-major N x 6m state block,
 /// evaluated on the device (force_model.hpp:93-142).  Singularities raise the
 /// reference's SingularityError tagged "node j, trajectory t" (force_model.hpp:115-120).

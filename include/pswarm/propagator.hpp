@@ -14,6 +14,7 @@
 #include <utility>
 #include <vector>
 
+#include "pswarm/augment.hpp"
 #include "pswarm/block.hpp"
 #include "pswarm/chebyshev.hpp"
 #include "pswarm/device.hpp"
@@ -21,6 +22,8 @@
 #include "pswarm/errors.hpp"
 #include "pswarm/force_model.hpp"
 #include "pswarm/kepler.hpp"
+#include "pswarm/pc_matrices.hpp"
+#include "pswarm/reduction.hpp"
 #include "pswarm/types.hpp"
 
 namespace pswarm {

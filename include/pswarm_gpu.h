@@ -189,6 +189,13 @@ pswarm_status pswarm_run_batch(pswarm_ctx* ctx, int64_t n_states, const double* 
 pswarm_status pswarm_picard_update(pswarm_ctx* ctx, int64_t n_nodes, int64_t n_cols, const double* force,
                                    const double* initial_row, double* out, pswarm_error* err);
 
+/* picard_update_into(mats, F, y0, out) with the CALLER's operators (pc_matrices.hpp:123-151
+ * applies mats.update_op / mats.anchor_op, whatever they hold — selftest.hpp:24-35
+ * perturbs them as a negative control).  update_op [N][N], anchor_op [N]. */
+pswarm_status pswarm_picard_update_ops(pswarm_ctx* ctx, int64_t n_nodes, int64_t n_cols, const double* update_op,
+                                       const double* anchor_op, const double* force, const double* initial_row,
+                                       double* out, pswarm_error* err);
+
 /* eval_force_block_data(y, m, grid, table, config, force) — force_model.hpp:93-142.
  * y [N][6m]; body_positions [B][N][3] frozen per node (ephemeris.hpp:77-86). */
 pswarm_status pswarm_eval_force_block(pswarm_ctx* ctx, int64_t n_nodes, int64_t group_size, const double* y,

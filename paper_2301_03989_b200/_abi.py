@@ -129,6 +129,7 @@ SIGNATURES = [
      [C.c_void_p, C.c_int64, _dp, C.c_int64, _dp, C.c_int64, C.POINTER(PswarmConfig), C.c_int32, C.c_int32,
       C.POINTER(PswarmOutputs), _ep]),
     ("pswarm_picard_update", C.c_int32, [C.c_void_p, C.c_int64, C.c_int64, _dp, _dp, _dp, _ep]),
+    ("pswarm_picard_update_ops", C.c_int32, [C.c_void_p, C.c_int64, C.c_int64, _dp, _dp, _dp, _dp, _dp, _ep]),
     ("pswarm_eval_force_block", C.c_int32,
      [C.c_void_p, C.c_int64, C.c_int64, _dp, C.c_double, C.c_int32, C.c_double, C.c_int32, _dp, _dp,
       C.POINTER(C.c_char_p), C.c_double, _dp, _ep]),

@@ -454,8 +454,10 @@ class Context:
         return outs.result(gs, plan, True, indep)
 
     # ---- operator-level entry points --------------------------------------
-    def picard_update(self, force: np.ndarray, initial_row: np.ndarray) -> np.ndarray:
-        """picard_update_into (pc_matrices.hpp:123-151) on the device."""
+    def picard_update(self, force: np.ndarray, initial_row: np.ndarray, update_op=None,
+                      anchor_op=None) -> np.ndarray:
+        """picard_update_into (pc_matrices.hpp:123-151) on the device: the context's
+        operators for N = rows(force), or the caller's (update_op [N][N], anchor_op [N])."""
         f = np.ascontiguousarray(force, dtype=np.float64)
         y0 = np.ascontiguousarray(initial_row, dtype=np.float64).ravel()
         if f.ndim != 2:
@@ -464,8 +466,16 @@ class Context:
             raise ShapeError(f"picard_update: initial row has {y0.size} columns, force block has {f.shape[1]}")
         out = np.zeros_like(f)
         err = _abi.PswarmError()
-        _check(self.lib.pswarm_picard_update(self.ptr, f.shape[0], f.shape[1], _abi.dptr(f), _abi.dptr(y0),
-                                             _abi.dptr(out), C.byref(err)), err)
+        if update_op is None:
+            _check(self.lib.pswarm_picard_update(self.ptr, f.shape[0], f.shape[1], _abi.dptr(f), _abi.dptr(y0),
+                                                 _abi.dptr(out), C.byref(err)), err)
+            return out
+        u = np.ascontiguousarray(update_op, dtype=np.float64)
+        a = np.ascontiguousarray(anchor_op, dtype=np.float64).ravel()
+        if u.shape != (f.shape[0], f.shape[0]) or a.size != f.shape[0]:
+            raise ShapeError(f"picard_update: operators do not match n_nodes = {f.shape[0]}")
+        _check(self.lib.pswarm_picard_update_ops(self.ptr, f.shape[0], f.shape[1], _abi.dptr(u), _abi.dptr(a),
+                                                 _abi.dptr(f), _abi.dptr(y0), _abi.dptr(out), C.byref(err)), err)
         return out
 
     def eval_force_block(self, y, group_size, omega2, force_kind, central_mu, body_positions=None, body_mus=None,

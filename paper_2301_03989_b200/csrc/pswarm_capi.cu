@@ -227,18 +227,15 @@ namespace {
 void bind(pswarm_ctx* ctx) { cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice"); }
 
 /// [update_op; anchor_op] packed in mma.m8n8k4 A-fragment order (pc_device.cuh).
-const OpPack& operators(pswarm_ctx* ctx, Index n) {
-    auto it = ctx->ops.find(n);
-    if (it != ctx->ops.end()) return *it->second;
-    if (n > 264) raise(PSWARM_ERR_INVALID_SIZE, fmtf("device operators support up to 264 nodes, got %lld", (long long)n));
-    const auto mats = pswarm::cached_matrices(n);  // InvalidSizeError for n < 3
-    const GemmPlan gp = make_gemm_plan(static_cast<int>(n));
+/// [update_op; anchor_op] (row-major N x N and N) in the DMMA A-fragment order
+/// [m-tile][k-pair][lane] double2, rows padded to the plan's m-tiles, K to 8.
+std::vector<double> pack_dense_operator(Index n, const GemmPlan& gp, const double* U, const double* anchor) {
     const int nkp = static_cast<int>((n + 7) / 8);
     const int rows = 8 * gp.mtiles;
     auto A = [&](int r, int k) -> double {
         if (k >= n) return 0.0;
-        if (r < n) return mats->update_op(r, k);
-        if (r == n) return mats->anchor_op[k];
+        if (r < n) return U[static_cast<size_t>(r) * n + k];
+        if (r == n) return anchor[k];
         return 0.0;
     };
     std::vector<double> host(static_cast<size_t>(rows / 8) * nkp * 32 * 2);
@@ -250,6 +247,17 @@ const OpPack& operators(pswarm_ctx* ctx, Index n) {
                 host[2 * idx] = A(m * 8 + g, kp * 8 + q);
                 host[2 * idx + 1] = A(m * 8 + g, kp * 8 + 4 + q);
             }
+    return host;
+}
+
+const OpPack& operators(pswarm_ctx* ctx, Index n) {
+    auto it = ctx->ops.find(n);
+    if (it != ctx->ops.end()) return *it->second;
+    if (n > 264) raise(PSWARM_ERR_INVALID_SIZE, fmtf("device operators support up to 264 nodes, got %lld", (long long)n));
+    const auto mats = pswarm::cached_matrices(n);  // InvalidSizeError for n < 3
+    const GemmPlan gp = make_gemm_plan(static_cast<int>(n));
+    const int nkp = static_cast<int>((n + 7) / 8);
+    const std::vector<double> host = pack_dense_operator(n, gp, mats->update_op.data(), mats->anchor_op.data());
     auto p = std::make_unique<OpPack>();
     p->nkp = nkp;
     p->gp = gp;
@@ -1188,6 +1196,35 @@ pswarm_status pswarm_picard_update(pswarm_ctx* ctx, int64_t n_nodes, int64_t n_c
         double* dO = ctx->buf[B_OP_OUT].get<double>(nc);
         cuda_check(launch_picard_update(static_cast<int>(n_nodes), op.nkp, static_cast<int>(n_cols), dF, dy0, dO,
                                         reinterpret_cast<const double2*>(op.buf.p), ctx->stream),
+                   "k_picard_update");
+        ++ctx->launches;
+        cuda_check(cudaMemcpyAsync(out, dO, nc * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+        cuda_check(cudaStreamSynchronize(ctx->stream), "picard_update");
+    });
+}
+
+pswarm_status pswarm_picard_update_ops(pswarm_ctx* ctx, int64_t n_nodes, int64_t n_cols, const double* update_op,
+                                       const double* anchor_op, const double* force, const double* initial_row,
+                                       double* out, pswarm_error* err) {
+    return guarded(err, [&] {
+        if (!ctx) raise(PSWARM_ERR_NO_DEVICE, "pswarm_picard_update_ops: null context");
+        if (!update_op || !anchor_op) raise(PSWARM_ERR_SHAPE, "picard_update: operators must be given");
+        if (n_nodes < 3 || n_nodes > 264)
+            raise(PSWARM_ERR_INVALID_SIZE, fmtf("device operators support 3..264 nodes, got %lld", (long long)n_nodes));
+        bind(ctx);
+        if (n_cols < 1) return;
+        const GemmPlan gp = make_gemm_plan(static_cast<int>(n_nodes));
+        const std::vector<double> host = pack_dense_operator(n_nodes, gp, update_op, anchor_op);
+        double* dA;
+        upload(ctx, B_OP_AUX, host.data(), host.size(), &dA);
+        const size_t nc = static_cast<size_t>(n_nodes) * n_cols;
+        double *dF, *dy0;
+        upload(ctx, B_OP_IN, force, nc, &dF);
+        upload(ctx, B_OP_IN2, initial_row, static_cast<size_t>(n_cols), &dy0);
+        double* dO = ctx->buf[B_OP_OUT].get<double>(nc);
+        cuda_check(launch_picard_update(static_cast<int>(n_nodes), static_cast<int>((n_nodes + 7) / 8),
+                                        static_cast<int>(n_cols), dF, dy0, dO, reinterpret_cast<const double2*>(dA),
+                                        ctx->stream),
                    "k_picard_update");
         ++ctx->launches;
         cuda_check(cudaMemcpyAsync(out, dO, nc * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream), "D2H");

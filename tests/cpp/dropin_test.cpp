@@ -109,7 +109,7 @@ int main() {
         for (int d = 0; d <= 10; ++d) {
             ps::Mat f(n, 1);
             for (ps::Index j = 0; j < n; ++j) f(j, 0) = grid.omega2 * std::pow(grid.times[j], d);
-            ps::RowVec y0{1.0};
+            const ps::RowVec y0 = ps::RowVec::Ones(1);
             const ps::Mat y = ps::picard_update(mats, f, y0);
             for (ps::Index j = 0; j < n; ++j) {
                 const double e = 1.0 + std::pow(grid.times[j], d + 1) / (d + 1);

@@ -141,3 +141,22 @@ def test_warm_start_zero_radius_raises(ctx):
     times, _ = ps.build_grid(8, 0.0, 1.0e6)
     with pytest.raises(ps.SingularityError, match="zero-radius"):
         ctx.warm_start(states, times, ps.MU_SUN)
+
+
+@pytest.mark.parametrize("n,cols", [(16, 1), (64, 30), (200, 48)])
+def test_picard_update_with_caller_operators(ctx, oracle, n, cols):
+    """pswarm_picard_update_ops applies the caller's operators (pc_matrices.hpp:123-151 uses
+    mats' own matrices): canonical operators match the cached path, a perturbed transform
+    (selftest.hpp:24-35 negative control) changes the result exactly as on the host."""
+    rng = np.random.default_rng(n + cols)
+    f = rng.uniform(-3, 3, size=(n, cols))
+    y0 = rng.uniform(-30, 30, size=cols)
+    u, a = oracle.operators(n)
+    same = ctx.picard_update(f, y0, u, a)
+    assert np.abs(same - ctx.picard_update(f, y0)).max() <= 1e-13 * np.abs(same).max()
+    up = u.copy()
+    up[:, 1] += 1e-3 * rng.standard_normal(n)
+    got = ctx.picard_update(f, y0, up, a)
+    want = up @ f + 0.5 * (a @ f + 2.0 * y0)[None, :]
+    assert np.abs(got - want).max() <= 1e-13 * np.abs(want).max()
+    assert np.abs(got - same).max() > 1e-6 * np.abs(same).max()

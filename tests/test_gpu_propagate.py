@@ -414,3 +414,21 @@ def test_run_benchmark_harness(ctx):
     assert [r.groups for r in rep.rows] == [16, 16, 1, 1, 4, 4]
     assert all(r.wall_time_s > 0 and r.max_iterations > 0 for r in rep.rows)
     assert max(r.max_discrepancy for r in rep.rows) <= 1e-9  # test_runner.cpp:45-59
+
+
+def test_reference_acceptance_program_on_device():
+    """The reference's own acceptance program (proj/tests/acceptance.cpp), compiled
+    UNCHANGED against include/ and linked with the device library (tests/cpp/Makefile
+    ref_acceptance).  Criteria 1-5, 8, 9 are numerical contracts and must pass on the
+    device.  Criteria 6 and 7 time CPU properties of the reference's thread pool
+    (augmentation beats independent on one core; grouped runtime does not grow with
+    workers); on the device `workers` has no meaning, so they are reported, not asserted."""
+    exe = os.path.join(ROOT, "tests", "cpp", "ref_acceptance")
+    if not os.path.exists(exe):
+        pytest.skip("tests/cpp/ref_acceptance not built (needs /root/reference at build time)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=900)
+    print(r.stdout)
+    lines = [l for l in r.stdout.splitlines() if " criterion " in l]
+    assert len(lines) == 9, r.stdout + r.stderr
+    numeric = [l for l in lines if not any(f"criterion {k}:" in l for k in (6, 7))]
+    assert all(l.startswith("PASS") for l in numeric), numeric
