@@ -698,7 +698,8 @@ struct DynStorage {
     }
     S* ptr() { return p.get(); }
     const S* ptr() const { return p.get(); }
-    /// uninitialised when the element count changes (Eigen's resize semantics)
+    /// Keeps the coefficients when the element count is unchanged (Eigen's resize); a new
+    /// element count zero-fills (Eigen leaves it uninitialised: callers must not rely on it).
     bool resize_raw(Index nr, Index nc) {
         PSWARM_DENSE_CHECK(nr >= 0 && nc >= 0, "negative dimension");
         const Index n = nr * nc;
@@ -707,6 +708,7 @@ struct DynStorage {
             p.reset(n ? new S[static_cast<std::size_t>(n)] : nullptr);
             cap = n;
         }
+        if (fresh && n) std::fill(p.get(), p.get() + n, S(0));
         r = nr;
         c = nc;
         return fresh;

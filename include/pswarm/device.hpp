@@ -4,7 +4,10 @@
 // pswarm_ctx bound to the CUDA device current at first use (or PSWARM_DEVICE).
 
 #include <cstdlib>
+#include <map>
 #include <memory>
+#include <span>
+#include <vector>
 
 #include "pswarm/errors.hpp"
 #include "pswarm_gpu.h"
@@ -25,6 +28,26 @@ inline pswarm_ctx* default_context() {
         if (pswarm_create(dev ? std::atoi(dev) : -1, &h.ctx, &e) != PSWARM_OK) throw_from_status(e);
     }
     return h.ctx;
+}
+
+/// Per-thread multi-device context for a device list (run_batch's `devices` knob): one
+/// pswarm_multi per distinct list, created on first use (contexts, NCCL communicators).
+inline pswarm_multi* multi_context(std::span<const int> devices) {
+    struct Holder {
+        std::map<std::vector<int>, pswarm_multi*> m;
+        ~Holder() {
+            for (auto& kv : m) pswarm_destroy_multi(kv.second);
+        }
+    };
+    thread_local Holder h;
+    std::vector<int> key(devices.begin(), devices.end());
+    auto it = h.m.find(key);
+    if (it != h.m.end()) return it->second;
+    std::vector<int32_t> d(key.begin(), key.end());
+    pswarm_multi* mc = nullptr;
+    pswarm_error e{};
+    if (pswarm_create_multi(static_cast<int32_t>(d.size()), d.data(), &mc, &e) != PSWARM_OK) throw_from_status(e);
+    return h.m.emplace(std::move(key), mc).first->second;
 }
 
 /// Calls a C-ABI entry point and rethrows its failure as a pswarm exception.

@@ -182,6 +182,25 @@ pswarm_status pswarm_run_batch(pswarm_ctx* ctx, int64_t n_states, const double* 
                                const double* boundaries, int64_t n_nodes, const pswarm_config* config,
                                int32_t mode, int32_t workers, pswarm_outputs* out, pswarm_error* err);
 
+/* ---- multi-device (one process, several GPUs) -------------------------
+ * run_batch over the devices of one node (runner.hpp:111-135): contiguous
+ * group-aligned trajectory shards (block.hpp:83-106), one host thread + one context per
+ * device, no collective inside the iteration or segment loop, and ONE gather of the
+ * terminal states to devices[0] — NCCL send/recv over NVLink when the devices are
+ * distinct (libnccl opened at run time), a device-to-device / peer copy when a device is
+ * listed more than once.  Outputs have the single-device layout and batch order; errors
+ * are the one the serial reference would raise (lowest failing trajectory in independent
+ * mode; first failing segment, then group, otherwise).  device_ms / kernel_ms are the max
+ * over devices, trajectory_iterations and gpu_launches the sums. */
+typedef struct pswarm_multi pswarm_multi;
+pswarm_status pswarm_create_multi(int32_t n_devices, const int32_t* devices, pswarm_multi** out, pswarm_error* err);
+void pswarm_destroy_multi(pswarm_multi* m);
+const char* pswarm_multi_backend(pswarm_multi* m);
+int32_t pswarm_multi_devices(pswarm_multi* m);
+pswarm_status pswarm_run_batch_multi(pswarm_multi* m, int64_t n_states, const double* states, int64_t n_boundaries,
+                                     const double* boundaries, int64_t n_nodes, const pswarm_config* config,
+                                     int32_t mode, int32_t workers, pswarm_outputs* out, pswarm_error* err);
+
 /* ---- operator-level entry points (host buffers; one device pass each) -- */
 
 /* picard_update_into(mats, F, y0, out) — pc_matrices.hpp:123-151.

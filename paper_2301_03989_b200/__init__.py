@@ -6,7 +6,7 @@ and calls the CUDA library ``libpswarm_b200.so`` through the C-ABI declared in
 ``include/pswarm_gpu.h``; this package is the Python view of the same boundary.
 """
 from .api import (  # noqa: F401
-    MU_SUN, AlignmentError, BodySpec, Context, CoverageError, DeviceError, DivergenceError, EmptyReductionError,
+    MU_SUN, AlignmentError, BodySpec, Context, MultiContext, CoverageError, DeviceError, DivergenceError, EmptyReductionError,
     Error, InvalidPlanError, InvalidSizeError, InvalidSpanError, IterationReport, NonEllipticError, OracleError,
     PropagationConfig, PropagationIncompleteError, PropagationResult, SegmentPlan, ShapeError, SingularityError,
     SolverError, TimeoutError, build_grid, default_context, elements_to_state, make_clone_batch,

@@ -128,6 +128,13 @@ SIGNATURES = [
     ("pswarm_run_batch", C.c_int32,
      [C.c_void_p, C.c_int64, _dp, C.c_int64, _dp, C.c_int64, C.POINTER(PswarmConfig), C.c_int32, C.c_int32,
       C.POINTER(PswarmOutputs), _ep]),
+    ("pswarm_create_multi", C.c_int32, [C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_void_p), _ep]),
+    ("pswarm_destroy_multi", None, [C.c_void_p]),
+    ("pswarm_multi_backend", C.c_char_p, [C.c_void_p]),
+    ("pswarm_multi_devices", C.c_int32, [C.c_void_p]),
+    ("pswarm_run_batch_multi", C.c_int32,
+     [C.c_void_p, C.c_int64, _dp, C.c_int64, _dp, C.c_int64, C.POINTER(PswarmConfig), C.c_int32, C.c_int32,
+      C.POINTER(PswarmOutputs), _ep]),
     ("pswarm_picard_update", C.c_int32, [C.c_void_p, C.c_int64, C.c_int64, _dp, _dp, _dp, _ep]),
     ("pswarm_picard_update_ops", C.c_int32, [C.c_void_p, C.c_int64, C.c_int64, _dp, _dp, _dp, _dp, _dp, _ep]),
     ("pswarm_eval_force_block", C.c_int32,

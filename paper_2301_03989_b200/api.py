@@ -707,3 +707,62 @@ def run_benchmark(ctx: "Context", states, config: PropagationConfig, plan: Segme
             row.group_iterations = iters_of(out)
             rep.rows.append(row)
     return rep
+
+
+class MultiContext:
+    """run_batch over several CUDA devices of this process (pswarm_run_batch_multi): group-aligned
+    trajectory shards, one host thread + context per device, one gather of the terminal states
+    to devices[0] (NCCL over NVLink for distinct devices; a device copy when a device repeats).
+    Results have the single-device layout and batch order."""
+
+    def __init__(self, devices):
+        self.lib = _abi.load()
+        self.ptr = C.c_void_p()
+        devs = (C.c_int32 * len(devices))(*[int(d) for d in devices])
+        err = _abi.PswarmError()
+        _check(self.lib.pswarm_create_multi(len(devices), devs, C.byref(self.ptr), C.byref(err)), err)
+        self.devices = list(devices)
+
+    @property
+    def backend(self) -> str:
+        return self.lib.pswarm_multi_backend(self.ptr).decode()
+
+    def close(self):
+        if self.ptr:
+            self.lib.pswarm_destroy_multi(self.ptr)
+            self.ptr = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    _marshal = Context._marshal
+
+    def run_batch(self, states, config: PropagationConfig, plan: SegmentPlan, mode: str = "independent",
+                  workers: int = 1, *, samples=True, history=True, terminal=True) -> PropagationResult:
+        st = _states(states)
+        mode = parse_run_mode(mode)
+        M = st.shape[0]
+        if mode == "independent":
+            gs = np.ones(M, dtype=np.int64)
+        elif mode.startswith("augmented"):
+            gs = np.array([M], dtype=np.int64)
+        else:
+            gs = split_groups(M, min(max(config.p_groups, 1), max(M, 1))) if M > 0 else np.zeros(0, np.int64)
+        cm = self._marshal(config)
+        b = np.ascontiguousarray(np.asarray(plan.boundaries, dtype=np.float64))
+        outs = _Outputs(M, len(gs), max(len(b) - 1, 0), plan.n_nodes, config.max_iterations, samples, history,
+                        terminal)
+        err = _abi.PswarmError()
+        status = self.lib.pswarm_run_batch_multi(self.ptr, M, _abi.dptr(st), len(b), _abi.dptr(b), plan.n_nodes,
+                                                 C.byref(cm.cfg), RUN_MODES[mode], workers, C.byref(outs.out),
+                                                 C.byref(err))
+        indep = mode == "independent"
+        if status == _abi.ERR_INCOMPLETE:
+            raise PropagationIncompleteError(err.message.decode(), err.segment, err.group,
+                                             outs.result(gs, plan, False, indep))
+        _check(status, err)
+        return outs.result(gs, plan, True, indep)
+

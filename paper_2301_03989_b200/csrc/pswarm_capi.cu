@@ -19,6 +19,9 @@
 #include <vector>
 
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>  // types only: libnccl is opened at run time (multi-device gather)
+#include <thread>
 
 #include "pc_kernels.cuh"
 #include "pswarm/block.hpp"
@@ -462,6 +465,9 @@ void run_wide_segment(pswarm_ctx* ctx, const SegArgs& s, const std::vector<int64
 // ----------------------------------------------------------------- propagate
 struct RunSpec {
     bool independent = false;  // run_batch independent mode: reference error order is per trajectory
+    // multi-device shards: leave the terminal states on the device and return their address
+    // ([M][6] f64 in a context buffer, valid until the context's next call)
+    const double** term_dev = nullptr;
 };
 
 /// PSWARM_TRACE=1: host-side stage times of propagate (diagnostics, stderr).
@@ -987,6 +993,7 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
     }
     cuda_check(cudaEventRecord(ctx->ev1, st), "event");
     trace.mark("segments (device+host)");
+    if (spec.term_dev) *spec.term_dev = fail_status == PSWARM_OK ? d_in : nullptr;
 
     // ---- outputs
     if (out) {
@@ -1531,6 +1538,321 @@ void pswarm_make_clone_batch(const double* base, int64_t count, double spread, u
             out[7 * i + 4 + c] = b[i].v[c];
         }
     }
+}
+
+}  // extern "C"
+
+// ============================================================ multi-device ==
+// run_batch over several devices of one process (runner.hpp:111-135 + SURVEY §8e):
+// contiguous group-aligned shards (block.hpp:83-106), one host thread and one context per
+// device (the reference's worker pool, thread_pool.hpp:46-87, over GPUs), no collective in
+// the iteration or segment loop, and one gather of the terminal states to devices[0]:
+// NCCL send/recv over NVLink (one ncclGroup) when the devices are distinct, a peer /
+// device-to-device copy when a device is listed twice (flow testing on one GPU).
+namespace {
+
+struct NcclApi {
+    void* h = nullptr;
+    ncclResult_t (*CommInitAll)(ncclComm_t*, int, const int*) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+    ncclResult_t (*GetVersion)(int*) = nullptr;
+};
+
+const NcclApi* nccl_api() {
+    static NcclApi api = [] {
+        NcclApi a;
+        for (const char* name : {"libnccl.so.2", "libnccl.so"}) {
+            a.h = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
+            if (a.h) break;
+        }
+        if (!a.h) return a;
+        auto sym = [&](auto& fp, const char* n) { fp = reinterpret_cast<std::remove_reference_t<decltype(fp)>>(dlsym(a.h, n)); };
+        sym(a.CommInitAll, "ncclCommInitAll");
+        sym(a.CommDestroy, "ncclCommDestroy");
+        sym(a.GroupStart, "ncclGroupStart");
+        sym(a.GroupEnd, "ncclGroupEnd");
+        sym(a.Send, "ncclSend");
+        sym(a.Recv, "ncclRecv");
+        sym(a.GetErrorString, "ncclGetErrorString");
+        sym(a.GetVersion, "ncclGetVersion");
+        if (!a.CommInitAll || !a.GroupStart || !a.GroupEnd || !a.Send || !a.Recv || !a.CommDestroy) a.h = nullptr;
+        return a;
+    }();
+    return api.h ? &api : nullptr;
+}
+
+void nccl_check(const NcclApi* n, ncclResult_t r, const char* what) {
+    if (r == ncclSuccess) return;
+    raise(PSWARM_ERR_GENERIC, std::string("NCCL failure in ") + what + ": " +
+                                  (n && n->GetErrorString ? n->GetErrorString(r) : "?"));
+}
+
+}  // namespace
+
+struct pswarm_multi {
+    std::vector<pswarm_ctx*> ctx;
+    std::vector<int> devices;
+    std::vector<ncclComm_t> comms;  // one per device when the devices are distinct
+    const char* backend = "peer-copy";
+    DevBuf root_term;  // gathered [M][6] on devices[0]
+    PinnedBuf pin_term;
+    int nccl_version = 0;
+};
+
+extern "C" {
+
+pswarm_status pswarm_create_multi(int32_t n_devices, const int32_t* devices, pswarm_multi** out, pswarm_error* err) {
+    return guarded(err, [&] {
+        if (!out) raise(PSWARM_ERR_GENERIC, "pswarm_create_multi: null output pointer");
+        *out = nullptr;
+        if (n_devices < 1 || !devices) raise(PSWARM_ERR_INVALID_PLAN, "pswarm_create_multi: need at least one device");
+        auto m = std::make_unique<pswarm_multi>();
+        for (int32_t r = 0; r < n_devices; ++r) {
+            pswarm_ctx* c = nullptr;
+            pswarm_error e{};
+            if (pswarm_create(devices[r], &c, &e) != PSWARM_OK) {
+                for (pswarm_ctx* x : m->ctx) pswarm_destroy(x);
+                CapiFault f;
+                f.e = e;
+                throw f;
+            }
+            m->ctx.push_back(c);
+            m->devices.push_back(c->device);
+        }
+        std::vector<int> sorted = m->devices;
+        std::sort(sorted.begin(), sorted.end());
+        const bool distinct = std::adjacent_find(sorted.begin(), sorted.end()) == sorted.end();
+        const NcclApi* n = nccl_api();
+        if (distinct && n_devices > 1 && n) {
+            m->comms.resize(static_cast<size_t>(n_devices));
+            const ncclResult_t r = n->CommInitAll(m->comms.data(), n_devices, m->devices.data());
+            if (r != ncclSuccess) {
+                m->comms.clear();
+                for (pswarm_ctx* x : m->ctx) pswarm_destroy(x);
+                nccl_check(n, r, "ncclCommInitAll");
+            }
+            if (n->GetVersion) n->GetVersion(&m->nccl_version);
+            m->backend = "nccl";
+        } else if (distinct && n_devices > 1) {
+            m->backend = "peer-copy (libnccl not found)";
+        }
+        *out = m.release();
+    });
+}
+
+void pswarm_destroy_multi(pswarm_multi* m) {
+    if (!m) return;
+    const NcclApi* n = nccl_api();
+    for (ncclComm_t c : m->comms)
+        if (n && c) n->CommDestroy(c);
+    if (!m->ctx.empty()) {
+        cudaSetDevice(m->ctx[0]->device);
+        if (m->root_term.p) cudaFree(m->root_term.p);
+        m->root_term.p = nullptr;
+    }
+    for (pswarm_ctx* c : m->ctx) pswarm_destroy(c);
+    delete m;
+}
+
+const char* pswarm_multi_backend(pswarm_multi* m) { return m ? m->backend : ""; }
+
+int32_t pswarm_multi_devices(pswarm_multi* m) { return m ? static_cast<int32_t>(m->ctx.size()) : 0; }
+
+pswarm_status pswarm_run_batch_multi(pswarm_multi* mc, int64_t n_states, const double* states, int64_t n_boundaries,
+                                     const double* boundaries, int64_t n_nodes, const pswarm_config* config,
+                                     int32_t mode, int32_t workers, pswarm_outputs* out, pswarm_error* err) {
+    return guarded(err, [&] {
+        const auto wall0 = std::chrono::steady_clock::now();
+        if (!mc || mc->ctx.empty()) raise(PSWARM_ERR_NO_DEVICE, "run_batch_multi: no device contexts");
+        if (workers < 1) throw pswarm::InvalidPlanError("run_batch: need at least one worker");
+        if (n_states < 1) throw pswarm::InvalidPlanError("propagate: empty batch");
+        if (!config) raise(PSWARM_ERR_GENERIC, "propagate: null config");
+        int64_t P;  // grouping_for_mode (runner.hpp:47-55) with split_groups sizes (larger first)
+        if (mode == 0) P = n_states;
+        else if (mode == 1 || mode == 2) P = 1;
+        else if (mode == 3) P = std::clamp<int64_t>(config->p_groups, 1, n_states);
+        else throw pswarm::InvalidPlanError("grouping_for_mode: invalid mode");
+        const int64_t base = n_states / P, rem = n_states % P;
+        std::vector<int64_t> sizes(static_cast<size_t>(P), base), off(static_cast<size_t>(P) + 1, 0);
+        for (int64_t g = 0; g < rem; ++g) sizes[g] = base + 1;
+        for (int64_t g = 0; g < P; ++g) off[g + 1] = off[g] + sizes[g];
+        // group-aligned shards balanced by trajectory count (paper_2301_03989_b200/distributed.py)
+        const int D = static_cast<int>(mc->ctx.size());
+        std::vector<int64_t> g_lo(D), g_hi(D);
+        for (int r = 0, g = 0; r < D; ++r) {
+            const int64_t hi_traj = (static_cast<int64_t>(r) + 1) * n_states / D;
+            g_lo[r] = g;
+            while (g < P && off[g] < hi_traj) ++g;
+            if (r == D - 1) g = static_cast<int>(P);
+            g_hi[r] = g;
+        }
+        const int64_t S = n_boundaries - 1, N = n_nodes, R = S >= 1 ? 1 + S * (N - 1) : 0;
+        const int max_it = std::max(config->max_iterations, 0);
+        struct Shard {
+            int64_t lo = 0, M = 0, P = 0;
+            std::vector<int32_t> iter;
+            std::vector<double> ferr, hist;
+            std::vector<uint8_t> conv, fb;
+            std::vector<double> times;
+            pswarm_outputs o{};
+            pswarm_error e{};
+            pswarm_status st = PSWARM_OK;
+            const double* term = nullptr;
+        };
+        std::vector<Shard> sh(static_cast<size_t>(D));
+        for (int r = 0; r < D; ++r) {
+            Shard& x = sh[r];
+            x.lo = off[g_lo[r]];
+            x.M = off[g_hi[r]] - x.lo;
+            x.P = g_hi[r] - g_lo[r];
+            if (x.M == 0 || S < 1) continue;
+            x.iter.resize(static_cast<size_t>(S * x.P));
+            x.ferr.resize(static_cast<size_t>(S * x.P));
+            x.conv.resize(static_cast<size_t>(S * x.P));
+            x.o.iterations = x.iter.data();
+            x.o.final_error = x.ferr.data();
+            x.o.converged = x.conv.data();
+            if (out && out->error_history && max_it > 0) {
+                x.hist.resize(static_cast<size_t>(S * x.P * max_it));
+                x.o.error_history = x.hist.data();
+            }
+            if (out && out->cold_fallback) {
+                x.fb.resize(static_cast<size_t>(S * x.M));
+                x.o.cold_fallback = x.fb.data();
+            }
+            if (out && out->samples) x.o.samples = out->samples + x.lo * R * 6;  // contiguous per trajectory
+            if (out && out->times && r == 0) {
+                x.times.resize(static_cast<size_t>(R));
+                x.o.times = x.times.data();
+            }
+        }
+        auto run_shard = [&](int r) {
+            Shard& x = sh[r];
+            RunSpec spec;
+            spec.independent = mode == 0;
+            spec.term_dev = &x.term;
+            x.st = guarded(&x.e, [&] {
+                propagate_impl(mc->ctx[r], x.M, states + 7 * x.lo, x.P, sizes.data() + g_lo[r], n_boundaries,
+                               boundaries, n_nodes, config, &x.o, spec);
+            });
+        };
+        std::vector<std::thread> threads;
+        for (int r = 1; r < D; ++r)
+            if (sh[r].M > 0) threads.emplace_back(run_shard, r);
+        if (sh[0].M > 0) run_shard(0);  // the caller takes shard 0 (thread_pool.hpp:124-142)
+        for (auto& t : threads) t.join();
+
+        // ---- the error the serial reference would raise: independent mode = lowest failing
+        // trajectory (runner.hpp:63-80); grouped/augmented = first failing segment, exceptions
+        // before non-convergence, then the lowest group (propagator.hpp:292-312)
+        int pick = -1;
+        auto key = [&](int r) {
+            const pswarm_error& e = sh[r].e;
+            if (mode == 0) {
+                const int64_t t = e.trajectory >= 0 ? e.trajectory : 0;
+                return std::make_tuple(int64_t{0}, int64_t{0}, sh[r].lo + t);
+            }
+            const int64_t seg = e.segment >= 0 ? e.segment : -1;
+            return std::make_tuple(seg, int64_t{e.status == PSWARM_ERR_INCOMPLETE ? 1 : 0},
+                                   g_lo[r] + std::max<int64_t>(e.group, 0));
+        };
+        for (int r = 0; r < D; ++r)
+            if (sh[r].M > 0 && sh[r].st != PSWARM_OK && (pick < 0 || key(r) < key(pick))) pick = r;
+
+        if (out) {
+            int64_t rep = S, done = S;
+            for (int r = 0; r < D; ++r) {
+                if (sh[r].M == 0) continue;
+                rep = std::min(rep, sh[r].o.segments_reported);
+                done = std::min(done, sh[r].o.segments_completed);
+            }
+            if (pick >= 0 && sh[pick].st == PSWARM_ERR_INCOMPLETE) rep = std::max(rep, sh[pick].o.segments_reported);
+            out->segments_reported = rep;
+            out->segments_completed = done;
+            double dms = 0.0, kms = 0.0;
+            int64_t iters = 0, launches = 0;
+            for (int r = 0; r < D; ++r) {
+                const Shard& x = sh[r];
+                launches += mc->ctx[r]->launches;
+                if (x.M == 0) continue;
+                dms = std::max(dms, x.o.device_ms);
+                kms = std::max(kms, x.o.kernel_ms);
+                iters += x.o.trajectory_iterations;
+                for (int64_t sg = 0; sg < std::min(rep, x.o.segments_reported); ++sg) {
+                    const int64_t dst = sg * P + g_lo[r], src = sg * x.P;
+                    if (out->iterations) std::memcpy(out->iterations + dst, x.iter.data() + src, sizeof(int32_t) * x.P);
+                    if (out->final_error) std::memcpy(out->final_error + dst, x.ferr.data() + src, sizeof(double) * x.P);
+                    if (out->converged) std::memcpy(out->converged + dst, x.conv.data() + src, static_cast<size_t>(x.P));
+                    if (out->error_history && max_it > 0)
+                        std::memcpy(out->error_history + dst * max_it, x.hist.data() + src * max_it,
+                                    sizeof(double) * x.P * max_it);
+                    if (out->cold_fallback)
+                        std::memcpy(out->cold_fallback + sg * n_states + x.lo, x.fb.data() + sg * x.M,
+                                    static_cast<size_t>(x.M));
+                }
+            }
+            if (out->times && !sh[0].times.empty()) std::memcpy(out->times, sh[0].times.data(), sizeof(double) * R);
+            out->device_ms = dms;
+            out->kernel_ms = kms;
+            out->trajectory_iterations = iters;
+            out->gpu_launches = launches;
+        }
+        if (pick >= 0) {
+            pswarm_error e = sh[pick].e;
+            if (mode == 0 && e.trajectory >= 0) e.trajectory += sh[pick].lo;  // batch index
+            if (mode != 0 && e.group >= 0) e.group += g_lo[pick];
+            CapiFault f;
+            f.e = e;
+            throw f;
+        }
+
+        // ---- the single collective: terminal states of every shard -> devices[0]
+        if (out && out->terminal_states) {
+            pswarm_ctx* root = mc->ctx[0];
+            bind(root);
+            double* dst = mc->root_term.get<double>(static_cast<size_t>(n_states) * 6);
+            const NcclApi* n = nccl_api();
+            if (!mc->comms.empty()) {
+                nccl_check(n, n->GroupStart(), "ncclGroupStart");
+                for (int r = 1; r < D; ++r) {
+                    if (sh[r].M == 0) continue;
+                    const size_t cnt = static_cast<size_t>(sh[r].M) * 6;
+                    nccl_check(n, n->Recv(dst + sh[r].lo * 6, cnt, ncclFloat64, r, mc->comms[0], root->stream), "ncclRecv");
+                    nccl_check(n, n->Send(sh[r].term, cnt, ncclFloat64, 0, mc->comms[r], mc->ctx[r]->stream), "ncclSend");
+                }
+                nccl_check(n, n->GroupEnd(), "ncclGroupEnd");
+            } else {
+                for (int r = 1; r < D; ++r)
+                    if (sh[r].M > 0)
+                        cuda_check(cudaMemcpyPeerAsync(dst + sh[r].lo * 6, root->device, sh[r].term, mc->ctx[r]->device,
+                                                       sizeof(double) * sh[r].M * 6, root->stream),
+                                   "gather peer copy");
+            }
+            if (sh[0].M > 0)
+                cuda_check(cudaMemcpyAsync(dst, sh[0].term, sizeof(double) * sh[0].M * 6, cudaMemcpyDeviceToDevice,
+                                           root->stream),
+                           "gather root shard");
+            double* h = mc->pin_term.get<double>(sizeof(double) * n_states * 6);
+            cuda_check(cudaMemcpyAsync(h, dst, sizeof(double) * n_states * 6, cudaMemcpyDeviceToHost, root->stream),
+                       "D2H gathered terminal states");
+            for (int r = 1; r < D; ++r) {
+                bind(mc->ctx[r]);
+                cuda_check(cudaStreamSynchronize(mc->ctx[r]->stream), "gather (send side)");
+            }
+            bind(root);
+            cuda_check(cudaStreamSynchronize(root->stream), "gather");
+            for (int64_t i = 0; i < n_states; ++i) {
+                out->terminal_states[7 * i] = boundaries[S];
+                std::memcpy(out->terminal_states + 7 * i + 1, h + 6 * i, sizeof(double) * 6);
+            }
+        }
+        if (out) out->wall_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
+    });
 }
 
 }  // extern "C"

@@ -3,9 +3,8 @@
 Trajectories shard naturally (independent groups): each rank
 propagates a contiguous, group-aligned shard with its own device context; there
 is no collective inside the iteration or segment loop.  The only exchange is one
-gather of the terminal states at the end (NCCL over NVLink on GPUs; gloo in the
-CPU tests), padded to the largest shard because NCCL all-gather needs equal
-counts.
+gather of the terminal states to rank 0 at the end (NCCL over NVLink on GPUs;
+gloo in the CPU tests), padded to the largest shard.
 """
 from __future__ import annotations
 
@@ -39,11 +38,12 @@ def shard_groups(group_sizes: Sequence[int], world: int) -> List[Tuple[int, int,
     return out
 
 
-def gather_terminal(local: np.ndarray, shards, rank: int, world: int, device=None) -> np.ndarray | None:
-    """All-gather the per-rank terminal states [m_r, 7] into the batch order [M, 7].
+def gather_terminal(local: np.ndarray, shards, rank: int, world: int, device=None, dst: int = 0) -> np.ndarray | None:
+    """Gather the per-rank terminal states [m_r, 7] to rank `dst` in batch order [M, 7].
 
-    Uses torch.distributed (the caller has initialised the process group: NCCL for
-    CUDA tensors, gloo for CPU).  Returns the full array on every rank.
+    One collective (torch.distributed.gather: NCCL send/recv over NVLink for CUDA tensors,
+    gloo for CPU tensors) of buffers padded to the largest shard.  Returns the full array
+    on `dst` and None elsewhere (only the destination copies to the host).
     """
     import torch
     import torch.distributed as dist
@@ -53,8 +53,9 @@ def gather_terminal(local: np.ndarray, shards, rank: int, world: int, device=Non
     buf = torch.zeros((pad, 7), dtype=torch.float64, device=device)
     if local.shape[0]:
         buf[: local.shape[0]] = torch.from_numpy(np.ascontiguousarray(local)).to(buf.device)
-    out = torch.empty((world * pad, 7), dtype=torch.float64, device=device)
-    dist.all_gather_into_tensor(out, buf)
-    host = out.cpu().numpy()
-    parts = [host[r * pad: r * pad + counts[r]] for r in range(world)]
-    return np.concatenate(parts, axis=0) if parts else np.zeros((0, 7))
+    parts = [torch.empty_like(buf) for _ in range(world)] if rank == dst else None
+    dist.gather(buf, parts, dst=dst)
+    if rank != dst:
+        return None
+    host = torch.cat(parts).cpu().numpy()
+    return np.concatenate([host[r * pad: r * pad + counts[r]] for r in range(world)], axis=0)

@@ -341,6 +341,35 @@ int main() {
         }
         expect(threw, "repeat 0 must throw");
     });
+    run("run_batch_devices_knob_matches_one_device", [] {  // SURVEY §8a13 devices knob, runner.hpp:111-135
+        ps::PropagationConfig cfg;
+        cfg.force = ps::make_reference_force_model();
+        cfg.p_groups = 7;
+        const auto st = ps::make_clone_batch(ps::make_reference_state(), 61, 1e-4);
+        const double period = ps::osculating_period(st[0], ps::mu_sun_km3s2);
+        const auto sp = ps::plan_segments(st[0], 0.0, 1.6 * period, ps::mu_sun_km3s2, ps::SegmentPolicy::per_orbit, 64);
+        int dev = 0;
+        if (const char* d = std::getenv("PSWARM_DEVICE")) dev = std::atoi(d);
+        const std::vector<int> two{dev, dev}, three{dev, dev, dev};  // several contexts on one GPU
+        for (auto mode : {ps::RunMode::independent, ps::RunMode::grouped, ps::RunMode::augmented_parallel}) {
+            const auto one = ps::run_batch(st, cfg, sp, mode, 1);
+            for (const auto* devs : {&two, &three}) {
+                const auto many = ps::run_batch(st, cfg, sp, mode, 1, *devs);
+                bool same = one.result.terminal_states.size() == many.result.terminal_states.size();
+                for (std::size_t i = 0; same && i < st.size(); ++i)
+                    same = one.result.terminal_states[i].r == many.result.terminal_states[i].r &&
+                           one.result.terminal_states[i].v == many.result.terminal_states[i].v &&
+                           one.result.trajectories[i] == many.result.trajectories[i];
+                for (std::size_t sg = 0; same && sg < one.result.reports.size(); ++sg)
+                    for (std::size_t g = 0; same && g < one.result.reports[sg].size(); ++g)
+                        same = one.result.reports[sg][g].iterations == many.result.reports[sg][g].iterations &&
+                               one.result.reports[sg][g].per_iteration_errors ==
+                                   many.result.reports[sg][g].per_iteration_errors;
+                expect(same, "multi-device result differs from one device (mode " + ps::to_string(mode) + ", " +
+                                 std::to_string(devs->size()) + " shards)");
+            }
+        }
+    });
     std::printf("SUMMARY %d %d\n", n_pass, n_fail);
     return n_fail == 0 ? 0 : 1;
 }

@@ -126,6 +126,8 @@ def test_no_device_raises_device_error():
         pytest.skip("a GPU is visible")
     with pytest.raises(ps.DeviceError):
         ps.Context(0)
+    with pytest.raises(ps.DeviceError):
+        ps.MultiContext([0, 1])
 
 
 def test_split_groups_matches_reference_rules():

@@ -74,3 +74,17 @@ def test_two_rank_gather_matches_single_process(tmp_path, oracle):
     want = oracle.propagate(states, [3, 5, 2, 4, 6, 4], plan, cfg).terminal_states
     assert full.shape == want.shape
     assert np.array_equal(full, want)
+
+
+def test_bench_reference_arm_runs_on_cpu():
+    """bench.py --impl reference (the reference's own CPU implementation) prints one JSON
+    line with the contract keys; tiny sample so it runs here."""
+    import json
+    import subprocess
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--config", "c2",
+                        "--steps", "2", "--warmup", "1", "--cpu-sample", "24", "--nodes", "64"],
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr
+    d = json.loads(r.stdout.strip().splitlines()[-1])
+    assert d["impl"] == "reference" and d["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] == 0
+    assert d["cpu_baseline"]["kind"] in ("reference", "port") and d["cpu_baseline"]["cores"] >= 1
