@@ -1566,10 +1566,12 @@ struct NcclApi {
 const NcclApi* nccl_api() {
     static NcclApi api = [] {
         NcclApi a;
-        for (const char* name : {"libnccl.so.2", "libnccl.so"}) {
-            a.h = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
-            if (a.h) break;
-        }
+        // an NCCL already in the process (e.g. the one PyTorch links) first: loading a second
+        // libnccl.so.2 would shadow it for libraries that resolve it later by soname
+        a.h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        if (!a.h)
+            if (const char* p = std::getenv("PSWARM_NCCL_LIB")) a.h = dlopen(p, RTLD_NOW | RTLD_LOCAL);
+        if (!a.h) a.h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
         if (!a.h) return a;
         auto sym = [&](auto& fp, const char* n) { fp = reinterpret_cast<std::remove_reference_t<decltype(fp)>>(dlsym(a.h, n)); };
         sym(a.CommInitAll, "ncclCommInitAll");
@@ -1627,8 +1629,8 @@ pswarm_status pswarm_create_multi(int32_t n_devices, const int32_t* devices, psw
         std::vector<int> sorted = m->devices;
         std::sort(sorted.begin(), sorted.end());
         const bool distinct = std::adjacent_find(sorted.begin(), sorted.end()) == sorted.end();
-        const NcclApi* n = nccl_api();
-        if (distinct && n_devices > 1 && n) {
+        const NcclApi* n = distinct && n_devices > 1 ? nccl_api() : nullptr;  // loaded only when used
+        if (n) {
             m->comms.resize(static_cast<size_t>(n_devices));
             const ncclResult_t r = n->CommInitAll(m->comms.data(), n_devices, m->devices.data());
             if (r != ncclSuccess) {
@@ -1647,7 +1649,7 @@ pswarm_status pswarm_create_multi(int32_t n_devices, const int32_t* devices, psw
 
 void pswarm_destroy_multi(pswarm_multi* m) {
     if (!m) return;
-    const NcclApi* n = nccl_api();
+    const NcclApi* n = m->comms.empty() ? nullptr : nccl_api();
     for (ncclComm_t c : m->comms)
         if (n && c) n->CommDestroy(c);
     if (!m->ctx.empty()) {
@@ -1816,8 +1818,8 @@ pswarm_status pswarm_run_batch_multi(pswarm_multi* mc, int64_t n_states, const d
             pswarm_ctx* root = mc->ctx[0];
             bind(root);
             double* dst = mc->root_term.get<double>(static_cast<size_t>(n_states) * 6);
-            const NcclApi* n = nccl_api();
             if (!mc->comms.empty()) {
+                const NcclApi* n = nccl_api();
                 nccl_check(n, n->GroupStart(), "ncclGroupStart");
                 for (int r = 1; r < D; ++r) {
                     if (sh[r].M == 0) continue;
