@@ -9,6 +9,8 @@ from __future__ import annotations
 
 import json
 import math
+import os
+import re
 from dataclasses import dataclass, field
 from typing import List
 
@@ -27,12 +29,44 @@ def format_double(x: float) -> str:
     return format(float(x), ".17g")
 
 
+# std::from_chars(double, chars_format::general) grammar (io.hpp:35-48): optional '-', decimal
+# mantissa, optional exponent, or inf / infinity / nan[(chars)] — no '+', no '_', no hex
+_NUMBER = re.compile(r"-?(?:(?:[0-9]+\.?[0-9]*|\.[0-9]+)(?:[eE][+-]?[0-9]+)?|(?i:inf(?:inity)?|nan(?:\([0-9A-Za-z_]*\))?))")
+
+
 def _parse_double(text: str, ctx: str) -> float:
-    t = text.strip(" \t\r")
+    t = text.lstrip(" \t").rstrip(" \t\r")  # io.hpp:36-43
+    if not _NUMBER.fullmatch(t):
+        raise ParseError(f"{ctx}: cannot parse number '{t}'")
+    return float(t.split("(")[0]) if t.lower().lstrip("-").startswith("nan") else float(t)
+
+
+def _open_output(path):
+    """open_output (io.hpp:75-84): creates the parent directories; failures raise ParseError."""
+    path = os.fspath(path)
     try:
-        return float(t)
-    except ValueError:
-        raise ParseError(f"{ctx}: cannot parse number '{t}'") from None
+        parent = os.path.dirname(path)
+        if parent:
+            os.makedirs(parent, exist_ok=True)
+        return open(path, "w")
+    except OSError:
+        raise ParseError(f"cannot open '{path}' for writing") from None
+
+
+def _json_value(x):
+    """nlohmann::json serialises non-finite doubles as null (io.hpp:479-480 dump)."""
+    if isinstance(x, float) and not math.isfinite(x):
+        return None
+    if isinstance(x, dict):
+        return {k: _json_value(v) for k, v in x.items()}
+    if isinstance(x, (list, tuple)):
+        return [_json_value(v) for v in x]
+    return x
+
+
+def _dump_json(root, f):
+    json.dump(_json_value(root), f, indent=2, allow_nan=False)
+    f.write("\n")
 
 
 def read_batch_csv(path) -> np.ndarray:
@@ -66,7 +100,7 @@ def read_batch_csv(path) -> np.ndarray:
 def write_batch_csv(path, states) -> None:
     """write_batch_csv (io.hpp:162-178)."""
     st = np.asarray(states, dtype=np.float64).reshape(-1, 7)
-    with open(path, "w") as f:
+    with _open_output(path) as f:
         f.write(BATCH_CSV_HEADER + "\n")
         for s in st:
             f.write(",".join(format_double(x) for x in s) + "\n")
@@ -160,9 +194,8 @@ def write_system_json(path, model: SystemModel) -> None:
                                 "coeffs_y": list(map(float, cy)), "coeffs_z": list(map(float, cz))}
                                for t0, t1, cx, cy, cz in b.segments]
         root["bodies"].append(jb)
-    with open(path, "w") as f:
-        json.dump(root, f, indent=2)
-        f.write("\n")
+    with _open_output(path) as f:
+        _dump_json(root, f)
 
 
 # ---------------------------------------------------------------------------
@@ -282,7 +315,7 @@ def write_samples_csv(path, result, oracle_errors=None) -> None:
     if traj is None:
         raise ParseError("write_samples_csv: the result carries no node samples (run with samples=True)")
     times = np.asarray(result.times)
-    with open(path, "w") as f:
+    with _open_output(path) as f:
         f.write("trajectory_id,node_index,t_s,x_km,y_km,z_km,vx_kms,vy_kms,vz_kms")
         f.write(",oracle_rel_err\n" if oracle_errors is not None else "\n")
         for i in range(traj.shape[0]):
@@ -309,14 +342,13 @@ def write_report_json(path, result, metadata=None, oracle_max_per_trajectory=Non
     if oracle_max_per_trajectory is not None:
         v = [float(x) for x in oracle_max_per_trajectory]
         root["oracle_check"] = {"per_trajectory_max": v, "max": max(v)}
-    with open(path, "w") as f:
-        json.dump(root, f, indent=2)
-        f.write("\n")
+    with _open_output(path) as f:
+        _dump_json(root, f)
 
 
 def write_error_history_csv(path, result) -> None:
     """write_error_history_csv (io.hpp:488-503); needs a run with history=True."""
-    with open(path, "w") as f:
+    with _open_output(path) as f:
         f.write("segment,group,iteration,error\n")
         for seg, row in enumerate(result.reports):
             for g in range(len(row)):
@@ -326,7 +358,7 @@ def write_error_history_csv(path, result) -> None:
 
 def write_benchmark_csv(path, report) -> None:
     """write_benchmark_csv (io.hpp:505-515) of api.run_benchmark's report."""
-    with open(path, "w") as f:
+    with _open_output(path) as f:
         f.write("mode,threads,groups,wall_time_s,speedup,max_iterations,max_discrepancy\n")
         for r in report.rows:
             f.write(f"{r.mode},{r.threads},{r.groups},{format_double(r.wall_time_s)},{format_double(r.speedup)},"

@@ -93,3 +93,37 @@ def test_benchmark_csv_and_summary(tmp_path):
     assert float(rows[2][6]) == 1.5e-13  # 17 significant digits (io.hpp format_double)
     s = io.benchmark_summary(rep)
     assert s.startswith("machine: test, median of 2 run(s)\n") and "augmented_parallel" in s.splitlines()[3]
+
+
+def test_writers_create_parent_dirs_and_map_open_failures(tmp_path, result):
+    """open_output (io.hpp:75-84): parent directories are created; an unopenable path is a
+    ParseError 'cannot open ... for writing'."""
+    p = tmp_path / "a" / "b" / "report.json"
+    io.write_report_json(p, result)
+    assert p.exists()
+    blocker = tmp_path / "file"
+    blocker.write_text("x")
+    with pytest.raises(io.ParseError, match="cannot open .* for writing"):
+        io.write_samples_csv(blocker / "samples.csv", result)
+
+
+def test_report_json_non_finite_is_null(tmp_path, result):
+    """nlohmann::json writes non-finite doubles as null; the file stays valid JSON."""
+    p = tmp_path / "r.json"
+    io.write_report_json(p, result, metadata={"inf": float("inf"), "nan": float("nan"), "ok": 1.5})
+    text = p.read_text()
+    assert "Infinity" not in text and "NaN" not in text
+    d = json.loads(text)
+    assert d["metadata"] == {"inf": None, "nan": None, "ok": 1.5}
+
+
+@pytest.mark.parametrize("text", ["+1", "1_0", "0x10", "1e", "", "e5", "1.2.3", "1 2"])
+def test_number_grammar_is_from_chars(text):
+    """parse_double (io.hpp:35-48) = std::from_chars: no '+', no '_', no hex."""
+    with pytest.raises(io.ParseError, match="cannot parse number"):
+        io._parse_double(text, "ctx")
+
+
+def test_number_grammar_accepts_from_chars_forms():
+    for t, v in (("-1.5e3", -1500.0), (" 2.0\r", 2.0), (".5", 0.5), ("5.", 5.0), ("-inf", float("-inf"))):
+        assert io._parse_double(t, "ctx") == v
