@@ -11,6 +11,7 @@
 #include <optional>
 #include <span>
 #include <string>
+#include <thread>
 #include <utility>
 #include <vector>
 
@@ -248,48 +249,96 @@ struct ConfigMarshal {
 };
 
 /// Host buffers of one device call and their conversion into a PropagationResult.
+/// Per-thread, grow-only page-locked staging for the large per-call outputs (node samples,
+/// error histories, terminal states): the device writes them at DMA speed and no call pays
+/// fresh-page faults for megabytes of result buffers.  to_result copies out of it, so it is
+/// free again when a propagate / run_batch call returns.
+struct PinnedScratch {
+    void* p = nullptr;
+    std::size_t cap = 0;
+    template <typename T>
+    T* get(std::size_t count) {
+        const std::size_t bytes = std::max<std::size_t>(count * sizeof(T), 64);
+        if (bytes > cap) {
+            pswarm_pinned_free(p);
+            p = pswarm_pinned_alloc(bytes);
+            cap = p ? bytes : 0;
+            if (!p) throw Error("pswarm_pinned_alloc: cannot allocate " + std::to_string(bytes) + " bytes");
+        }
+        return static_cast<T*>(p);
+    }
+    PinnedScratch() = default;
+    PinnedScratch(const PinnedScratch&) = delete;
+    PinnedScratch& operator=(const PinnedScratch&) = delete;
+    ~PinnedScratch() { pswarm_pinned_free(p); }
+};
+inline PinnedScratch& scratch(int which) {
+    thread_local PinnedScratch s[3];
+    return s[which];
+}
+
 struct OutputBuffers {
     Index M, P, S, R, max_it;
-    std::vector<double> terminal, samples, times, final_err, history;
+    double *terminal, *samples, *history;  // pinned scratch (see PinnedScratch)
+    std::vector<double> times, final_err;
     std::vector<int32_t> iters;
     std::vector<uint8_t> conv, fallback;
     pswarm_outputs out{};
 
     OutputBuffers(Index m, Index p, Index s, Index n, int max_iterations)
         : M(m), P(p), S(s), R(1 + s * (n - 1)), max_it(std::max(max_iterations, 0)) {
-        terminal.assign(static_cast<std::size_t>(M * 7), 0.0);
-        samples.assign(static_cast<std::size_t>(M * R * 6), 0.0);
+        terminal = scratch(0).get<double>(static_cast<std::size_t>(M * 7));
+        samples = scratch(1).get<double>(static_cast<std::size_t>(M * R * 6));
+        history = scratch(2).get<double>(static_cast<std::size_t>(S * P * std::max<Index>(max_it, 1)));
         times.assign(static_cast<std::size_t>(R), 0.0);
         iters.assign(static_cast<std::size_t>(S * P), 0);
         final_err.assign(static_cast<std::size_t>(S * P), 0.0);
         conv.assign(static_cast<std::size_t>(S * P), 0);
-        history.assign(static_cast<std::size_t>(S * P * std::max<Index>(max_it, 1)), 0.0);
         fallback.assign(static_cast<std::size_t>(S * M), 0);
-        out.terminal_states = terminal.data();
-        out.samples = samples.data();
+        out.terminal_states = terminal;
+        out.samples = samples;
         out.times = times.data();
         out.iterations = iters.data();
         out.final_error = final_err.data();
         out.converged = conv.data();
-        out.error_history = history.data();
+        out.error_history = history;
         out.cold_fallback = fallback.data();
     }
 
+    /// `workers` host threads assemble the per-trajectory sample matrices (the reference's
+    /// worker count is a host thread count; on the device path the host work left is this
+    /// copy of M x R x 6 doubles out of the pinned staging).
     PropagationResult to_result(const GroupingPlan& plan, const SegmentPlan& sp, bool complete,
-                                bool independent_warnings) const {
+                                bool independent_warnings, unsigned workers = 1) const {
         PropagationResult r;
         r.plan = plan;
         r.segments = sp;
         r.times.resize(R);
         for (Index j = 0; j < R; ++j) r.times[j] = times[j];
         r.trajectories.reserve(static_cast<std::size_t>(M));
-        for (Index i = 0; i < M; ++i) {
-            Mat t(R, state_dim);
-            std::copy(samples.begin() + i * R * 6, samples.begin() + (i + 1) * R * 6, t.data());
-            r.trajectories.push_back(std::move(t));
+        // rows of completed segments only: a failed segment's rows stay zero, as the
+        // reference appends a segment's samples after it converged (propagator.hpp:314-330)
+        const Index done = out.segments_completed;
+        const Index rows = complete ? R : (done > 0 && S > 0 ? 1 + done * ((R - 1) / S) : 0);
+        r.trajectories.resize(static_cast<std::size_t>(M));
+        auto fill = [&](Index lo, Index hi) {
+            for (Index i = lo; i < hi; ++i) {
+                Mat t(R, state_dim);
+                std::copy(samples + i * R * 6, samples + (i * R + rows) * 6, t.data());
+                r.trajectories[static_cast<std::size_t>(i)] = std::move(t);
+            }
+        };
+        const Index W = std::clamp<Index>(static_cast<Index>(workers), 1, std::max<Index>(M, 1));
+        if (W == 1 || M * R * 6 < (Index{1} << 16)) {
+            fill(0, M);
+        } else {  // contiguous chunks, as the reference pool's parallel_chunks (thread_pool.hpp:44-62)
+            std::vector<std::thread> pool;
+            for (Index w = 1; w < W; ++w) pool.emplace_back(fill, M * w / W, M * (w + 1) / W);
+            fill(0, M / W);
+            for (auto& t : pool) t.join();
         }
         if (complete)
-            for (Index i = 0; i < M; ++i) r.terminal_states.push_back(unpack_state(terminal.data() + 7 * i));
+            for (Index i = 0; i < M; ++i) r.terminal_states.push_back(unpack_state(terminal + 7 * i));
         for (Index s = 0; s < out.segments_reported; ++s) {
             std::vector<IterationReport> seg(static_cast<std::size_t>(P));
             for (Index g = 0; g < P; ++g) {
@@ -321,7 +370,8 @@ struct OutputBuffers {
 inline PropagationResult propagate(std::span<const StateVector> states, const GroupingPlan& plan,
                                    const SegmentPlan& segment_plan, const PropagationConfig& config,
                                    const ExecutionPolicy& exec = {}) {
-    (void)exec;
+    // the pool size of the reference (propagator.hpp:228-236) sizes the host-side assembly
+    const unsigned workers = std::max({exec.group_workers, exec.inner_workers, 1u});
     detail::ConfigMarshal cm(config);
     const auto packed = detail::pack_states(states);
     const Index S = std::max<Index>(segment_plan.segments(), 0);
@@ -333,11 +383,11 @@ inline PropagationResult propagate(std::span<const StateVector> states, const Gr
                          plan.group_sizes.data(), static_cast<int64_t>(segment_plan.boundaries.size()),
                          segment_plan.boundaries.data(), segment_plan.n_nodes, &cm.cfg, &ob.out, &e);
     if (st == PSWARM_ERR_INCOMPLETE) {
-        auto partial = std::make_shared<PropagationResult>(ob.to_result(plan, segment_plan, false, false));
+        auto partial = std::make_shared<PropagationResult>(ob.to_result(plan, segment_plan, false, false, workers));
         throw PropagationIncompleteError(e.message, e.segment, e.group, std::move(partial));
     }
     if (st != PSWARM_OK) throw_from_status(e);
-    return ob.to_result(plan, segment_plan, true, false);
+    return ob.to_result(plan, segment_plan, true, false, workers);
 }
 
 }  // namespace pswarm

@@ -159,7 +159,7 @@ pswarm_status pswarm_set_option(pswarm_ctx* ctx, const char* key, int64_t value)
 pswarm_status pswarm_get_phase_cycles(pswarm_ctx* ctx, uint64_t* out, int32_t n);
 
 /* Diagnostics: name of the solver kernel the last propagate/run_batch call used
- * ("k_pc_ws_fold", "k_pc_uni", "k_pc_ws", "k_pc_segment", "k_wide_iter" or "" before the
+ * ("k_pc_ws_fold", "k_pc_uni", "k_pc_ws", "k_pc_segment" or "" before the
  * first call). */
 const char* pswarm_last_kernel(pswarm_ctx* ctx);
 
@@ -267,6 +267,11 @@ pswarm_status pswarm_build_grid(int64_t n_nodes, double t_start, double t_end, d
 /* make_clone_batch (synthetic.hpp:66-83), bit-exact splitmix64 stream; out [count][7]. */
 void pswarm_make_clone_batch(const double* base, int64_t count, double relative_spread, uint64_t seed,
                              double* out);
+
+/* Page-locked host memory for result buffers (no reference analogue): device->host copies
+ * into it run at DMA speed and it is never re-faulted between calls.  NULL on failure. */
+void* pswarm_pinned_alloc(size_t bytes);
+void pswarm_pinned_free(void* p);
 
 #ifdef __cplusplus
 }

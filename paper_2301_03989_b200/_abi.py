@@ -151,6 +151,8 @@ SIGNATURES = [
      [_dp, C.c_double, C.c_double, C.c_double, C.c_int32, C.c_int64, C.c_double, C.c_int64, _dp, _ip, _ep]),
     ("pswarm_build_grid", C.c_int32, [C.c_int64, C.c_double, C.c_double, _dp, _dp, _ep]),
     ("pswarm_make_clone_batch", None, [_dp, C.c_int64, C.c_double, C.c_uint64, _dp]),
+    ("pswarm_pinned_alloc", C.c_void_p, [C.c_size_t]),
+    ("pswarm_pinned_free", None, [C.c_void_p]),
 ]
 
 _lib = None

@@ -178,11 +178,11 @@ __global__ void __launch_bounds__(MAXT, 1) k_pc_segment(const SegArgs a) {
                 for (int gi = g0; gi < g1; ++gi) {
                     int lg = 0;
                     while (st.grp_id[lg] >= 0) ++lg;
-                    const int off = static_cast<int>(a.group_off[gi]);
-                    const int size = static_cast<int>(a.group_off[gi + 1]) - off;
-                    st.grp_id[lg] = gi;
+                    int off, size, gid;
+                    claim_group(a, gi, off, size, gid);
+                    st.grp_id[lg] = gid;
                     st.grp_size[lg] = size;
-                    st.grp_iter[lg] = 0;
+                    st.grp_iter[lg] = start_iteration(a, off);
                     int t = 0;
                     for (int mbr = 0; mbr < size; ++mbr) {
                         while ((am >> t) & 1) ++t;
@@ -235,20 +235,25 @@ __global__ void __launch_bounds__(MAXT, 1) k_pc_segment(const SegArgs a) {
                 const double r[3] = {st.y0[t][0], st.y0[t][1], st.y0[t][2]};
                 const double v[3] = {st.y0[t][3], st.y0[t][4], st.y0[t][5]};
                 double ro[3] = {r[0], r[1], r[2]}, vo[3] = {v[0], v[1], v[2]};
-                if (!a.cold_start) {
-                    const int chk = conic_check(r, v, a.fd.central_mu);
-                    if (chk == CONIC_ZERO_RADIUS) {
-                        atomicMin(&st.warm_key[t], j * 4 + CONIC_ZERO_RADIUS);
-                    } else if (chk == CONIC_OK) {
-                        double mf, ef;
-                        if (kepler_propagate(r, v, a.fd.central_mu, a.times[j] - a.epoch, ro, vo, &mf, &ef) !=
-                            CONIC_OK)
-                            atomicMin(&st.warm_key[t], j * 4 + CONIC_SOLVER);
+                if (start_iteration(a, st.slot_traj[t]) > 0) {  // wide-group round: resume the saved iterate
+                    resume_node(a, st.slot_traj[t], j, ro, vo);
+                } else {
+                    if (!a.cold_start) {
+                        const int chk = conic_check(r, v, a.fd.central_mu);
+                        if (chk == CONIC_ZERO_RADIUS) {
+                            atomicMin(&st.warm_key[t], j * 4 + CONIC_ZERO_RADIUS);
+                        } else if (chk == CONIC_OK) {
+                            double mf, ef;
+                            if (kepler_propagate(r, v, a.fd.central_mu, a.times[j] - a.epoch, ro, vo, &mf, &ef) !=
+                                CONIC_OK)
+                                atomicMin(&st.warm_key[t], j * 4 + CONIC_SOLVER);
+                        }
+                        if (j == 0 && a.cold_fallback)
+                            a.cold_fallback[st.slot_traj[t]] = (chk == CONIC_NON_ELLIPTIC) ? 1 : 0;
                     }
-                    if (j == 0 && a.cold_fallback)
-                        a.cold_fallback[st.slot_traj[t]] = (chk == CONIC_NON_ELLIPTIC) ? 1 : 0;
+                    if (a.hot)
+                        hot_start_node(a.hot + (static_cast<size_t>(st.slot_traj[t]) * N + j) * 6, a.hot_apply, ro, vo);
                 }
-                if (a.hot) hot_start_node(a.hot + (static_cast<size_t>(st.slot_traj[t]) * N + j) * 6, a.hot_apply, ro, vo);
 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
                     ybuf[yidx(j, c, t)] = ro[c];
@@ -523,10 +528,10 @@ __global__ void __launch_bounds__(MAXT, 1) k_pc_segment(const SegArgs a) {
                         fl->column = nf_best % (6LL * size);
                         retire = true;
                     } else {
-                        if (a.rep_hist) a.rep_hist[static_cast<size_t>(gid) * a.max_it + (it - 1)] = gerr;
-                        if (gerr <= a.tol) {
+                        if (a.rep_hist) a.rep_hist[static_cast<size_t>(gid) * a.hist_stride + (it - 1)] = gerr;
+                        if (gerr <= a.tol && may_converge(a, gid, it)) {
                             retire = ok = conv = true;
-                        } else if (it >= a.max_it) {
+                        } else if (at_cap(a, gid, it)) {
                             retire = ok = true;
                         }
                     }
@@ -565,6 +570,8 @@ __global__ void __launch_bounds__(MAXT, 1) k_pc_segment(const SegArgs a) {
                 }
                 if (a.hot)
                     for (int c = 0; c < 6; ++c) hot_retire_node(a.hot + (tr * N + j) * 6, c, ybuf[yidx(j, c, t)]);
+                if (a.blk)  // wide-group round: the full iterate (resume source)
+                    for (int c = 0; c < 6; ++c) a.blk[(tr * N + j) * 6 + c] = ybuf[yidx(j, c, t)];
                 if (j == N - 1) {
 #pragma unroll
                     for (int c = 0; c < 6; ++c) a.state_out[tr * 6 + c] = ybuf[yidx(j, c, t)];
@@ -723,6 +730,74 @@ cudaError_t launch_repack_states(const double* s7, double* s6, long long M, cuda
     const long long n = M * 6;
     const int grid = static_cast<int>(std::min<long long>((n + 255) / 256, 148 * 16));
     k_repack_states<<<grid, 256, 0, s>>>(s7, s6, M);
+    return cudaGetLastError();
+}
+
+/// Trajectory list 0..n-1 (first member-level round of the wide-group path).
+__global__ void k_iota(int32_t* out, int n) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = i;
+}
+
+cudaError_t launch_iota(int32_t* out, int n, cudaStream_t s) {
+    const int grid = std::max(1, std::min((n + 255) / 256, 148 * 8));
+    k_iota<<<grid, 256, 0, s>>>(out, n);
+    return cudaGetLastError();
+}
+
+/// Group error history of a wide-group segment (augment.hpp:137 via pc_solve's history): the
+/// group's error at iteration k is the max over its members (block_max_error), k < K[g].
+/// Members' squared-free errors are non-negative doubles, so their IEEE bits order as
+/// unsigned integers: warps whose lanes share a group reduce first, then one atomicMax.
+/// gh [P][stride] must be zero on entry; k_group_hist_fill writes NaN past each K[g].
+__global__ void k_group_hist(const double* __restrict__ mh, int stride, const int64_t* __restrict__ group_off, int P,
+                             const int32_t* __restrict__ gK, int M, unsigned long long* gh) {
+    const int m0 = blockIdx.x * blockDim.x + threadIdx.x;
+    for (int base = m0 - threadIdx.x % 32; base < M; base += gridDim.x * blockDim.x) {
+        const int m = base + threadIdx.x % 32;
+        int g = -1;
+        if (m < M) {  // upper_bound over the group offsets
+            int lo = 0, hi = P;
+            while (hi - lo > 1) {
+                const int mid = (lo + hi) / 2;
+                if (group_off[mid] <= m) lo = mid; else hi = mid;
+            }
+            g = lo;
+        }
+        const int g0 = __shfl_sync(0xffffffffu, g, 0);
+        const bool uniform = __all_sync(0xffffffffu, g == g0);
+        const int K = g >= 0 ? gK[g] : 0;
+        const int Kmax = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(K));
+        for (int k = 0; k < Kmax; ++k) {
+            unsigned long long b = (m < M && k < K) ? static_cast<unsigned long long>(
+                                                          __double_as_longlong(mh[static_cast<size_t>(m) * stride + k]))
+                                                    : 0ull;
+            if (uniform) {
+                const unsigned hi = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(b >> 32));
+                const unsigned lo = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(b >> 32) == hi
+                                                                       ? static_cast<unsigned>(b) : 0u);
+                if (threadIdx.x % 32 == 0 && g0 >= 0)
+                    atomicMax(gh + static_cast<size_t>(g0) * stride + k, (static_cast<unsigned long long>(hi) << 32) | lo);
+            } else if (m < M && k < K) {
+                atomicMax(gh + static_cast<size_t>(g) * stride + k, b);
+            }
+        }
+    }
+}
+
+__global__ void k_group_hist_fill(int stride, const int32_t* __restrict__ gK, int P, unsigned long long* gh) {
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < static_cast<long long>(P) * stride;
+         i += static_cast<long long>(gridDim.x) * blockDim.x)
+        if (i % stride >= gK[i / stride]) gh[i] = ~0ull;
+}
+
+cudaError_t launch_group_hist(const double* mh, int stride, const int64_t* group_off, int P, const int32_t* gK, int M,
+                              double* gh, cudaStream_t s) {
+    auto* ghb = reinterpret_cast<unsigned long long*>(gh);
+    const int grid = std::max(1, std::min((M + 255) / 256, 148 * 8));
+    k_group_hist<<<grid, 256, 0, s>>>(mh, stride, group_off, P, gK, M, ghb);
+    const long long n = static_cast<long long>(P) * stride;
+    k_group_hist_fill<<<static_cast<int>(std::max<long long>(1, std::min<long long>((n + 255) / 256, 148 * 8))), 256, 0,
+                        s>>>(stride, gK, P, ghb);
     return cudaGetLastError();
 }
 

@@ -82,7 +82,50 @@ struct SegArgs {
     int b0_mma;                 // 1: folded b0 from the anchor pair row when N/2 % 8 != 0
     int fast_decide;            // 1: singleton-group decisions fast path (gmax == 1)
     const double* anc_fold;     // [8 nkp] anchor weights of the folded F layout
+    // ---- wide groups (groups larger than one CTA): member-level rounds (pswarm_capi.cu
+    //      solve_wide_rounds).  All nullptr for ordinary launches.
+    const int32_t* traj_list;   // [P] virtual singleton group gi -> trajectory; reports indexed by trajectory
+    const int32_t* it_start;    // [M] > 0: resume from blk at this iteration count (no warm start)
+    const int32_t* it_floor;    // [M] converge only at it >= floor
+    const int32_t* it_cap;      // [M] stop at min(max_it, cap)
+    double* blk;                // [M][N][6] full iterate of every retired trajectory (resume source)
+    int hist_stride;            // row stride of rep_hist (the configured max_iterations)
+    int pad1;
 };
+
+/// Group claimed from the queue: offset of its first trajectory, size and the report index
+/// (the group, or for a member-level round the trajectory itself).
+__device__ __forceinline__ void claim_group(const SegArgs& a, int gi, int& off, int& size, int& gid) {
+    if (a.traj_list) {
+        off = a.traj_list[gi];
+        size = 1;
+        gid = off;
+    } else {
+        off = static_cast<int>(a.group_off[gi]);
+        size = static_cast<int>(a.group_off[gi + 1]) - off;
+        gid = gi;
+    }
+}
+/// Iteration count a claimed trajectory starts from (> 0: resumed from a.blk).
+__device__ __forceinline__ int start_iteration(const SegArgs& a, int traj) { return a.it_start ? a.it_start[traj] : 0; }
+/// pc_solve's stopping rule with the member-level floor / cap of a wide-group round.
+__device__ __forceinline__ bool may_converge(const SegArgs& a, int gid, int it) { return !a.it_floor || it >= a.it_floor[gid]; }
+__device__ __forceinline__ bool at_cap(const SegArgs& a, int gid, int it) {
+    return it >= a.max_it || (a.it_cap && it >= a.it_cap[gid]);
+}
+/// Resumed slot (wide-group round): node row j of the saved iterate; the hot-start record
+/// (the previous retire's correction) is turned back into this segment's base.
+__device__ __forceinline__ void resume_node(const SegArgs& a, int traj, int j, double ro[3], double vo[3]) {
+    const double* b = a.blk + (static_cast<size_t>(traj) * a.N + j) * 6;
+    for (int c = 0; c < 3; ++c) {
+        ro[c] = b[c];
+        vo[c] = b[3 + c];
+    }
+    if (a.hot) {
+        double* hb = a.hot + (static_cast<size_t>(traj) * a.N + j) * 6;
+        for (int c = 0; c < 6; ++c) hb[c] = b[c] - hb[c];
+    }
+}
 
 /// Perturbing bodies on the device (ephemeris.hpp:44-73): analytic elements or
 /// tabulated Chebyshev segments, flattened.
@@ -108,47 +151,12 @@ cudaError_t launch_ephemeris(int N, const double* times, double central_mu, cons
                              double* indirect, unsigned long long* fault_key, double* vel, double* rel_tab, double ic2,
                              cudaStream_t s);
 
-/// Arguments of the wide-group path (groups larger than one CTA's 8 slots).
-struct WideArgs {
-    int N, nkp;
-    GemmPlan gp;
-    int xrows;
-    int M, P, seg, cold_start, error_mode, max_it;
-    double tol, omega2, epoch;
-    ForceData fd;
-    const double2* upack;
-    const double* times;
-    const int64_t* group_off;     // [P+1]
-    const int* traj_group;        // [M]
-    const double* state_in;       // [M][6]
-    double* state_out;            // [M][6]
-    double* Y;                    // [tiles][N][48] state blocks in HBM
-    double* samples;
-    int64_t R, row0;
-    int* g_active;                // [P]
-    int* g_iter;                  // [P]
-    unsigned long long* g_err2;   // [P] max squared error ratio (bits) of the running iteration
-    unsigned long long* g_nf;     // [P] first non-finite (node, column) key
-    unsigned long long* g_sing;   // [P] first singular sample key (s << 6 | check)
-    unsigned long long* t_sing_key;  // [M]
-    double* t_sing_val;           // [M]
-    int32_t* rep_iter;
-    double* rep_err;
-    uint8_t* rep_conv;
-    double* rep_hist;
-    GroupFault* faults;
-    uint8_t* cold_fallback;
-    unsigned long long* warm_key; // min trajectory*4 + kind of a warm-start fault
-    int* active_count;            // groups still iterating after the last finalize
-    double* hot;                  // [M][N][6] hot-start corrections (EXTENSION) or nullptr
-    int hot_apply;
-};
+/// Wide-group path (member-level rounds): trajectory list 0..n-1 and the group error history
+/// gh[P][stride] = max over members of mh[M][stride] for k < K[g], NaN beyond (gh zeroed first).
+cudaError_t launch_iota(int32_t* out, int n, cudaStream_t s);
+cudaError_t launch_group_hist(const double* mh, int stride, const int64_t* group_off, int P, const int32_t* gK, int M,
+                              double* gh, cudaStream_t s);
 
-size_t wide_iter_smem_bytes(int N, int nkp, int xrows);
-cudaError_t launch_wide_start(const WideArgs& a, cudaStream_t s);
-cudaError_t launch_wide_iter(const WideArgs& a, int grid, cudaStream_t s);
-cudaError_t launch_wide_finalize(const WideArgs& a, cudaStream_t s);
-cudaError_t launch_wide_output(const WideArgs& a, cudaStream_t s);
 
 /// Batched RKF7(8) verifier (pc_rk.cu; oracle.hpp:63-183): one thread per trajectory.
 struct RkArgs {

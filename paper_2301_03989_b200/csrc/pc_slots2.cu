@@ -694,14 +694,14 @@ __device__ __forceinline__ void decide_single(const SegArgs& a, WsState& st, int
                 fl->column = key % 6;
                 retire = true;
             } else {
-                if (a.rep_hist) a.rep_hist[static_cast<size_t>(gid) * a.max_it + (it - 1)] = sqrt(gerr2);
+                if (a.rep_hist) a.rep_hist[static_cast<size_t>(gid) * a.hist_stride + (it - 1)] = sqrt(gerr2);
                 const bool le_tol = PSWARM_ABLATE == 0 &&
                     (e2b <= __double_as_longlong(a.tol2_lo)
                          ? true
                          : (e2b > __double_as_longlong(a.tol2_hi) ? false : sqrt(gerr2) <= a.tol));
-                if (le_tol) {
+                if (le_tol && may_converge(a, gid, it)) {
                     retire = ok = conv = true;
-                } else if (it >= a.max_it) {
+                } else if (at_cap(a, gid, it)) {
                     retire = ok = true;
                 }
             }
@@ -825,7 +825,7 @@ __device__ __forceinline__ void decide_half(const SegArgs& a, WsState& st, int h
                 fl->column = nf_best % (6LL * size);
                 retire = true;
             } else {
-                if (a.rep_hist) a.rep_hist[static_cast<size_t>(gid) * a.max_it + (it - 1)] = gerr_of();
+                if (a.rep_hist) a.rep_hist[static_cast<size_t>(gid) * a.hist_stride + (it - 1)] = gerr_of();
                 // squared-error bands as integer compares of the IEEE bits (non-negative doubles
                 // order like integers; NaN sorts above every finite band): off the FP64 pipe
                 const long long e2b = __double_as_longlong(gerr2);
@@ -833,9 +833,9 @@ __device__ __forceinline__ void decide_half(const SegArgs& a, WsState& st, int h
                     (e2b <= __double_as_longlong(a.tol2_lo)
                          ? true
                          : (e2b > __double_as_longlong(a.tol2_hi) ? false : gerr_of() <= a.tol));
-                if (le_tol) {
+                if (le_tol && may_converge(a, gid, it)) {
                     retire = ok = conv = true;
-                } else if (it >= a.max_it) {
+                } else if (at_cap(a, gid, it)) {
                     retire = ok = true;
                 }
             }
@@ -1207,6 +1207,8 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
                     }
                     if (a.hot)
                         for (int c = 0; c < 6; ++c) hot_retire_node(a.hot + (tr * N + j) * 6, c, ybuf[y2(j, h, c, s)]);
+                    if (a.blk)  // wide-group round: the full iterate (resume source)
+                        for (int c = 0; c < 6; ++c) a.blk[(tr * N + j) * 6 + c] = ybuf[y2(j, h, c, s)];
                     if (j == N - 1) {
 #pragma unroll
                         for (int c = 0; c < 6; ++c) a.state_out[tr * 6 + c] = ybuf[y2(j, h, c, s)];
@@ -1234,11 +1236,11 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
                     for (int gi = g0; gi < g1; ++gi) {
                         int lg = h * HS;  // group records of half h (a group never spans halves)
                         while (st.grp_id[lg] >= 0) ++lg;
-                        const int off = static_cast<int>(a.group_off[gi]);
-                        const int size = static_cast<int>(a.group_off[gi + 1]) - off;
-                        st.grp_id[lg] = gi;
+                        int off, size, gid;
+                        claim_group(a, gi, off, size, gid);
+                        st.grp_id[lg] = gid;
                         st.grp_size[lg] = size;
-                        st.grp_iter[lg] = 0;
+                        st.grp_iter[lg] = start_iteration(a, off);
                         int t = h * HS;
                         for (int mbr = 0; mbr < size; ++mbr) {
                             while ((am >> t) & 1) ++t;
@@ -1293,21 +1295,26 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
                     const double r[3] = {st.y0[t][0], st.y0[t][1], st.y0[t][2]};
                     const double v[3] = {st.y0[t][3], st.y0[t][4], st.y0[t][5]};
                     double ro[3] = {r[0], r[1], r[2]}, vo[3] = {v[0], v[1], v[2]};
-                    if (!a.cold_start) {
-                        const int chk = conic_check(r, v, a.fd.central_mu);
-                        if (chk == CONIC_ZERO_RADIUS) {
-                            atomicMin(&st.warm_key[t], j * 4 + CONIC_ZERO_RADIUS);
-                        } else if (chk == CONIC_OK) {
-                            double mf, ef;
-                            if (kepler_propagate(r, v, a.fd.central_mu, a.times[j] - a.epoch, ro, vo, &mf, &ef) !=
-                                CONIC_OK)
-                                atomicMin(&st.warm_key[t], j * 4 + CONIC_SOLVER);
+                    if (start_iteration(a, st.slot_traj[t]) > 0) {  // wide-group round: resume the saved iterate
+                        resume_node(a, st.slot_traj[t], j, ro, vo);
+                    } else {
+                        if (!a.cold_start) {
+                            const int chk = conic_check(r, v, a.fd.central_mu);
+                            if (chk == CONIC_ZERO_RADIUS) {
+                                atomicMin(&st.warm_key[t], j * 4 + CONIC_ZERO_RADIUS);
+                            } else if (chk == CONIC_OK) {
+                                double mf, ef;
+                                if (kepler_propagate(r, v, a.fd.central_mu, a.times[j] - a.epoch, ro, vo, &mf, &ef) !=
+                                    CONIC_OK)
+                                    atomicMin(&st.warm_key[t], j * 4 + CONIC_SOLVER);
+                            }
+                            if (j == 0 && a.cold_fallback)
+                                a.cold_fallback[st.slot_traj[t]] = (chk == CONIC_NON_ELLIPTIC) ? 1 : 0;
                         }
-                        if (j == 0 && a.cold_fallback)
-                            a.cold_fallback[st.slot_traj[t]] = (chk == CONIC_NON_ELLIPTIC) ? 1 : 0;
+                        if (a.hot)
+                            hot_start_node(a.hot + (static_cast<size_t>(st.slot_traj[t]) * N + j) * 6, a.hot_apply,
+                                           ro, vo);
                     }
-                    if (a.hot)
-                        hot_start_node(a.hot + (static_cast<size_t>(st.slot_traj[t]) * N + j) * 6, a.hot_apply, ro, vo);
 #pragma unroll
                     for (int c = 0; c < 3; ++c) {
                         ybuf[y2(j, h, c, s)] = ro[c];
@@ -1648,6 +1655,8 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_uni(const SegArgs a) {
                 }
                 if (a.hot)
                     for (int c = 0; c < 6; ++c) hot_retire_node(a.hot + (tr * N + j) * 6, c, ybuf[y2(j, h, c, s)]);
+                if (a.blk)  // wide-group round: the full iterate (resume source)
+                    for (int c = 0; c < 6; ++c) a.blk[(tr * N + j) * 6 + c] = ybuf[y2(j, h, c, s)];
                 if (j == N - 1) {
 #pragma unroll
                     for (int c = 0; c < 6; ++c) a.state_out[tr * 6 + c] = ybuf[y2(j, h, c, s)];
@@ -1676,11 +1685,11 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_uni(const SegArgs a) {
                     for (int gi = g0; gi < g1; ++gi) {
                         int lg = h * HS;
                         while (st.grp_id[lg] >= 0) ++lg;
-                        const int off = static_cast<int>(a.group_off[gi]);
-                        const int size = static_cast<int>(a.group_off[gi + 1]) - off;
-                        st.grp_id[lg] = gi;
+                        int off, size, gid;
+                        claim_group(a, gi, off, size, gid);
+                        st.grp_id[lg] = gid;
                         st.grp_size[lg] = size;
-                        st.grp_iter[lg] = 0;
+                        st.grp_iter[lg] = start_iteration(a, off);
                         int t = h * HS;
                         for (int mbr = 0; mbr < size; ++mbr) {
                             while ((am >> t) & 1) ++t;
@@ -1730,18 +1739,23 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_uni(const SegArgs a) {
                 const double r[3] = {st.y0[t][0], st.y0[t][1], st.y0[t][2]};
                 const double v[3] = {st.y0[t][3], st.y0[t][4], st.y0[t][5]};
                 double ro[3] = {r[0], r[1], r[2]}, vo[3] = {v[0], v[1], v[2]};
-                if (!a.cold_start) {
-                    const int chk = conic_check(r, v, a.fd.central_mu);
-                    if (chk == CONIC_ZERO_RADIUS) {
-                        atomicMin(&st.warm_key[t], j * 4 + CONIC_ZERO_RADIUS);
-                    } else if (chk == CONIC_OK) {
-                        double mf, ef;
-                        if (kepler_propagate(r, v, a.fd.central_mu, a.times[j] - a.epoch, ro, vo, &mf, &ef) != CONIC_OK)
-                            atomicMin(&st.warm_key[t], j * 4 + CONIC_SOLVER);
+                if (start_iteration(a, st.slot_traj[t]) > 0) {  // wide-group round: resume the saved iterate
+                    resume_node(a, st.slot_traj[t], j, ro, vo);
+                } else {
+                    if (!a.cold_start) {
+                        const int chk = conic_check(r, v, a.fd.central_mu);
+                        if (chk == CONIC_ZERO_RADIUS) {
+                            atomicMin(&st.warm_key[t], j * 4 + CONIC_ZERO_RADIUS);
+                        } else if (chk == CONIC_OK) {
+                            double mf, ef;
+                            if (kepler_propagate(r, v, a.fd.central_mu, a.times[j] - a.epoch, ro, vo, &mf, &ef) != CONIC_OK)
+                                atomicMin(&st.warm_key[t], j * 4 + CONIC_SOLVER);
+                        }
+                        if (j == 0 && a.cold_fallback) a.cold_fallback[st.slot_traj[t]] = (chk == CONIC_NON_ELLIPTIC) ? 1 : 0;
                     }
-                    if (j == 0 && a.cold_fallback) a.cold_fallback[st.slot_traj[t]] = (chk == CONIC_NON_ELLIPTIC) ? 1 : 0;
+                    if (a.hot)
+                        hot_start_node(a.hot + (static_cast<size_t>(st.slot_traj[t]) * N + j) * 6, a.hot_apply, ro, vo);
                 }
-                if (a.hot) hot_start_node(a.hot + (static_cast<size_t>(st.slot_traj[t]) * N + j) * 6, a.hot_apply, ro, vo);
 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
                     ybuf[y2(j, h, c, s)] = ro[c];

@@ -1,5 +1,5 @@
 // Tile-level device routines shared by the persistent slot kernel (pc_kernels.cu)
-// and the wide-group per-iteration kernel (pc_wide.cu).
+// (groups wider than a CTA run on the same kernels in member-level rounds).
 #pragma once
 
 #include <climits>

@@ -13,6 +13,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <memory>
 #include <string>
@@ -155,7 +156,7 @@ enum BufId {
     B_REP_ITER, B_REP_ERR, B_REP_CONV, B_REP_HIST, B_FAULTS, B_FALLBACK, B_SAMPLES, B_DEAD,
     B_OP_IN, B_OP_IN2, B_OP_OUT, B_OP_AUX, B_OP_KEY,
     B_BT_KIND, B_BT_SOFF, B_BT_NC, B_BT_EL, B_BT_BND, B_BT_COFF, B_BT_CF, B_PHASES,
-    B_W_TG, B_W_Y, B_W_ACT, B_W_ITER, B_W_ERR, B_W_NF, B_W_SING, B_W_TSK, B_W_TSV, B_W_WK, B_W_CNT,
+    B_W_REP, B_W_LIST, B_W_CTL, B_W_HIST, B_W_BLK, B_W_GK,
     B_IN_PACK, B_REPORT, B_BODY_VEL, B_REL_TAB, B_HOT, B_STATES7, B_COUNT
 };
 
@@ -216,13 +217,8 @@ struct pswarm_ctx {
                              // k_pc_uni for the force-bound 1PN model (N <= 200), else k_pc_ws_fold
                              // (measured, tools/probe_uni.py)
     unsigned long long phase_host[pswarm_dev::PHASES] = {};
-    PinnedBuf pin_in, pin_rep, pin_term;
-    // wide-group path
-    cudaEvent_t wide_ev[4] = {};
-    int* wide_count_host = nullptr;  // pinned ring of active-group counts
-    unsigned long long wide_warm_key = ~0ull;
-    double wide_warm_vals[2] = {0.0, 0.0};
-    bool wide_timeout = false;
+    PinnedBuf pin_in, pin_rep, pin_term, pin_wide;
+    int wide_rounds = 0;  // member-level rounds of the last wide-group segment (diagnostics)
 };
 
 namespace {
@@ -367,99 +363,230 @@ void upload(pswarm_ctx* ctx, BufId id, const T* host, size_t count, T** dev) {
 }
 
 // ------------------------------------------------------------- wide groups
-/// One segment of groups larger than a CTA's slots: warm start into HBM, then
-/// lockstep iterations (k_wide_iter + k_wide_finalize) until no group is active,
-/// with at most two iterations in flight before the host reads the active count.
-void run_wide_segment(pswarm_ctx* ctx, const SegArgs& s, const std::vector<int64_t>& h_off,
-                      std::chrono::steady_clock::time_point deadline) {
+/// One segment of groups larger than a CTA's slots (augmented / big grouped modes), solved on
+/// the same persistent slot kernels as singleton groups.
+///
+/// A group's Picard iterates are column-separable: every member's update, force and error
+/// depend on that member alone (augment.hpp:32-104); only the stopping rule couples them --
+/// the group stops at the first iteration K where the max of its members' errors is <= tol
+/// (pc_solve, picard.hpp:46-83), or at max_iterations, or at the first fault.  So the members
+/// run as independent slots in rounds, each retiring with its full iterate saved in HBM:
+///   round 0: every member stops at its own first crossing k_m (err <= tol);
+///   round r: per group K_cand = max over members of their stop; members that stopped earlier
+///            resume from the saved iterate and stop at the first k >= K_cand with err <= tol.
+/// K_cand never passes K (below K_cand some member's error is above tol), so the rounds end
+/// when every member of a group stops at the same K -- exactly the reference's K, with the
+/// reference's arithmetic per member.  A member that hits max_iterations makes the others run
+/// to max_iterations; a fault at iteration f makes every member that stopped before f run to f
+/// so an earlier fault of another member is not missed.  The group's report, fault
+/// coordinates (sample / column order of the whole group block) and error history are then
+/// formed from the member records.  One round is the common case (a clone cloud converges in
+/// step); each further round is one more launch over the lagging members only.
+void solve_wide_rounds(pswarm_ctx* ctx, SegArgs a, const std::function<cudaError_t(const SegArgs&, int)>& launch,
+                       int cta_cap, const std::vector<int64_t>& h_off, int64_t P, int max_it,
+                       std::chrono::steady_clock::time_point deadline, int32_t* d_iter, double* d_err, uint8_t* d_conv,
+                       GroupFault* d_faults, double* d_hist_seg, const int64_t* d_off, double& kernel_ms) {
     cudaStream_t st = ctx->stream;
-    const int M = s.M, P = s.P, N = s.N;
-    const int tiles = (M + SLOTS - 1) / SLOTS;
-    WideArgs a{};
-    a.N = N;
-    a.nkp = s.nkp;
-    a.gp = s.gp;
-    a.xrows = s.xrows;
-    a.M = M;
-    a.P = P;
-    a.seg = s.seg;
-    a.cold_start = s.cold_start;
-    a.error_mode = s.error_mode;
-    a.max_it = s.max_it;
-    a.tol = s.tol;
-    a.omega2 = s.omega2;
-    a.epoch = s.epoch;
-    a.fd = s.fd;
-    a.upack = s.upack;
-    a.times = s.times;
-    a.group_off = s.group_off;
-    a.state_in = s.state_in;
-    a.state_out = s.state_out;
-    a.samples = s.samples;
-    a.R = s.R;
-    a.row0 = s.row0;
-    a.rep_iter = s.rep_iter;
-    a.rep_err = s.rep_err;
-    a.rep_conv = s.rep_conv;
-    a.rep_hist = s.rep_hist;
-    a.faults = s.faults;
-    a.cold_fallback = s.cold_fallback;
-    a.hot = s.hot;
-    a.hot_apply = s.hot_apply;
-    std::vector<int> tg(static_cast<size_t>(M));
-    for (int g = 0; g < P; ++g)
-        for (int64_t i = h_off[g]; i < h_off[g + 1]; ++i) tg[i] = g;
-    int* d_tg;
-    upload(ctx, B_W_TG, tg.data(), tg.size(), &d_tg);
-    a.traj_group = d_tg;
-    a.Y = ctx->buf[B_W_Y].get<double>(static_cast<size_t>(tiles) * N * COLS);
-    a.g_active = ctx->buf[B_W_ACT].get<int>(P);
-    a.g_iter = ctx->buf[B_W_ITER].get<int>(P);
-    a.g_err2 = ctx->buf[B_W_ERR].get<unsigned long long>(P);
-    a.g_nf = ctx->buf[B_W_NF].get<unsigned long long>(P);
-    a.g_sing = ctx->buf[B_W_SING].get<unsigned long long>(P);
-    a.t_sing_key = ctx->buf[B_W_TSK].get<unsigned long long>(M);
-    a.t_sing_val = ctx->buf[B_W_TSV].get<double>(M);
-    a.warm_key = ctx->buf[B_W_WK].get<unsigned long long>(2);
-    a.active_count = ctx->buf[B_W_CNT].get<int>(8);
-    std::vector<int> ones(static_cast<size_t>(P), 1);
-    cuda_check(cudaMemcpyAsync(a.g_active, ones.data(), sizeof(int) * P, cudaMemcpyHostToDevice, st), "H2D");
-    cuda_check(cudaMemsetAsync(a.g_iter, 0, sizeof(int) * P, st), "memset");
-    cuda_check(cudaMemsetAsync(a.g_err2, 0, sizeof(unsigned long long) * P, st), "memset");
-    cuda_check(cudaMemsetAsync(a.g_nf, 0xff, sizeof(unsigned long long) * P, st), "memset");
-    cuda_check(cudaMemsetAsync(a.g_sing, 0xff, sizeof(unsigned long long) * P, st), "memset");
-    cuda_check(cudaMemsetAsync(a.warm_key, 0xff, sizeof(unsigned long long), st), "memset");
-    cuda_check(cudaEventRecord(ctx->evk0, st), "event");
-    cuda_check(launch_wide_start(a, st), "k_wide_start");
+    const int64_t M = a.M, N = a.N;
+    // member reports: [M] iterations | converged | error, then [M] fault records
+    Pack mp;
+    const size_t o_it = mp.add(sizeof(int32_t) * M), o_cv = mp.add(M), o_er = mp.add(sizeof(double) * M),
+                 o_head = mp.total, o_fl = mp.add(sizeof(GroupFault) * M);
+    char* dm = ctx->buf[B_W_REP].get<char>(mp.total);
+    char* hm = ctx->pin_wide.get<char>(mp.total);
+    int32_t* d_list = ctx->buf[B_W_LIST].get<int32_t>(M);
+    int32_t* d_ctl = ctx->buf[B_W_CTL].get<int32_t>(3 * M);  // it_start | floor | cap
+    a.blk = ctx->buf[B_W_BLK].get<double>(static_cast<size_t>(M) * N * 6);
+    a.rep_iter = reinterpret_cast<int32_t*>(dm + o_it);
+    a.rep_conv = reinterpret_cast<uint8_t*>(dm + o_cv);
+    a.rep_err = reinterpret_cast<double*>(dm + o_er);
+    a.faults = reinterpret_cast<GroupFault*>(dm + o_fl);
+    double* m_hist = d_hist_seg ? ctx->buf[B_W_HIST].get<double>(static_cast<size_t>(M) * max_it) : nullptr;
+    a.rep_hist = m_hist;
+    a.hist_stride = max_it;
+    a.traj_list = d_list;
+    a.gmax = 1;
+    cuda_check(cudaMemsetAsync(dm, 0, mp.total, st), "memset member reports");
+    cuda_check(launch_iota(d_list, static_cast<int>(M), st), "k_iota");
     ++ctx->launches;
-    const int grid = std::max(1, std::min(tiles, ctx->sm_count));
-    ctx->wide_timeout = false;
-    constexpr int RING = 4;
-    for (int it = 1; it <= a.max_it; ++it) {
-        if (it > 2) {  // read the active count of iteration it-2 (two launches in flight)
-            cuda_check(cudaEventSynchronize(ctx->wide_ev[(it - 2) % RING]), "wide poll");
-            if (ctx->wide_count_host[(it - 2) % RING] == 0) break;
+
+    std::vector<int32_t> h_list, ctl(static_cast<size_t>(3 * M), 0);
+    int32_t *c_start = ctl.data(), *c_floor = ctl.data() + M, *c_cap = ctl.data() + 2 * M;
+    std::vector<uint8_t> decided(static_cast<size_t>(P), 0);
+    std::vector<int32_t> g_iter(static_cast<size_t>(P), 0);
+    std::vector<double> g_err(static_cast<size_t>(P), 0.0);
+    std::vector<uint8_t> g_conv(static_cast<size_t>(P), 0);
+    std::vector<GroupFault> g_fault(static_cast<size_t>(P));
+    const int32_t* m_it = reinterpret_cast<const int32_t*>(hm + o_it);
+    const uint8_t* m_cv = reinterpret_cast<const uint8_t*>(hm + o_cv);
+    const double* m_er = reinterpret_cast<const double*>(hm + o_er);
+    const GroupFault* m_fl = reinterpret_cast<const GroupFault*>(hm + o_fl);
+    int64_t listed = M;
+    ctx->wide_rounds = 0;
+    for (int round = 0;; ++round) {
+        // ---- launch the listed members
+        a.P = static_cast<int>(listed);
+        const bool ctl_on = round > 0;
+        a.it_start = ctl_on ? d_ctl : nullptr;
+        a.it_floor = ctl_on ? d_ctl + M : nullptr;
+        a.it_cap = ctl_on ? d_ctl + 2 * M : nullptr;
+        cuda_check(cudaMemsetAsync(a.queue, 0, sizeof(int), st), "memset queue");
+        const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((listed + SLOTS - 1) / SLOTS, cta_cap)));
+        cuda_check(cudaEventRecord(ctx->evk0, st), "event");
+        cuda_check(launch(a, grid), "slot kernel launch (wide-group round)");
+        cuda_check(cudaEventRecord(ctx->evk1, st), "event");
+        ++ctx->launches;
+        ++ctx->wide_rounds;
+        cuda_check(cudaMemcpyAsync(hm, dm, o_head, cudaMemcpyDeviceToHost, st), "D2H member reports");
+        cuda_check(cudaStreamSynchronize(st), "wide-group round");
+        float kms = 0.f;
+        cudaEventElapsedTime(&kms, ctx->evk0, ctx->evk1);
+        kernel_ms += kms;
+        bool any_fault = false;
+        for (int64_t m = 0; m < M && !any_fault; ++m) any_fault = !m_cv[m];
+        if (any_fault) {  // fault records only when some member stopped unconverged
+            cuda_check(cudaMemcpyAsync(hm + o_fl, dm + o_fl, sizeof(GroupFault) * M, cudaMemcpyDeviceToHost, st), "D2H");
+            cuda_check(cudaStreamSynchronize(st), "wide-group faults");
         }
-        if (std::chrono::steady_clock::now() > deadline) {
-            ctx->wide_timeout = true;
-            break;
+        auto faulted = [&](int64_t m) { return any_fault && !m_cv[m] && m_fl[m].status != FAULT_NONE; };
+        // ---- warm-start faults stop the batch before any solve (propagator.hpp:252-270)
+        bool warm = false, timeout = std::chrono::steady_clock::now() > deadline;
+        for (int64_t m = 0; m < M; ++m)
+            if (faulted(m)) {
+                warm |= m_fl[m].status == FAULT_WARM_ZERO_RADIUS || m_fl[m].status == FAULT_WARM_SOLVER;
+                timeout |= m_fl[m].status == FAULT_TIMEOUT;
+            }
+        h_list.clear();
+        for (int64_t g = 0; g < P; ++g) {
+            if (decided[g]) continue;
+            const int64_t lo = h_off[g], hi = h_off[g + 1], G = hi - lo;
+            GroupFault& gf = g_fault[g];
+            auto decide = [&](int32_t it, double err, bool conv) {
+                decided[g] = 1;
+                g_iter[g] = it;
+                g_err[g] = err;
+                g_conv[g] = conv ? 1 : 0;
+            };
+            if (warm || timeout) {
+                gf = GroupFault{};
+                for (int64_t m = lo; m < hi; ++m)
+                    if (faulted(m) && (m_fl[m].status == FAULT_WARM_ZERO_RADIUS || m_fl[m].status == FAULT_WARM_SOLVER) &&
+                        (gf.status == FAULT_NONE || m_fl[m].trajectory < gf.trajectory))
+                        gf = m_fl[m];
+                if (gf.status == FAULT_NONE && timeout) {
+                    bool hit = false;  // a member cut by the deadline, or never reached
+                    int32_t itg = 0;
+                    for (int64_t m = lo; m < hi; ++m) {
+                        hit |= (faulted(m) && m_fl[m].status == FAULT_TIMEOUT) || (!m_cv[m] && !faulted(m) && m_it[m] < max_it);
+                        itg = std::max(itg, m_it[m]);
+                    }
+                    if (hit) {
+                        gf.status = FAULT_TIMEOUT;
+                        gf.iteration = itg;
+                    }
+                }
+                decide(gf.status == FAULT_NONE ? 0 : gf.iteration, 0.0, false);
+                continue;
+            }
+            // ---- earliest solve fault of the group (singularity / divergence)
+            int32_t fmin = INT32_MAX;
+            for (int64_t m = lo; m < hi; ++m)
+                if (faulted(m)) fmin = std::min(fmin, m_fl[m].iteration);
+            auto resume = [&](int64_t m, int32_t floor, int32_t cap) {
+                c_start[m] = m_it[m];
+                c_floor[m] = floor;
+                c_cap[m] = cap;
+                h_list.push_back(static_cast<int32_t>(m));
+            };
+            if (fmin != INT32_MAX) {
+                bool pending = false;
+                for (int64_t m = lo; m < hi; ++m)
+                    if (!faulted(m) && m_it[m] < fmin) {
+                        resume(m, fmin, fmin);
+                        pending = true;
+                    }
+                if (pending) continue;
+                // the group block's order at iteration fmin: singularity (sample = node * G + member,
+                // force_model.hpp:93-142) before divergence ((node, column), column = comp * G + member)
+                gf = GroupFault{};
+                long long best_s = LLONG_MAX, best_d = LLONG_MAX;
+                for (int64_t m = lo; m < hi; ++m) {
+                    if (!faulted(m) || m_fl[m].iteration != fmin) continue;
+                    const GroupFault& f = m_fl[m];
+                    const int64_t mbr = m - lo;
+                    if (f.status == FAULT_SINGULARITY) {
+                        const long long key = f.node * G + mbr;
+                        if (key < best_s) {
+                            best_s = key;
+                            gf = f;
+                            gf.trajectory = mbr;
+                        }
+                    }
+                }
+                if (best_s == LLONG_MAX)
+                    for (int64_t m = lo; m < hi; ++m) {
+                        if (!faulted(m) || m_fl[m].iteration != fmin || m_fl[m].status != FAULT_DIVERGENCE) continue;
+                        const long long key = m_fl[m].node * 6 * G + m_fl[m].column * G + (m - lo);
+                        if (key < best_d) {
+                            best_d = key;
+                            gf = m_fl[m];
+                            gf.column = m_fl[m].column * G + (m - lo);
+                        }
+                    }
+                decide(fmin, 0.0, false);
+                continue;
+            }
+            // ---- a member out of iterations: the whole group runs to max_iterations
+            bool capped = false;
+            for (int64_t m = lo; m < hi; ++m) capped |= !m_cv[m];
+            if (capped) {
+                bool pending = false;
+                for (int64_t m = lo; m < hi; ++m)
+                    if (m_it[m] < max_it) {
+                        resume(m, max_it, max_it);
+                        pending = true;
+                    }
+                if (pending) continue;
+                double e = 0.0;
+                for (int64_t m = lo; m < hi; ++m) e = std::max(e, m_er[m]);
+                decide(max_it, e, false);
+                continue;
+            }
+            // ---- every member below tol at its stop: the group stops at the latest one if all agree
+            int32_t K = 0;
+            for (int64_t m = lo; m < hi; ++m) K = std::max(K, m_it[m]);
+            bool pending = false;
+            for (int64_t m = lo; m < hi; ++m)
+                if (m_it[m] < K) {
+                    resume(m, K, max_it);
+                    pending = true;
+                }
+            if (pending) continue;
+            double e = 0.0;
+            for (int64_t m = lo; m < hi; ++m) e = std::max(e, m_er[m]);
+            decide(K, e, true);
         }
-        cuda_check(cudaMemsetAsync(a.active_count, 0, sizeof(int), st), "memset");
-        cuda_check(launch_wide_iter(a, grid, st), "k_wide_iter");
-        cuda_check(launch_wide_finalize(a, st), "k_wide_finalize");
-        ctx->launches += 2;
-        cuda_check(cudaMemcpyAsync(ctx->wide_count_host + it % RING, a.active_count, sizeof(int),
-                                   cudaMemcpyDeviceToHost, st),
-                   "D2H count");
-        cuda_check(cudaEventRecord(ctx->wide_ev[it % RING], st), "event");
+        if (h_list.empty()) break;
+        // ---- next round: the lagging members only
+        listed = static_cast<int64_t>(h_list.size());
+        cuda_check(cudaMemcpyAsync(d_list, h_list.data(), sizeof(int32_t) * listed, cudaMemcpyHostToDevice, st), "H2D");
+        cuda_check(cudaMemcpyAsync(d_ctl, ctl.data(), sizeof(int32_t) * 3 * M, cudaMemcpyHostToDevice, st), "H2D");
+        a.cold_fallback = nullptr;  // written by round 0 (resumed members skip the warm start)
     }
-    cuda_check(launch_wide_output(a, st), "k_wide_output");
-    ++ctx->launches;
-    cuda_check(cudaEventRecord(ctx->evk1, st), "event");
-    cuda_check(cudaMemcpyAsync(&ctx->wide_warm_key, a.warm_key, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st),
-               "D2H");
-    cuda_check(cudaStreamSynchronize(st), "wide segment");
-    ctx->wide_warm_vals[0] = ctx->wide_warm_vals[1] = 0.0;
+    // ---- group reports into the segment's report block (the caller reads them back as usual)
+    cuda_check(cudaMemcpyAsync(d_iter, g_iter.data(), sizeof(int32_t) * P, cudaMemcpyHostToDevice, st), "H2D");
+    cuda_check(cudaMemcpyAsync(d_err, g_err.data(), sizeof(double) * P, cudaMemcpyHostToDevice, st), "H2D");
+    cuda_check(cudaMemcpyAsync(d_conv, g_conv.data(), P, cudaMemcpyHostToDevice, st), "H2D");
+    cuda_check(cudaMemcpyAsync(d_faults, g_fault.data(), sizeof(GroupFault) * P, cudaMemcpyHostToDevice, st), "H2D");
+    if (d_hist_seg) {
+        int32_t* d_gk = ctx->buf[B_W_GK].get<int32_t>(P);
+        cuda_check(cudaMemcpyAsync(d_gk, g_iter.data(), sizeof(int32_t) * P, cudaMemcpyHostToDevice, st), "H2D");
+        cuda_check(cudaMemsetAsync(d_hist_seg, 0, sizeof(double) * P * max_it, st), "memset");
+        cuda_check(launch_group_hist(m_hist, max_it, d_off, static_cast<int>(P), d_gk, static_cast<int>(M), d_hist_seg, st),
+                   "k_group_hist");
+        ctx->launches += 2;
+    }
+    cuda_check(cudaStreamSynchronize(st), "wide-group reports");  // host vectors go out of scope
 }
 
 // ----------------------------------------------------------------- propagate
@@ -468,6 +595,8 @@ struct RunSpec {
     // multi-device shards: leave the terminal states on the device and return their address
     // ([M][6] f64 in a context buffer, valid until the context's next call)
     const double** term_dev = nullptr;
+    // independent mode: batch index of the trajectory whose error is raised (-1: none)
+    int64_t* fail_index = nullptr;
 };
 
 /// PSWARM_TRACE=1: host-side stage times of propagate (diagnostics, stderr).
@@ -509,7 +638,6 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
     if (states[0] != boundaries[0])
         throw pswarm::AlignmentError("propagate: batch epoch does not match the first segment boundary");
     if (cfg->tolerance <= 0.0) throw pswarm::Error("pc_solve: tolerance must be positive");
-    const bool wide = gmax > SLOTS;  // groups spanning CTAs: lockstep iterations through HBM
     if (N < 3) throw pswarm::InvalidSizeError("build_matrices: need at least 3 nodes, got " + std::to_string(N));
     if (!ctx) raise(PSWARM_ERR_NO_DEVICE, "propagate: no device context (the B200 path has no CPU fallback)");
     bind(ctx);
@@ -628,34 +756,40 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
         gpu_deadline = t0 + static_cast<unsigned long long>(std::max<int64_t>(left.count(), 1));
     }
 
-    // kernel choice: warp-specialised slot kernel (groups <= 4, N in its tile range),
-    // the generic slot kernel (groups <= 8), or the wide-group path
+    // kernel choice -- by N, the force model and the options only, never by the grouping, so
+    // every grouping (and every multi-device shard) runs the same per-trajectory arithmetic:
+    // the warp-specialised slot kernel when N is in its tile range, else the generic one.
+    // Groups up to the kernel's in-CTA limit (4 / 8 members) take their decisions in the
+    // kernel; larger ones run as member-level rounds on the same kernel (solve_wide_rounds).
     constexpr size_t SMEM_MAX = 227 * 1024 - 1024;  // opt-in limit minus the kernels' static __shared__ (< 1 KB)
     const int Ni = static_cast<int>(N);
     // mirror-folded update when N allows it (half the DMMAs); "fold" option 0 forces the dense one
-    const bool fold = !wide && gmax <= 4 && ctx->fold && op.nkp_fold > 0 && ws_supported(Ni, true) &&
-                      ctx->slot_kernel != 1 &&
+    const bool fold = ctx->fold && op.nkp_fold > 0 && ws_supported(Ni, true) && ctx->slot_kernel != 1 &&
                       ws_smem_bytes(Ni, op.nkp, ws_extra_rows(Ni, true), nb, 0, true) <= SMEM_MAX;
-    const bool use_ws = fold || (!wide && gmax <= 4 && ws_supported(Ni, false) && ctx->slot_kernel != 1 &&
+    const bool use_ws = fold || (ws_supported(Ni, false) && ctx->slot_kernel != 1 &&
                                  ws_smem_bytes(Ni, op.nkp, ws_extra_rows(Ni, false), nb, 0, false) <= SMEM_MAX);
+    const bool wide = gmax > (use_ws ? SLOTS / 2 : SLOTS);
+    const int64_t gk = wide ? 1 : gmax;  // group size the slot kernel sees
     const int xrows = use_ws ? ws_extra_rows(Ni, fold) : extra_rows(Ni, op.gp);
     // auto: the unified kernel for the force-bound 1PN model up to N = 200 (at N = 256 the
     // warp-specialised one is faster, profiles/bench_r01_c5_n*.json)
     const bool uni = fold && (ctx->unified == 1 || (ctx->unified == 2 && rel && Ni <= 200)) && uni_supported(Ni);
-    ctx->last_kernel = wide ? "k_wide_iter" : uni ? "k_pc_uni" : fold ? "k_pc_ws_fold" : use_ws ? "k_pc_ws" : "k_pc_segment";
+    ctx->last_kernel = uni ? "k_pc_uni" : fold ? "k_pc_ws_fold" : use_ws ? "k_pc_ws" : "k_pc_segment";
     // stage the frozen ephemeris in shared memory when it fits next to the state blocks
     const int stage_eph = nb > 0 && !rel &&
                                   (use_ws ? ws_smem_bytes(Ni, op.nkp, xrows, nb, 1, fold)
                                           : segment_smem_bytes(Ni, op.nkp, xrows, nb, 1)) <= SMEM_MAX
                               ? 1
                               : 0;
-    if (!wide && !use_ws && segment_smem_bytes(Ni, op.nkp, xrows, nb, stage_eph) > SMEM_MAX)
+    if (!use_ws && segment_smem_bytes(Ni, op.nkp, xrows, nb, stage_eph) > SMEM_MAX)
         raise(PSWARM_ERR_INVALID_SIZE, fmtf("propagate: %lld nodes exceed the per-SM shared memory of the slot kernel",
                                             (long long)N));
-    const int per_cta = std::max<int64_t>(1, SLOTS / std::min<int64_t>(gmax, SLOTS));
-    const int64_t want_ctas = (P + per_cta - 1) / per_cta;
+    const int per_cta = static_cast<int>(SLOTS / gk);
     const int cap = ctx->max_ctas > 0 ? ctx->max_ctas : ctx->sm_count * ctx->ctas_per_sm;
-    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want_ctas, cap)));
+    auto grid_for = [&](int64_t groups) {
+        const int64_t want_ctas = (groups + per_cta - 1) / per_cta;
+        return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want_ctas, cap)));
+    };
 
     BodyTable bt{};
     double *d_pos = nullptr, *d_ind = nullptr, *d_mu = nullptr;
@@ -713,6 +847,16 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
     int32_t fail_status = PSWARM_OK;
     pswarm_error fail{};
     init_err(&fail, PSWARM_OK, "");
+    // run_independent (runner.hpp:63-80) solves trajectory after trajectory, so the error the
+    // caller sees is the one of the LOWEST failing trajectory, whichever segment it fails in.
+    // Segment-synchronous processing meets the failures segment by segment: on the first one
+    // the lowest failing index c becomes pending and only trajectories [0, c) keep going; a
+    // failure among them in a later segment replaces it.  The partial outputs stay those of
+    // the first failing segment (every trajectory has rows up to there).
+    int64_t P_act = P, M_act = M;
+    bool pend = false;
+    pswarm_error pend_err{};
+    int64_t pend_rep = 0, pend_done = 0;
 
     for (int64_t seg = 0; seg < S; ++seg) {
         const double* seg_times = grid_times.data() + seg * N;
@@ -740,9 +884,9 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
         a.gp = op.gp;
         a.xrows = xrows;
         a.stage_eph = stage_eph;
-        a.M = static_cast<int>(M);
-        a.P = static_cast<int>(P);
-        a.gmax = static_cast<int>(gmax);
+        a.M = static_cast<int>(M_act);
+        a.P = static_cast<int>(P_act);
+        a.gmax = static_cast<int>(gk);
         a.seg = static_cast<int>(seg);
         a.cold_start = (seg == 0 && cfg->start_mode == 1) ? 1 : 0;
         a.error_mode = cfg->error_mode;
@@ -785,15 +929,18 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
         a.b0_mma = ctx->b0_mma;
         a.fast_decide = ctx->fast_decide;
         a.anc_fold = fold ? reinterpret_cast<const double*>(op.anc_fold.p) : nullptr;
+        a.hist_stride = max_it;
+        auto launch = [&](const SegArgs& x, int grid) {
+            return uni ? launch_segment_uni(x, grid, st) : use_ws ? launch_segment_ws(x, grid, st) : launch_segment(x, grid, st);
+        };
         if (max_it > 0 && !wide) {
             cuda_check(cudaEventRecord(ctx->evk0, st), "event");
-            cuda_check(uni ? launch_segment_uni(a, grid, st)
-                           : use_ws ? launch_segment_ws(a, grid, st) : launch_segment(a, grid, st),
-                       "slot kernel launch");
+            cuda_check(launch(a, grid_for(P_act)), "slot kernel launch");
             cuda_check(cudaEventRecord(ctx->evk1, st), "event");
             ++ctx->launches;
         } else if (max_it > 0) {
-            run_wide_segment(ctx, a, h_off, deadline);
+            solve_wide_rounds(ctx, a, launch, cap, h_off, P, max_it, deadline, d_iter, d_err, d_conv, d_faults,
+                              a.rep_hist, d_off, kernel_ms);
         }
         if (overlap_samples) {  // rows [row0 + jb, row0 + N - 1] of every trajectory, pitch R rows
             const int64_t jb = seg == 0 ? 0 : 1, row = seg * (N - 1) + jb, nrows = N - jb;
@@ -816,11 +963,10 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
         std::memcpy(h_conv.data() + seg * P, hrep + r_conv, P);
         std::memcpy(h_fb.data() + seg * M, hrep + r_fb, M);
         // fault records (48 B per group) only when some group stopped unconverged: every fault
-        // retires its group with converged = 0; the wide path adds host-side records below
+        // retires its group with converged = 0 (the wide rounds write their group records so too)
         bool any_unconverged = false;
-        for (int64_t gi = 0; gi < P && !any_unconverged; ++gi) any_unconverged = !h_conv[seg * P + gi];
-        const bool need_faults =
-            any_unconverged || (wide && (ctx->wide_timeout || ctx->wide_warm_key != ~0ull));
+        for (int64_t gi = 0; gi < P_act && !any_unconverged; ++gi) any_unconverged = !h_conv[seg * P + gi];
+        const bool need_faults = any_unconverged;
         if (need_faults) {
             h_faults.resize(static_cast<size_t>(P));
             cuda_check(cudaMemcpyAsync(h_faults.data(), drep + r_faults, sizeof(GroupFault) * P, cudaMemcpyDeviceToHost,
@@ -858,31 +1004,108 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
                 break;
             }
         }
-        if (max_it > 0) {
+        if (max_it > 0 && !wide) {  // (the wide rounds add their own launches)
             float kms = 0.f;
             cudaEventElapsedTime(&kms, ctx->evk0, ctx->evk1);
             kernel_ms += kms;
         }
-        for (int64_t gi = 0; gi < P; ++gi) traj_iters += static_cast<int64_t>(h_iter[seg * P + gi]) * group_sizes[gi];
-        if (wide && ctx->wide_timeout) {  // deadline between lockstep iterations (augment.hpp:117-121)
-            for (int64_t gi = 0; gi < P; ++gi)
+        for (int64_t gi = 0; gi < P_act; ++gi) traj_iters += static_cast<int64_t>(h_iter[seg * P + gi]) * group_sizes[gi];
+
+        // ---- the reference exception of one group's record (warm start, solve faults, timeout)
+        auto fault_error = [&](const GroupFault& f, int64_t gi, int64_t report_g, pswarm_error& e) {
+            if (f.status == FAULT_WARM_ZERO_RADIUS) {
+                init_err(&e, PSWARM_ERR_SINGULARITY, "kepler_propagate: zero-radius state");
+                e.trajectory = f.trajectory;
+            } else if (f.status == FAULT_WARM_SOLVER) {
+                init_err(&e, PSWARM_ERR_SOLVER,
+                         "solve_kepler: Newton iteration did not converge for M = " + std::to_string(f.value) +
+                             ", e = " + std::to_string(f.value2));
+                e.trajectory = f.trajectory;
+            } else if (f.status == FAULT_DIVERGENCE) {
+                init_err(&e, PSWARM_ERR_DIVERGENCE,
+                         "group " + std::to_string(report_g) + ": picard iteration produced a non-finite value at node " +
+                             std::to_string(f.node) + ", column " + std::to_string(f.column));
+                e.node = f.node;
+                e.column = f.column;
+            } else if (f.status == FAULT_SINGULARITY) {
+                std::string what, body;
+                if (f.body < 0) {
+                    what = "central-body acceleration at zero radius";
+                } else {
+                    body = bu.names[f.body];
+                    what = "close approach to body '" + body + "': distance " + std::to_string(f.value) +
+                           " km below floor " + std::to_string(cfg->proximity_floor_km) + " km";
+                }
+                init_err(&e, PSWARM_ERR_SINGULARITY,
+                         "node " + std::to_string(f.node) + ", trajectory " + std::to_string(f.trajectory) + ": " + what);
+                std::snprintf(e.body_name, sizeof e.body_name, "%s", body.c_str());
+                e.body = f.body;
+                e.node = f.node;
+                e.trajectory = f.trajectory;
+                e.value = f.value;
+            } else {
+                init_err(&e, PSWARM_ERR_TIMEOUT,
+                         "solve_group: wall-clock budget exhausted in group " + std::to_string(report_g));
+            }
+            if (f.status != FAULT_WARM_ZERO_RADIUS && f.status != FAULT_WARM_SOLVER) {
+                e.group = spec.independent ? 0 : gi;
+                e.iterations = f.iteration;
+            }
+            e.segment = seg;
+        };
+        // ---- non-convergence (propagator.hpp:300-312)
+        auto incomplete_error = [&](int64_t gi, pswarm_error& e) {
+            const int64_t report_g = spec.independent ? 0 : gi;
+            init_err(&e, PSWARM_ERR_INCOMPLETE,
+                     "propagate: group " + std::to_string(report_g) + " did not converge in segment " +
+                         std::to_string(seg) + " (error " + std::to_string(h_err[seg * P + gi]) + " after " +
+                         std::to_string(h_iter[seg * P + gi]) + " iterations)");
+            e.segment = seg;
+            e.group = report_g;
+            e.trajectory = spec.independent ? gi : -1;
+            e.iterations = h_iter[seg * P + gi];
+            e.value = h_err[seg * P + gi];
+        };
+        const auto solve_fault = [&](int64_t gi) {
+            return need_faults && h_faults[gi].status != FAULT_NONE &&
+                   (max_it > 0 || h_faults[gi].status == FAULT_WARM_ZERO_RADIUS ||
+                    h_faults[gi].status == FAULT_WARM_SOLVER);
+        };
+
+        if (spec.independent) {
+            // run_independent (runner.hpp:63-80): the lowest trajectory that fails in ANY way --
+            // warm start, solve fault or plain non-convergence (every fault retires its group
+            // with converged = 0) -- is the one the serial reference raises for
+            int64_t c = -1;
+            for (int64_t gi = 0; gi < P_act; ++gi)
                 if (!h_conv[seg * P + gi]) {
-                    h_faults[gi].status = FAULT_TIMEOUT;
+                    c = gi;
                     break;
                 }
-        }
-        if (wide && ctx->wide_warm_key != ~0ull) {  // warm-start fault of the wide path -> group record
-            const int64_t tr = static_cast<int64_t>(ctx->wide_warm_key / 4);
-            const int64_t gi = std::upper_bound(h_off.begin(), h_off.end(), tr) - h_off.begin() - 1;
-            GroupFault& f = h_faults[gi];
-            f = GroupFault{};
-            f.status = (ctx->wide_warm_key % 4) == CONIC_ZERO_RADIUS ? FAULT_WARM_ZERO_RADIUS : FAULT_WARM_SOLVER;
-            f.trajectory = tr;
-            f.value = ctx->wide_warm_vals[0];
-            f.value2 = ctx->wide_warm_vals[1];
+            if (c >= 0) {
+                if (solve_fault(c))
+                    fault_error(h_faults[c], c, 0, pend_err);
+                else
+                    incomplete_error(c, pend_err);
+                if (!pend) {  // partial outputs: every trajectory up to the first failing segment
+                    pend_rep = pend_err.status == PSWARM_ERR_INCOMPLETE ? seg + 1 : seg;
+                    pend_done = seg;
+                }
+                pend = true;
+                if (spec.fail_index) *spec.fail_index = c;
+                if (c == 0 || seg == S - 1) break;  // no lower trajectory is left to fail later
+                P_act = M_act = c;                  // only trajectories [0, c) continue
+            }
+            std::swap(d_in, d_out);
+            if (!pend) {
+                seg_done = seg + 1;
+                if (out) out->segments_reported = seg + 1;
+            }
+            continue;
         }
 
-        // ---- faults, in the order the serial reference would raise them
+        // ---- grouped / augmented: propagate's order -- warm start of the whole batch first
+        //      (lowest trajectory), then the groups' solves in group order
         int64_t warm_traj = -1, warm_g = -1, first_g = -1;
         for (int64_t gi = 0; gi < (need_faults ? P : 0); ++gi) {
             const GroupFault& f = h_faults[gi];
@@ -896,75 +1119,12 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
             }
         }
         if (max_it == 0 && P > 0) first_g = -1;
-        if (spec.independent && (warm_g >= 0 || first_g >= 0)) {
-            // run_independent: trajectory-major order; the lowest failing trajectory wins
-            // (runner.hpp:63-80).  Segment-synchronous processing reaches the first failing
-            // segment of every trajectory at the same time only if no lower index fails later;
-            // report the lowest index of this segment.
-            int64_t best = -1;
-            for (int64_t gi = 0; gi < P; ++gi)  // (reached only with fault records read back)
-                if (h_faults[gi].status != FAULT_NONE) {
-                    best = gi;
-                    break;
-                }
-            if (h_faults[best].status == FAULT_WARM_ZERO_RADIUS || h_faults[best].status == FAULT_WARM_SOLVER) {
-                warm_g = best;
-                first_g = -1;
-            } else {
-                warm_g = -1;
-                first_g = best;
-            }
-        }
-        if (warm_g >= 0) {
-            const GroupFault& f = h_faults[warm_g];
-            if (f.status == FAULT_WARM_ZERO_RADIUS) {
-                init_err(&fail, PSWARM_ERR_SINGULARITY, "kepler_propagate: zero-radius state");
-            } else {
-                init_err(&fail, PSWARM_ERR_SOLVER,
-                         "solve_kepler: Newton iteration did not converge for M = " + std::to_string(f.value) +
-                             ", e = " + std::to_string(f.value2));
-            }
-            fail.segment = seg;
-            fail.trajectory = f.trajectory;
+        if (warm_g >= 0 || first_g >= 0) {
+            fault_error(h_faults[warm_g >= 0 ? warm_g : first_g], warm_g >= 0 ? warm_g : first_g,
+                        warm_g >= 0 ? warm_g : first_g, fail);
             fail_status = fail.status;
             break;
         }
-        if (first_g >= 0) {
-            const GroupFault& f = h_faults[first_g];
-            const int64_t report_g = spec.independent ? 0 : first_g;
-            if (f.status == FAULT_DIVERGENCE) {
-                init_err(&fail, PSWARM_ERR_DIVERGENCE,
-                         "group " + std::to_string(report_g) + ": picard iteration produced a non-finite value at node " +
-                             std::to_string(f.node) + ", column " + std::to_string(f.column));
-                fail.node = f.node;
-                fail.column = f.column;
-            } else if (f.status == FAULT_SINGULARITY) {
-                std::string what, body;
-                if (f.body < 0) {
-                    what = "central-body acceleration at zero radius";
-                } else {
-                    body = bu.names[f.body];
-                    what = "close approach to body '" + body + "': distance " + std::to_string(f.value) +
-                           " km below floor " + std::to_string(cfg->proximity_floor_km) + " km";
-                }
-                init_err(&fail, PSWARM_ERR_SINGULARITY,
-                         "node " + std::to_string(f.node) + ", trajectory " + std::to_string(f.trajectory) + ": " + what);
-                std::snprintf(fail.body_name, sizeof fail.body_name, "%s", body.c_str());
-                fail.body = f.body;
-                fail.node = f.node;
-                fail.trajectory = f.trajectory;
-                fail.value = f.value;
-            } else {
-                init_err(&fail, PSWARM_ERR_TIMEOUT,
-                         "solve_group: wall-clock budget exhausted in group " + std::to_string(report_g));
-            }
-            fail.segment = seg;
-            fail.group = first_g;
-            fail.iterations = f.iteration;
-            fail_status = fail.status;
-            break;
-        }
-        // ---- non-convergence (propagator.hpp:300-312)
         int64_t nc = -1;
         for (int64_t gi = 0; gi < P; ++gi)
             if (!h_conv[seg * P + gi]) {
@@ -972,16 +1132,7 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
                 break;
             }
         if (nc >= 0) {
-            const int64_t report_g = spec.independent ? 0 : nc;
-            init_err(&fail, PSWARM_ERR_INCOMPLETE,
-                     "propagate: group " + std::to_string(report_g) + " did not converge in segment " +
-                         std::to_string(seg) + " (error " + std::to_string(h_err[seg * P + nc]) + " after " +
-                         std::to_string(h_iter[seg * P + nc]) + " iterations)");
-            fail.segment = seg;
-            fail.group = spec.independent ? 0 : nc;
-            fail.trajectory = spec.independent ? nc : -1;
-            fail.iterations = h_iter[seg * P + nc];
-            fail.value = h_err[seg * P + nc];
+            incomplete_error(nc, fail);
             fail_status = PSWARM_ERR_INCOMPLETE;
             seg_done = seg;
             if (out) out->segments_reported = seg + 1;
@@ -990,6 +1141,14 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
         std::swap(d_in, d_out);
         seg_done = seg + 1;
         if (out) out->segments_reported = seg + 1;
+    }
+    if (pend && fail_status == PSWARM_OK) {  // independent mode: the lowest failing trajectory
+        fail = pend_err;
+        fail_status = pend_err.status;
+    }
+    if (pend) {
+        seg_done = std::min(seg_done, pend_done);
+        if (out) out->segments_reported = pend_rep;
     }
     cuda_check(cudaEventRecord(ctx->ev1, st), "event");
     trace.mark("segments (device+host)");
@@ -1099,8 +1258,6 @@ pswarm_status pswarm_create(int32_t device, pswarm_ctx** out, pswarm_error* err)
         cuda_check(cudaEventCreate(&ctx->ev1), "cudaEventCreate");
         cuda_check(cudaEventCreate(&ctx->evk0), "cudaEventCreate");
         cuda_check(cudaEventCreate(&ctx->evk1), "cudaEventCreate");
-        for (auto& e : ctx->wide_ev) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
-        cuda_check(cudaHostAlloc(&ctx->wide_count_host, 4 * sizeof(int), cudaHostAllocDefault), "cudaHostAlloc");
         *out = ctx.release();
     });
 }
@@ -1124,9 +1281,6 @@ void pswarm_destroy(pswarm_ctx* ctx) {
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
     if (ctx->evk0) cudaEventDestroy(ctx->evk0);
     if (ctx->evk1) cudaEventDestroy(ctx->evk1);
-    for (auto& e : ctx->wide_ev)
-        if (e) cudaEventDestroy(e);
-    if (ctx->wide_count_host) cudaFreeHost(ctx->wide_count_host);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
 }
@@ -1540,6 +1694,19 @@ void pswarm_make_clone_batch(const double* base, int64_t count, double spread, u
     }
 }
 
+void* pswarm_pinned_alloc(size_t bytes) {
+    void* p = nullptr;
+    if (cudaHostAlloc(&p, std::max<size_t>(bytes, 64), cudaHostAllocDefault) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return p;
+}
+
+void pswarm_pinned_free(void* p) {
+    if (p) cudaFreeHost(p);
+}
+
 }  // extern "C"
 
 // ============================================================ multi-device ==
@@ -1705,6 +1872,7 @@ pswarm_status pswarm_run_batch_multi(pswarm_multi* mc, int64_t n_states, const d
             pswarm_error e{};
             pswarm_status st = PSWARM_OK;
             const double* term = nullptr;
+            int64_t fail_index = -1;
         };
         std::vector<Shard> sh(static_cast<size_t>(D));
         for (int r = 0; r < D; ++r) {
@@ -1738,6 +1906,7 @@ pswarm_status pswarm_run_batch_multi(pswarm_multi* mc, int64_t n_states, const d
             RunSpec spec;
             spec.independent = mode == 0;
             spec.term_dev = &x.term;
+            spec.fail_index = &x.fail_index;
             x.st = guarded(&x.e, [&] {
                 propagate_impl(mc->ctx[r], x.M, states + 7 * x.lo, x.P, sizes.data() + g_lo[r], n_boundaries,
                                boundaries, n_nodes, config, &x.o, spec);
@@ -1755,10 +1924,8 @@ pswarm_status pswarm_run_batch_multi(pswarm_multi* mc, int64_t n_states, const d
         int pick = -1;
         auto key = [&](int r) {
             const pswarm_error& e = sh[r].e;
-            if (mode == 0) {
-                const int64_t t = e.trajectory >= 0 ? e.trajectory : 0;
-                return std::make_tuple(int64_t{0}, int64_t{0}, sh[r].lo + t);
-            }
+            if (mode == 0)  // ephemeris / validation errors (no failing trajectory) come first
+                return std::make_tuple(int64_t{0}, int64_t{0}, sh[r].fail_index >= 0 ? sh[r].lo + sh[r].fail_index : -1);
             const int64_t seg = e.segment >= 0 ? e.segment : -1;
             return std::make_tuple(seg, int64_t{e.status == PSWARM_ERR_INCOMPLETE ? 1 : 0},
                                    g_lo[r] + std::max<int64_t>(e.group, 0));
@@ -1806,7 +1973,9 @@ pswarm_status pswarm_run_batch_multi(pswarm_multi* mc, int64_t n_states, const d
         }
         if (pick >= 0) {
             pswarm_error e = sh[pick].e;
-            if (mode == 0 && e.trajectory >= 0) e.trajectory += sh[pick].lo;  // batch index
+            // batch index (a solve singularity names the trajectory within its singleton group)
+            if (mode == 0 && e.trajectory >= 0 && !(e.status == PSWARM_ERR_SINGULARITY && e.node >= 0))
+                e.trajectory += sh[pick].lo;
             if (mode != 0 && e.group >= 0) e.group += g_lo[pick];
             CapiFault f;
             f.e = e;

@@ -17,7 +17,7 @@ HEADER = os.path.join(ROOT, "include", "pswarm_gpu.h")
 
 def declared_symbols():
     text = open(HEADER).read()
-    decl = r"^\s*(?:pswarm_status|void|int32_t|const char\s*\*)\s+(pswarm_[a-z_0-9]+)\s*\("
+    decl = r"^\s*(?:pswarm_status|void\s*\*|void|int32_t|const char\s*\*)\s*(pswarm_[a-z_0-9]+)\s*\("
     return sorted(set(re.findall(decl, text, flags=re.M)))
 
 

@@ -94,8 +94,8 @@ def test_c2_nbody_independent(ctx, oracle, bodies):
 @pytest.mark.parametrize("mode,p,m", [("grouped", 8, 64), ("grouped", 16, 64), ("augmented", 1, 8),
                                       ("augmented", 1, 64), ("grouped", 2, 64), ("grouped", 3, 50)])
 def test_group_modes_match_oracle(ctx, oracle, mode, p, m):
-    """Groups within one CTA (<= 8 members, slot kernel) and wide groups (lockstep
-    iterations through HBM): a group stops only when its worst member converges."""
+    """Groups within one CTA (<= 8 members, slot kernel) and wide groups (member-level
+    rounds on the slot kernels): a group stops only when its worst member converges."""
     states, plan, cfg = _setup(m, 128, 0.6)
     cfg.p_groups = p
     got = ctx.run_batch(states, cfg, plan, mode)
@@ -345,14 +345,14 @@ def test_unified_tile_plans(ctx, oracle, n, kind):
 @pytest.mark.parametrize("n", [17, 23, 31, 49, 55, 63, 225, 241])
 @pytest.mark.parametrize("mode,p", [("independent", 1), ("grouped", 3), ("augmented", 1)])
 def test_small_n_staged_rows(ctx, oracle, n, mode, p):
-    """The 128-thread small-N plan of the generic and wide-group kernels stages up to 31
+    """The 128-thread small-N plan of the generic slot kernel (also the wide-group rounds) stages up to 31
     rows x 8 slots (more items than threads): every staged row must be finalised."""
     states, plan, cfg = _setup(12, n, 0.4, "planets8")
     cfg.p_groups = p
     ctx.set_option("slot_kernel", 1)  # the generic slot kernel where the mode allows it
     try:
         got = ctx.run_batch(states, cfg, plan, mode)
-        assert ctx.kernel_name() in ("k_pc_segment", "k_wide_iter")
+        assert ctx.kernel_name() == "k_pc_segment"
     finally:
         ctx.set_option("slot_kernel", 0)
     want = oracle.run_batch(states, cfg, plan, mode, 8)
@@ -432,3 +432,115 @@ def test_reference_acceptance_program_on_device():
     assert len(lines) == 9, r.stdout + r.stderr
     numeric = [l for l in lines if not any(f"criterion {k}:" in l for k in (6, 7))]
     assert all(l.startswith("PASS") for l in numeric), numeric
+
+
+def _raise_info(fn):
+    try:
+        fn()
+    except ps.Error as e:
+        return type(e).__name__, str(e), getattr(e, "segment", None)
+    return None
+
+
+def test_independent_error_order_lowest_trajectory(ctx, oracle):
+    """run_independent (runner.hpp:63-80) solves trajectory after trajectory: trajectory 0
+    running out of iterations is raised before trajectory 5's divergence in the same
+    segment (the serial reference never reaches trajectory 5)."""
+    states, plan, cfg = _setup(8, 64, 0.5, bodies="two_body", start="cold")
+    el = [0.8e8, 0.3, 0.05, 0.4, 0.9, 0.0, 0.0]  # tighter orbit: needs more iterations
+    states[0, 1:] = ps.elements_to_state(el, ps.MU_SUN, 0.0)[1:]
+    states[5, 1:4] = [1e-110, 0.0, 0.0]
+    ok = ctx.run_batch(np.delete(states, 5, axis=0), cfg, plan, "independent")
+    it = ok.iterations[0]
+    assert it[0] > it[1:].max()  # trajectory 0 is the slow one
+    cfg.max_iterations = int(it[1:].max()) + 1
+    got = _raise_info(lambda: ctx.run_batch(states, cfg, plan, "independent"))
+    want = _raise_info(lambda: oracle.run_batch(states, cfg, plan, "independent", 1))
+    assert want[0] == "PropagationIncompleteError"
+    assert got == want
+
+
+def test_independent_error_order_later_segment(ctx, oracle):
+    """Trajectory 1 diverges in segment 0, trajectory 0 fails to converge in segment 1:
+    the serial reference raises trajectory 0's error (segment 1)."""
+    states, plan, cfg = _setup(4, 64, 0.5, bodies="reference", start="cold")
+    period = ps.osculating_period(ps.reference_state(), ps.MU_SUN)
+    plan = ps.SegmentPlan(np.array([0.0, 0.05 * period, 0.9 * period]), 64)
+    ok = ctx.run_batch(states, cfg, plan, "independent")
+    k0, k1 = int(ok.iterations[0].max()), int(ok.iterations[1].max())
+    assert k1 > k0
+    cfg.max_iterations = k0 + 1
+    states[1, 1:4] = [1e-110, 0.0, 0.0]
+    got = _raise_info(lambda: ctx.run_batch(states, cfg, plan, "independent"))
+    want = _raise_info(lambda: oracle.run_batch(states, cfg, plan, "independent", 1))
+    assert want[0] == "PropagationIncompleteError" and want[2] == 1
+    assert got == want
+
+
+_FAR = ([0.8e8, 0.3, 0.05, 0.4, 0.9, 0.0, 0.0], [0.9e8, 0.2, 0.1, 0.2, 0.5, 0.3, 0.0])
+_NEAR = ([1.15e8, 0.2, 0.05, 0.4, 0.9, 0.0, 0.0], [1.3e8, 0.08, 0.1, 0.2, 0.5, 0.3, 0.0])
+
+
+def _mixed_states(m, elements=_FAR):
+    """Clones of three different orbits interleaved: members of one group converge at
+    different iteration counts, so a wide group needs several member-level rounds."""
+    base = ps.reference_state()
+    other = [ps.elements_to_state(el, ps.MU_SUN, 0.0) for el in elements]
+    states = ps.make_clone_batch(base, m, 1e-5)
+    for i in range(m):
+        if i % 3:
+            states[i, 1:] = other[i % 3 - 1][1:] * (1.0 + 1e-6 * i)
+    return states
+
+
+@pytest.mark.parametrize("mode,p", [("augmented", 1), ("grouped", 3), ("grouped", 5)])
+@pytest.mark.parametrize("start", ["warm", "cold"])
+def test_wide_groups_heterogeneous(ctx, oracle, mode, p, start):
+    """Wide groups whose members converge at different counts (several rounds): group
+    iterations exact, states within 1e-10, and the group error history equal to the
+    oracle's max over members while it is above the noise floor."""
+    states, plan, cfg = _setup(60, 64, 0.5, bodies="reference", start=start)
+    states = _mixed_states(60)
+    cfg.p_groups = p
+    got = ctx.run_batch(states, cfg, plan, mode)
+    want = oracle.run_batch(states, cfg, plan, mode, 4)
+    _parity(got, want)
+    assert np.array_equal(got.iterations, want.iterations)
+    ind = oracle.run_batch(states, cfg, plan, "independent", 8)
+    assert ind.iterations.min() < got.iterations.max()  # members really differ
+    for g in range(p):
+        a, b = got.reports[0][g].per_iteration_errors, want.reports[0][g].per_iteration_errors
+        assert len(a) == len(b)
+        big = b > 1e-8
+        assert np.allclose(a[big], b[big], rtol=1e-4, atol=0)
+
+
+def test_wide_groups_multisegment_hot(ctx, oracle):
+    """Wide groups across per-orbit segments with hot start (EXTENSION): resumed members
+    carry the hot-start correction of the group's final iterate."""
+    base = ps.reference_state()
+    states = _mixed_states(40, _NEAR)
+    period = ps.osculating_period(base, ps.MU_SUN)
+    plan = ps.plan_segments(base, 0.0, 2.0 * period, ps.MU_SUN, "per_orbit", 64)
+    cfg = ps.reference_force_config("n_body", bodies=ps.reference_bodies(), n_nodes=64, start_mode="hot")
+    got = ctx.propagate(states, [13, 27], plan, cfg)
+    want = oracle.propagate(states, [13, 27], plan, cfg)
+    _parity(got, want)
+
+
+def test_wide_group_nonconvergence_runs_all_members(ctx, oracle):
+    """One slow member out of iterations: the whole wide group runs to max_iterations and
+    reports the group error there (propagator.hpp:300-312)."""
+    states = _mixed_states(30)
+    _, plan, cfg = _setup(30, 64, 0.5, bodies="two_body", start="cold")
+    ind = oracle.run_batch(states, cfg, plan, "independent", 8)
+    cfg.max_iterations = int(ind.iterations.max()) - 4  # group error ~1e-10, above the noise floor
+    errs = []
+    for impl in (ctx, oracle):
+        with pytest.raises(ps.PropagationIncompleteError) as e:
+            impl.propagate(states, [30], plan, cfg)
+        errs.append(e.value)
+    assert (errs[0].segment, errs[0].group) == (errs[1].segment, errs[1].group)
+    a, b = errs[0].partial.reports[0][0], errs[1].partial.reports[0][0]
+    assert a.iterations == b.iterations == cfg.max_iterations
+    assert abs(a.final_error - b.final_error) <= 1e-3 * b.final_error
