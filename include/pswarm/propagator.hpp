@@ -6,6 +6,10 @@
 // the host receives terminal states, node samples and per-(segment, group) reports.
 
 #include <chrono>
+#include <condition_variable>
+#include <cstdint>
+#include <functional>
+#include <mutex>
 #include <cmath>
 #include <memory>
 #include <optional>
@@ -249,6 +253,74 @@ struct ConfigMarshal {
 };
 
 /// Host buffers of one device call and their conversion into a PropagationResult.
+/// Persistent host helper threads for the result assembly (created on first use, kept for
+/// the process): a call with W workers costs no thread creation, and each helper keeps its
+/// malloc arena warm across calls.  run(n, fn) executes fn(0..n-1), the caller taking 0.
+class HostPool {
+public:
+    static HostPool& instance() {
+        static HostPool pool;
+        return pool;
+    }
+    void run(unsigned n, const std::function<void(unsigned)>& fn) {
+        if (n <= 1) {
+            if (n == 1) fn(0);
+            return;
+        }
+        std::lock_guard call(call_mu_);  // one assembly at a time
+        {
+            std::unique_lock lk(mu_);
+            while (threads_.size() < n - 1) {
+                const unsigned id = static_cast<unsigned>(threads_.size()) + 1;
+                threads_.emplace_back([this, id] { loop(id); });
+            }
+            job_ = &fn;
+            active_ = n;
+            pending_ = n - 1;
+            ++generation_;
+        }
+        cv_start_.notify_all();
+        fn(0);
+        std::unique_lock lk(mu_);
+        cv_done_.wait(lk, [&] { return pending_ == 0; });
+        job_ = nullptr;
+    }
+    ~HostPool() {
+        {
+            std::lock_guard lk(mu_);
+            stop_ = true;
+        }
+        cv_start_.notify_all();
+        for (auto& t : threads_) t.join();
+    }
+
+private:
+    void loop(unsigned id) {
+        std::uint64_t seen = 0;
+        for (;;) {
+            const std::function<void(unsigned)>* job;
+            {
+                std::unique_lock lk(mu_);
+                cv_start_.wait(lk, [&] { return stop_ || generation_ != seen; });
+                if (stop_) return;
+                seen = generation_;
+                if (id >= active_) continue;
+                job = job_;
+            }
+            (*job)(id);
+            std::lock_guard lk(mu_);
+            if (--pending_ == 0) cv_done_.notify_all();
+        }
+    }
+    std::mutex call_mu_, mu_;
+    std::condition_variable cv_start_, cv_done_;
+    std::vector<std::thread> threads_;
+    const std::function<void(unsigned)>* job_ = nullptr;
+    unsigned active_ = 0, pending_ = 0;
+    std::uint64_t generation_ = 0;
+    bool stop_ = false;
+};
+
 /// Per-thread, grow-only page-locked staging for the large per-call outputs (node samples,
 /// error histories, terminal states): the device writes them at DMA speed and no call pays
 /// fresh-page faults for megabytes of result buffers.  to_result copies out of it, so it is
@@ -332,10 +404,8 @@ struct OutputBuffers {
         if (W == 1 || M * R * 6 < (Index{1} << 16)) {
             fill(0, M);
         } else {  // contiguous chunks, as the reference pool's parallel_chunks (thread_pool.hpp:44-62)
-            std::vector<std::thread> pool;
-            for (Index w = 1; w < W; ++w) pool.emplace_back(fill, M * w / W, M * (w + 1) / W);
-            fill(0, M / W);
-            for (auto& t : pool) t.join();
+            HostPool::instance().run(static_cast<unsigned>(W),
+                                     [&](unsigned w) { fill(M * w / W, M * (w + 1) / W); });
         }
         if (complete)
             for (Index i = 0; i < M; ++i) r.terminal_states.push_back(unpack_state(terminal + 7 * i));

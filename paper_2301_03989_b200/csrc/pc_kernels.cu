@@ -40,6 +40,8 @@ struct CtaState {
     int grp_id[SLOTS];         // global group id, -1 = free
     int grp_size[SLOTS];
     int grp_iter[SLOTS];
+    int grp_floor[SLOTS];  // wide-group round: converge only at it >= floor
+    int grp_cap[SLOTS];    // stop at it >= cap (max_iterations, or a round's target)
     int active_mask;
     int new_mask;
     int retire_mask;           // slots whose results are written out this tick
@@ -183,6 +185,8 @@ __global__ void __launch_bounds__(MAXT, 1) k_pc_segment(const SegArgs a) {
                     st.grp_id[lg] = gid;
                     st.grp_size[lg] = size;
                     st.grp_iter[lg] = start_iteration(a, off);
+                    st.grp_floor[lg] = claim_floor(a, gid);
+                    st.grp_cap[lg] = claim_cap(a, gid);
                     int t = 0;
                     for (int mbr = 0; mbr < size; ++mbr) {
                         while ((am >> t) & 1) ++t;
@@ -529,9 +533,9 @@ __global__ void __launch_bounds__(MAXT, 1) k_pc_segment(const SegArgs a) {
                         retire = true;
                     } else {
                         if (a.rep_hist) a.rep_hist[static_cast<size_t>(gid) * a.hist_stride + (it - 1)] = gerr;
-                        if (gerr <= a.tol && may_converge(a, gid, it)) {
+                        if (gerr <= a.tol && it >= st.grp_floor[lg]) {
                             retire = ok = conv = true;
-                        } else if (at_cap(a, gid, it)) {
+                        } else if (it >= st.grp_cap[lg]) {
                             retire = ok = true;
                         }
                     }

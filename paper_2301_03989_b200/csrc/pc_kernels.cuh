@@ -108,10 +108,12 @@ __device__ __forceinline__ void claim_group(const SegArgs& a, int gi, int& off, 
 }
 /// Iteration count a claimed trajectory starts from (> 0: resumed from a.blk).
 __device__ __forceinline__ int start_iteration(const SegArgs& a, int traj) { return a.it_start ? a.it_start[traj] : 0; }
-/// pc_solve's stopping rule with the member-level floor / cap of a wide-group round.
-__device__ __forceinline__ bool may_converge(const SegArgs& a, int gid, int it) { return !a.it_floor || it >= a.it_floor[gid]; }
-__device__ __forceinline__ bool at_cap(const SegArgs& a, int gid, int it) {
-    return it >= a.max_it || (a.it_cap && it >= a.it_cap[gid]);
+/// pc_solve's stopping rule with the member-level floor / cap of a wide-group round, fixed
+/// at claim time into the CTA's group record: the decisions (on the kernel's critical
+/// chain) compare against shared memory only.
+__device__ __forceinline__ int claim_floor(const SegArgs& a, int gid) { return a.it_floor ? a.it_floor[gid] : 0; }
+__device__ __forceinline__ int claim_cap(const SegArgs& a, int gid) {
+    return a.it_cap ? min(a.max_it, a.it_cap[gid]) : a.max_it;
 }
 /// Resumed slot (wide-group round): node row j of the saved iterate; the hot-start record
 /// (the previous retire's correction) is turned back into this segment's base.

@@ -96,6 +96,8 @@ struct WsState {
     int grp_id[SLOTS];
     int grp_size[SLOTS];
     int grp_iter[SLOTS];
+    int grp_floor[SLOTS];  // wide-group round: converge only at it >= floor
+    int grp_cap[SLOTS];    // stop at it >= cap (max_iterations, or a round's target)
     int act_word[2];     // active slots of half h (bits h*HS..h*HS+3); the MMA group reads
                          // act_word[h] while the FP group claims into act_word[h ^ 1]
     int new_mask[2];     // slots claimed at the last refill of each half
@@ -699,9 +701,9 @@ __device__ __forceinline__ void decide_single(const SegArgs& a, WsState& st, int
                     (e2b <= __double_as_longlong(a.tol2_lo)
                          ? true
                          : (e2b > __double_as_longlong(a.tol2_hi) ? false : sqrt(gerr2) <= a.tol));
-                if (le_tol && may_converge(a, gid, it)) {
+                if (le_tol && it >= st.grp_floor[lg]) {
                     retire = ok = conv = true;
-                } else if (at_cap(a, gid, it)) {
+                } else if (it >= st.grp_cap[lg]) {
                     retire = ok = true;
                 }
             }
@@ -833,9 +835,9 @@ __device__ __forceinline__ void decide_half(const SegArgs& a, WsState& st, int h
                     (e2b <= __double_as_longlong(a.tol2_lo)
                          ? true
                          : (e2b > __double_as_longlong(a.tol2_hi) ? false : gerr_of() <= a.tol));
-                if (le_tol && may_converge(a, gid, it)) {
+                if (le_tol && it >= st.grp_floor[lg]) {
                     retire = ok = conv = true;
-                } else if (at_cap(a, gid, it)) {
+                } else if (it >= st.grp_cap[lg]) {
                     retire = ok = true;
                 }
             }
@@ -1241,6 +1243,8 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
                         st.grp_id[lg] = gid;
                         st.grp_size[lg] = size;
                         st.grp_iter[lg] = start_iteration(a, off);
+                        st.grp_floor[lg] = claim_floor(a, gid);
+                        st.grp_cap[lg] = claim_cap(a, gid);
                         int t = h * HS;
                         for (int mbr = 0; mbr < size; ++mbr) {
                             while ((am >> t) & 1) ++t;
@@ -1690,6 +1694,8 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_uni(const SegArgs a) {
                         st.grp_id[lg] = gid;
                         st.grp_size[lg] = size;
                         st.grp_iter[lg] = start_iteration(a, off);
+                        st.grp_floor[lg] = claim_floor(a, gid);
+                        st.grp_cap[lg] = claim_cap(a, gid);
                         int t = h * HS;
                         for (int mbr = 0; mbr < size; ++mbr) {
                             while ((am >> t) & 1) ++t;
