@@ -39,6 +39,44 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 #endif
 }
 
+// ------------------------------------------------- bulk copy (TMA engine) ---
+/// One-shot global -> shared staging through the TMA unit: cp.async.bulk (SASS UBLKCP)
+/// completing on an mbarrier's transaction count.  One thread arms the barrier and issues
+/// the copies; every consumer waits on phase 0.  Addresses 16-byte aligned, sizes
+/// multiples of 16 bytes, at most 2^20 - 1 bytes per barrier phase.
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+/// Stage `bytes` (multiple of 16) from global to shared memory in <= 64 KB bulk copies on
+/// one barrier (thread `leader` issues; the caller waits with mbar_wait(bar, 0)).
+__device__ __forceinline__ void bulk_stage(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    mbar_expect_tx(bar, bytes);
+    for (unsigned o = 0; o < bytes; o += 65536u)
+        bulk_g2s(static_cast<char*>(dst) + o, static_cast<const char*>(src) + o, min(65536u, bytes - o), bar);
+}
+
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -272,7 +310,8 @@ struct ForceData {
     int n_bodies;      // 0 for two-body
     int rel;           // 1: n_body_1pn (EXTENSION) -> add rel_correction()
     double ic2;        // 1 / c^2 (km^-2 s^2)
-    const double* rel_tab;  // [N][B+1][REL_W]: Sun + bodies at each node (k_ephemeris)
+    const double* rel_tab;  // [N][rel_stride(B)]: Sun + bodies + indirect term at each node (k_ephemeris)
+    const double* eph_t;    // [3B + 3][eph_ld(N)]: positions (3b + c) then the indirect term, node-contiguous
 };
 
 // ------------------------------------------------------- relativistic (EXTENSION) ---
@@ -280,6 +319,17 @@ struct ForceData {
 /// position, velocity, Newtonian heliocentric acceleration, mu and
 /// K_A = (2 v_A^2 - phi_A) / c^2 with phi_A the potential of the other massive bodies at A.
 constexpr int REL_W = 12;
+/// Node stride of the relativistic table (doubles): B + 1 rows of REL_W, then the node's
+/// indirect term [3]; odd, so consecutive nodes (the force threads of a warp) fall in
+/// distinct shared-memory banks when the table is staged.
+__host__ __device__ constexpr int rel_stride(int B) { return (B + 1) * REL_W + 3; }
+/// Row length of the node-contiguous ephemeris eph_t (N rounded up to even: 16-byte rows).
+__host__ __device__ constexpr int eph_ld(int N) { return (N + 1) & ~1; }
+/// Doubles of the per-segment table a slot kernel stages in shared memory (16-byte multiple).
+__host__ __device__ constexpr size_t eph_stage_doubles(int N, int B, bool rel) {
+    return rel ? ((static_cast<size_t>(N) * rel_stride(B) + 1) & ~static_cast<size_t>(1))
+               : static_cast<size_t>(3 * B + 3) * eph_ld(N);
+}
 
 /// First post-Newtonian (EIH, beta = gamma = 1) correction for a massless particle
 /// (Explanatory Supplement 1992 eq. 8.1) in one pass over the massive

@@ -622,7 +622,8 @@ cudaError_t launch_segment(const SegArgs& a, int grid, cudaStream_t s) {
 
 __global__ void k_ephemeris(int N, const double* __restrict__ times, double central_mu, BodyTable bt,
                             double* __restrict__ pos, double* __restrict__ indirect, unsigned long long* fault_key,
-                            double* __restrict__ vel, double* __restrict__ rel_tab, double ic2) {
+                            double* __restrict__ vel, double* __restrict__ rel_tab, double ic2,
+                            double* __restrict__ eph_t) {
     const int j = blockIdx.x, b = threadIdx.x;
     const double t = times[j];
     const bool rel = rel_tab != nullptr;
@@ -659,6 +660,8 @@ __global__ void k_ephemeris(int N, const double* __restrict__ times, double cent
         o[0] = p[0];
         o[1] = p[1];
         o[2] = p[2];
+        if (eph_t)  // node-contiguous copy for the slot kernels' bulk staging
+            for (int c = 0; c < 3; ++c) eph_t[static_cast<size_t>(3 * b + c) * eph_ld(N) + j] = p[c];
         if (rel) {
             double* w = vel + (static_cast<size_t>(j) * bt.B + b) * 3;
             w[0] = v[0];
@@ -677,12 +680,16 @@ __global__ void k_ephemeris(int N, const double* __restrict__ times, double cent
             for (int c = 0; c < 3; ++c) s[c] += mu * (q[c] / bn3);
         }
         for (int c = 0; c < 3; ++c) indirect[j * 3 + c] = s[c];
+        if (eph_t)
+            for (int c = 0; c < 3; ++c) eph_t[static_cast<size_t>(3 * bt.B + c) * eph_ld(N) + j] = s[c];
+        if (rel)  // the node row of the relativistic table ends with the indirect term
+            for (int c = 0; c < 3; ++c) rel_tab[static_cast<size_t>(j) * rel_stride(bt.B) + (bt.B + 1) * REL_W + c] = s[c];
     }
     if (rel && b <= bt.B) {
         // EXTENSION: relativistic node table row A = b (0 = Sun): Newtonian heliocentric
         // acceleration of body A and the potential of the other massive bodies at A
         const double* P = pos + static_cast<size_t>(j) * bt.B * 3;
-        double* row = rel_tab + (static_cast<size_t>(j) * (bt.B + 1) + b) * REL_W;
+        double* row = rel_tab + static_cast<size_t>(j) * rel_stride(bt.B) + b * REL_W;
         double r[3] = {0.0, 0.0, 0.0}, v[3] = {0.0, 0.0, 0.0}, acc[3] = {0.0, 0.0, 0.0}, phi = 0.0, mu = central_mu;
         if (b == 0) {
             for (int k = 0; k < bt.B; ++k) {
@@ -807,10 +814,10 @@ cudaError_t launch_group_hist(const double* mh, int stride, const int64_t* group
 
 cudaError_t launch_ephemeris(int N, const double* times, double central_mu, const BodyTable& bt, double* pos,
                              double* indirect, unsigned long long* fault_key, double* vel, double* rel_tab, double ic2,
-                             cudaStream_t s) {
+                             double* eph_t, cudaStream_t s) {
     if (bt.B <= 0 && rel_tab == nullptr) return cudaSuccess;
     const int threads = 32 * ((bt.B + 1 + 31) / 32);
-    k_ephemeris<<<N, threads, 0, s>>>(N, times, central_mu, bt, pos, indirect, fault_key, vel, rel_tab, ic2);
+    k_ephemeris<<<N, threads, 0, s>>>(N, times, central_mu, bt, pos, indirect, fault_key, vel, rel_tab, ic2, eph_t);
     return cudaGetLastError();
 }
 

@@ -147,11 +147,12 @@ struct BodyTable {
 /// times and the indirect term [N][3] (ephemeris.hpp:89-107, force_model.hpp:50-51).
 /// fault_key = min over (body, node) of (b*N + j)*4 + kind (1 coverage, 3 solver).
 /// Relativistic model (EXTENSION, rel_tab != nullptr): also body velocities vel [N][B][3]
-/// and the node table rel_tab [N][B+1][REL_W] (Sun row first).
+/// and the node table rel_tab [N][rel_stride(B)] (Sun row first, the indirect term last).
+/// eph_t (optional): positions and indirect term node-contiguous, [3B + 3][eph_ld(N)].
 cudaError_t launch_repack_states(const double* s7, double* s6, long long M, cudaStream_t s);
 cudaError_t launch_ephemeris(int N, const double* times, double central_mu, const BodyTable& bt, double* pos,
                              double* indirect, unsigned long long* fault_key, double* vel, double* rel_tab, double ic2,
-                             cudaStream_t s);
+                             double* eph_t, cudaStream_t s);
 
 /// Wide-group path (member-level rounds): trajectory list 0..n-1 and the group error history
 /// gh[P][stride] = max over members of mh[M][stride] for k < K[g], NaN beyond (gh zeroed first).
@@ -181,7 +182,7 @@ cudaError_t launch_rk_check(const RkArgs& a, cudaStream_t s);
 
 /// Warp-specialised slot kernel (pc_slots2.cu) for groups of <= 4 trajectories.
 /// fold: mirror-folded update (two half-size contractions, pc_slots2.cu ws_layout notes).
-size_t ws_smem_bytes(int N, int nkp, int xrows, int B, int stage_eph, bool fold);
+size_t ws_smem_bytes(int N, int nkp, int xrows, int B, int stage_eph, bool fold, bool rel = false);
 int ws_main_tiles(int N, bool fold);
 int ws_extra_rows(int N, bool fold);
 bool ws_supported(int N, bool fold);

@@ -81,6 +81,7 @@ __device__ __forceinline__ void bar_arrive(int id, int n) {
 }
 
 struct WsState {
+    uint64_t stage_bar;  // mbarrier of the per-launch bulk staging of the ephemeris
     int slot_traj[SLOTS];
     int slot_grp[SLOTS];
     int slot_member[SLOTS];
@@ -127,7 +128,7 @@ __host__ __device__ inline int ws_fold_ksteps(int N, int nkp) {
     return need > 2 * nkp ? need + (need & 1) : 2 * nkp;
 }
 
-__host__ __device__ inline WsLayout ws_layout(int N, int nkp, int xrows, int B, int stage_eph, int fold) {
+__host__ __device__ inline WsLayout ws_layout(int N, int nkp, int xrows, int B, int stage_eph, int fold, bool rel = false) {
     WsLayout L;
     L.ybuf = 0;
     L.fbuf0 = L.ybuf + sizeof(double) * static_cast<size_t>(N) * YS2;
@@ -136,8 +137,10 @@ __host__ __device__ inline WsLayout ws_layout(int N, int nkp, int xrows, int B, 
     L.xstage = L.fbuf1 + fb;  // [2 halves][fold ? lo, hi : 1][xrows][HC]
     L.anchor = L.xstage + sizeof(double) * (fold ? 4 : 2) * static_cast<size_t>(xrows) * HC;
     L.b0part = L.anchor + sizeof(double) * static_cast<size_t>(8 * nkp);
-    L.eph = L.b0part + sizeof(double) * 2 * B0_PARTS * HC;  // [half][part][HC] (k_pc_uni forms both at once)
-    L.state = L.eph + (stage_eph ? sizeof(double) * static_cast<size_t>(N) * (3 * B + 3) : 0);
+    // staged table (bulk copy target, 16-byte aligned): Newtonian eph_t [3B + 3][eph_ld(N)], or
+    // the relativistic node table [N][rel_stride(B)]
+    L.eph = (L.b0part + sizeof(double) * 2 * B0_PARTS * HC + 15) & ~static_cast<size_t>(15);  // b0part: [half][part][HC]
+    L.state = L.eph + (stage_eph ? sizeof(double) * eph_stage_doubles(N, B, rel) : 0);
     L.total = L.state + sizeof(WsState);
     return L;
 }
@@ -356,14 +359,13 @@ __device__ __forceinline__ void gemm_half_fold(const double2* __restrict__ upf, 
 /// Newtonian sum and the EIH 1PN terms from the same d, |d|^-1 (see rel_correction for the
 /// factorisation); the reference's singularity guards run exactly on the slow path.
 template <int NS>
-__device__ __forceinline__ void force_half_rel(const ForceData& fd, const double* ybuf, double* fb,
-                                               int* sing_key, int act_h, int h, int j, int s_begin) {
+__device__ __forceinline__ void force_half_rel(const ForceData& fd, const double* rel_base, const double* ybuf,
+                                               double* fb, int* sing_key, int act_h, int h, int j, int s_begin) {
     constexpr int PAIR = NS < 2 ? NS : 2;  // slots per fused pass
     const int B = fd.n_bodies, nb1 = B + 1;
     const double ic2 = fd.ic2;
-    const double* rt = fd.rel_tab + static_cast<size_t>(j) * nb1 * REL_W;
-    const double ix = B > 0 ? fd.indirect[3 * j] : 0.0, iy = B > 0 ? fd.indirect[3 * j + 1] : 0.0,
-                 iz = B > 0 ? fd.indirect[3 * j + 2] : 0.0;
+    const double* rt = rel_base + static_cast<size_t>(j) * rel_stride(B);  // staged (smem) or global
+    const double ix = rt[nb1 * REL_W], iy = rt[nb1 * REL_W + 1], iz = rt[nb1 * REL_W + 2];
 #pragma unroll 1
     for (int s0 = s_begin; s0 < s_begin + NS; s0 += PAIR) {
         double rx[PAIR], ry[PAIR], rz[PAIR], vx[PAIR], vy[PAIR], vz[PAIR];
@@ -385,6 +387,8 @@ __device__ __forceinline__ void force_half_rel(const ForceData& fd, const double
             wx[k] = wy[k] = wz[k] = qx[k] = qy[k] = qz[k] = 0.0;
             flag |= !(rx[k] * rx[k] + ry[k] * ry[k] + rz[k] * rz[k] > 0.0);
         }
+        // single chain (small N): 3 bodies in flight for ILP; slot pairs already give 2 chains
+#pragma unroll(PAIR == 1 ? 3 : 1)
         for (int A = 0; A < nb1; ++A) {
             const double* t = rt + A * REL_W;
             const double tx = t[0], ty = t[1], tz = t[2], vax = t[3], vay = t[4], vaz = t[5];
@@ -870,7 +874,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
     const int N = a.N, B = a.fd.n_bodies;
     const int xrows = a.xrows;
     const int half = N / 2;
-    const WsLayout L = ws_layout(N, a.nkp, xrows, B, STAGE ? 1 : 0, FOLD ? 1 : 0);
+    const WsLayout L = ws_layout(N, a.nkp, xrows, B, STAGE ? 1 : 0, FOLD ? 1 : 0, REL);
     double* ybuf = reinterpret_cast<double*>(smem_raw + L.ybuf);
     const size_t fb_bytes = L.fbuf1 - L.fbuf0;
     double* fb0 = reinterpret_cast<double*>(smem_raw + L.fbuf0);
@@ -898,6 +902,15 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
     hp.mb = MAIN * MMA_WARPS;
     hp.extras = (mtiles - hp.mb) * 3;
 
+    // ---- per-launch staging of the frozen ephemeris through the TMA unit: bulk copies of the
+    //      segment's node table (k_ephemeris wrote it in the staged layout) completing on an
+    //      mbarrier, overlapped with the rest of the prologue
+    constexpr bool kStaged = STAGE;
+    if (kStaged && tid == 0) {
+        mbar_init(&st.stage_bar, 1);
+        bulk_stage(eph, REL ? a.fd.rel_tab : a.fd.eph_t, static_cast<unsigned>(sizeof(double) * eph_stage_doubles(N, B, REL)),
+                   &st.stage_bar);
+    }
     const int fb_doubles = (FOLD ? ws_fold_ksteps(N, a.nkp) : 2 * a.nkp) * FKS;
     for (int i = tid; i < 2 * fb_doubles; i += WS_THREADS) fb0[i] = 0.0;  // both halves (contiguous)
     if (FOLD) {  // anchor weights of the folded F layout (s at k, a at p >= N/2)
@@ -909,17 +922,12 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
             anc[k] = k < N ? up[2 * ((static_cast<size_t>(amt) * a.nkp + (k >> 3)) * 32 + ag * 4 + (k & 3)) + ((k >> 2) & 1)]
                            : 0.0;
     }
-    if (STAGE && B > 0) {  // node-contiguous [B*3][N] + [3][N]: the force threads (one node each) read conflict-free
-        for (int i = tid; i < N * 3 * B; i += WS_THREADS) {  // smem-contiguous order (conflict-free stores)
-            const int r = i / N, j = i % N;
-            eph[i] = a.fd.body_pos[j * 3 * B + r];
-        }
-        for (int i = tid; i < N * 3; i += WS_THREADS) eph[N * 3 * B + i] = a.fd.indirect[(i % N) * 3 + i / N];
-    }
     const double* pos_base = STAGE ? eph : a.fd.body_pos;
-    const double* ind_base = STAGE ? eph + N * 3 * B : a.fd.indirect;
-    // element (node j, body b, coordinate c) at pos_base[j * psj + (3b + c) * psc]
-    const int psj = STAGE ? 1 : 3 * B, psc = STAGE ? N : 1;
+    const double* ind_base = STAGE ? eph + 3 * B * eph_ld(N) : a.fd.indirect;
+    // element (node j, body b, coordinate c) at pos_base[j * psj + (3b + c) * psc]: staged
+    // node-contiguous, so the force threads (one node each) read conflict-free
+    const int psj = STAGE ? 1 : 3 * B, psc = STAGE ? eph_ld(N) : 1;
+    const double* rel_base = STAGE ? eph : a.fd.rel_tab;  // relativistic node table
     if (tid == 0) {
         for (int t = 0; t < SLOTS; ++t) {
             st.slot_traj[t] = -1;
@@ -936,6 +944,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
         st.exit_flag = 0;
     }
     __syncthreads();
+    if (kStaged) mbar_wait(&st.stage_bar, 0);
 
     if (warp < MMA_WARPS) {
         // ============================================================ MMA group
@@ -1362,7 +1371,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
                 } else if (N > FP_THREADS / 2) {
                     for (int j = ft; j < N; j += FP_THREADS) {
                         if constexpr (REL)
-                            force_half_rel<4>(a.fd, ybuf, fbh, st.sing_key, act_h, h, j, 0);
+                            force_half_rel<4>(a.fd, rel_base, ybuf, fbh, st.sing_key, act_h, h, j, 0);
                         else
                             force_half<4>(a.fd, ybuf, fbh, st.sing_key, pos_base, ind_base, psj, psc, act_h, h, j, 0);
                     }
@@ -1370,7 +1379,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
                     for (int w = ft; w < 2 * N; w += FP_THREADS) {
                         const int j = w % N, s0 = (w / N) * 2;
                         if constexpr (REL)
-                            force_half_rel<2>(a.fd, ybuf, fbh, st.sing_key, act_h, h, j, s0);
+                            force_half_rel<2>(a.fd, rel_base, ybuf, fbh, st.sing_key, act_h, h, j, s0);
                         else
                             force_half<2>(a.fd, ybuf, fbh, st.sing_key, pos_base, ind_base, psj, psc, act_h, h, j, s0);
                     }
@@ -1378,7 +1387,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
                     for (int w = ft; w < 4 * N; w += FP_THREADS) {
                         const int j = w % N, s0 = w / N;
                         if constexpr (REL)
-                            force_half_rel<1>(a.fd, ybuf, fbh, st.sing_key, act_h, h, j, s0);
+                            force_half_rel<1>(a.fd, rel_base, ybuf, fbh, st.sing_key, act_h, h, j, s0);
                         else
                             force_half<1>(a.fd, ybuf, fbh, st.sing_key, pos_base, ind_base, psj, psc, act_h, h, j, s0);
                     }
@@ -1591,7 +1600,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_uni(const SegArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int N = a.N, B = a.fd.n_bodies;
     const int half = N / 2;
-    const WsLayout L = ws_layout(N, a.nkp, 0, B, STAGE ? 1 : 0, 1);
+    const WsLayout L = ws_layout(N, a.nkp, 0, B, STAGE ? 1 : 0, 1, REL);
     double* ybuf = reinterpret_cast<double*>(smem_raw + L.ybuf);
     const size_t fb_bytes = L.fbuf1 - L.fbuf0;
     double* fb0 = reinterpret_cast<double*>(smem_raw + L.fbuf0);
@@ -1608,19 +1617,19 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_uni(const SegArgs a) {
     if (tid < PHASES) s_pc[tid] = 0;
     if (tid == 0) s_prev = clock64();
 
+    // ---- TMA bulk staging of the segment's node table (as k_pc_ws), overlapped with the prologue
+    if (STAGE && tid == 0) {
+        mbar_init(&st.stage_bar, 1);
+        bulk_stage(eph, REL ? a.fd.rel_tab : a.fd.eph_t, static_cast<unsigned>(sizeof(double) * eph_stage_doubles(N, B, REL)),
+                   &st.stage_bar);
+    }
     const int fb_doubles = ws_fold_ksteps(N, a.nkp) * FKS;
     for (int i = tid; i < 2 * fb_doubles; i += T) fb0[i] = 0.0;
     for (int k = tid; k < KP; k += T) anc[k] = k < N ? a.anc_fold[k] : 0.0;
-    if (STAGE && B > 0) {
-        for (int i = tid; i < N * 3 * B; i += T) {
-            const int r = i / N, j = i % N;
-            eph[i] = a.fd.body_pos[j * 3 * B + r];
-        }
-        for (int i = tid; i < N * 3; i += T) eph[N * 3 * B + i] = a.fd.indirect[(i % N) * 3 + i / N];
-    }
     const double* pos_base = STAGE ? eph : a.fd.body_pos;
-    const double* ind_base = STAGE ? eph + N * 3 * B : a.fd.indirect;
-    const int psj = STAGE ? 1 : 3 * B, psc = STAGE ? N : 1;
+    const double* ind_base = STAGE ? eph + 3 * B * eph_ld(N) : a.fd.indirect;
+    const int psj = STAGE ? 1 : 3 * B, psc = STAGE ? eph_ld(N) : 1;
+    const double* rel_base = STAGE ? eph : a.fd.rel_tab;
     if (tid == 0) {
         for (int t = 0; t < SLOTS; ++t) {
             st.slot_traj[t] = -1;
@@ -1638,6 +1647,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_uni(const SegArgs a) {
         st.exit_flag = 0;
     }
     __syncthreads();
+    if (STAGE) mbar_wait(&st.stage_bar, 0);
     bool first = true;
     for (;;) {
         // ---- decisions of both halves (warp h), after the previous iteration's epilogue
@@ -1793,9 +1803,9 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_uni(const SegArgs a) {
                 if (!act_h) continue;
                 double* fbh = fb0 + h * (fb_bytes / sizeof(double));
                 const int j = r % N, s0 = (r / N) * ns;
-                if (ns == 4) force_half_rel<4>(a.fd, ybuf, fbh, st.sing_key, act_h, h, j, s0);
-                else if (ns == 2) force_half_rel<2>(a.fd, ybuf, fbh, st.sing_key, act_h, h, j, s0);
-                else force_half_rel<1>(a.fd, ybuf, fbh, st.sing_key, act_h, h, j, s0);
+                if (ns == 4) force_half_rel<4>(a.fd, rel_base, ybuf, fbh, st.sing_key, act_h, h, j, s0);
+                else if (ns == 2) force_half_rel<2>(a.fd, rel_base, ybuf, fbh, st.sing_key, act_h, h, j, s0);
+                else force_half_rel<1>(a.fd, rel_base, ybuf, fbh, st.sing_key, act_h, h, j, s0);
             }
             __syncthreads();
             for (int hc = warp; hc < 2 * HC; hc += NW) {  // fold: s_k at k, a_k = F_k - F_{N-1-k} at N-1-k
@@ -1931,7 +1941,7 @@ static cudaError_t launch_uni_t(const SegArgs& a, int grid, size_t smem, cudaStr
 
 template <int MAIN, int XMW, bool FOLD = false>
 static cudaError_t launch_ws_t(const SegArgs& a, int grid, size_t smem, cudaStream_t s) {
-    // relativistic launches never stage the ephemeris (the host clears stage_eph)
+    // relativistic launches of this kernel never stage the node table (the host clears stage_eph)
     auto kern = a.fd.rel ? k_pc_ws<MAIN, XMW, false, true, FOLD>
                          : (a.stage_eph ? k_pc_ws<MAIN, XMW, true, false, FOLD> : k_pc_ws<MAIN, XMW, false, false, FOLD>);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
@@ -1980,8 +1990,8 @@ bool ws_supported(int N, bool fold) {
     return main >= 1 && main <= 4 && ws_extras(N, false) <= 3 * MMA_WARPS && (main < 4 || ws_extras(N, false) <= MMA_WARPS);
 }
 
-size_t ws_smem_bytes(int N, int nkp, int xrows, int B, int stage_eph, bool fold) {
-    return ws_layout(N, nkp, xrows, B, stage_eph, fold ? 1 : 0).total;
+size_t ws_smem_bytes(int N, int nkp, int xrows, int B, int stage_eph, bool fold, bool rel) {
+    return ws_layout(N, nkp, xrows, B, stage_eph, fold ? 1 : 0, rel).total;
 }
 
 /// Unified folded kernel (N % 8 == 0): units of 2 x ceil(N/16) pair tiles over 16 warps.
@@ -1990,9 +2000,12 @@ bool uni_supported(int N) { return N % 8 == 0 && (2 * ws_mtiles(N, true) + 15) /
 cudaError_t launch_segment_uni(const SegArgs& a, int grid, cudaStream_t s) {
     if (!uni_supported(a.N) || a.upack_fold == nullptr) return cudaErrorNotSupported;
     const int nv = (2 * ws_mtiles(a.N, true) + 15) / 16;
-    const size_t smem = ws_smem_bytes(a.N, a.nkp, 0, a.fd.n_bodies, a.stage_eph, true);
-    if (a.fd.rel)  // relativistic launches never stage the ephemeris (the host clears stage_eph)
+    const size_t smem = ws_smem_bytes(a.N, a.nkp, 0, a.fd.n_bodies, a.stage_eph, true, a.fd.rel != 0);
+    if (a.fd.rel) {  // relativistic: the node table is staged when it fits (host: stage_eph)
+        if (a.stage_eph)
+            return nv == 1 ? launch_uni_t<1, true, true>(a, grid, smem, s) : launch_uni_t<2, true, true>(a, grid, smem, s);
         return nv == 1 ? launch_uni_t<1, false, true>(a, grid, smem, s) : launch_uni_t<2, false, true>(a, grid, smem, s);
+    }
     if (a.stage_eph)
         return nv == 1 ? launch_uni_t<1, true>(a, grid, smem, s) : launch_uni_t<2, true>(a, grid, smem, s);
     return nv == 1 ? launch_uni_t<1, false>(a, grid, smem, s) : launch_uni_t<2, false>(a, grid, smem, s);

@@ -136,7 +136,7 @@ __device__ __forceinline__ void force_chains(const ForceData& fd, double w2, con
             if (!on[k]) continue;
             double o[3];
             rel_correction(rx[k], ry[k], rz[k], ybuf[yidx(jj[k], 3, tt[k])], ybuf[yidx(jj[k], 4, tt[k])],
-                           ybuf[yidx(jj[k], 5, tt[k])], fd.rel_tab + static_cast<size_t>(jj[k]) * (B + 1) * REL_W,
+                           ybuf[yidx(jj[k], 5, tt[k])], fd.rel_tab + static_cast<size_t>(jj[k]) * rel_stride(B),
                            B + 1, fd.ic2, o);
             ax[k] += o[0];
             ay[k] += o[1];

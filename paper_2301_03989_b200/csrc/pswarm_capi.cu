@@ -157,7 +157,7 @@ enum BufId {
     B_OP_IN, B_OP_IN2, B_OP_OUT, B_OP_AUX, B_OP_KEY,
     B_BT_KIND, B_BT_SOFF, B_BT_NC, B_BT_EL, B_BT_BND, B_BT_COFF, B_BT_CF, B_PHASES,
     B_W_REP, B_W_LIST, B_W_CTL, B_W_HIST, B_W_BLK, B_W_GK,
-    B_IN_PACK, B_REPORT, B_BODY_VEL, B_REL_TAB, B_HOT, B_STATES7, B_COUNT
+    B_IN_PACK, B_REPORT, B_BODY_VEL, B_REL_TAB, B_HOT, B_STATES7, B_EPH_T, B_COUNT
 };
 
 /// Page-locked host staging (grow-only): every host<->device transfer of a solve goes
@@ -775,12 +775,13 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
     // warp-specialised one is faster, profiles/bench_r01_c5_n*.json)
     const bool uni = fold && (ctx->unified == 1 || (ctx->unified == 2 && rel && Ni <= 200)) && uni_supported(Ni);
     ctx->last_kernel = uni ? "k_pc_uni" : fold ? "k_pc_ws_fold" : use_ws ? "k_pc_ws" : "k_pc_segment";
-    // stage the frozen ephemeris in shared memory when it fits next to the state blocks
-    const int stage_eph = nb > 0 && !rel &&
-                                  (use_ws ? ws_smem_bytes(Ni, op.nkp, xrows, nb, 1, fold)
-                                          : segment_smem_bytes(Ni, op.nkp, xrows, nb, 1)) <= SMEM_MAX
-                              ? 1
-                              : 0;
+    // stage the frozen ephemeris in shared memory when it fits next to the state blocks (the
+    // slot kernels copy it with the TMA unit); relativistic: the node table, k_pc_uni only
+    const int stage_eph = rel ? (uni && ws_smem_bytes(Ni, op.nkp, 0, nb, 1, true, true) <= SMEM_MAX ? 1 : 0)
+                              : (nb > 0 && (use_ws ? ws_smem_bytes(Ni, op.nkp, xrows, nb, 1, fold)
+                                                   : segment_smem_bytes(Ni, op.nkp, xrows, nb, 1)) <= SMEM_MAX
+                                     ? 1
+                                     : 0);
     if (!use_ws && segment_smem_bytes(Ni, op.nkp, xrows, nb, stage_eph) > SMEM_MAX)
         raise(PSWARM_ERR_INVALID_SIZE, fmtf("propagate: %lld nodes exceed the per-SM shared memory of the slot kernel",
                                             (long long)N));
@@ -792,7 +793,7 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
     };
 
     BodyTable bt{};
-    double *d_pos = nullptr, *d_ind = nullptr, *d_mu = nullptr;
+    double *d_pos = nullptr, *d_ind = nullptr, *d_mu = nullptr, *d_eph_t = nullptr;
     if (nb > 0) {
         d_mu = reinterpret_cast<double*>(din + o_mu);
         bt = BodyTable{nb,
@@ -806,13 +807,15 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
                        reinterpret_cast<double*>(din + o_cf)};
         d_pos = ctx->buf[B_BODY_POS].get<double>(static_cast<size_t>(N) * nb * 3);
         d_ind = ctx->buf[B_INDIRECT].get<double>(static_cast<size_t>(N) * 3);
+        if (stage_eph && use_ws && !rel)  // node-contiguous copy, the bulk-staging source
+            d_eph_t = ctx->buf[B_EPH_T].get<double>(eph_stage_doubles(Ni, nb, false));
     }
     double* d_hot = cfg->start_mode == 2 ? ctx->buf[B_HOT].get<double>(static_cast<size_t>(M) * N * 6) : nullptr;
     double *d_vel = nullptr, *d_rel = nullptr;
     if (rel) {  // EXTENSION: body velocities + per-node relativistic table (Sun row first)
         bt.B = nb;
         d_vel = ctx->buf[B_BODY_VEL].get<double>(static_cast<size_t>(N) * std::max(nb, 1) * 3);
-        d_rel = ctx->buf[B_REL_TAB].get<double>(static_cast<size_t>(N) * (nb + 1) * REL_W);
+        d_rel = ctx->buf[B_REL_TAB].get<double>(eph_stage_doubles(Ni, nb, true));
         if (!d_pos) d_pos = ctx->buf[B_BODY_POS].get<double>(static_cast<size_t>(N) * 3);
         if (!d_ind) d_ind = ctx->buf[B_INDIRECT].get<double>(static_cast<size_t>(N) * 3);
     }
@@ -873,7 +876,7 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
         cuda_check(cudaMemsetAsync(d_faults, 0, sizeof(GroupFault) * P, st), "memset faults");
         if (nb > 0 || rel) {  // frozen per-node ephemeris of this segment, evaluated on the device
             cuda_check(launch_ephemeris(static_cast<int>(N), d_times, cfg->central_mu, bt, d_pos, d_ind, d_ekey, d_vel,
-                                        d_rel, 1.0 / (c_light * c_light), st),
+                                        d_rel, 1.0 / (c_light * c_light), d_eph_t, st),
                        "k_ephemeris");
             ++ctx->launches;
         }
@@ -904,6 +907,7 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
             a.fd.ic2 = 1.0 / (c_light * c_light);
             a.fd.rel_tab = d_rel;
         }
+        a.fd.eph_t = d_eph_t;
         a.upack = reinterpret_cast<const double2*>(op.buf.p);
         a.times = d_times;
         a.group_off = d_off;
