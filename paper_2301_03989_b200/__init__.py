@@ -12,4 +12,5 @@ from .api import (  # noqa: F401
     SolverError, TimeoutError, build_grid, default_context, elements_to_state, make_clone_batch,
     max_state_discrepancy, osculating_period, parse_run_mode, plan_segments, planets8, reference_bodies,
     reference_force_config, reference_state, split_groups, BenchmarkReport, BenchmarkRow, run_benchmark,
+    pinned_sample_buffer, pinned_terminal_buffer,
 )

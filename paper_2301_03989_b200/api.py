@@ -271,12 +271,25 @@ def pinned_sample_buffer(n_states: int, plan: "SegmentPlan") -> np.ndarray:
     return torch.zeros((n_states, R, 6), dtype=torch.float64, pin_memory=True).numpy()
 
 
+def pinned_terminal_buffer(n_states: int) -> np.ndarray:
+    """Page-locked [M, 7] buffer for `terminal=` of propagate/run_batch: the library then
+    writes the terminal states (epoch, r, v) with one device->host DMA straight into it
+    (no staging copy, no page faults on a fresh array).  Allocate once and reuse."""
+    import torch
+    return torch.zeros((n_states, 7), dtype=torch.float64, pin_memory=True).numpy()
+
+
 class _Outputs:
     def __init__(self, M, P, S, N, max_it, samples=True, history=True, terminal=True):
         R = 1 + S * (N - 1)
         self.M, self.P, self.S, self.R, self.max_it = M, P, S, R, max(max_it, 0)
-        # np.empty: the C side writes every element a reported segment / complete call exposes
-        self.terminal = np.empty((M, 7)) if terminal else None
+        if isinstance(terminal, np.ndarray):  # caller-owned (e.g. pinned_terminal_buffer) output
+            if terminal.shape != (M, 7) or terminal.dtype != np.float64 or not terminal.flags.c_contiguous:
+                raise ShapeError(f"terminal buffer must be float64 C-contiguous of shape {(M, 7)}")
+            self.terminal = terminal
+        else:
+            # np.empty: the C side writes every element a reported segment / complete call exposes
+            self.terminal = np.empty((M, 7)) if terminal else None
         if isinstance(samples, np.ndarray):  # caller-owned (e.g. pinned_sample_buffer) output
             if samples.shape != (M, R, 6) or samples.dtype != np.float64 or not samples.flags.c_contiguous:
                 raise ShapeError(f"samples buffer must be float64 C-contiguous of shape {(M, R, 6)}")

@@ -737,6 +737,23 @@ __global__ void k_repack_states(const double* __restrict__ s7, double* __restric
         s6[k] = s7[(k / 6) * 7 + 1 + k % 6];
 }
 
+/// Terminal states [M][6] -> the caller's [M][7] = (epoch, r, v) layout on the device, so one
+/// DMA lands them in a page-locked caller buffer.
+__global__ void k_pack_states7(const double* __restrict__ s6, double epoch, double* __restrict__ s7, long long M) {
+    for (long long k = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; k < M * 7;
+         k += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long i = k / 7, c = k % 7;
+        s7[k] = c == 0 ? epoch : s6[i * 6 + c - 1];
+    }
+}
+
+cudaError_t launch_pack_states7(const double* s6, double epoch, double* s7, long long M, cudaStream_t s) {
+    const long long n = M * 7;
+    const int grid = static_cast<int>(std::max<long long>(1, std::min<long long>((n + 255) / 256, 148 * 16)));
+    k_pack_states7<<<grid, 256, 0, s>>>(s6, epoch, s7, M);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_repack_states(const double* s7, double* s6, long long M, cudaStream_t s) {
     const long long n = M * 6;
     const int grid = static_cast<int>(std::min<long long>((n + 255) / 256, 148 * 16));

@@ -61,7 +61,7 @@ struct SegArgs {
     ForceData fd;
     const double2* upack;       // packed [U; anchor] operator
     const double* times;        // [N]
-    const int64_t* group_off;   // [P+1]
+    const int64_t* group_off;   // [P+1], nullptr for singleton groups
     const double* state_in;     // [M][6] segment initial states
     double* state_out;          // [M][6] terminal rows (chained)
     double* samples;            // [M][R][6] or nullptr
@@ -100,9 +100,13 @@ __device__ __forceinline__ void claim_group(const SegArgs& a, int gi, int& off, 
         off = a.traj_list[gi];
         size = 1;
         gid = off;
-    } else {
+    } else if (a.group_off) {
         off = static_cast<int>(a.group_off[gi]);
         size = static_cast<int>(a.group_off[gi + 1]) - off;
+        gid = gi;
+    } else {  // singleton groups (no offsets uploaded): group gi is trajectory gi
+        off = gi;
+        size = 1;
         gid = gi;
     }
 }
@@ -150,6 +154,7 @@ struct BodyTable {
 /// and the node table rel_tab [N][rel_stride(B)] (Sun row first, the indirect term last).
 /// eph_t (optional): positions and indirect term node-contiguous, [3B + 3][eph_ld(N)].
 cudaError_t launch_repack_states(const double* s7, double* s6, long long M, cudaStream_t s);
+cudaError_t launch_pack_states7(const double* s6, double epoch, double* s7, long long M, cudaStream_t s);
 cudaError_t launch_ephemeris(int N, const double* times, double central_mu, const BodyTable& bt, double* pos,
                              double* indirect, unsigned long long* fault_key, double* vel, double* rel_tab, double ic2,
                              double* eph_t, cudaStream_t s);

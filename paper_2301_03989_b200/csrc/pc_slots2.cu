@@ -1377,7 +1377,9 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
                     }
                 } else if (N > FP_THREADS / 4) {
                     for (int w = ft; w < 2 * N; w += FP_THREADS) {
-                        const int j = w % N, s0 = (w / N) * 2;
+                        // relativistic: the slot pairs of a node in adjacent lanes (one table row
+                        // read per node, broadcast)
+                        const int j = REL ? w >> 1 : w % N, s0 = REL ? (w & 1) * 2 : (w / N) * 2;
                         if constexpr (REL)
                             force_half_rel<2>(a.fd, rel_base, ybuf, fbh, st.sing_key, act_h, h, j, s0);
                         else
@@ -1385,7 +1387,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
                     }
                 } else {
                     for (int w = ft; w < 4 * N; w += FP_THREADS) {
-                        const int j = w % N, s0 = w / N;
+                        const int j = REL ? w >> 2 : w % N, s0 = REL ? w & 3 : w / N;
                         if constexpr (REL)
                             force_half_rel<1>(a.fd, rel_base, ybuf, fbh, st.sing_key, act_h, h, j, s0);
                         else
@@ -1796,13 +1798,15 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_uni(const SegArgs a) {
         //      node with the fused 1PN pass, then folded in place
         if constexpr (REL) {
             const int ns = N > 64 ? 2 : 1;  // slots per item (2 fused chains; N = 200: 800 items, all warps)
-            const int per_h = N * (4 / ns);
-            for (int w = tid; w < 2 * per_h; w += T) {
-                const int h = w / per_h, r = w % per_h;
+            // items node-major: the 8 / ns (half, slot group) items of a node sit in adjacent lanes,
+            // so a warp reads 32 ns / 8 distinct table rows per load (shared-memory broadcast)
+            const int per_node = 2 * (4 / ns);
+            for (int w = tid; w < N * per_node; w += T) {
+                const int j = w / per_node, r = w % per_node, h = r / (4 / ns);
                 const int act_h = (am >> (h * HS)) & 0xF;
                 if (!act_h) continue;
                 double* fbh = fb0 + h * (fb_bytes / sizeof(double));
-                const int j = r % N, s0 = (r / N) * ns;
+                const int s0 = (r % (4 / ns)) * ns;
                 if (ns == 4) force_half_rel<4>(a.fd, rel_base, ybuf, fbh, st.sing_key, act_h, h, j, s0);
                 else if (ns == 2) force_half_rel<2>(a.fd, rel_base, ybuf, fbh, st.sing_key, act_h, h, j, s0);
                 else force_half_rel<1>(a.fd, rel_base, ybuf, fbh, st.sing_key, act_h, h, j, s0);

@@ -590,6 +590,27 @@ void solve_wide_rounds(pswarm_ctx* ctx, SegArgs a, const std::function<cudaError
 }
 
 // ----------------------------------------------------------------- propagate
+/// Lowest i with states[i].epoch != states[0].epoch (propagator.hpp:205-212), -1 if none.
+/// The scan touches every cache line of the [M][7] batch; large batches are split over host
+/// threads (56 MB at 10^6 states: ~4 ms on one core).
+int64_t first_epoch_mismatch(const double* states, int64_t M) {
+    auto scan = [&](int64_t lo, int64_t hi) {
+        for (int64_t i = std::max<int64_t>(lo, 1); i < hi; ++i)
+            if (states[7 * i] != states[0]) return i;
+        return int64_t{-1};
+    };
+    const int64_t W = M >= (int64_t{1} << 17) ? std::min<int64_t>(8, std::max(1u, std::thread::hardware_concurrency())) : 1;
+    if (W == 1) return scan(0, M);
+    std::vector<int64_t> hit(static_cast<size_t>(W), -1);
+    std::vector<std::thread> pool;
+    for (int64_t w = 1; w < W; ++w) pool.emplace_back([&, w] { hit[w] = scan(M * w / W, M * (w + 1) / W); });
+    hit[0] = scan(0, M / W);
+    for (auto& t : pool) t.join();
+    for (int64_t h : hit)
+        if (h >= 0) return h;
+    return -1;
+}
+
 struct RunSpec {
     bool independent = false;  // run_batch independent mode: reference error order is per trajectory
     // multi-device shards: leave the terminal states on the device and return their address
@@ -630,11 +651,10 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
                                        " states, batch has " + std::to_string(M));
     const int64_t S = n_boundaries - 1;
     if (S < 1) throw pswarm::InvalidSpanError("propagate: empty segment plan");
-    for (int64_t i = 1; i < M; ++i)
-        if (states[7 * i] != states[0])
-            throw pswarm::AlignmentError("propagate: state " + std::to_string(i) + " epoch " +
-                                         std::to_string(states[7 * i]) + " differs from shared epoch " +
-                                         std::to_string(states[0]));
+    if (const int64_t i = first_epoch_mismatch(states, M); i >= 0)
+        throw pswarm::AlignmentError("propagate: state " + std::to_string(i) + " epoch " +
+                                     std::to_string(states[7 * i]) + " differs from shared epoch " +
+                                     std::to_string(states[0]));
     if (states[0] != boundaries[0])
         throw pswarm::AlignmentError("propagate: batch epoch does not match the first segment boundary");
     if (cfg->tolerance <= 0.0) throw pswarm::Error("pc_solve: tolerance must be positive");
@@ -672,7 +692,9 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
     }
     // ---- one packed host->device transfer: states, group offsets, grids, body table
     Pack in;
-    const size_t o_off = in.add(sizeof(int64_t) * (P + 1)),
+    // group offsets: not uploaded for singleton groups (independent mode), group gi = trajectory gi
+    const bool unit_groups = gmax == 1;
+    const size_t o_off = in.add(unit_groups ? 0 : sizeof(int64_t) * (P + 1)),
                  o_times = in.add(sizeof(double) * S * N), o_kind = in.add(sizeof(int) * bu.kind.size()),
                  o_soff = in.add(sizeof(int) * bu.seg_off.size()), o_nc = in.add(sizeof(int) * bu.ncoef.size()),
                  o_el = in.add(sizeof(double) * bu.elements.size()), o_mu = in.add(sizeof(double) * bu.mu.size()),
@@ -682,9 +704,11 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
     const size_t o_s6 = in.add(sizeof(double) * M * 6);  // filled on the device (k_repack_states)
     char* hin = ctx->pin_in.get<char>(o_s6);
     {
-        int64_t* off = reinterpret_cast<int64_t*>(hin + o_off);
-        off[0] = 0;
-        for (int64_t g = 0; g < P; ++g) off[g + 1] = off[g] + group_sizes[g];
+        if (!unit_groups) {
+            int64_t* off = reinterpret_cast<int64_t*>(hin + o_off);
+            off[0] = 0;
+            for (int64_t g = 0; g < P; ++g) off[g + 1] = off[g] + group_sizes[g];
+        }
         auto put = [&](size_t o, const auto& v) {
             if (!v.empty()) std::memcpy(hin + o, v.data(), v.size() * sizeof(v[0]));
         };
@@ -707,9 +731,8 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
         cuda_check(launch_repack_states(d7, reinterpret_cast<double*>(din + o_s6), M, st), "k_repack_states");
         ++ctx->launches;
     }
-    std::vector<int64_t> h_off(reinterpret_cast<int64_t*>(hin + o_off), reinterpret_cast<int64_t*>(hin + o_off) + P + 1);
     double* d_in = reinterpret_cast<double*>(din + o_s6);
-    const int64_t* d_off = reinterpret_cast<const int64_t*>(din + o_off);
+    const int64_t* d_off = unit_groups ? nullptr : reinterpret_cast<const int64_t*>(din + o_off);
     double* d_out = ctx->buf[B_STATE_B].get<double>(static_cast<size_t>(M) * 6);
     if (d_in == d_out) raise(PSWARM_ERR_GENERIC, "propagate: state buffers alias");
     double* d_samples = out && out->samples ? ctx->buf[B_SAMPLES].get<double>(static_cast<size_t>(M) * R * 6) : nullptr;
@@ -735,7 +758,16 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
     GroupFault* d_faults = reinterpret_cast<GroupFault*>(drep + r_faults);
     uint8_t* d_fb = reinterpret_cast<uint8_t*>(drep + r_fb);
     unsigned long long* d_ekey = reinterpret_cast<unsigned long long*>(drep + r_ekey);
-    double* h_term = out && out->terminal_states ? ctx->pin_term.get<double>(sizeof(double) * M * 6) : nullptr;
+    // terminal states: straight into a page-locked caller buffer as [M][7] (one DMA after a
+    // device-side pack), else through the context's pinned staging
+    bool term_direct = false;
+    if (out && out->terminal_states) {
+        cudaPointerAttributes pa{};
+        term_direct = cudaPointerGetAttributes(&pa, out->terminal_states) == cudaSuccess && pa.type == cudaMemoryTypeHost;
+        cudaGetLastError();
+    }
+    double* h_term =
+        out && out->terminal_states && !term_direct ? ctx->pin_term.get<double>(sizeof(double) * M * 6) : nullptr;
     bool term_ready = false;
 
     std::vector<int32_t> h_iter(static_cast<size_t>(S * P), 0);
@@ -943,6 +975,8 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
             cuda_check(cudaEventRecord(ctx->evk1, st), "event");
             ++ctx->launches;
         } else if (max_it > 0) {
+            std::vector<int64_t> h_off(static_cast<size_t>(P) + 1, 0);
+            for (int64_t g = 0; g < P; ++g) h_off[g + 1] = h_off[g] + group_sizes[g];
             solve_wide_rounds(ctx, a, launch, cap, h_off, P, max_it, deadline, d_iter, d_err, d_conv, d_faults,
                               a.rep_hist, d_off, kernel_ms);
         }
@@ -958,6 +992,14 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
         cuda_check(cudaMemcpyAsync(hrep, drep, r_faults, cudaMemcpyDeviceToHost, st), "D2H reports");
         if (h_term && seg == S - 1) {  // terminal states ride along with the last segment's reports
             cuda_check(cudaMemcpyAsync(h_term, d_out, sizeof(double) * M * 6, cudaMemcpyDeviceToHost, st), "D2H terminal");
+            term_ready = true;
+        }
+        if (term_direct && seg == S - 1) {
+            double* d7 = ctx->buf[B_STATES7].get<double>(static_cast<size_t>(M) * 7);  // input copy: consumed
+            cuda_check(launch_pack_states7(d_out, boundaries[S], d7, M, st), "k_pack_states7");
+            ++ctx->launches;
+            cuda_check(cudaMemcpyAsync(out->terminal_states, d7, sizeof(double) * M * 7, cudaMemcpyDeviceToHost, st),
+                       "D2H terminal");
             term_ready = true;
         }
         cuda_check(cudaStreamSynchronize(st), "segment solve");
@@ -1176,7 +1218,7 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
             cuda_check(cudaMemcpyAsync(out->samples, d_samples, sizeof(double) * M * R * 6, cudaMemcpyDeviceToHost, st),
                        "D2H samples");
         if (overlap_samples) cuda_check(cudaStreamSynchronize(ctx->copy_stream), "segment samples");
-        if (out->terminal_states && fail_status == PSWARM_OK && !term_ready) {
+        if (h_term && fail_status == PSWARM_OK && !term_ready) {
             cuda_check(cudaMemcpyAsync(h_term, d_in, sizeof(double) * M * 6, cudaMemcpyDeviceToHost, st),
                        "D2H terminal");
         }
@@ -1185,7 +1227,7 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
                                        cudaMemcpyDeviceToHost, st),
                        "D2H phases");
         cuda_check(cudaStreamSynchronize(st), "outputs");
-        if (out->terminal_states && fail_status == PSWARM_OK)
+        if (h_term && fail_status == PSWARM_OK)
             for (int64_t i = 0; i < M; ++i) {
                 out->terminal_states[7 * i] = boundaries[S];
                 for (int c = 0; c < 6; ++c) out->terminal_states[7 * i + 1 + c] = h_term[i * 6 + c];

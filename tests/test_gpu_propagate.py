@@ -544,3 +544,17 @@ def test_wide_group_nonconvergence_runs_all_members(ctx, oracle):
     a, b = errs[0].partial.reports[0][0], errs[1].partial.reports[0][0]
     assert a.iterations == b.iterations == cfg.max_iterations
     assert abs(a.final_error - b.final_error) <= 1e-3 * b.final_error
+
+
+def test_pinned_terminal_buffer_direct_copy(ctx):
+    """A page-locked caller buffer receives the terminal states by one DMA (device-side
+    [M][7] pack): identical to the staged path, and reused across calls."""
+    states, plan, cfg = _setup(37, 64, 0.4)
+    ref = ctx.run_batch(states, cfg, plan, "independent", samples=False)
+    buf = ps.pinned_terminal_buffer(37)
+    for _ in range(2):
+        got = ctx.run_batch(states, cfg, plan, "independent", samples=False, terminal=buf)
+        assert got.terminal_states is buf
+        assert np.array_equal(buf, ref.terminal_states)
+    with pytest.raises(ps.ShapeError):
+        ctx.run_batch(states, cfg, plan, "independent", terminal=np.zeros((36, 7)))
