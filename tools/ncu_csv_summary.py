@@ -65,11 +65,13 @@ def main():
     }
     if len(sys.argv) > 4:
         b = json.loads(open(sys.argv[4]).read().strip().splitlines()[-1])
-        f = b["roofline"]["flops_per_launch"]
+        segs = int(b.get("config", {}).get("segments", 1) or 1)
+        f = b["roofline"]["flops_per_launch"] / segs  # one captured launch = one segment
         rec["algorithmic"] = {"flops_per_launch": f, "tflops": f / (dur_ms * 1e-3) / 1e12,
                               "frac_of_peak": f / (dur_ms * 1e-3) / 1e12 / peak_tf,
                               "note": "reference-algorithmic flops of the same workload (SURVEY §8d), from "
-                                      "the bench line of the same config; ncu duration is cold-cache, serialised"}
+                                      "the bench line of the same config (per segment launch: the step's "
+                                      "flops / segments); ncu duration is cold-cache, serialised"}
     json.dump(rec, open(out, "w"), indent=1)
     print(json.dumps({k: rec[k] for k in ("label", "duration_ms", "dram_bytes", "dmma_pipe_active_pct",
                                           "fp64_pipe_active_pct")}), json.dumps(rec["executed"]))
