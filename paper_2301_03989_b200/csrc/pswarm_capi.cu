@@ -803,9 +803,10 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
     const bool wide = gmax > (use_ws ? SLOTS / 2 : SLOTS);
     const int64_t gk = wide ? 1 : gmax;  // group size the slot kernel sees
     const int xrows = use_ws ? ws_extra_rows(Ni, fold) : extra_rows(Ni, op.gp);
-    // auto: the unified kernel for the force-bound 1PN model up to N = 200 (at N = 256 the
-    // warp-specialised one is faster, profiles/bench_r01_c5_n*.json)
-    const bool uni = fold && (ctx->unified == 1 || (ctx->unified == 2 && rel && Ni <= 200)) && uni_supported(Ni);
+    // auto: the unified kernel for the force-bound 1PN model (node-major force items: 1PN kernel
+    // time 15.0 vs 19.2 ms at N = 200, 17.8 vs 27.0 ms at N = 256 against k_pc_ws_fold,
+    // profiles/sanitizer_r02.json run); Newtonian forces stay on the warp-specialised kernel
+    const bool uni = fold && (ctx->unified == 1 || (ctx->unified == 2 && rel)) && uni_supported(Ni);
     ctx->last_kernel = uni ? "k_pc_uni" : fold ? "k_pc_ws_fold" : use_ws ? "k_pc_ws" : "k_pc_segment";
     // stage the frozen ephemeris in shared memory when it fits next to the state blocks (the
     // slot kernels copy it with the TMA unit); relativistic: the node table, k_pc_uni only
