@@ -293,12 +293,12 @@ __device__ __forceinline__ void gemm_core_fold(const double2* __restrict__ upf, 
 #pragma unroll
         for (int i = 0; i < NA; ++i)
 #pragma unroll
-            for (int u = 0; u < 2; ++u) c.m[i][u] = __ldg(am[i][u] + kp * 32);
+            for (int u = 0; u < 2; ++u) c.m[i][u] = __ldg(am[i][u] + (PSWARM_ABLATE == 5 ? 0 : kp * 32));  // 5: L1-hot A
     };
     auto compute = [&](int kp, const Pair& c) {
 #pragma unroll
         for (int sub = 0; sub < 2; ++sub) {
-            const int ks = 2 * kp + sub;
+            const int ks = PSWARM_ABLATE == 6 ? sub : 2 * kp + sub;  // 6: diagnostic, B from k-steps 0-1 only
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
                 const double* fk = (u ? fb_lo : fb_hi) + ks * FKS;
@@ -1680,52 +1680,60 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_uni(const SegArgs a) {
             }
             __syncthreads();  // slot_traj is rewritten by the claim below
         }
-        // ---- free + claim into both halves (thread 0; the order of k_pc_ws: half 0, then 1)
+        // ---- free + claim into both halves (thread 0): ONE queue atomic for both halves (half 0's
+        //      groups first, as k_pc_ws claims them), so a tick pays one global round trip
         if (tid == 0) {
+            int am = st.act_word[0] | st.act_word[1];
+            if (!first) {
+                const int fm = st.free_mask[0] | st.free_mask[1];
+                am &= ~fm;
+                for (int t = 0; t < SLOTS; ++t)
+                    if ((fm >> t) & 1) st.slot_traj[t] = -1;
+            }
+            int want[2] = {0, 0}, gq = 0, gend = 0;
             for (int h = 0; h < 2; ++h) {
-                int am = st.act_word[0] | st.act_word[1];
-                if (!first) {
-                    const int fm = st.free_mask[h];
-                    am &= ~fm;
-                    for (int t = 0; t < SLOTS; ++t)
-                        if ((fm >> t) & 1) st.slot_traj[t] = -1;
-                }
+                const int free_h = HS - __popc(static_cast<unsigned>(am & (0xF << (h * HS))));
+                want[h] = !st.queue_done && free_h >= a.gmax ? free_h / a.gmax : 0;
+            }
+            if (want[0] + want[1] > 0) {
+                gq = atomicAdd(a.queue, want[0] + want[1]);
+                gend = min(gq + want[0] + want[1], a.P);
+                if (gq + want[0] + want[1] >= a.P) st.queue_done = 1;
+            }
+            for (int h = 0; h < 2; ++h) {
                 int new_mask = 0;
                 const int hmask = 0xF << (h * HS);
-                const int free_h = HS - __popc(static_cast<unsigned>(am & hmask));
-                if (!st.queue_done && free_h >= a.gmax) {
-                    const int k = free_h / a.gmax;
-                    const int g0 = atomicAdd(a.queue, k);
-                    const int g1 = min(g0 + k, a.P);
-                    if (g0 + k >= a.P) st.queue_done = 1;
-                    for (int gi = g0; gi < g1; ++gi) {
-                        int lg = h * HS;
-                        while (st.grp_id[lg] >= 0) ++lg;
-                        int off, size, gid;
-                        claim_group(a, gi, off, size, gid);
-                        st.grp_id[lg] = gid;
-                        st.grp_size[lg] = size;
-                        st.grp_iter[lg] = start_iteration(a, off);
-                        st.grp_floor[lg] = claim_floor(a, gid);
-                        st.grp_cap[lg] = claim_cap(a, gid);
-                        int t = h * HS;
-                        for (int mbr = 0; mbr < size; ++mbr) {
-                            while ((am >> t) & 1) ++t;
-                            am |= 1 << t;
-                            new_mask |= 1 << t;
-                            st.slot_traj[t] = off + mbr;
-                            st.slot_grp[t] = lg;
-                            st.slot_member[t] = mbr;
-                            st.warm_key[t] = INT_MAX;
-                        }
+                const int g0 = gq + (h ? want[0] : 0), g1 = min(g0 + want[h], gend);
+                for (int gi = g0; gi < g1; ++gi) {
+                    int lg = h * HS;
+                    while (st.grp_id[lg] >= 0) ++lg;
+                    int off, size, gid;
+                    claim_group(a, gi, off, size, gid);
+                    st.grp_id[lg] = gid;
+                    st.grp_size[lg] = size;
+                    st.grp_iter[lg] = start_iteration(a, off);
+                    st.grp_floor[lg] = claim_floor(a, gid);
+                    st.grp_cap[lg] = claim_cap(a, gid);
+                    int t = h * HS;
+                    for (int mbr = 0; mbr < size; ++mbr) {
+                        while ((am >> t) & 1) ++t;
+                        am |= 1 << t;
+                        new_mask |= 1 << t;
+                        st.slot_traj[t] = off + mbr;
+                        st.slot_grp[t] = lg;
+                        st.slot_member[t] = mbr;
+                        st.warm_key[t] = INT_MAX;
                     }
                 }
-                st.act_word[h] = am & hmask;
                 st.new_mask[h] = new_mask;
-                st.half_active[h] = (am & hmask) != 0;
-                // (free / retire masks: rewritten by decide_half every iteration; every thread read
-                //  retire_mask above without a barrier when nothing retired)
             }
+            for (int h = 0; h < 2; ++h) {
+                const int hmask = 0xF << (h * HS);
+                st.act_word[h] = am & hmask;
+                st.half_active[h] = (am & hmask) != 0;
+            }
+            // (free / retire masks: rewritten by decide_half every iteration; every thread read
+            //  retire_mask above without a barrier when nothing retired)
             if (a.deadline_ns != 0ull && globaltimer_ns() > a.deadline_ns) st.timeout = 1;
         }
         __syncthreads();
