@@ -67,3 +67,22 @@ def test_multi_error_is_the_single_device_error(ctx, multi3):
     with pytest.raises(ps.Error) as e2:
         multi3.run_batch(bad, cfg, plan, "independent")
     assert type(e1.value) is type(e2.value) and str(e1.value) == str(e2.value)
+
+
+def test_multi_independent_lowest_failing_trajectory(ctx, multi3):
+    """Independent mode over three shards: a divergence in shard 2 and a non-convergence of a
+    LOWER trajectory in shard 1 -> the error of the lower trajectory, as one device (and the
+    serial reference, runner.hpp:63-80) raises it."""
+    states, plan, cfg = _case(m=40, n=48, span=0.5, policy="single")
+    cfg.start_mode = "cold"
+    states[20, 1:] = ps.elements_to_state([0.8e8, 0.3, 0.05, 0.4, 0.9, 0.0, 0.0], ps.MU_SUN, 0.0)[1:]
+    ok = ctx.run_batch(np.delete(states, 20, axis=0), cfg, plan, "independent")
+    cfg.max_iterations = int(ok.iterations.max()) + 1
+    states[35, 1:4] = [1e-110, 0.0, 0.0]
+    errs = []
+    for impl in (ctx, multi3):
+        with pytest.raises(ps.Error) as e:
+            impl.run_batch(states, cfg, plan, "independent")
+        errs.append(e.value)
+    assert type(errs[0]) is type(errs[1]) is ps.PropagationIncompleteError
+    assert str(errs[0]) == str(errs[1])

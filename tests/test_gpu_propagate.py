@@ -558,3 +558,18 @@ def test_pinned_terminal_buffer_direct_copy(ctx):
         assert np.array_equal(buf, ref.terminal_states)
     with pytest.raises(ps.ShapeError):
         ctx.run_batch(states, cfg, plan, "independent", terminal=np.zeros((36, 7)))
+
+
+def test_wide_group_singularity_member(ctx, oracle):
+    """A wide group (12 members, member-level rounds) with one member 0.4 km from a planet:
+    the group's SingularityError carries the reference's node, trajectory-in-group and body
+    (force_model.hpp:115-120), formed from the member records."""
+    states, plan, cfg = _setup(12, 16, 0.05, start="cold")
+    pos = oracle.body_positions(ps.reference_bodies(), ps.MU_SUN, np.array([0.0]))
+    states[7, 1:4] = pos[0, 0] + np.array([0.4, 0.0, 0.0])
+    errs = []
+    for impl in (ctx, oracle):
+        with pytest.raises(ps.SingularityError) as e:
+            impl.propagate(states, [12], plan, cfg)
+        errs.append(e.value)
+    assert str(errs[0]) == str(errs[1]) and errs[0].body == errs[1].body
