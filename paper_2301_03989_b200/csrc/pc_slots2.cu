@@ -1999,7 +1999,10 @@ bool ws_supported(int N, bool fold) {
     const int main = ws_main_tiles(N, fold);
     if (fold)  // whole k-quads per part, 1-2 pair tiles per warp
         return N % 8 == 0 && main >= 1 && main <= 2;
-    return main >= 1 && main <= 4 && ws_extras(N, false) <= 3 * MMA_WARPS && (main < 4 || ws_extras(N, false) <= MMA_WARPS);
+    // <3, 3> (N = 233..247: 18-21 extra tiles on 3 full m-tiles per warp) spills and loses to
+    // k_pc_segment (profiles/dense_plans_r02.json); every other dense plan beats it
+    return main >= 1 && main <= 4 && ws_extras(N, false) <= 3 * MMA_WARPS && (main < 4 || ws_extras(N, false) <= MMA_WARPS) &&
+           !(main == 3 && ws_extras(N, false) > 2 * MMA_WARPS);
 }
 
 size_t ws_smem_bytes(int N, int nkp, int xrows, int B, int stage_eph, bool fold, bool rel) {
@@ -2043,7 +2046,6 @@ cudaError_t launch_segment_ws(const SegArgs& a, int grid, cudaStream_t s) {
     case 11: return launch_ws_t<2, 3>(a, grid, smem, s);
     case 13: return launch_ws_t<3, 1>(a, grid, smem, s);
     case 14: return launch_ws_t<3, 2>(a, grid, smem, s);
-    case 15: return launch_ws_t<3, 3>(a, grid, smem, s);
     case 17: return launch_ws_t<4, 1>(a, grid, smem, s);
     default: return cudaErrorNotSupported;
     }

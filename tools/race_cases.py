@@ -20,7 +20,7 @@ CASES = [(200, "independent", 1, "n_body", "warm", {}),                      # k
          (64, "grouped", 4, "n_body", "warm", {}),                           # grouped, folded kernels
          (216, "independent", 1, "n_body", "warm", {}),                      # k_pc_ws_fold, no extras, b0 from DMMA
          (55, "independent", 1, "n_body", "warm", {"slot_kernel": 1}),       # generic small-N, 23 staged rows
-         (241, "augmented", 1, "n_body", "warm", {}),                        # wide rounds on dense k_pc_ws (N % 8 != 0)
+         (241, "augmented", 1, "n_body", "warm", {}),                        # wide rounds on k_pc_segment (32 m-tiles)
          (72, "grouped", 4, "n_body", "warm", {}),                           # groups of 6 -> wide rounds on k_pc_ws_fold
          (64, "augmented", 1, "n_body", "warm", {}),                         # wide rounds on k_pc_ws_fold (resume)
          (64, "independent", 1, "n_body_1pn", "warm", {}),                   # k_pc_uni, 1PN table bulk-staged
