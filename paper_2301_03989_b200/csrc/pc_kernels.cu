@@ -774,41 +774,35 @@ cudaError_t launch_iota(int32_t* out, int n, cudaStream_t s) {
 
 /// Group error history of a wide-group segment (augment.hpp:137 via pc_solve's history): the
 /// group's error at iteration k is the max over its members (block_max_error), k < K[g].
-/// Members' squared-free errors are non-negative doubles, so their IEEE bits order as
-/// unsigned integers: warps whose lanes share a group reduce first, then one atomicMax.
-/// gh [P][stride] must be zero on entry; k_group_hist_fill writes NaN past each K[g].
+/// Block = a chunk of HIST_CHUNK consecutive members, thread = iteration k (coalesced rows of
+/// the member history); each thread keeps the running max of the current group and flushes it
+/// with one atomicMax when the group changes or the chunk ends.  Non-negative doubles order
+/// like their IEEE bits.  gh [P][stride] must be zero on entry; k_group_hist_fill writes NaN
+/// past each K[g].
+constexpr int HIST_CHUNK = 256;
 __global__ void k_group_hist(const double* __restrict__ mh, int stride, const int64_t* __restrict__ group_off, int P,
                              const int32_t* __restrict__ gK, int M, unsigned long long* gh) {
-    const int m0 = blockIdx.x * blockDim.x + threadIdx.x;
-    for (int base = m0 - threadIdx.x % 32; base < M; base += gridDim.x * blockDim.x) {
-        const int m = base + threadIdx.x % 32;
-        int g = -1;
-        if (m < M) {  // upper_bound over the group offsets
-            int lo = 0, hi = P;
-            while (hi - lo > 1) {
-                const int mid = (lo + hi) / 2;
-                if (group_off[mid] <= m) lo = mid; else hi = mid;
+    const int lo = blockIdx.x * HIST_CHUNK, hi = min(lo + HIST_CHUNK, M);
+    if (lo >= hi) return;
+    int g0 = 0, gh_ = P;  // group of member lo: upper_bound over the offsets
+    while (gh_ - g0 > 1) {
+        const int mid = (g0 + gh_) / 2;
+        if (group_off[mid] <= lo) g0 = mid; else gh_ = mid;
+    }
+    for (int k = threadIdx.x; k < stride; k += blockDim.x) {
+        int g = g0;
+        long long gend = group_off[g + 1];
+        unsigned long long run = 0ull;
+        for (int m = lo; m < hi; ++m) {
+            if (m >= gend) {  // next group: flush the finished one
+                if (k < gK[g]) atomicMax(gh + static_cast<size_t>(g) * stride + k, run);
+                run = 0ull;
+                while (m >= gend) gend = group_off[++g + 1];
             }
-            g = lo;
+            if (k < gK[g])
+                run = max(run, static_cast<unsigned long long>(__double_as_longlong(mh[static_cast<size_t>(m) * stride + k])));
         }
-        const int g0 = __shfl_sync(0xffffffffu, g, 0);
-        const bool uniform = __all_sync(0xffffffffu, g == g0);
-        const int K = g >= 0 ? gK[g] : 0;
-        const int Kmax = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(K));
-        for (int k = 0; k < Kmax; ++k) {
-            unsigned long long b = (m < M && k < K) ? static_cast<unsigned long long>(
-                                                          __double_as_longlong(mh[static_cast<size_t>(m) * stride + k]))
-                                                    : 0ull;
-            if (uniform) {
-                const unsigned hi = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(b >> 32));
-                const unsigned lo = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(b >> 32) == hi
-                                                                       ? static_cast<unsigned>(b) : 0u);
-                if (threadIdx.x % 32 == 0 && g0 >= 0)
-                    atomicMax(gh + static_cast<size_t>(g0) * stride + k, (static_cast<unsigned long long>(hi) << 32) | lo);
-            } else if (m < M && k < K) {
-                atomicMax(gh + static_cast<size_t>(g) * stride + k, b);
-            }
-        }
+        if (k < gK[g]) atomicMax(gh + static_cast<size_t>(g) * stride + k, run);
     }
 }
 
@@ -821,8 +815,8 @@ __global__ void k_group_hist_fill(int stride, const int32_t* __restrict__ gK, in
 cudaError_t launch_group_hist(const double* mh, int stride, const int64_t* group_off, int P, const int32_t* gK, int M,
                               double* gh, cudaStream_t s) {
     auto* ghb = reinterpret_cast<unsigned long long*>(gh);
-    const int grid = std::max(1, std::min((M + 255) / 256, 148 * 8));
-    k_group_hist<<<grid, 256, 0, s>>>(mh, stride, group_off, P, gK, M, ghb);
+    const int threads = std::min(256, 32 * ((stride + 31) / 32));
+    k_group_hist<<<(M + HIST_CHUNK - 1) / HIST_CHUNK, threads, 0, s>>>(mh, stride, group_off, P, gK, M, ghb);
     const long long n = static_cast<long long>(P) * stride;
     k_group_hist_fill<<<static_cast<int>(std::max<long long>(1, std::min<long long>((n + 255) / 256, 148 * 8))), 256, 0,
                         s>>>(stride, gK, P, ghb);
