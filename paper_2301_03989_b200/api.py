@@ -387,7 +387,7 @@ class Context:
     WS_PHASE_NAMES = ("mma_wait_f", "mma_dmma", "mma_epilogue", "mma_wait_b0", "fp_wait_y", "fp_staged_decisions",
                       "fp_retire_claim", "fp_warm_start", "fp_force", "fp_b0", "fp_staged",
                       "mma_bar_epi", "mma_staged", "mma_decisions")
-    UNI_PHASE_NAMES = ("decisions", "retire_claim", "warm_start", "force", "sing_b0", "dmma", "epilogue")
+    UNI_PHASE_NAMES = ("decisions", "retire_claim", "warm_start", "force", "sing_b0", "dmma", "epilogue", "fold_b0")
     N_PHASES = 16
 
     def phase_cycles(self) -> dict:

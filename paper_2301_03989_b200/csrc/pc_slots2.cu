@@ -368,9 +368,16 @@ __device__ __forceinline__ void force_half_rel(const ForceData& fd, const double
     const double ix = rt[nb1 * REL_W], iy = rt[nb1 * REL_W + 1], iz = rt[nb1 * REL_W + 2];
 #pragma unroll 1
     for (int s0 = s_begin; s0 < s_begin + NS; s0 += PAIR) {
+        // Per body A (d = r_A - r, rho = |d|, g = mu_A / rho^3):
+        //   U += mu_A / rho,  n += g d,  b += g [K_A - (4 v.v_A + 1.5 (d.v_A / rho)^2 - 0.5 d.a_A) / c^2] d,
+        //   w_A = -g d.(4v - 3 v_A) = -g (4 d.v - 3 d.v_A),
+        //   sum_A w_A (v - v_A) = v W - sum_A w_A v_A  (W = sum_A w_A),  q += (mu_A / rho) a_A
+        // -- the EIH terms of rel_correction with d.(4v - 3v_A) and the (v - v_A) factor expanded
+        // (8 FP64 operations fewer per body; the expansion changes only the rounding of the 1/c^2
+        // terms, ~1e-8 of the acceleration)
         double rx[PAIR], ry[PAIR], rz[PAIR], vx[PAIR], vy[PAIR], vz[PAIR];
-        double U[PAIR], nx[PAIR], ny[PAIR], nz[PAIR], bx[PAIR], by[PAIR], bz[PAIR], wx[PAIR], wy[PAIR], wz[PAIR],
-            qx[PAIR], qy[PAIR], qz[PAIR];
+        double U[PAIR], nx[PAIR], ny[PAIR], nz[PAIR], bx[PAIR], by[PAIR], bz[PAIR], W[PAIR], wx[PAIR], wy[PAIR],
+            wz[PAIR], qx[PAIR], qy[PAIR], qz[PAIR];
         bool on[PAIR];
         bool flag = false;
 #pragma unroll
@@ -384,7 +391,7 @@ __device__ __forceinline__ void force_half_rel(const ForceData& fd, const double
             vy[k] = on[k] ? ybuf[y2(j, h, 4, s)] : 0.0;
             vz[k] = on[k] ? ybuf[y2(j, h, 5, s)] : 0.0;
             U[k] = nx[k] = ny[k] = nz[k] = bx[k] = by[k] = bz[k] = 0.0;
-            wx[k] = wy[k] = wz[k] = qx[k] = qy[k] = qz[k] = 0.0;
+            W[k] = wx[k] = wy[k] = wz[k] = qx[k] = qy[k] = qz[k] = 0.0;
             flag |= !(rx[k] * rx[k] + ry[k] * ry[k] + rz[k] * rz[k] > 0.0);
         }
         // single chain (small N): 3 bodies in flight for ILP; slot pairs already give 2 chains
@@ -397,7 +404,7 @@ __device__ __forceinline__ void force_half_rel(const ForceData& fd, const double
             for (int k = 0; k < PAIR; ++k) {
                 const double dx = tx - rx[k], dy = ty - ry[k], dz = tz - rz[k];
                 const double d2 = dx * dx + dy * dy + dz * dz;
-                if (A > 0) flag |= d2 < fd.floor2_hi;
+                if (A > 0) flag |= below_bits(d2, fd.floor2_hi_bits);  // integer pre-test, off the FP64 pipe
                 double ir = rsqrt_newton(d2, rsqrt_seed(d2));
                 if (A == 0) ir = rsqrt_newton(d2, ir);  // central term: full precision
                 const double mi = mu * ir, g = mi * ir * ir;
@@ -407,20 +414,28 @@ __device__ __forceinline__ void force_half_rel(const ForceData& fd, const double
                 nz[k] = fma(g, dz, nz[k]);
                 const double vva = vx[k] * vax + vy[k] * vay + vz[k] * vaz;
                 const double dva = dx * vax + dy * vay + dz * vaz;
+                const double dv = dx * vx[k] + dy * vy[k] + dz * vz[k];
                 const double daa = dx * aax + dy * aay + dz * aaz;
-                const double br = g * (K - ic2 * (4.0 * vva + 1.5 * dva * dva * (ir * ir) - 0.5 * daa));
+                const double di = dva * ir;
+                const double br = g * (K - ic2 * fma(4.0, vva, fma(1.5 * di, di, -0.5 * daa)));
                 bx[k] = fma(br, dx, bx[k]);
                 by[k] = fma(br, dy, by[k]);
                 bz[k] = fma(br, dz, bz[k]);
-                const double w = -g * (dx * (4.0 * vx[k] - 3.0 * vax) + dy * (4.0 * vy[k] - 3.0 * vay) +
-                                       dz * (4.0 * vz[k] - 3.0 * vaz));
-                wx[k] = fma(w, vx[k] - vax, wx[k]);
-                wy[k] = fma(w, vy[k] - vay, wy[k]);
-                wz[k] = fma(w, vz[k] - vaz, wz[k]);
+                const double w = g * fma(3.0, dva, -4.0 * dv);
+                W[k] += w;
+                wx[k] = fma(w, vax, wx[k]);
+                wy[k] = fma(w, vay, wy[k]);
+                wz[k] = fma(w, vaz, wz[k]);
                 qx[k] = fma(mi, aax, qx[k]);
                 qy[k] = fma(mi, aay, qy[k]);
                 qz[k] = fma(mi, aaz, qz[k]);
             }
+        }
+#pragma unroll
+        for (int k = 0; k < PAIR; ++k) {  // sum_A w_A (v - v_A) = v W - sum_A w_A v_A
+            wx[k] = fma(vx[k], W[k], -wx[k]);
+            wy[k] = fma(vy[k], W[k], -wy[k]);
+            wz[k] = fma(vz[k], W[k], -wz[k]);
         }
         if (flag) {  // rare: exact guard order of table_acceleration (force_model.hpp:57-69)
 #pragma unroll
@@ -1359,7 +1374,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
                 // issue in the DMMA stream's gaps, so their count sets the force throughput)
                 double* fbh = reinterpret_cast<double*>(smem_raw + L.fbuf0 + h * fb_bytes);
                 if constexpr (FOLD && !REL) {  // mirrored node pairs, F folded as it is written
-                    if (half > FP_THREADS / 4) {
+                    if (a.force_ns == 2 || (a.force_ns == 0 && half > FP_THREADS / 4)) {
                         for (int w = ft; w < 2 * half; w += FP_THREADS)
                             force_pair<2>(a.fd, ybuf, fbh, st.sing_key, pos_base, ind_base, psj, psc, act_h, h,
                                           w % half, N, (w / half) * 2);
@@ -1820,17 +1835,26 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_uni(const SegArgs a) {
                 else force_half_rel<1>(a.fd, rel_base, ybuf, fbh, st.sing_key, act_h, h, j, s0);
             }
             __syncthreads();
-            for (int hc = warp; hc < 2 * HC; hc += NW) {  // fold: s_k at k, a_k = F_k - F_{N-1-k} at N-1-k
-                const int h = hc / HC, col = hc % HC;       // warp per (half, column), lane per node
+            UNI_PHASE(7);
+            // fold: s_k at k, a_k = F_k - F_{N-1-k} at N-1-k (warp per (half, column), lane per node),
+            // with b0 = (omega2 anchor.F + 2 y0) / 2 of the column formed in the same pass
+            for (int hc = warp; hc < 2 * HC; hc += NW) {
+                const int h = hc / HC, col = hc % HC;
                 if (!((am >> (h * HS)) & 0xF)) continue;
                 double* fbh = fb0 + h * (fb_bytes / sizeof(double));
                 const int c = 2 * (col >> 3) + (col & 1), sl = (col & 7) >> 1;
+                double part = 0.0;
                 for (int k = lane; k < half; k += 32) {
                     const int lo = f2(k, c, sl), hi = f2(N - 1 - k, c, sl);
                     const double flo = fbh[lo], fhi = fbh[hi];
-                    fbh[lo] = flo + fhi;
-                    fbh[hi] = flo - fhi;
+                    const double sk = flo + fhi, ak = flo - fhi;
+                    fbh[lo] = sk;
+                    fbh[hi] = ak;
+                    part = fma(anc[k], sk, fma(anc[N - 1 - k], ak, part));
                 }
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) part += __shfl_xor_sync(0xffffffffu, part, off);
+                if (lane == 0) st.b0h[h][col] = 0.5 * fma(a.omega2, part, 2.0 * st.y0[h * HS + sl][c]);
             }
         } else {
             const int npw = half > T / 8 ? 2 : 4;  // work items per (half, node pair): slot pairs or slots
@@ -1853,8 +1877,9 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_uni(const SegArgs a) {
             const int t = tid, h = t / HS, s = t % HS, key = st.sing_key[t], j = key / (B + 1), chk = key % (B + 1);
             st.sing_val[t] = check_distance(ybuf[y2(j, h, 0, s)], ybuf[y2(j, h, 1, s)], ybuf[y2(j, h, 2, s)], j, chk, a.fd);
         }
-        // ---- b0 = anchor.F + 2 y0 of both halves (warps 0-7: half 0, 8-15: half 1; fixed order)
-        {
+        // ---- b0 = anchor.F + 2 y0 of both halves (warps 0-7: half 0, 8-15: half 1; fixed order);
+        //      relativistic: formed by the fold pass above
+        if constexpr (!REL) {
             const int h = warp >> 3, fw = warp & 7;
             if ((am >> (h * HS)) & 0xF) {
                 const double* fbh = fb0 + h * (fb_bytes / sizeof(double));
@@ -1882,8 +1907,8 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_uni(const SegArgs a) {
                 }
             }
         }
-        __syncthreads();
-        if (tid < 2 * HC) {
+        if constexpr (!REL) __syncthreads();
+        if (!REL && tid < 2 * HC) {
             const int h = tid / HC, ft = tid % HC;
             if ((am >> (h * HS)) & 0xF) {
                 const int c = 2 * (ft >> 3) + (ft & 1), s = (ft & 7) >> 1;

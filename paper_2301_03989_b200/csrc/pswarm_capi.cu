@@ -212,6 +212,7 @@ struct pswarm_ctx {
     int poison_outputs = 0;  // 1: NaN-fill device outputs before each solve (tests)
     int fold = 1;            // 1: mirror-folded update when N % 8 == 0 (k_pc_ws_fold)
     int fast_decide = 1;     // singleton-group decisions fast path
+    int force_ns = 0;        // folded Newtonian force items: slots per item (0 auto; diagnostics)
     int b0_mma = 1;          // folded: b0 from the anchor pair row (spare row, N/2 % 8 != 0)
     int unified = 2;         // folded solves: 1 k_pc_uni (all warps per phase), 0 k_pc_ws_fold, 2 auto =
                              // k_pc_uni for the force-bound 1PN model (N <= 200), else k_pc_ws_fold
@@ -965,6 +966,7 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
         a.nkp_fold = op.nkp_fold;
         a.b0_mma = ctx->b0_mma;
         a.fast_decide = ctx->fast_decide;
+        a.force_ns = ctx->force_ns;
         a.anc_fold = fold ? reinterpret_cast<const double*>(op.anc_fold.p) : nullptr;
         a.hist_stride = max_it;
         auto launch = [&](const SegArgs& x, int grid) {
@@ -1343,6 +1345,7 @@ pswarm_status pswarm_set_option(pswarm_ctx* ctx, const char* key, int64_t value)
         else if (k == "fold") ctx->fold = value != 0;
         else if (k == "b0_mma") ctx->b0_mma = value != 0;
         else if (k == "fast_decide") ctx->fast_decide = value != 0;
+        else if (k == "force_ns") ctx->force_ns = static_cast<int>(value);
         else if (k == "unified") ctx->unified = static_cast<int>(std::clamp<int64_t>(value, 0, 2));
         else raise(PSWARM_ERR_GENERIC, "pswarm_set_option: unknown key '" + k + "'");
     });
