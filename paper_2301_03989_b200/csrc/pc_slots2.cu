@@ -1835,7 +1835,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_uni(const SegArgs a) {
                 else force_half_rel<1>(a.fd, rel_base, ybuf, fbh, st.sing_key, act_h, h, j, s0);
             }
             __syncthreads();
-            UNI_PHASE(7);
+            UNI_PHASE(3);
             // fold: s_k at k, a_k = F_k - F_{N-1-k} at N-1-k (warp per (half, column), lane per node),
             // with b0 = (omega2 anchor.F + 2 y0) / 2 of the column formed in the same pass
             for (int hc = warp; hc < 2 * HC; hc += NW) {
@@ -1872,7 +1872,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_uni(const SegArgs a) {
             }
         }
         __syncthreads();
-        UNI_PHASE(3);
+        UNI_PHASE(REL ? 7 : 3);  // relativistic: the fold + b0 pass
         if (tid < SLOTS && st.sing_key[tid] != INT_MAX) {
             const int t = tid, h = t / HS, s = t % HS, key = st.sing_key[t], j = key / (B + 1), chk = key % (B + 1);
             st.sing_val[t] = check_distance(ybuf[y2(j, h, 0, s)], ybuf[y2(j, h, 1, s)], ybuf[y2(j, h, 2, s)], j, chk, a.fd);
