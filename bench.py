@@ -63,7 +63,7 @@ DESCR = {
            "{span} periods (1/1/1/0.5), hot starts (EXTENSION) on the equal-span segments"),
     "c4": ("C4: {m}-trajectory cloud total (reference spacecraft clones, spread 1e-5) sharded over the GPUs, "
            "Sun + 8 planets Newtonian N-body, {span} period single segment"),
-    "c5": ("C5: relativistic (EIH 1PN, EXTENSION) Sun + 8 planets, {m} ICs total in four quarters with clone "
+    "c5": ("C5: {force} Sun + 8 planets, {m} ICs total in four quarters with clone "
            "spreads 1e-7/1e-5/1e-3/1e-2 (convergence-mask stress), {span} period single segment"),
 }
 MODES = ("independent", "grouped", "augmented_parallel", "augmented_sequential")
@@ -81,6 +81,8 @@ def parse():
     ap.add_argument("--per-gpu", type=int, default=None, help="override the trajectory count")
     ap.add_argument("--nodes", type=int, default=200)
     ap.add_argument("--bodies", default=None, choices=["planets8", "reference", "none"])
+    ap.add_argument("--force", default=None, choices=["n_body", "n_body_1pn"],
+                    help="force model override (C5: Newtonian leg with --force n_body)")
     ap.add_argument("--span", type=float, default=None, help="span in osculating periods")
     ap.add_argument("--p-groups", type=int, default=None, help="grouped mode: number of groups")
     ap.add_argument("--cpu-sample", type=int, default=2000, help="trajectories in the bounded CPU baseline sample")
@@ -99,7 +101,7 @@ def parse():
     a.m = a.per_gpu if a.per_gpu is not None else m
     a.scaling = scaling
     a.bodies = a.bodies or bodies
-    a.kind = kind
+    a.kind = a.force or kind
     a.span = a.span if a.span is not None else span
     a.policy, a.start, a.spreads = policy, start, spreads
     return a
@@ -134,7 +136,17 @@ def workload(args, world, rank):
     if args.p_groups:
         cfg.p_groups = args.p_groups
     sizes = group_sizes(args, cfg, total)
-    shards = shard_groups(sizes, world)  # group-aligned contiguous shards (block.hpp:83-106)
+    if args.mode == "independent" and world > 1:
+        # singleton groups: interleaved shards -- rank r takes trajectories r, r + world, ...
+        # so every rank gets the same mix of the C5 spread quarters (heterogeneous iteration counts).
+        # The batch is reordered so the shards are contiguous; the metric does not depend on the order.
+        perm = np.concatenate([np.arange(r, total, world) for r in range(world)])
+        states = np.ascontiguousarray(states[perm])
+        counts = [len(range(r, total, world)) for r in range(world)]
+        offs = np.concatenate([[0], np.cumsum(counts)]).astype(int)
+        shards = [(int(offs[r]), int(offs[r + 1]), int(offs[r]), int(offs[r + 1])) for r in range(world)]
+    else:
+        shards = shard_groups(sizes, world)  # group-aligned contiguous shards (block.hpp:83-106)
     lo, hi = shards[rank][2], shards[rank][3]
     return states, (lo, hi), plan, cfg, shards
 
@@ -153,13 +165,15 @@ def config_dict(args, world, plan=None, cfg=None, launcher=None):
     nb = {"planets8": 8, "reference": 2, "none": 0}[args.bodies]
     mode = args.mode + (f" (p_groups={cfg.p_groups})" if cfg is not None and args.mode == "grouped" else "")
     return {
-        "workload": DESCR[args.config].format(m=args.m, span=args.span) +
+        "workload": DESCR[args.config].format(m=args.m, span=args.span, force="relativistic (EIH 1PN, EXTENSION)"
+                                              if args.kind == "n_body_1pn" else "Newtonian") +
                     f", N={args.nodes} nodes, {args.start} start, tol 1e-12, run mode {mode}" +
                     (" = per-trajectory convergence masking" if args.mode == "independent" else ""),
         "name": args.config, "mode": args.mode, "trajectories_per_gpu": total // world, "trajectories_total": total,
         "nodes": args.nodes, "bodies": nb, "force": args.kind,
         "segments": None if plan is None else len(plan.boundaries) - 1, "dtype": "f64",
-        "parallelism": f"dp{world} (trajectory shards, no collective in the iteration loop; terminal states "
+        "parallelism": f"dp{world} (" + ("interleaved " if args.mode == "independent" and world > 1 else "") +
+                       "trajectory shards, no collective in the iteration loop; terminal states "
                        "gathered to rank 0)" + (f"; {launcher}" if launcher else ""),
         "l2": "flushed between steps (512 MiB device write, outside the timed region)",
     }
@@ -229,7 +243,7 @@ def fp64_peak():
 
 def profile_tag(args):
     if args.config == "c5" or args.nodes != 200:
-        return f"{args.config}_n{args.nodes}"
+        return f"{args.config}_n{args.nodes}" + ("_newton" if args.config == "c5" and args.kind == "n_body" else "")
     return args.config + ("" if args.mode == "independent" else f"_{args.mode}")
 
 
