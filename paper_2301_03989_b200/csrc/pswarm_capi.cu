@@ -468,26 +468,31 @@ void solve_wide_rounds(pswarm_ctx* ctx, SegArgs a, const std::function<cudaError
                 g_err[g] = err;
                 g_conv[g] = conv ? 1 : 0;
             };
-            if (warm || timeout) {
+            if (warm) {  // the batch fails with the lowest warm-start fault (the caller picks it)
                 gf = GroupFault{};
                 for (int64_t m = lo; m < hi; ++m)
                     if (faulted(m) && (m_fl[m].status == FAULT_WARM_ZERO_RADIUS || m_fl[m].status == FAULT_WARM_SOLVER) &&
                         (gf.status == FAULT_NONE || m_fl[m].trajectory < gf.trajectory))
                         gf = m_fl[m];
-                if (gf.status == FAULT_NONE && timeout) {
-                    bool hit = false;  // a member cut by the deadline, or never reached
-                    int32_t itg = 0;
-                    for (int64_t m = lo; m < hi; ++m) {
-                        hit |= (faulted(m) && m_fl[m].status == FAULT_TIMEOUT) || (!m_cv[m] && !faulted(m) && m_it[m] < max_it);
-                        itg = std::max(itg, m_it[m]);
-                    }
-                    if (hit) {
-                        gf.status = FAULT_TIMEOUT;
-                        gf.iteration = itg;
-                    }
-                }
-                decide(gf.status == FAULT_NONE ? 0 : gf.iteration, 0.0, false);
+                decide(0, 0.0, false);
                 continue;
+            }
+            if (timeout) {  // a member cut by the device deadline, or never reached: the group timed out
+                bool hit = false;
+                int32_t itg = 0;
+                for (int64_t m = lo; m < hi; ++m) {
+                    hit |= (faulted(m) && m_fl[m].status == FAULT_TIMEOUT) || (!m_cv[m] && !faulted(m) && m_it[m] < max_it);
+                    itg = std::max(itg, m_it[m]);
+                }
+                if (hit) {
+                    gf = GroupFault{};
+                    gf.status = FAULT_TIMEOUT;
+                    gf.iteration = itg;
+                    decide(itg, 0.0, false);
+                    continue;
+                }
+                // every member stopped before the deadline: the group's outcome stands (below);
+                // a further round would meet the device deadline and report the timeout there
             }
             // ---- earliest solve fault of the group (singularity / divergence)
             int32_t fmin = INT32_MAX;
