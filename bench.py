@@ -424,7 +424,7 @@ def main():
         states, (lo, hi), plan, cfg, shards = workload(args, world, rank)
     shard = torch.from_numpy(states[lo:hi].copy()).pin_memory().numpy()  # pinned host ICs
     M = hi - lo
-    term_out = ps.pinned_terminal_buffer(M) if not native else True  # pinned host result (one DMA per step)
+    term_out = ps.pinned_terminal_buffer(M)  # pinned host result: one DMA per step
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
     def barrier():
@@ -434,7 +434,7 @@ def main():
 
     def step():
         if native:
-            r = mctx.run_batch(shard, cfg, plan, args.mode, samples=False, history=False)
+            r = mctx.run_batch(shard, cfg, plan, args.mode, samples=False, history=False, terminal=term_out)
             r.gathered = r.terminal_states
             return r
         r = ctx.run_batch(shard, cfg, plan, args.mode, samples=False, history=False, terminal=term_out)

@@ -1823,7 +1823,8 @@ struct pswarm_multi {
     std::vector<int> devices;
     std::vector<ncclComm_t> comms;  // one per device when the devices are distinct
     const char* backend = "peer-copy";
-    DevBuf root_term;  // gathered [M][6] on devices[0]
+    DevBuf root_term;   // gathered [M][6] on devices[0]
+    DevBuf root_term7;  // the same packed to the caller's [M][7] (one D2H)
     PinnedBuf pin_term;
     int nccl_version = 0;
 };
@@ -1878,6 +1879,8 @@ void pswarm_destroy_multi(pswarm_multi* m) {
         cudaSetDevice(m->ctx[0]->device);
         if (m->root_term.p) cudaFree(m->root_term.p);
         m->root_term.p = nullptr;
+        if (m->root_term7.p) cudaFree(m->root_term7.p);
+        m->root_term7.p = nullptr;
     }
     for (pswarm_ctx* c : m->ctx) pswarm_destroy(c);
     delete m;
@@ -2063,8 +2066,16 @@ pswarm_status pswarm_run_batch_multi(pswarm_multi* mc, int64_t n_states, const d
                 cuda_check(cudaMemcpyAsync(dst, sh[0].term, sizeof(double) * sh[0].M * 6, cudaMemcpyDeviceToDevice,
                                            root->stream),
                            "gather root shard");
-            double* h = mc->pin_term.get<double>(sizeof(double) * n_states * 6);
-            cuda_check(cudaMemcpyAsync(h, dst, sizeof(double) * n_states * 6, cudaMemcpyDeviceToHost, root->stream),
+            // packed to [M][7] on the device: one DMA straight into a page-locked caller buffer
+            double* d7 = mc->root_term7.get<double>(static_cast<size_t>(n_states) * 7);
+            cuda_check(launch_pack_states7(dst, boundaries[S], d7, n_states, root->stream), "k_pack_states7");
+            ++root->launches;
+            cudaPointerAttributes pa{};
+            const bool direct = cudaPointerGetAttributes(&pa, out->terminal_states) == cudaSuccess &&
+                                pa.type == cudaMemoryTypeHost;
+            cudaGetLastError();
+            double* h = direct ? out->terminal_states : mc->pin_term.get<double>(sizeof(double) * n_states * 7);
+            cuda_check(cudaMemcpyAsync(h, d7, sizeof(double) * n_states * 7, cudaMemcpyDeviceToHost, root->stream),
                        "D2H gathered terminal states");
             for (int r = 1; r < D; ++r) {
                 bind(mc->ctx[r]);
@@ -2072,10 +2083,7 @@ pswarm_status pswarm_run_batch_multi(pswarm_multi* mc, int64_t n_states, const d
             }
             bind(root);
             cuda_check(cudaStreamSynchronize(root->stream), "gather");
-            for (int64_t i = 0; i < n_states; ++i) {
-                out->terminal_states[7 * i] = boundaries[S];
-                std::memcpy(out->terminal_states + 7 * i + 1, h + 6 * i, sizeof(double) * 6);
-            }
+            if (!direct) std::memcpy(out->terminal_states, h, sizeof(double) * n_states * 7);
         }
         if (out) out->wall_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
     });
