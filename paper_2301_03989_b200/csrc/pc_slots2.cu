@@ -1717,7 +1717,6 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_uni(const SegArgs a) {
             }
             for (int h = 0; h < 2; ++h) {
                 int new_mask = 0;
-                const int hmask = 0xF << (h * HS);
                 const int g0 = gq + (h ? want[0] : 0), g1 = min(g0 + want[h], gend);
                 for (int gi = g0; gi < g1; ++gi) {
                     int lg = h * HS;
