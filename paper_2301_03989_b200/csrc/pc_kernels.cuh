@@ -81,7 +81,7 @@ struct SegArgs {
     int nkp_fold;               // k-pairs per folded part
     int b0_mma;                 // 1: folded b0 from the anchor pair row when N/2 % 8 != 0
     int fast_decide;            // 1: singleton-group decisions fast path (gmax == 1)
-    int force_ns;               // folded Newtonian force: slots per item (0 auto, 1, 2; diagnostics)
+    int force_ns;               // force items: slots per item (0 auto, 1, 2; diagnostics)
     const double* anc_fold;     // [8 nkp] anchor weights of the folded F layout
     // ---- wide groups (groups larger than one CTA): member-level rounds (pswarm_capi.cu
     //      solve_wide_rounds).  All nullptr for ordinary launches.

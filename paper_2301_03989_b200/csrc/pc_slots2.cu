@@ -1819,7 +1819,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_uni(const SegArgs a) {
         // ---- force of both halves, folded as written (mirrored node pairs); relativistic: per
         //      node with the fused 1PN pass, then folded in place
         if constexpr (REL) {
-            const int ns = N > 64 ? 2 : 1;  // slots per item (2 fused chains; N = 200: 800 items, all warps)
+            const int ns = a.force_ns ? a.force_ns : (N > 64 ? 2 : 1);  // slots per item (2 fused chains; N = 200: 800 items)
             // items node-major: the 8 / ns (half, slot group) items of a node sit in adjacent lanes,
             // so a warp reads 32 ns / 8 distinct table rows per load (shared-memory broadcast)
             const int per_node = 2 * (4 / ns);
