@@ -500,7 +500,9 @@ def main():
                            "dmma_pipe_active_pct": prof["dmma_pipe_active_pct"],
                            "fp64_pipe_active_pct": prof["fp64_pipe_active_pct"],
                            "executed_fp64_flops": ex,
-                           "executed_frac": round(ex / (kms_mean * 1e-3) / 1e12 / peak, 4),
+                           # one captured launch = one segment: against this run's mean kernel time per segment
+                           "executed_frac": round(ex / (kms_mean / max(len(plan.boundaries) - 1, 1) * 1e-3) / 1e12 /
+                                                  peak, 4),
                            "note": "executed = DMMA + 2 DFMA + DADD + DMUL of the captured launch over this "
                                    "run's kernel time (the mirror-folded update executes half the reference's "
                                    "update flops, so executed_frac < frac)"}
