@@ -195,6 +195,16 @@ bool ws_supported(int N, bool fold);
 bool uni_supported(int N);
 cudaError_t launch_segment_uni(const SegArgs& a, int grid, cudaStream_t s);
 cudaError_t launch_segment_ws(const SegArgs& a, int grid, cudaStream_t s);
+/// The same kernels with 4 MMA + 4 FP warps (256 threads) and two CTAs per SM, for small N
+/// (pc_slots2.cu compiled with -DPSWARM_SLOTS_SMALL).
+namespace small {
+size_t ws_smem_bytes(int N, int nkp, int xrows, int B, int stage_eph, bool fold, bool rel = false);
+int ws_extra_rows(int N, bool fold);
+bool ws_supported(int N, bool fold);
+bool uni_supported(int N);
+cudaError_t launch_segment_uni(const SegArgs& a, int grid, cudaStream_t s);
+cudaError_t launch_segment_ws(const SegArgs& a, int grid, cudaStream_t s);
+}  // namespace small
 
 GemmPlan make_gemm_plan(int N);
 int extra_rows(int N, const GemmPlan& gp);

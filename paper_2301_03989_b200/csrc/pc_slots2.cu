@@ -31,6 +31,12 @@
 #include "pc_tile.cuh"
 
 namespace pswarm_dev {
+// The same source compiles twice (csrc/Makefile): the default 512-thread kernels (8 MMA + 8 FP
+// warps, one CTA per SM) and, with -DPSWARM_SLOTS_SMALL, 256-thread kernels (4 + 4 warps) that
+// run two CTAs per SM for small N, in namespace pswarm_dev::small.
+#ifdef PSWARM_SLOTS_SMALL
+namespace small {
+#endif
 
 namespace {
 
@@ -43,7 +49,13 @@ constexpr int YS2 = 2 * HC + 4;
 #ifndef PSWARM_MMA_WARPS
 #define PSWARM_MMA_WARPS 8
 #endif
-constexpr int MMA_WARPS = PSWARM_MMA_WARPS, FP_WARPS = 8;
+#ifndef PSWARM_FP_WARPS
+#define PSWARM_FP_WARPS 8
+#endif
+#ifndef PSWARM_MIN_BLOCKS
+#define PSWARM_MIN_BLOCKS 1  // CTAs per SM the launch bounds promise (2 for the small variant)
+#endif
+constexpr int MMA_WARPS = PSWARM_MMA_WARPS, FP_WARPS = PSWARM_FP_WARPS;
 constexpr int MMA_THREADS = 32 * MMA_WARPS, FP_THREADS = 32 * FP_WARPS, WS_THREADS = MMA_THREADS + FP_THREADS;
 constexpr int BAR_F0 = 1, BAR_Y0 = 3, BAR_MMA = 5, BAR_FP = 6, BAR_B0 = 7;  // F_h = 1+h, Y_h = 3+h, B_h = 7+h
 
@@ -884,7 +896,7 @@ __device__ __forceinline__ void decide_half(const SegArgs& a, WsState& st, int h
 }
 
 template <int MAIN, int XMW, bool STAGE, bool REL, bool FOLD>
-__global__ void __launch_bounds__(WS_THREADS, 1) k_pc_ws(const SegArgs a) {
+__global__ void __launch_bounds__(WS_THREADS, PSWARM_MIN_BLOCKS) k_pc_ws(const SegArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int N = a.N, B = a.fd.n_bodies;
     const int xrows = a.xrows;
@@ -1612,7 +1624,7 @@ __device__ __forceinline__ void epilogue_unit_fold(const SegArgs& a, WsState& st
     } while (0)
 
 template <int NV, bool STAGE, bool REL>
-__global__ void __launch_bounds__(WS_THREADS, 1) k_pc_uni(const SegArgs a) {
+__global__ void __launch_bounds__(WS_THREADS, PSWARM_MIN_BLOCKS) k_pc_uni(const SegArgs a) {
     constexpr int T = WS_THREADS, NW = WS_THREADS / 32;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int N = a.N, B = a.fd.n_bodies;
@@ -1879,12 +1891,12 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_pc_uni(const SegArgs a) {
         // ---- b0 = anchor.F + 2 y0 of both halves (warps 0-7: half 0, 8-15: half 1; fixed order);
         //      relativistic: formed by the fold pass above
         if constexpr (!REL) {
-            const int h = warp >> 3, fw = warp & 7;
+            const int h = warp / (NW / 2), fw = warp % (NW / 2);  // (NW / 2 == B0_PARTS)
             if ((am >> (h * HS)) & 0xF) {
                 const double* fbh = fb0 + h * (fb_bytes / sizeof(double));
                 double s0 = 0.0, s1 = 0.0, s2 = 0.0;
                 const int jl = lane & 3;
-                for (int kq = fw; kq < a.nkp * 2; kq += 8) {
+                for (int kq = fw; kq < a.nkp * 2; kq += NW / 2) {
                     const double w = anc[4 * kq + jl];
                     const double* fq = fbh + kq * FKS + lane;
                     s0 = fma(w, fq[0], s0);
@@ -2033,12 +2045,13 @@ size_t ws_smem_bytes(int N, int nkp, int xrows, int B, int stage_eph, bool fold,
     return ws_layout(N, nkp, xrows, B, stage_eph, fold ? 1 : 0, rel).total;
 }
 
-/// Unified folded kernel (N % 8 == 0): units of 2 x ceil(N/16) pair tiles over 16 warps.
-bool uni_supported(int N) { return N % 8 == 0 && (2 * ws_mtiles(N, true) + 15) / 16 <= 2; }
+/// Unified folded kernel (N % 8 == 0): units of 2 x ceil(N/16) pair tiles over all warps.
+constexpr int UNI_WARPS = WS_THREADS / 32;
+bool uni_supported(int N) { return N % 8 == 0 && (2 * ws_mtiles(N, true) + UNI_WARPS - 1) / UNI_WARPS <= 2; }
 
 cudaError_t launch_segment_uni(const SegArgs& a, int grid, cudaStream_t s) {
     if (!uni_supported(a.N) || a.upack_fold == nullptr) return cudaErrorNotSupported;
-    const int nv = (2 * ws_mtiles(a.N, true) + 15) / 16;
+    const int nv = (2 * ws_mtiles(a.N, true) + UNI_WARPS - 1) / UNI_WARPS;
     const size_t smem = ws_smem_bytes(a.N, a.nkp, 0, a.fd.n_bodies, a.stage_eph, true, a.fd.rel != 0);
     if (a.fd.rel) {  // relativistic: the node table is staged when it fits (host: stage_eph)
         if (a.stage_eph)
@@ -2075,4 +2088,7 @@ cudaError_t launch_segment_ws(const SegArgs& a, int grid, cudaStream_t s) {
     }
 }
 
+#ifdef PSWARM_SLOTS_SMALL
+}  // namespace small
+#endif
 }  // namespace pswarm_dev

@@ -212,7 +212,9 @@ struct pswarm_ctx {
     int poison_outputs = 0;  // 1: NaN-fill device outputs before each solve (tests)
     int fold = 1;            // 1: mirror-folded update when N % 8 == 0 (k_pc_ws_fold)
     int fast_decide = 1;     // singleton-group decisions fast path
-    int force_ns = 0;        // folded Newtonian force items: slots per item (0 auto; diagnostics)
+    int force_ns = 0;        // force items: slots per item (0 auto; diagnostics)
+    int small_ctas = 1;      // small N: 256-thread slot kernels, two CTAs per SM
+    int small_max_n = 0;     // largest N for them (0: by force model, measured)
     int b0_mma = 1;          // folded: b0 from the anchor pair row (spare row, N/2 % 8 != 0)
     int unified = 2;         // folded solves: 1 k_pc_uni (all warps per phase), 0 k_pc_ws_fold, 2 auto =
                              // k_pc_uni for the force-bound 1PN model (N <= 200), else k_pc_ws_fold
@@ -813,19 +815,42 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
     // time 15.0 vs 19.2 ms at N = 200, 17.8 vs 27.0 ms at N = 256 against k_pc_ws_fold,
     // profiles/sanitizer_r02.json run); Newtonian forces stay on the warp-specialised kernel
     const bool uni = fold && (ctx->unified == 1 || (ctx->unified == 2 && rel)) && uni_supported(Ni);
-    ctx->last_kernel = uni ? "k_pc_uni" : fold ? "k_pc_ws_fold" : use_ws ? "k_pc_ws" : "k_pc_segment";
+    // small N: the 256-thread variants of the same kernels (4 + 4 warps, pswarm_dev::small) run two
+    // CTAs per SM, so one CTA's barrier / decision / claim latencies overlap the other's work;
+    // each CTA's shared memory must leave room for the second
+    constexpr size_t SMEM_PAIR = 228 * 1024 / 2 - 2 * 1024;
+    bool small_k = false;
+    int small_stage = 0, small_xrows = 0;
+    // measured (tools/probe_ab_opt.py small_ctas): Newtonian -32 % kernel time at N = 64, -10 % at 96,
+    // +14 % at 128; 1PN -16 % at 64, +1 % at 96, -6 % at 128
+    const int small_max = ctx->small_max_n > 0 ? ctx->small_max_n : (rel ? 128 : 96);
+    if (ctx->small_ctas && fold && Ni <= small_max && small::ws_supported(Ni, true) &&
+        (!uni || small::uni_supported(Ni))) {
+        small_xrows = uni ? 0 : small::ws_extra_rows(Ni, true);
+        auto bytes = [&](int stg) { return small::ws_smem_bytes(Ni, op.nkp, small_xrows, nb, stg, true, rel && uni); };
+        if (bytes(0) <= SMEM_PAIR) {
+            small_k = true;
+            small_stage = (rel ? uni : nb > 0) && bytes(1) <= SMEM_PAIR ? 1 : 0;
+        }
+    }
+    ctx->last_kernel = small_k ? (uni ? "k_pc_uni.x2" : "k_pc_ws_fold.x2")
+                       : uni   ? "k_pc_uni"
+                       : fold  ? "k_pc_ws_fold"
+                       : use_ws ? "k_pc_ws"
+                                : "k_pc_segment";
     // stage the frozen ephemeris in shared memory when it fits next to the state blocks (the
     // slot kernels copy it with the TMA unit); relativistic: the node table, k_pc_uni only
-    const int stage_eph = rel ? (uni && ws_smem_bytes(Ni, op.nkp, 0, nb, 1, true, true) <= SMEM_MAX ? 1 : 0)
-                              : (nb > 0 && (use_ws ? ws_smem_bytes(Ni, op.nkp, xrows, nb, 1, fold)
-                                                   : segment_smem_bytes(Ni, op.nkp, xrows, nb, 1)) <= SMEM_MAX
-                                     ? 1
-                                     : 0);
+    const int stage_eph = small_k ? small_stage
+                          : rel   ? (uni && ws_smem_bytes(Ni, op.nkp, 0, nb, 1, true, true) <= SMEM_MAX ? 1 : 0)
+                                  : (nb > 0 && (use_ws ? ws_smem_bytes(Ni, op.nkp, xrows, nb, 1, fold)
+                                                       : segment_smem_bytes(Ni, op.nkp, xrows, nb, 1)) <= SMEM_MAX
+                                         ? 1
+                                         : 0);
     if (!use_ws && segment_smem_bytes(Ni, op.nkp, xrows, nb, stage_eph) > SMEM_MAX)
         raise(PSWARM_ERR_INVALID_SIZE, fmtf("propagate: %lld nodes exceed the per-SM shared memory of the slot kernel",
                                             (long long)N));
     const int per_cta = static_cast<int>(SLOTS / gk);
-    const int cap = ctx->max_ctas > 0 ? ctx->max_ctas : ctx->sm_count * ctx->ctas_per_sm;
+    const int cap = ctx->max_ctas > 0 ? ctx->max_ctas : ctx->sm_count * (small_k ? 2 : ctx->ctas_per_sm);
     auto grid_for = [&](int64_t groups) {
         const int64_t want_ctas = (groups + per_cta - 1) / per_cta;
         return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want_ctas, cap)));
@@ -924,7 +949,7 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
         a.N = static_cast<int>(N);
         a.nkp = op.nkp;
         a.gp = op.gp;
-        a.xrows = xrows;
+        a.xrows = small_k ? small_xrows : xrows;
         a.stage_eph = stage_eph;
         a.M = static_cast<int>(M_act);
         a.P = static_cast<int>(P_act);
@@ -975,6 +1000,7 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
         a.anc_fold = fold ? reinterpret_cast<const double*>(op.anc_fold.p) : nullptr;
         a.hist_stride = max_it;
         auto launch = [&](const SegArgs& x, int grid) {
+            if (small_k) return uni ? small::launch_segment_uni(x, grid, st) : small::launch_segment_ws(x, grid, st);
             return uni ? launch_segment_uni(x, grid, st) : use_ws ? launch_segment_ws(x, grid, st) : launch_segment(x, grid, st);
         };
         if (max_it > 0 && !wide) {
@@ -1351,6 +1377,8 @@ pswarm_status pswarm_set_option(pswarm_ctx* ctx, const char* key, int64_t value)
         else if (k == "b0_mma") ctx->b0_mma = value != 0;
         else if (k == "fast_decide") ctx->fast_decide = value != 0;
         else if (k == "force_ns") ctx->force_ns = static_cast<int>(value);
+        else if (k == "small_ctas") ctx->small_ctas = value != 0;
+        else if (k == "small_max_n") ctx->small_max_n = static_cast<int>(value);
         else if (k == "unified") ctx->unified = static_cast<int>(std::clamp<int64_t>(value, 0, 2));
         else raise(PSWARM_ERR_GENERIC, "pswarm_set_option: unknown key '" + k + "'");
     });

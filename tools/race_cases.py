@@ -24,7 +24,9 @@ CASES = [(200, "independent", 1, "n_body", "warm", {}),                      # k
          (72, "grouped", 4, "n_body", "warm", {}),                           # groups of 6 -> wide rounds on k_pc_ws_fold
          (64, "augmented", 1, "n_body", "warm", {}),                         # wide rounds on k_pc_ws_fold (resume)
          (64, "independent", 1, "n_body_1pn", "warm", {}),                   # k_pc_uni, 1PN table bulk-staged
-         (64, "independent", 1, "n_body", "hot", {})]                        # hot start, multi-segment
+         (64, "independent", 1, "n_body", "hot", {}),                        # hot start, multi-segment
+         (96, "grouped", 4, "n_body", "warm", {}),                           # k_pc_ws_fold.x2 (two CTAs per SM)
+         (128, "augmented", 1, "n_body_1pn", "warm", {})]                    # k_pc_uni.x2, wide rounds
 for n, mode, p, kind, start, opts in CASES:
     plan = ps.plan_segments(base, 0.0, (2.2 if start == "hot" else 0.4) * period, ps.MU_SUN,
                             "per_orbit" if start == "hot" else "single", n)
