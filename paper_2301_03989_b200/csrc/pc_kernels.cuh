@@ -205,13 +205,6 @@ bool uni_supported(int N);
 cudaError_t launch_segment_uni(const SegArgs& a, int grid, cudaStream_t s);
 cudaError_t launch_segment_ws(const SegArgs& a, int grid, cudaStream_t s);
 }  // namespace small
-/// k_pc_uni with ONE half (4 slots) per CTA and 4 + 4 warps: two CTAs per SM whose phases
-/// interleave (pc_slots2.cu compiled with -DPSWARM_SLOTS_HALF1 -DPSWARM_HALVES=1).
-namespace half1 {
-size_t ws_smem_bytes(int N, int nkp, int xrows, int B, int stage_eph, bool fold, bool rel = false);
-bool uni_supported(int N);
-cudaError_t launch_segment_uni(const SegArgs& a, int grid, cudaStream_t s);
-}  // namespace half1
 
 GemmPlan make_gemm_plan(int N);
 int extra_rows(int N, const GemmPlan& gp);

@@ -34,24 +34,18 @@ namespace pswarm_dev {
 // The same source compiles twice (csrc/Makefile): the default 512-thread kernels (8 MMA + 8 FP
 // warps, one CTA per SM) and, with -DPSWARM_SLOTS_SMALL, 256-thread kernels (4 + 4 warps) that
 // run two CTAs per SM for small N, in namespace pswarm_dev::small.
-#if defined(PSWARM_SLOTS_SMALL)
+#ifdef PSWARM_SLOTS_SMALL
 namespace small {
-#elif defined(PSWARM_SLOTS_HALF1)
-namespace half1 {
 #endif
 
 namespace {
 
 constexpr int HS = 4;            // slots per half
 constexpr int HC = 6 * HS;       // columns per half
-#ifndef PSWARM_HALVES
-#define PSWARM_HALVES 2  // 1: k_pc_uni with one half (4 slots) per CTA, two CTAs per SM (half1)
-#endif
-constexpr int NH = PSWARM_HALVES;
 // Ybuf row stride 52 doubles (= 4 mod 16): a half-warp touching 4 rows x 4 slots (epilogue,
 // retire, warm start) covers 16 distinct banks; the slot index is XOR-swizzled with
 // (j >> 2) & 3 so the force's 16 consecutive rows of one column do as well.
-constexpr int YS2 = NH * HC + (NH == 2 ? 4 : 12);  // 52 or 36 doubles: both 4 mod 16
+constexpr int YS2 = 2 * HC + 4;
 #ifndef PSWARM_MMA_WARPS
 #define PSWARM_MMA_WARPS 8
 #endif
@@ -132,8 +126,7 @@ struct WsLayout {
     size_t ybuf, fbuf0, fbuf1, xstage, anchor, b0part, eph, state, total;
 };
 
-constexpr int B0_PARTS = (MMA_WARPS + FP_WARPS) / NH;  // b0 partial sums per column: one per FP warp
-                                                       // (k_pc_ws), one per warp of a half (k_pc_uni)
+constexpr int B0_PARTS = FP_WARPS;  // one partial sum per FP warp and b0 column
 
 /// Mirror-folded update (fold = 1): U anticommutes with the node reversal
 /// (U[N-1-j][N-1-k] = -U[j][k], Chebyshev-Lobatto nodes are mirrored, chebyshev.hpp:33-43),
@@ -153,12 +146,12 @@ __host__ __device__ inline WsLayout ws_layout(int N, int nkp, int xrows, int B, 
     L.fbuf0 = L.ybuf + sizeof(double) * static_cast<size_t>(N) * YS2;
     const size_t fb = sizeof(double) * static_cast<size_t>(fold ? ws_fold_ksteps(N, nkp) : 2 * nkp) * FKS;
     L.fbuf1 = L.fbuf0 + fb;
-    L.xstage = L.fbuf0 + NH * fb;  // [halves][fold ? lo, hi : 1][xrows][HC]
-    L.anchor = L.xstage + sizeof(double) * (fold ? 2 : 1) * NH * static_cast<size_t>(xrows) * HC;
+    L.xstage = L.fbuf1 + fb;  // [2 halves][fold ? lo, hi : 1][xrows][HC]
+    L.anchor = L.xstage + sizeof(double) * (fold ? 4 : 2) * static_cast<size_t>(xrows) * HC;
     L.b0part = L.anchor + sizeof(double) * static_cast<size_t>(8 * nkp);
     // staged table (bulk copy target, 16-byte aligned): Newtonian eph_t [3B + 3][eph_ld(N)], or
     // the relativistic node table [N][rel_stride(B)]
-    L.eph = (L.b0part + sizeof(double) * NH * B0_PARTS * HC + 15) & ~static_cast<size_t>(15);  // b0part: [half][part][HC]
+    L.eph = (L.b0part + sizeof(double) * 2 * B0_PARTS * HC + 15) & ~static_cast<size_t>(15);  // b0part: [half][part][HC]
     L.state = L.eph + (stage_eph ? sizeof(double) * eph_stage_doubles(N, B, rel) : 0);
     L.total = L.state + sizeof(WsState);
     return L;
@@ -956,13 +949,11 @@ __global__ void __launch_bounds__(WS_THREADS, PSWARM_MIN_BLOCKS) k_pc_ws(const S
             anc[k] = k < N ? up[2 * ((static_cast<size_t>(amt) * a.nkp + (k >> 3)) * 32 + ag * 4 + (k & 3)) + ((k >> 2) & 1)]
                            : 0.0;
     }
+    const double* pos_base = STAGE ? eph : a.fd.body_pos;
+    const double* ind_base = STAGE ? eph + 3 * B * eph_ld(N) : a.fd.indirect;
     // element (node j, body b, coordinate c) at pos_base[j * psj + (3b + c) * psc]: staged
-    // node-contiguous, so the force threads (one node each) read conflict-free; unstaged, the
-    // node-contiguous global copy when the host passes one (coalesced), else [N][B][3]
-    const bool nodec = STAGE || a.fd.eph_t != nullptr;
-    const double* pos_base = STAGE ? eph : nodec ? a.fd.eph_t : a.fd.body_pos;
-    const double* ind_base = STAGE ? eph + 3 * B * eph_ld(N) : nodec ? a.fd.eph_t + 3 * B * eph_ld(N) : a.fd.indirect;
-    const int psj = nodec ? 1 : 3 * B, psc = nodec ? eph_ld(N) : 1;
+    // node-contiguous, so the force threads (one node each) read conflict-free
+    const int psj = STAGE ? 1 : 3 * B, psc = STAGE ? eph_ld(N) : 1;
     const double* rel_base = STAGE ? eph : a.fd.rel_tab;  // relativistic node table
     if (tid == 0) {
         for (int t = 0; t < SLOTS; ++t) {
@@ -1662,12 +1653,11 @@ __global__ void __launch_bounds__(WS_THREADS, PSWARM_MIN_BLOCKS) k_pc_uni(const 
                    &st.stage_bar);
     }
     const int fb_doubles = ws_fold_ksteps(N, a.nkp) * FKS;
-    for (int i = tid; i < NH * fb_doubles; i += T) fb0[i] = 0.0;
+    for (int i = tid; i < 2 * fb_doubles; i += T) fb0[i] = 0.0;
     for (int k = tid; k < KP; k += T) anc[k] = k < N ? a.anc_fold[k] : 0.0;
-    const bool nodec = STAGE || a.fd.eph_t != nullptr;  // (as k_pc_ws)
-    const double* pos_base = STAGE ? eph : nodec ? a.fd.eph_t : a.fd.body_pos;
-    const double* ind_base = STAGE ? eph + 3 * B * eph_ld(N) : nodec ? a.fd.eph_t + 3 * B * eph_ld(N) : a.fd.indirect;
-    const int psj = nodec ? 1 : 3 * B, psc = nodec ? eph_ld(N) : 1;
+    const double* pos_base = STAGE ? eph : a.fd.body_pos;
+    const double* ind_base = STAGE ? eph + 3 * B * eph_ld(N) : a.fd.indirect;
+    const int psj = STAGE ? 1 : 3 * B, psc = STAGE ? eph_ld(N) : 1;
     const double* rel_base = STAGE ? eph : a.fd.rel_tab;
     if (tid == 0) {
         for (int t = 0; t < SLOTS; ++t) {
@@ -1690,7 +1680,7 @@ __global__ void __launch_bounds__(WS_THREADS, PSWARM_MIN_BLOCKS) k_pc_uni(const 
     bool first = true;
     for (;;) {
         // ---- decisions of both halves (warp h), after the previous iteration's epilogue
-        if (!first && warp < NH) decide_half(a, st, warp, lane, B);
+        if (!first && warp < 2) decide_half(a, st, warp, lane, B);
         __syncthreads();
         UNI_PHASE(0);
         // ---- retire outputs (both halves)
@@ -1728,7 +1718,7 @@ __global__ void __launch_bounds__(WS_THREADS, PSWARM_MIN_BLOCKS) k_pc_uni(const 
                     if ((fm >> t) & 1) st.slot_traj[t] = -1;
             }
             int want[2] = {0, 0}, gq = 0, gend = 0;
-            for (int h = 0; h < NH; ++h) {
+            for (int h = 0; h < 2; ++h) {
                 const int free_h = HS - __popc(static_cast<unsigned>(am & (0xF << (h * HS))));
                 want[h] = !st.queue_done && free_h >= a.gmax ? free_h / a.gmax : 0;
             }
@@ -1737,7 +1727,7 @@ __global__ void __launch_bounds__(WS_THREADS, PSWARM_MIN_BLOCKS) k_pc_uni(const 
                 gend = min(gq + want[0] + want[1], a.P);
                 if (gq + want[0] + want[1] >= a.P) st.queue_done = 1;
             }
-            for (int h = 0; h < NH; ++h) {
+            for (int h = 0; h < 2; ++h) {
                 int new_mask = 0;
                 const int g0 = gq + (h ? want[0] : 0), g1 = min(g0 + want[h], gend);
                 for (int gi = g0; gi < g1; ++gi) {
@@ -1763,7 +1753,7 @@ __global__ void __launch_bounds__(WS_THREADS, PSWARM_MIN_BLOCKS) k_pc_uni(const 
                 }
                 st.new_mask[h] = new_mask;
             }
-            for (int h = 0; h < NH; ++h) {
+            for (int h = 0; h < 2; ++h) {
                 const int hmask = 0xF << (h * HS);
                 st.act_word[h] = am & hmask;
                 st.half_active[h] = (am & hmask) != 0;
@@ -1844,7 +1834,7 @@ __global__ void __launch_bounds__(WS_THREADS, PSWARM_MIN_BLOCKS) k_pc_uni(const 
             const int ns = a.force_ns ? a.force_ns : (N > 64 ? 2 : 1);  // slots per item (2 fused chains; N = 200: 800 items)
             // items node-major: the 8 / ns (half, slot group) items of a node sit in adjacent lanes,
             // so a warp reads 32 ns / 8 distinct table rows per load (shared-memory broadcast)
-            const int per_node = NH * (4 / ns);
+            const int per_node = 2 * (4 / ns);
             for (int w = tid; w < N * per_node; w += T) {
                 const int j = w / per_node, r = w % per_node, h = r / (4 / ns);
                 const int act_h = (am >> (h * HS)) & 0xF;
@@ -1859,7 +1849,7 @@ __global__ void __launch_bounds__(WS_THREADS, PSWARM_MIN_BLOCKS) k_pc_uni(const 
             UNI_PHASE(3);
             // fold: s_k at k, a_k = F_k - F_{N-1-k} at N-1-k (warp per (half, column), lane per node),
             // with b0 = (omega2 anchor.F + 2 y0) / 2 of the column formed in the same pass
-            for (int hc = warp; hc < NH * HC; hc += NW) {
+            for (int hc = warp; hc < 2 * HC; hc += NW) {
                 const int h = hc / HC, col = hc % HC;
                 if (!((am >> (h * HS)) & 0xF)) continue;
                 double* fbh = fb0 + h * (fb_bytes / sizeof(double));
@@ -1878,8 +1868,8 @@ __global__ void __launch_bounds__(WS_THREADS, PSWARM_MIN_BLOCKS) k_pc_uni(const 
                 if (lane == 0) st.b0h[h][col] = 0.5 * fma(a.omega2, part, 2.0 * st.y0[h * HS + sl][c]);
             }
         } else {
-            const int npw = NH * 4 * half > T ? 2 : 4;  // work items per (half, node pair): slot pairs or slots
-            for (int w = tid; w < NH * npw * half; w += T) {
+            const int npw = half > T / 8 ? 2 : 4;  // work items per (half, node pair): slot pairs or slots
+            for (int w = tid; w < 2 * npw * half; w += T) {
                 const int h = w / (npw * half), r = w % (npw * half);
                 const int act_h = (am >> (h * HS)) & 0xF;
                 if (!act_h) continue;
@@ -1901,12 +1891,12 @@ __global__ void __launch_bounds__(WS_THREADS, PSWARM_MIN_BLOCKS) k_pc_uni(const 
         // ---- b0 = anchor.F + 2 y0 of both halves (warps 0-7: half 0, 8-15: half 1; fixed order);
         //      relativistic: formed by the fold pass above
         if constexpr (!REL) {
-            const int h = warp / (NW / NH), fw = warp % (NW / NH);  // (NW / NH == B0_PARTS)
+            const int h = warp / (NW / 2), fw = warp % (NW / 2);  // (NW / 2 == B0_PARTS)
             if ((am >> (h * HS)) & 0xF) {
                 const double* fbh = fb0 + h * (fb_bytes / sizeof(double));
                 double s0 = 0.0, s1 = 0.0, s2 = 0.0;
                 const int jl = lane & 3;
-                for (int kq = fw; kq < a.nkp * 2; kq += NW / NH) {
+                for (int kq = fw; kq < a.nkp * 2; kq += NW / 2) {
                     const double w = anc[4 * kq + jl];
                     const double* fq = fbh + kq * FKS + lane;
                     s0 = fma(w, fq[0], s0);
@@ -1929,7 +1919,7 @@ __global__ void __launch_bounds__(WS_THREADS, PSWARM_MIN_BLOCKS) k_pc_uni(const 
             }
         }
         if constexpr (!REL) __syncthreads();
-        if (!REL && tid < NH * HC) {
+        if (!REL && tid < 2 * HC) {
             const int h = tid / HC, ft = tid % HC;
             if ((am >> (h * HS)) & 0xF) {
                 const int c = 2 * (ft >> 3) + (ft & 1), s = (ft & 7) >> 1;
@@ -1943,7 +1933,7 @@ __global__ void __launch_bounds__(WS_THREADS, PSWARM_MIN_BLOCKS) k_pc_uni(const 
         UNI_PHASE(4);
         // ---- DMMA + epilogue: units (pair tile, half), unit u = warp + 16 i
         {
-            const int nunits = NH * mtiles;
+            const int nunits = 2 * mtiles;
             int tl[NV], hh[NV];
             const double* fbu[NV];
             int nv = 0;
@@ -1997,7 +1987,6 @@ static cudaError_t launch_uni_t(const SegArgs& a, int grid, size_t smem, cudaStr
     return cudaGetLastError();
 }
 
-#if PSWARM_HALVES == 2  // (the warp-specialised kernel ping-pongs two halves)
 template <int MAIN, int XMW, bool FOLD = false>
 static cudaError_t launch_ws_t(const SegArgs& a, int grid, size_t smem, cudaStream_t s) {
     // relativistic launches of this kernel never stage the node table (the host clears stage_eph)
@@ -2008,8 +1997,6 @@ static cudaError_t launch_ws_t(const SegArgs& a, int grid, size_t smem, cudaStre
     kern<<<grid, WS_THREADS, smem, s>>>(a);
     return cudaGetLastError();
 }
-
-#endif
 
 /// Tiles of one half: m-tiles of node rows, or (folded) of row pairs.
 static int ws_mtiles(int N, bool fold) { return fold ? (N / 2 + 7) / 8 : (N + 7) / 8; }
@@ -2060,11 +2047,11 @@ size_t ws_smem_bytes(int N, int nkp, int xrows, int B, int stage_eph, bool fold,
 
 /// Unified folded kernel (N % 8 == 0): units of 2 x ceil(N/16) pair tiles over all warps.
 constexpr int UNI_WARPS = WS_THREADS / 32;
-bool uni_supported(int N) { return N % 8 == 0 && (NH * ws_mtiles(N, true) + UNI_WARPS - 1) / UNI_WARPS <= 2; }
+bool uni_supported(int N) { return N % 8 == 0 && (2 * ws_mtiles(N, true) + UNI_WARPS - 1) / UNI_WARPS <= 2; }
 
 cudaError_t launch_segment_uni(const SegArgs& a, int grid, cudaStream_t s) {
     if (!uni_supported(a.N) || a.upack_fold == nullptr) return cudaErrorNotSupported;
-    const int nv = (NH * ws_mtiles(a.N, true) + UNI_WARPS - 1) / UNI_WARPS;
+    const int nv = (2 * ws_mtiles(a.N, true) + UNI_WARPS - 1) / UNI_WARPS;
     const size_t smem = ws_smem_bytes(a.N, a.nkp, 0, a.fd.n_bodies, a.stage_eph, true, a.fd.rel != 0);
     if (a.fd.rel) {  // relativistic: the node table is staged when it fits (host: stage_eph)
         if (a.stage_eph)
@@ -2076,7 +2063,6 @@ cudaError_t launch_segment_uni(const SegArgs& a, int grid, cudaStream_t s) {
     return nv == 1 ? launch_uni_t<1, false>(a, grid, smem, s) : launch_uni_t<2, false>(a, grid, smem, s);
 }
 
-#if PSWARM_HALVES == 2
 cudaError_t launch_segment_ws(const SegArgs& a, int grid, cudaStream_t s) {
     const bool fold = a.upack_fold != nullptr;
     if (!ws_supported(a.N, fold)) return cudaErrorNotSupported;
@@ -2101,9 +2087,8 @@ cudaError_t launch_segment_ws(const SegArgs& a, int grid, cudaStream_t s) {
     default: return cudaErrorNotSupported;
     }
 }
-#endif
 
-#if defined(PSWARM_SLOTS_SMALL) || defined(PSWARM_SLOTS_HALF1)
-}  // namespace small / half1
+#ifdef PSWARM_SLOTS_SMALL
+}  // namespace small
 #endif
 }  // namespace pswarm_dev

@@ -215,7 +215,6 @@ struct pswarm_ctx {
     int force_ns = 0;        // force items: slots per item (0 auto; diagnostics)
     int small_ctas = 1;      // small N: 256-thread slot kernels, two CTAs per SM
     int small_max_n = 0;     // largest N for them (0: by force model, measured)
-    int half1 = 0;           // k_pc_uni with one half per CTA, two CTAs per SM (experimental)
     int b0_mma = 1;          // folded: b0 from the anchor pair row (spare row, N/2 % 8 != 0)
     int unified = 2;         // folded solves: 1 k_pc_uni (all warps per phase), 0 k_pc_ws_fold, 2 auto =
                              // k_pc_uni for the force-bound 1PN model (N <= 200), else k_pc_ws_fold
@@ -834,21 +833,14 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
             small_stage = (rel ? uni : nb > 0) && bytes(1) <= SMEM_PAIR ? 1 : 0;
         }
     }
-    // half1: k_pc_uni with one half (4 slots) per CTA, two CTAs per SM (option "half1")
-    bool half1_k = false;
-    if (ctx->half1 && !small_k && fold && gk <= SLOTS / 2 && half1::uni_supported(Ni) &&
-        half1::ws_smem_bytes(Ni, op.nkp, 0, nb, 0, true, false) <= SMEM_PAIR)
-        half1_k = true;
-    ctx->last_kernel = half1_k ? "k_pc_uni.h1"
-                       : small_k ? (uni ? "k_pc_uni.x2" : "k_pc_ws_fold.x2")
+    ctx->last_kernel = small_k ? (uni ? "k_pc_uni.x2" : "k_pc_ws_fold.x2")
                        : uni   ? "k_pc_uni"
                        : fold  ? "k_pc_ws_fold"
                        : use_ws ? "k_pc_ws"
                                 : "k_pc_segment";
     // stage the frozen ephemeris in shared memory when it fits next to the state blocks (the
     // slot kernels copy it with the TMA unit); relativistic: the node table, k_pc_uni only
-    const int stage_eph = half1_k ? 0
-                          : small_k ? small_stage
+    const int stage_eph = small_k ? small_stage
                           : rel   ? (uni && ws_smem_bytes(Ni, op.nkp, 0, nb, 1, true, true) <= SMEM_MAX ? 1 : 0)
                                   : (nb > 0 && (use_ws ? ws_smem_bytes(Ni, op.nkp, xrows, nb, 1, fold)
                                                        : segment_smem_bytes(Ni, op.nkp, xrows, nb, 1)) <= SMEM_MAX
@@ -857,8 +849,8 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
     if (!use_ws && segment_smem_bytes(Ni, op.nkp, xrows, nb, stage_eph) > SMEM_MAX)
         raise(PSWARM_ERR_INVALID_SIZE, fmtf("propagate: %lld nodes exceed the per-SM shared memory of the slot kernel",
                                             (long long)N));
-    const int per_cta = static_cast<int>((half1_k ? SLOTS / 2 : SLOTS) / gk);
-    const int cap = ctx->max_ctas > 0 ? ctx->max_ctas : ctx->sm_count * (small_k || half1_k ? 2 : ctx->ctas_per_sm);
+    const int per_cta = static_cast<int>(SLOTS / gk);
+    const int cap = ctx->max_ctas > 0 ? ctx->max_ctas : ctx->sm_count * (small_k ? 2 : ctx->ctas_per_sm);
     auto grid_for = [&](int64_t groups) {
         const int64_t want_ctas = (groups + per_cta - 1) / per_cta;
         return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want_ctas, cap)));
@@ -879,8 +871,8 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
                        reinterpret_cast<double*>(din + o_cf)};
         d_pos = ctx->buf[B_BODY_POS].get<double>(static_cast<size_t>(N) * nb * 3);
         d_ind = ctx->buf[B_INDIRECT].get<double>(static_cast<size_t>(N) * 3);
-        if ((stage_eph && use_ws && !rel) || (half1_k && !rel))  // node-contiguous copy: bulk-staging source
-            d_eph_t = ctx->buf[B_EPH_T].get<double>(eph_stage_doubles(Ni, nb, false));  // (half1: read from L1)
+        if (stage_eph && use_ws && !rel)  // node-contiguous copy, the bulk-staging source
+            d_eph_t = ctx->buf[B_EPH_T].get<double>(eph_stage_doubles(Ni, nb, false));
     }
     double* d_hot = cfg->start_mode == 2 ? ctx->buf[B_HOT].get<double>(static_cast<size_t>(M) * N * 6) : nullptr;
     double *d_vel = nullptr, *d_rel = nullptr;
@@ -957,7 +949,7 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
         a.N = static_cast<int>(N);
         a.nkp = op.nkp;
         a.gp = op.gp;
-        a.xrows = half1_k ? 0 : small_k ? small_xrows : xrows;
+        a.xrows = small_k ? small_xrows : xrows;
         a.stage_eph = stage_eph;
         a.M = static_cast<int>(M_act);
         a.P = static_cast<int>(P_act);
@@ -1008,7 +1000,6 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
         a.anc_fold = fold ? reinterpret_cast<const double*>(op.anc_fold.p) : nullptr;
         a.hist_stride = max_it;
         auto launch = [&](const SegArgs& x, int grid) {
-            if (half1_k) return half1::launch_segment_uni(x, grid, st);
             if (small_k) return uni ? small::launch_segment_uni(x, grid, st) : small::launch_segment_ws(x, grid, st);
             return uni ? launch_segment_uni(x, grid, st) : use_ws ? launch_segment_ws(x, grid, st) : launch_segment(x, grid, st);
         };
@@ -1388,7 +1379,6 @@ pswarm_status pswarm_set_option(pswarm_ctx* ctx, const char* key, int64_t value)
         else if (k == "force_ns") ctx->force_ns = static_cast<int>(value);
         else if (k == "small_ctas") ctx->small_ctas = value != 0;
         else if (k == "small_max_n") ctx->small_max_n = static_cast<int>(value);
-        else if (k == "half1") ctx->half1 = value != 0;
         else if (k == "unified") ctx->unified = static_cast<int>(std::clamp<int64_t>(value, 0, 2));
         else raise(PSWARM_ERR_GENERIC, "pswarm_set_option: unknown key '" + k + "'");
     });
