@@ -949,11 +949,13 @@ __global__ void __launch_bounds__(WS_THREADS, PSWARM_MIN_BLOCKS) k_pc_ws(const S
             anc[k] = k < N ? up[2 * ((static_cast<size_t>(amt) * a.nkp + (k >> 3)) * 32 + ag * 4 + (k & 3)) + ((k >> 2) & 1)]
                            : 0.0;
     }
-    const double* pos_base = STAGE ? eph : a.fd.body_pos;
-    const double* ind_base = STAGE ? eph + 3 * B * eph_ld(N) : a.fd.indirect;
     // element (node j, body b, coordinate c) at pos_base[j * psj + (3b + c) * psc]: staged
-    // node-contiguous, so the force threads (one node each) read conflict-free
-    const int psj = STAGE ? 1 : 3 * B, psc = STAGE ? eph_ld(N) : 1;
+    // node-contiguous, so the force threads (one node each) read conflict-free; unstaged, the
+    // node-contiguous global copy when the host passes one (coalesced), else [N][B][3]
+    const bool nodec = STAGE || a.fd.eph_t != nullptr;
+    const double* pos_base = STAGE ? eph : nodec ? a.fd.eph_t : a.fd.body_pos;
+    const double* ind_base = STAGE ? eph + 3 * B * eph_ld(N) : nodec ? a.fd.eph_t + 3 * B * eph_ld(N) : a.fd.indirect;
+    const int psj = nodec ? 1 : 3 * B, psc = nodec ? eph_ld(N) : 1;
     const double* rel_base = STAGE ? eph : a.fd.rel_tab;  // relativistic node table
     if (tid == 0) {
         for (int t = 0; t < SLOTS; ++t) {
@@ -1655,9 +1657,10 @@ __global__ void __launch_bounds__(WS_THREADS, PSWARM_MIN_BLOCKS) k_pc_uni(const 
     const int fb_doubles = ws_fold_ksteps(N, a.nkp) * FKS;
     for (int i = tid; i < 2 * fb_doubles; i += T) fb0[i] = 0.0;
     for (int k = tid; k < KP; k += T) anc[k] = k < N ? a.anc_fold[k] : 0.0;
-    const double* pos_base = STAGE ? eph : a.fd.body_pos;
-    const double* ind_base = STAGE ? eph + 3 * B * eph_ld(N) : a.fd.indirect;
-    const int psj = STAGE ? 1 : 3 * B, psc = STAGE ? eph_ld(N) : 1;
+    const bool nodec = STAGE || a.fd.eph_t != nullptr;  // (as k_pc_ws)
+    const double* pos_base = STAGE ? eph : nodec ? a.fd.eph_t : a.fd.body_pos;
+    const double* ind_base = STAGE ? eph + 3 * B * eph_ld(N) : nodec ? a.fd.eph_t + 3 * B * eph_ld(N) : a.fd.indirect;
+    const int psj = nodec ? 1 : 3 * B, psc = nodec ? eph_ld(N) : 1;
     const double* rel_base = STAGE ? eph : a.fd.rel_tab;
     if (tid == 0) {
         for (int t = 0; t < SLOTS; ++t) {

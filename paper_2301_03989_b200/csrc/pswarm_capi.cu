@@ -215,6 +215,8 @@ struct pswarm_ctx {
     int force_ns = 0;        // force items: slots per item (0 auto; diagnostics)
     int small_ctas = 1;      // small N: 256-thread slot kernels, two CTAs per SM
     int small_max_n = 0;     // largest N for them (0: by force model, measured)
+    int eph_nc = 1;          // unstaged ephemeris read node-contiguous from global (eph_t): coalesced
+                             // (-14 % kernel time at N = 256, tools/probe_ab_opt.py eph_nc)
     int b0_mma = 1;          // folded: b0 from the anchor pair row (spare row, N/2 % 8 != 0)
     int unified = 2;         // folded solves: 1 k_pc_uni (all warps per phase), 0 k_pc_ws_fold, 2 auto =
                              // k_pc_uni for the force-bound 1PN model (N <= 200), else k_pc_ws_fold
@@ -871,7 +873,8 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
                        reinterpret_cast<double*>(din + o_cf)};
         d_pos = ctx->buf[B_BODY_POS].get<double>(static_cast<size_t>(N) * nb * 3);
         d_ind = ctx->buf[B_INDIRECT].get<double>(static_cast<size_t>(N) * 3);
-        if (stage_eph && use_ws && !rel)  // node-contiguous copy, the bulk-staging source
+        // node-contiguous copy: the bulk-staging source, or (option eph_nc) read from global
+        if (use_ws && !rel && (stage_eph || ctx->eph_nc))
             d_eph_t = ctx->buf[B_EPH_T].get<double>(eph_stage_doubles(Ni, nb, false));
     }
     double* d_hot = cfg->start_mode == 2 ? ctx->buf[B_HOT].get<double>(static_cast<size_t>(M) * N * 6) : nullptr;
@@ -1379,6 +1382,7 @@ pswarm_status pswarm_set_option(pswarm_ctx* ctx, const char* key, int64_t value)
         else if (k == "force_ns") ctx->force_ns = static_cast<int>(value);
         else if (k == "small_ctas") ctx->small_ctas = value != 0;
         else if (k == "small_max_n") ctx->small_max_n = static_cast<int>(value);
+        else if (k == "eph_nc") ctx->eph_nc = value != 0;
         else if (k == "unified") ctx->unified = static_cast<int>(std::clamp<int64_t>(value, 0, 2));
         else raise(PSWARM_ERR_GENERIC, "pswarm_set_option: unknown key '" + k + "'");
     });
