@@ -215,6 +215,7 @@ struct pswarm_ctx {
     int force_ns = 0;        // force items: slots per item (0 auto; diagnostics)
     int small_ctas = 1;      // small N: 256-thread slot kernels, two CTAs per SM
     int small_max_n = 0;     // largest N for them (0: by force model, measured)
+    int stage = 1;           // stage the per-segment node table in shared memory when it fits (0: never)
     int eph_nc = 1;          // unstaged ephemeris read node-contiguous from global (eph_t): coalesced
                              // (-14 % kernel time at N = 256, tools/probe_ab_opt.py eph_nc)
     int b0_mma = 1;          // folded: b0 from the anchor pair row (spare row, N/2 % 8 != 0)
@@ -832,7 +833,9 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
         auto bytes = [&](int stg) { return small::ws_smem_bytes(Ni, op.nkp, small_xrows, nb, stg, true, rel && uni); };
         if (bytes(0) <= SMEM_PAIR) {
             small_k = true;
-            small_stage = (rel ? uni : nb > 0) && bytes(1) <= SMEM_PAIR ? 1 : 0;
+            // (1PN: the two CTAs read the node table from L1 at least as fast as from their own
+            // staged copies: -4 % kernel time unstaged at N = 64, tie at 128)
+            small_stage = !rel && nb > 0 && bytes(1) <= SMEM_PAIR ? 1 : 0;
         }
     }
     ctx->last_kernel = small_k ? (uni ? "k_pc_uni.x2" : "k_pc_ws_fold.x2")
@@ -842,7 +845,8 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
                                 : "k_pc_segment";
     // stage the frozen ephemeris in shared memory when it fits next to the state blocks (the
     // slot kernels copy it with the TMA unit); relativistic: the node table, k_pc_uni only
-    const int stage_eph = small_k ? small_stage
+    const int stage_eph = !ctx->stage ? 0
+                          : small_k ? small_stage
                           : rel   ? (uni && ws_smem_bytes(Ni, op.nkp, 0, nb, 1, true, true) <= SMEM_MAX ? 1 : 0)
                                   : (nb > 0 && (use_ws ? ws_smem_bytes(Ni, op.nkp, xrows, nb, 1, fold)
                                                        : segment_smem_bytes(Ni, op.nkp, xrows, nb, 1)) <= SMEM_MAX
@@ -1383,6 +1387,7 @@ pswarm_status pswarm_set_option(pswarm_ctx* ctx, const char* key, int64_t value)
         else if (k == "small_ctas") ctx->small_ctas = value != 0;
         else if (k == "small_max_n") ctx->small_max_n = static_cast<int>(value);
         else if (k == "eph_nc") ctx->eph_nc = value != 0;
+        else if (k == "stage") ctx->stage = value != 0;
         else if (k == "unified") ctx->unified = static_cast<int>(std::clamp<int64_t>(value, 0, 2));
         else raise(PSWARM_ERR_GENERIC, "pswarm_set_option: unknown key '" + k + "'");
     });
