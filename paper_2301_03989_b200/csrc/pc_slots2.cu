@@ -382,14 +382,16 @@ __device__ __forceinline__ void force_half_rel(const ForceData& fd, const double
     for (int s0 = s_begin; s0 < s_begin + NS; s0 += PAIR) {
         // Per body A (d = r_A - r, rho = |d|, g = mu_A / rho^3):
         //   U += mu_A / rho,  n += g d,  b += g [K_A - (4 v.v_A + 1.5 (d.v_A / rho)^2 - 0.5 d.a_A) / c^2] d,
-        //   w_A = -g d.(4v - 3 v_A) = -g (4 d.v - 3 d.v_A),
-        //   sum_A w_A (v - v_A) = v W - sum_A w_A v_A  (W = sum_A w_A),  q += (mu_A / rho) a_A
+        //   w_A = -g d.(4v - 3 v_A) = -g (4 d.v - 3 d.v_A),  W += w_A,
+        //   sum_A w_A (v - v_A) = v W - sum_A w_A v_A,  q += (mu_A / rho) a_A
         // -- the EIH terms of rel_correction with d.(4v - 3v_A) and the (v - v_A) factor expanded
-        // (8 FP64 operations fewer per body; the expansion changes only the rounding of the 1/c^2
-        // terms, ~1e-8 of the acceleration)
+        // (8 FP64 operations fewer per body).  b, -sum w_A v_A / c^2 and 3.5 q / c^2 share ONE
+        // accumulator C (14 doubles of state per chain instead of 20, fewer register spills); the
+        // correction is f n + C + v W / c^2.  Both rewrites change only the rounding of the 1/c^2
+        // terms, ~1e-8 of the acceleration
+        const double k35 = 3.5 * ic2;
         double rx[PAIR], ry[PAIR], rz[PAIR], vx[PAIR], vy[PAIR], vz[PAIR];
-        double U[PAIR], nx[PAIR], ny[PAIR], nz[PAIR], bx[PAIR], by[PAIR], bz[PAIR], W[PAIR], wx[PAIR], wy[PAIR],
-            wz[PAIR], qx[PAIR], qy[PAIR], qz[PAIR];
+        double U[PAIR], nx[PAIR], ny[PAIR], nz[PAIR], cx[PAIR], cy[PAIR], cz[PAIR], W[PAIR];
         bool on[PAIR];
         bool flag = false;
 #pragma unroll
@@ -402,8 +404,7 @@ __device__ __forceinline__ void force_half_rel(const ForceData& fd, const double
             vx[k] = on[k] ? ybuf[y2(j, h, 3, s)] : 0.0;
             vy[k] = on[k] ? ybuf[y2(j, h, 4, s)] : 0.0;
             vz[k] = on[k] ? ybuf[y2(j, h, 5, s)] : 0.0;
-            U[k] = nx[k] = ny[k] = nz[k] = bx[k] = by[k] = bz[k] = 0.0;
-            W[k] = wx[k] = wy[k] = wz[k] = qx[k] = qy[k] = qz[k] = 0.0;
+            U[k] = nx[k] = ny[k] = nz[k] = cx[k] = cy[k] = cz[k] = W[k] = 0.0;
             flag |= !(rx[k] * rx[k] + ry[k] * ry[k] + rz[k] * rz[k] > 0.0);
         }
         // single chain (small N): 3 bodies in flight for ILP; slot pairs already give 2 chains
@@ -430,24 +431,13 @@ __device__ __forceinline__ void force_half_rel(const ForceData& fd, const double
                 const double daa = dx * aax + dy * aay + dz * aaz;
                 const double di = dva * ir;
                 const double br = g * (K - ic2 * fma(4.0, vva, fma(1.5 * di, di, -0.5 * daa)));
-                bx[k] = fma(br, dx, bx[k]);
-                by[k] = fma(br, dy, by[k]);
-                bz[k] = fma(br, dz, bz[k]);
                 const double w = g * fma(3.0, dva, -4.0 * dv);
+                const double wv = -ic2 * w, qa = k35 * mi;
                 W[k] += w;
-                wx[k] = fma(w, vax, wx[k]);
-                wy[k] = fma(w, vay, wy[k]);
-                wz[k] = fma(w, vaz, wz[k]);
-                qx[k] = fma(mi, aax, qx[k]);
-                qy[k] = fma(mi, aay, qy[k]);
-                qz[k] = fma(mi, aaz, qz[k]);
+                cx[k] = fma(br, dx, fma(wv, vax, fma(qa, aax, cx[k])));
+                cy[k] = fma(br, dy, fma(wv, vay, fma(qa, aay, cy[k])));
+                cz[k] = fma(br, dz, fma(wv, vaz, fma(qa, aaz, cz[k])));
             }
-        }
-#pragma unroll
-        for (int k = 0; k < PAIR; ++k) {  // sum_A w_A (v - v_A) = v W - sum_A w_A v_A
-            wx[k] = fma(vx[k], W[k], -wx[k]);
-            wy[k] = fma(vy[k], W[k], -wy[k]);
-            wz[k] = fma(vz[k], W[k], -wz[k]);
         }
         if (flag) {  // rare: exact guard order of table_acceleration (force_model.hpp:57-69)
 #pragma unroll
@@ -466,9 +456,10 @@ __device__ __forceinline__ void force_half_rel(const ForceData& fd, const double
         for (int k = 0; k < PAIR; ++k) {
             const int s = s0 + k;
             const double f = ic2 * (vx[k] * vx[k] + vy[k] * vy[k] + vz[k] * vz[k] - 4.0 * U[k]);
-            const double ax = (nx[k] - ix) + (f * nx[k] + bx[k] + ic2 * wx[k] + 3.5 * ic2 * qx[k]);
-            const double ay = (ny[k] - iy) + (f * ny[k] + by[k] + ic2 * wy[k] + 3.5 * ic2 * qy[k]);
-            const double az = (nz[k] - iz) + (f * nz[k] + bz[k] + ic2 * wz[k] + 3.5 * ic2 * qz[k]);
+            const double iw = ic2 * W[k];
+            const double ax = (nx[k] - ix) + fma(f, nx[k], fma(iw, vx[k], cx[k]));
+            const double ay = (ny[k] - iy) + fma(f, ny[k], fma(iw, vy[k], cy[k]));
+            const double az = (nz[k] - iz) + fma(f, nz[k], fma(iw, vz[k], cz[k]));
             fb[f2(j, 0, s)] = on[k] ? vx[k] : 0.0;
             fb[f2(j, 1, s)] = on[k] ? vy[k] : 0.0;
             fb[f2(j, 2, s)] = on[k] ? vz[k] : 0.0;
