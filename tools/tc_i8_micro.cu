@@ -1,0 +1,166 @@
+// tcgen05 kind::i8 probe (diagnostics): D[M=128][N] (s32, TMEM) = A[128][K] . B[N][K]^T, both
+// operands int8 K-major without swizzle in shared memory (8-row x 16-byte core matrices), checked
+// against a host integer GEMM; then R back-to-back accumulating MMAs timed with clock64.
+// build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/tc_i8_micro tools/tc_i8_micro.cu
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#define CK(x)                                                                  \
+    do {                                                                       \
+        cudaError_t e_ = (x);                                                  \
+        if (e_ != cudaSuccess) {                                               \
+            printf("CUDA %s at %s:%d\n", cudaGetErrorString(e_), __FILE__, __LINE__); \
+            exit(1);                                                           \
+        }                                                                      \
+    } while (0)
+
+constexpr int M = 128, K = 128;
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+
+// canonical K-major no-swizzle offset of (row r, byte k) for an operand with K bytes per row
+__host__ __device__ __forceinline__ int kmaj(int r, int k, int kbytes) {
+    return (r >> 3) * (kbytes * 8) + (k >> 4) * 128 + (r & 7) * 16 + (k & 15);
+}
+
+__device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((addr >> 4) & 0x3FFF);
+    d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16;
+    d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32;
+    d |= 1ull << 46;  // version 1 (sm_100)
+    return d;         // base offset 0, lbo mode 0, SWIZZLE_NONE
+}
+
+__host__ __device__ constexpr uint32_t idesc_i8(int m, int n) {
+    return (2u << 4)      // D s32
+           | (1u << 7)    // A signed
+           | (1u << 10)   // B signed
+           | (0u << 15)   // A K-major
+           | (0u << 16)   // B K-major
+           | (static_cast<uint32_t>(n >> 3) << 17) | (static_cast<uint32_t>(m >> 4) << 24);
+}
+
+template <int N>
+__global__ void k_probe(const int8_t* A, const int8_t* B, int* D, int reps, long long* cyc, int swap_lbo) {
+    extern __shared__ __align__(1024) unsigned char sm[];
+    int8_t* sa = reinterpret_cast<int8_t*>(sm);
+    int8_t* sb = sa + M * K;
+    __shared__ __align__(8) uint64_t mbar;
+    __shared__ uint32_t tbase;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    for (int i = tid; i < M * K; i += blockDim.x) sa[kmaj(i / K, i % K, K)] = A[i];
+    for (int i = tid; i < N * K; i += blockDim.x) sb[kmaj(i / K, i % K, K)] = B[i];
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tbase)), "n"(N <= 32 ? 32 : N <= 64 ? 64 : 128));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&mbar)));
+        asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+    asm volatile("fence.proxy.async.shared::cta;");  // generic-proxy operand writes -> async proxy
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tm = tbase;
+    const uint32_t lbo = swap_lbo ? K * 8 : 128, sbo = swap_lbo ? 128 : K * 8;
+    long long t0 = 0, t1 = 0;
+    if (tid == 0) {
+        const uint32_t id = idesc_i8(M, N);
+        t0 = clock64();
+        for (int r = 0; r < reps; ++r)
+            for (int ks = 0; ks < K / 32; ++ks) {
+                const uint64_t da = sdesc(su32(sa) + ks * 256, lbo, sbo);
+                const uint64_t db = sdesc(su32(sb) + ks * 256, lbo, sbo);
+                const uint32_t acc = (r | ks) ? 1u : 0u;
+                asm volatile(
+                    "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                    "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tm),
+                    "l"(da), "l"(db), "r"(id), "r"(acc));
+            }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&mbar)));
+        uint32_t done = 0;
+        while (!done)
+            asm volatile("{\n\t.reg .pred q;\n\tmbarrier.try_wait.parity.shared::cta.b64 q, [%1], %2;\n\tselp.u32 %0, 1, 0, q;\n\t}"
+                         : "=r"(done) : "r"(su32(&mbar)), "r"(0));
+        t1 = clock64();
+        cyc[0] = t1 - t0;
+    }
+    __syncthreads();
+    {  // other threads: wait on the same phase
+        uint32_t done = 0;
+        while (!done)
+            asm volatile("{\n\t.reg .pred q;\n\tmbarrier.try_wait.parity.shared::cta.b64 q, [%1], %2;\n\tselp.u32 %0, 1, 0, q;\n\t}"
+                         : "=r"(done) : "r"(su32(&mbar)), "r"(0));
+    }
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    // drain: warp w reads lanes 32w..32w+31 (row = tid), 8 columns per load
+    const int row = tid;
+#pragma unroll
+    for (int c0 = 0; c0 < N; c0 += 8) {
+        uint32_t v[8];
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                     : "r"(tm + (static_cast<uint32_t>(warp * 32) << 16) + c0));
+        asm volatile("tcgen05.wait::ld.sync.aligned;");
+        for (int e = 0; e < 8; ++e) D[row * N + c0 + e] = static_cast<int>(v[e]);
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm), "n"(N <= 32 ? 32 : N <= 64 ? 64 : 128));
+}
+
+template <int N>
+static int run(int swap) {
+    std::vector<int8_t> a(M * K), b(N * K);
+    srand(7);
+    for (auto& x : a) x = static_cast<int8_t>(rand() % 256 - 128);
+    for (auto& x : b) x = static_cast<int8_t>(rand() % 256 - 128);
+    int8_t *da, *db;
+    int* dd;
+    long long* dc;
+    CK(cudaMalloc(&da, a.size()));
+    CK(cudaMalloc(&db, b.size()));
+    CK(cudaMalloc(&dd, M * N * 4));
+    CK(cudaMalloc(&dc, 8));
+    CK(cudaMemcpy(da, a.data(), a.size(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(db, b.data(), b.size(), cudaMemcpyHostToDevice));
+    const int smem = M * K + N * K;
+    CK(cudaFuncSetAttribute(k_probe<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    k_probe<N><<<1, 128, smem>>>(da, db, dd, 1, dc, swap);
+    CK(cudaDeviceSynchronize());
+    std::vector<int> d(M * N);
+    CK(cudaMemcpy(d.data(), dd, d.size() * 4, cudaMemcpyDeviceToHost));
+    int bad = 0;
+    for (int m = 0; m < M; ++m)
+        for (int n = 0; n < N; ++n) {
+            int s = 0;
+            for (int k = 0; k < K; ++k) s += a[m * K + k] * b[n * K + k];
+            if (s != d[m * N + n] && bad++ < 3) printf("  N=%d swap=%d mismatch (%d,%d): %d vs %d\n", N, swap, m, n, d[m * N + n], s);
+        }
+    long long cyc = 0;
+    const int reps = 256;
+    k_probe<N><<<1, 128, smem>>>(da, db, dd, reps, dc, swap);
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(&cyc, dc, 8, cudaMemcpyDeviceToHost));
+    printf("N=%d swap=%d: %s (%d bad); %.1f cycles per MMA (M128 N%d K32), %.0f MAC/cycle\n", N, swap,
+           bad ? "MISMATCH" : "exact", bad, double(cyc) / (reps * K / 32), N, double(M) * N * K * reps / cyc);
+    cudaFree(da);
+    cudaFree(db);
+    cudaFree(dd);
+    cudaFree(dc);
+    return bad;
+}
+
+int main() {
+    int bad = 0;
+    bad += run<48>(0);
+    if (bad) bad = run<48>(1);
+    run<32>(0);
+    run<64>(0);
+    run<128>(0);
+    return 0;
+}
