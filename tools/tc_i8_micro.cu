@@ -113,6 +113,157 @@ __global__ void k_probe(const int8_t* A, const int8_t* B, int* D, int reps, long
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm), "n"(N <= 32 ? 32 : N <= 64 ? 64 : 128));
 }
 
+
+// A-operand streaming: every CTA (one per SM) streams NCH chunks of A (104 rows x 32 K bytes in
+// the canonical layout, 3,328 B, L2-resident source) through an R-slot shared-memory ring with
+// cp.async.bulk + mbarriers, one M128 x NB x K32 MMA per chunk (B resident), and reports cycles
+// per chunk: is the U-digit stream of an emulated-FP64 update latency-bound with a small ring?
+constexpr int CH = 104 * 32;
+template <int R, int NB>
+__global__ void k_stream(const int8_t* A, int nsrc, int nch, long long* cyc, int* sink, int do_mma) {
+    extern __shared__ __align__(1024) unsigned char sm[];
+    int8_t* ring = reinterpret_cast<int8_t*>(sm);
+    int8_t* sb = ring + R * 4096;
+    __shared__ __align__(8) uint64_t full[R], empty[R];
+    __shared__ uint32_t tbase;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    for (int i = tid; i < NB * 32; i += blockDim.x) sb[kmaj(i / 32, i % 32, 32)] = static_cast<int8_t>(i % 7 - 3);
+    for (int i = tid; i < R * 4096; i += blockDim.x) ring[i] = 0;
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tbase)), "n"(256));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+        for (int r = 0; r < R; ++r) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&full[r])));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&empty[r])));
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+    asm volatile("fence.proxy.async.shared::cta;");
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    if (tid == 0) {
+        const uint32_t tm = tbase, id = idesc_i8(M, NB);
+        auto wait = [&](uint64_t* b, uint32_t ph) {  // test_wait spin (no suspend window)
+            uint32_t done = 0;
+            while (!done)
+                asm volatile("{\n\t.reg .pred q;\n\tmbarrier.test_wait.parity.shared::cta.b64 q, [%1], %2;\n\tselp.u32 %0, 1, 0, q;\n\t}"
+                             : "=r"(done) : "r"(su32(b)), "r"(ph));
+        };
+        auto issue = [&](int c) {  // chunk c into slot c % R
+            const int r = c % R;
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&full[r])), "r"(CH));
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                             su32(ring + r * 4096)), "l"(A + static_cast<size_t>(nsrc > 56 ? blockIdx.x * 56 + c % 56 : (c * 7 + blockIdx.x) % nsrc) * CH), "r"(CH), "r"(su32(&full[r])) : "memory");
+        };
+        const long long t0 = clock64();
+        for (int c = 0; c < R && c < nch; ++c) issue(c);  // then chunk j + R refills slot j
+        for (int c = 0; c < nch; ++c) {
+            wait(&full[c % R], (c / R) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            const uint64_t da = sdesc(su32(ring + (c % R) * 4096), 128, 256);
+            const uint64_t db = sdesc(su32(sb), 128, 256);
+            if (do_mma) {
+                asm volatile(
+                    "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                    "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tm),
+                    "l"(da), "l"(db), "r"(id), "r"(c ? 1u : 0u));
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&empty[c % R])));
+            } else {
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&empty[c % R])));
+            }
+            // refill the slot of chunk j = c - R/2 (its MMA was issued R/2 chunks ago): R/2 MMAs stay
+            // queued while the issuer waits, R/2 copies are in flight
+            const int j = c - R / 2;
+            if (j >= 0 && j + R < nch) {
+                wait(&empty[j % R], (j / R) & 1);
+                issue(j + R);
+            }
+        }
+        wait(&empty[(nch - 1) % R], ((nch - 1) / R) & 1);
+        const long long t1 = clock64();
+        cyc[blockIdx.x] = t1 - t0;
+    }
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    if (warp == 0) {
+        uint32_t v;
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(v) : "r"(tbase));
+        asm volatile("tcgen05.wait::ld.sync.aligned;");
+        if (tid == 0) sink[blockIdx.x] = static_cast<int>(v);
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "n"(256));
+    }
+}
+
+template <int R, int NB>
+static void stream(int nch, int do_mma = 1, int nsrc = 56, int grid = 148) {
+    int8_t* da;
+    long long* dc;
+    int* ds;
+    CK(cudaMalloc(&da, static_cast<size_t>(nsrc) * CH));
+    CK(cudaMemset(da, 1, static_cast<size_t>(nsrc) * CH));
+    CK(cudaMalloc(&dc, grid * 8));
+    CK(cudaMalloc(&ds, grid * 4));
+    const int smem = R * 4096 + NB * 32;
+    CK(cudaFuncSetAttribute(k_stream<R, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    for (int rep = 0; rep < 2; ++rep) k_stream<R, NB><<<grid, 128, smem>>>(da, nsrc, nch, dc, ds, do_mma);
+    CK(cudaDeviceSynchronize());
+    std::vector<long long> c(grid);
+    CK(cudaMemcpy(c.data(), dc, grid * 8, cudaMemcpyDeviceToHost));
+    double mean = 0;
+    for (auto x : c) mean += double(x) / grid;
+    printf("stream ring %d, N%d, mma %d, %s source: %.0f cycles per chunk (%d CTAs, %d chunks each)\n", R, NB, do_mma,
+           nsrc > 56 ? "per-CTA" : "shared", mean / nch, grid, nch);
+    cudaFree(da);
+    cudaFree(dc);
+    cudaFree(ds);
+}
+
+// L2 -> SM read bandwidth with plain 16-byte loads: every CTA (one per SM, T threads) sweeps a
+// private L2-resident region `reps` times; bytes per cycle per SM.
+template <int T>
+__global__ void k_ldg(const int4* src, size_t per_cta16, int reps, long long* cyc, int* sink) {
+    const int4* p = src + blockIdx.x * per_cta16;
+    int acc = 0;
+    __syncthreads();
+    const long long t0 = clock64();
+    for (int r = 0; r < reps; ++r)
+#pragma unroll 4
+        for (size_t i = threadIdx.x; i < per_cta16; i += T) {
+            const int4 v = __ldcg(p + i);
+            acc ^= v.x ^ v.y ^ v.z ^ v.w;
+        }
+    __syncthreads();
+    const long long t1 = clock64();
+    if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+    if (acc == 0x12345678) sink[0] = acc;
+}
+
+template <int T>
+static void ldg_bw(size_t per_cta_bytes, int reps) {
+    const int grid = 148;
+    int4* d;
+    long long* dc;
+    int* ds;
+    CK(cudaMalloc(&d, per_cta_bytes * grid));
+    CK(cudaMemset(d, 1, per_cta_bytes * grid));
+    CK(cudaMalloc(&dc, grid * 8));
+    CK(cudaMalloc(&ds, 4));
+    for (int rep = 0; rep < 2; ++rep) k_ldg<T><<<grid, T>>>(d, per_cta_bytes / 16, reps, dc, ds);
+    CK(cudaDeviceSynchronize());
+    std::vector<long long> c(grid);
+    CK(cudaMemcpy(c.data(), dc, grid * 8, cudaMemcpyDeviceToHost));
+    double mean = 0;
+    for (auto x : c) mean += double(x) / grid;
+    printf("ldg %d threads, %zu KB per CTA x %d: %.1f B/cycle/SM (%.2f TB/s at 1.9 GHz, 148 SMs)\n", T, per_cta_bytes / 1024, reps,
+           double(per_cta_bytes) * reps / mean, double(per_cta_bytes) * reps / mean * 148 * 1.9e9 / 1e12);
+    cudaFree(d);
+    cudaFree(dc);
+    cudaFree(ds);
+}
+
 template <int N>
 static int run(int swap) {
     std::vector<int8_t> a(M * K), b(N * K);
@@ -162,5 +313,24 @@ int main() {
     run<32>(0);
     run<64>(0);
     run<128>(0);
+    stream<3, 192>(1120);
+    stream<4, 192>(1120);
+    stream<8, 192>(1120);
+    stream<16, 192>(1120);
+    stream<4, 48>(1120);
+    stream<8, 48>(1120);
+    stream<4, 48>(1120, 0);
+    stream<16, 48>(1120, 0);
+    stream<4, 48>(1120, 0, 148 * 56);
+    stream<16, 48>(1120, 0, 148 * 56);
+    stream<16, 192>(1120, 1, 148 * 56);
+    stream<16, 48>(1120, 0, 56, 1);
+    stream<16, 48>(16, 0, 56, 1);
+    stream<16, 48>(1, 0, 56, 1);
+    stream<16, 48>(16, 0, 56, 148);
+    stream<4, 48>(1120, 0, 56, 1);
+    ldg_bw<512>(186 * 1024, 20);
+    ldg_bw<256>(186 * 1024, 20);
+    ldg_bw<512>(1024 * 1024, 4);
     return 0;
 }
