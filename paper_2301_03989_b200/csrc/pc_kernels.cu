@@ -42,6 +42,7 @@ struct CtaState {
     int grp_iter[SLOTS];
     int grp_floor[SLOTS];  // wide-group round: converge only at it >= floor
     int grp_cap[SLOTS];    // stop at it >= cap (max_iterations, or a round's target)
+    unsigned long long grp_t0[SLOTS];  // %globaltimer at the claim (per-trajectory budgets only)
     int active_mask;
     int new_mask;
     int retire_mask;           // slots whose results are written out this tick
@@ -187,6 +188,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_pc_segment(const SegArgs a) {
                     st.grp_iter[lg] = start_iteration(a, off);
                     st.grp_floor[lg] = claim_floor(a, gid);
                     st.grp_cap[lg] = claim_cap(a, gid);
+                    if (a.traj_ns) st.grp_t0[lg] = globaltimer_ns();
                     int t = 0;
                     for (int mbr = 0; mbr < size; ++mbr) {
                         while ((am >> t) & 1) ++t;
@@ -539,6 +541,11 @@ __global__ void __launch_bounds__(MAXT, 1) k_pc_segment(const SegArgs a) {
                             retire = ok = true;
                         }
                     }
+                }
+                if (a.traj_ns && traj_budget_spent(a, st.slot_traj[t], st.grp_t0[lg], retire)) {  // singleton groups
+                    fl->status = FAULT_TIMEOUT;
+                    fl->iteration = it;
+                    retire = true;
                 }
                 if (retire) {
                     a.rep_iter[gid] = it;

@@ -92,7 +92,29 @@ struct SegArgs {
     double* blk;                // [M][N][6] full iterate of every retired trajectory (resume source)
     int hist_stride;            // row stride of rep_hist (the configured max_iterations)
     int pad1;
+    // ---- independent mode with a timeout: each trajectory's OWN wall-clock budget, as the
+    //      reference's run_independent gives every trajectory a propagate call (and a deadline)
+    //      of its own (runner.hpp:63-80, propagator.hpp:233-236).  Device time a trajectory has
+    //      spent in its slots, summed over segments; nullptr when the batch deadline applies.
+    unsigned long long* traj_ns;     // [M]
+    unsigned long long traj_budget_ns;
 };
+
+/// Per-trajectory budget (independent mode, traj_ns != nullptr): called by a group's decision
+/// after iteration `it` with t0 = the %globaltimer of the group's claim.  Charges the slot time
+/// when the group stops; otherwise returns true when the budget is spent -- the reference
+/// checks its deadline before every force evaluation (augment.hpp:116-120), so a group that
+/// has not stopped after an iteration times out before the next one.
+__device__ __forceinline__ bool traj_budget_spent(const SegArgs& a, int traj, unsigned long long t0, bool stopping) {
+    const unsigned long long used = a.traj_ns[traj] + (globaltimer_ns() - t0);
+    if (stopping) {
+        a.traj_ns[traj] = used;
+        return false;
+    }
+    if (used <= a.traj_budget_ns) return false;
+    a.traj_ns[traj] = used;
+    return true;
+}
 
 /// Group claimed from the queue: offset of its first trajectory, size and the report index
 /// (the group, or for a member-level round the trajectory itself).

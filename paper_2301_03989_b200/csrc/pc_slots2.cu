@@ -111,6 +111,7 @@ struct WsState {
     int grp_iter[SLOTS];
     int grp_floor[SLOTS];  // wide-group round: converge only at it >= floor
     int grp_cap[SLOTS];    // stop at it >= cap (max_iterations, or a round's target)
+    unsigned long long grp_t0[SLOTS];  // %globaltimer at the claim (per-trajectory budgets only)
     int act_word[2];     // active slots of half h (bits h*HS..h*HS+3); the MMA group reads
                          // act_word[h] while the FP group claims into act_word[h ^ 1]
     int new_mask[2];     // slots claimed at the last refill of each half
@@ -730,6 +731,11 @@ __device__ __forceinline__ void decide_single(const SegArgs& a, WsState& st, int
                 }
             }
         }
+        if (a.traj_ns && traj_budget_spent(a, st.slot_traj[t], st.grp_t0[lg], retire)) {
+            fl->status = FAULT_TIMEOUT;  // own budget spent before the next force evaluation
+            fl->iteration = it;
+            retire = true;
+        }
         if (retire) {
             a.rep_iter[gid] = it;
             a.rep_err[gid] = sqrt(gerr2);
@@ -863,6 +869,11 @@ __device__ __forceinline__ void decide_half(const SegArgs& a, WsState& st, int h
                     retire = ok = true;
                 }
             }
+        }
+        if (a.traj_ns && traj_budget_spent(a, my_tr, st.grp_t0[lg], retire)) {  // singleton groups only
+            fl->status = FAULT_TIMEOUT;
+            fl->iteration = it;
+            retire = true;
         }
         if (retire) {
             a.rep_iter[gid] = it;
@@ -1274,6 +1285,7 @@ __global__ void __launch_bounds__(WS_THREADS, PSWARM_MIN_BLOCKS) k_pc_ws(const S
                         st.grp_iter[lg] = start_iteration(a, off);
                         st.grp_floor[lg] = claim_floor(a, gid);
                         st.grp_cap[lg] = claim_cap(a, gid);
+                        if (a.traj_ns) st.grp_t0[lg] = globaltimer_ns();
                         int t = h * HS;
                         for (int mbr = 0; mbr < size; ++mbr) {
                             while ((am >> t) & 1) ++t;
@@ -1734,6 +1746,7 @@ __global__ void __launch_bounds__(WS_THREADS, PSWARM_MIN_BLOCKS) k_pc_uni(const 
                     st.grp_iter[lg] = start_iteration(a, off);
                     st.grp_floor[lg] = claim_floor(a, gid);
                     st.grp_cap[lg] = claim_cap(a, gid);
+                    if (a.traj_ns) st.grp_t0[lg] = globaltimer_ns();
                     int t = h * HS;
                     for (int mbr = 0; mbr < size; ++mbr) {
                         while ((am >> t) & 1) ++t;

@@ -157,7 +157,7 @@ enum BufId {
     B_OP_IN, B_OP_IN2, B_OP_OUT, B_OP_AUX, B_OP_KEY,
     B_BT_KIND, B_BT_SOFF, B_BT_NC, B_BT_EL, B_BT_BND, B_BT_COFF, B_BT_CF, B_PHASES,
     B_W_REP, B_W_LIST, B_W_CTL, B_W_HIST, B_W_BLK, B_W_GK,
-    B_IN_PACK, B_REPORT, B_BODY_VEL, B_REL_TAB, B_HOT, B_STATES7, B_EPH_T, B_COUNT
+    B_IN_PACK, B_REPORT, B_BODY_VEL, B_REL_TAB, B_HOT, B_STATES7, B_EPH_T, B_TRAJ_NS, B_COUNT
 };
 
 /// Page-locked host staging (grow-only): every host<->device transfer of a solve goes
@@ -684,7 +684,11 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
     if (nb > 63) raise(PSWARM_ERR_INVALID_SIZE, "propagate: at most 63 perturbing bodies are supported");
     const BodyUpload bu = flatten_bodies(*cfg, nb);
 
-    const auto deadline = cfg->timeout_s > 0.0
+    // independent mode: every trajectory has a budget of its own (run_independent calls propagate
+    // per trajectory, runner.hpp:63-80), charged on the device with the time it spends in its slots;
+    // grouped / augmented: one propagate call, one deadline for the batch (propagator.hpp:233-236)
+    const bool traj_budget = spec.independent && cfg->timeout_s > 0.0;
+    const auto deadline = cfg->timeout_s > 0.0 && !traj_budget
                               ? std::chrono::steady_clock::now() +
                                     std::chrono::duration_cast<std::chrono::steady_clock::duration>(
                                         std::chrono::duration<double>(cfg->timeout_s))
@@ -788,7 +792,11 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
 
     // device deadline in %globaltimer units
     unsigned long long gpu_deadline = 0;
-    if (cfg->timeout_s > 0.0) {
+    unsigned long long* d_tns = nullptr;
+    if (traj_budget) {
+        d_tns = ctx->buf[B_TRAJ_NS].get<unsigned long long>(static_cast<size_t>(M));
+        cuda_check(cudaMemsetAsync(d_tns, 0, sizeof(unsigned long long) * M, st), "memset budgets");
+    } else if (cfg->timeout_s > 0.0) {
         unsigned long long* d_t = reinterpret_cast<unsigned long long*>(ctx->buf[B_OP_KEY].get<double>(1));
         k_read_timer<<<1, 1, 0, st>>>(d_t);
         ++ctx->launches;
@@ -1006,6 +1014,8 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
         a.force_ns = ctx->force_ns;
         a.anc_fold = fold ? reinterpret_cast<const double*>(op.anc_fold.p) : nullptr;
         a.hist_stride = max_it;
+        a.traj_ns = d_tns;
+        a.traj_budget_ns = traj_budget ? static_cast<unsigned long long>(cfg->timeout_s * 1e9) : 0ull;
         auto launch = [&](const SegArgs& x, int grid) {
             if (small_k) return uni ? small::launch_segment_uni(x, grid, st) : small::launch_segment_ws(x, grid, st);
             return uni ? launch_segment_uni(x, grid, st) : use_ws ? launch_segment_ws(x, grid, st) : launch_segment(x, grid, st);

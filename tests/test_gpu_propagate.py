@@ -180,6 +180,29 @@ def test_timeout(ctx):
         ctx.propagate(states, [4], plan, cfg)
 
 
+def test_independent_timeout_is_per_trajectory(ctx, oracle):
+    """run_independent gives every trajectory a propagate call -- and a deadline -- of its own
+    (runner.hpp:63-80, propagator.hpp:233-236): a budget shorter than the whole batch but longer
+    than any one trajectory's solve times nothing out in independent mode, while grouped mode
+    (one propagate call for the batch) times out; a budget below one iteration times out
+    trajectory 0 with the reference's message in both implementations."""
+    states, plan, cfg = _setup(100_000, 64, 0.87, bodies="planets8")
+    want = ctx.run_batch(states, cfg, plan, "independent", samples=False)
+    cfg.timeout_s = 2e-3  # batch: ~10 ms of device time; one trajectory: ~30 iterations of ~10 us
+    got = ctx.run_batch(states, cfg, plan, "independent", samples=False)
+    assert np.array_equal(got.terminal_states, want.terminal_states)
+    assert np.array_equal(got.iterations, want.iterations)
+    with pytest.raises(ps.TimeoutError):
+        ctx.run_batch(states, cfg, plan, "grouped", samples=False)
+    small, plan_s, cfg_s = _setup(6, 32, 0.3, bodies="planets8")
+    cfg_s.timeout_s = 1e-9
+    with pytest.raises(ps.TimeoutError) as e:
+        ctx.run_batch(small, cfg_s, plan_s, "independent")
+    with pytest.raises(ps.TimeoutError) as e_ref:
+        oracle.run_batch(small, cfg_s, plan_s, "independent", 1)
+    assert str(e.value) == str(e_ref.value)
+
+
 def test_mixed_epochs_rejected(ctx):
     states, plan, cfg = _setup(3, 16, 0.1, bodies="two_body")
     states[2, 0] = 10.0
