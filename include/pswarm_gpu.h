@@ -103,7 +103,9 @@ typedef struct pswarm_config {
     const pswarm_body* bodies;
     double proximity_floor_km;  /* default 1.0 */
     int64_t p_groups;           /* grouped mode group count */
-    double timeout_s;           /* 0 disables the wall-clock guard */
+    double timeout_s;           /* 0 disables the wall-clock guard; one budget per call, except
+                                   run_batch independent mode: one per trajectory, as the
+                                   reference's run_independent (runner.hpp:63-80) */
     double c_light;             /* n_body_1pn: speed of light in km/s (0 = 299792.458) */
 } pswarm_config;
 
