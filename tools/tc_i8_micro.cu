@@ -162,7 +162,7 @@ __global__ void k_stream(const int8_t* A, int nsrc, int nch, long long* cyc, int
         for (int c = 0; c < R && c < nch; ++c) issue(c);  // then chunk j + R refills slot j
         for (int c = 0; c < nch; ++c) {
             wait(&full[c % R], (c / R) & 1);
-            asm volatile("tcgen05.fence::after_thread_sync;");
+            if (do_mma) asm volatile("tcgen05.fence::after_thread_sync;");
             const uint64_t da = sdesc(su32(ring + (c % R) * 4096), 128, 256);
             const uint64_t db = sdesc(su32(sb), 128, 256);
             if (do_mma) {
@@ -264,6 +264,92 @@ static void ldg_bw(size_t per_cta_bytes, int reps) {
     cudaFree(ds);
 }
 
+// one CTA: a single 1-D bulk copy of `bytes` (L2-resident source) -> cycles (size dependence of the
+// bulk-copy rate: per-copy overhead vs bytes per cycle)
+__global__ void k_bulk_one(const int8_t* src, int bytes, long long* cyc) {
+    extern __shared__ __align__(1024) unsigned char sm[];
+    __shared__ __align__(8) uint64_t bar;
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bar)));
+        asm volatile("fence.mbarrier_init.release.cluster;");
+        for (int rep = 0; rep < 2; ++rep) {  // rep 0 warms L2
+            const long long t0 = clock64();
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&bar)), "r"(bytes));
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                             su32(sm)), "l"(src), "r"(bytes), "r"(su32(&bar)) : "memory");
+            uint32_t done = 0;
+            while (!done)
+                asm volatile("{\n\t.reg .pred q;\n\tmbarrier.try_wait.parity.shared::cta.b64 q, [%1], %2;\n\tselp.u32 %0, 1, 0, q;\n\t}"
+                             : "=r"(done) : "r"(su32(&bar)), "r"(rep & 1));
+            cyc[rep] = clock64() - t0;
+        }
+    }
+}
+
+static void bulk_one(int bytes) {
+    int8_t* d;
+    long long* dc;
+    CK(cudaMalloc(&d, bytes));
+    CK(cudaMemset(d, 3, bytes));
+    CK(cudaMalloc(&dc, 16));
+    CK(cudaFuncSetAttribute(k_bulk_one, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    k_bulk_one<<<1, 32, 200 * 1024>>>(d, bytes, dc);
+    CK(cudaDeviceSynchronize());
+    long long c[2];
+    CK(cudaMemcpy(c, dc, 16, cudaMemcpyDeviceToHost));
+    printf("bulk one copy %6d B: %lld cycles (%.1f B/cycle) [cold %lld]\n", bytes, c[1], double(bytes) / c[1], c[0]);
+    cudaFree(d);
+    cudaFree(dc);
+}
+
+// one CTA: k back-to-back 1-D bulk copies of `bytes` each (distinct sources and destinations),
+// either on ONE mbarrier (expect_tx k*bytes) or on k separate mbarriers waited in order
+__global__ void k_bulk_many(const int8_t* src, int bytes, int k, int separate, long long* cyc) {
+    extern __shared__ __align__(1024) unsigned char sm[];
+    __shared__ __align__(8) uint64_t bars[32];
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < 32; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bars[i])));
+        asm volatile("fence.mbarrier_init.release.cluster;");
+        for (int rep = 0; rep < 2; ++rep) {
+            const long long t0 = clock64();
+            if (!separate)
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&bars[0])), "r"(bytes * k));
+            for (int i = 0; i < k; ++i) {
+                uint64_t* b = separate ? &bars[i] : &bars[0];
+                if (separate)
+                    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes));
+                asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                                 su32(sm + i * 4096)), "l"(src + static_cast<size_t>(i) * bytes), "r"(bytes), "r"(su32(b)) : "memory");
+            }
+            for (int i = 0; i < (separate ? k : 1); ++i) {
+                uint32_t done = 0;
+                while (!done)
+                    asm volatile("{\n\t.reg .pred q;\n\tmbarrier.try_wait.parity.shared::cta.b64 q, [%1], %2;\n\tselp.u32 %0, 1, 0, q;\n\t}"
+                                 : "=r"(done) : "r"(su32(&bars[i])), "r"(rep & 1));
+            }
+            cyc[rep] = clock64() - t0;
+        }
+    }
+}
+
+static void bulk_many(int k, int separate) {
+    const int bytes = 3328;
+    int8_t* d;
+    long long* dc;
+    CK(cudaMalloc(&d, bytes * k));
+    CK(cudaMemset(d, 3, bytes * k));
+    CK(cudaMalloc(&dc, 16));
+    CK(cudaFuncSetAttribute(k_bulk_many, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    k_bulk_many<<<1, 32, 200 * 1024>>>(d, bytes, k, separate, dc);
+    CK(cudaDeviceSynchronize());
+    long long c[2];
+    CK(cudaMemcpy(c, dc, 16, cudaMemcpyDeviceToHost));
+    printf("bulk %2d x %d B, %s: %lld cycles (%.0f per copy)\n", k, bytes, separate ? "separate mbarriers" : "one mbarrier", c[1],
+           double(c[1]) / k);
+    cudaFree(d);
+    cudaFree(dc);
+}
+
 template <int N>
 static int run(int swap) {
     std::vector<int8_t> a(M * K), b(N * K);
@@ -329,6 +415,8 @@ int main() {
     stream<16, 48>(1, 0, 56, 1);
     stream<16, 48>(16, 0, 56, 148);
     stream<4, 48>(1120, 0, 56, 1);
+    for (int b : {3328, 16384, 65536, 196608}) bulk_one(b);
+    for (int k : {1, 4, 16, 32}) { bulk_many(k, 0); bulk_many(k, 1); }
     ldg_bw<512>(186 * 1024, 20);
     ldg_bw<256>(186 * 1024, 20);
     ldg_bw<512>(1024 * 1024, 4);
