@@ -128,7 +128,7 @@ __global__ void k_stream(const int8_t* A, int nsrc, int nch, long long* cyc, int
     __shared__ uint32_t tbase;
     const int tid = threadIdx.x, warp = tid >> 5;
     for (int i = tid; i < NB * 32; i += blockDim.x) sb[kmaj(i / 32, i % 32, 32)] = static_cast<int8_t>(i % 7 - 3);
-    for (int i = tid; i < R * 4096; i += blockDim.x) ring[i] = 0;
+    // (the ring is not pre-filled: async-proxy writes only)
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tbase)), "n"(256));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -144,7 +144,8 @@ __global__ void k_stream(const int8_t* A, int nsrc, int nch, long long* cyc, int
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
-    if (tid == 0) {
+    if (warp == 0) {  // the whole warp runs the loop (lane 0 issues): no lane parked at a CTA barrier
+        const bool l0 = (tid & 31) == 0;
         const uint32_t tm = tbase, id = idesc_i8(M, NB);
         auto wait = [&](uint64_t* b, uint32_t ph) {  // test_wait spin (no suspend window)
             uint32_t done = 0;
@@ -154,6 +155,7 @@ __global__ void k_stream(const int8_t* A, int nsrc, int nch, long long* cyc, int
         };
         auto issue = [&](int c) {  // chunk c into slot c % R
             const int r = c % R;
+            if (!l0) return;
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&full[r])), "r"(CH));
             asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                              su32(ring + r * 4096)), "l"(A + static_cast<size_t>(nsrc > 56 ? blockIdx.x * 56 + c % 56 : (c * 7 + blockIdx.x) % nsrc) * CH), "r"(CH), "r"(su32(&full[r])) : "memory");
@@ -165,15 +167,16 @@ __global__ void k_stream(const int8_t* A, int nsrc, int nch, long long* cyc, int
             if (do_mma) asm volatile("tcgen05.fence::after_thread_sync;");
             const uint64_t da = sdesc(su32(ring + (c % R) * 4096), 128, 256);
             const uint64_t db = sdesc(su32(sb), 128, 256);
-            if (do_mma) {
+            if (do_mma && l0) {
                 asm volatile(
                     "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
                     "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tm),
                     "l"(da), "l"(db), "r"(id), "r"(c ? 1u : 0u));
                 asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&empty[c % R])));
-            } else {
+            } else if (l0) {
                 asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&empty[c % R])));
             }
+            __syncwarp();
             // refill the slot of chunk j = c - R/2 (its MMA was issued R/2 chunks ago): R/2 MMAs stay
             // queued while the issuer waits, R/2 copies are in flight
             const int j = c - R / 2;
@@ -184,7 +187,7 @@ __global__ void k_stream(const int8_t* A, int nsrc, int nch, long long* cyc, int
         }
         wait(&empty[(nch - 1) % R], ((nch - 1) / R) & 1);
         const long long t1 = clock64();
-        cyc[blockIdx.x] = t1 - t0;
+        if (l0) cyc[blockIdx.x] = t1 - t0;
     }
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
@@ -304,7 +307,7 @@ static void bulk_one(int bytes) {
 
 // one CTA: k back-to-back 1-D bulk copies of `bytes` each (distinct sources and destinations),
 // either on ONE mbarrier (expect_tx k*bytes) or on k separate mbarriers waited in order
-__global__ void k_bulk_many(const int8_t* src, int bytes, int k, int separate, long long* cyc) {
+__global__ void k_bulk_many(const int8_t* src, int bytes, int k, int separate, long long* cyc, int stride) {
     extern __shared__ __align__(1024) unsigned char sm[];
     __shared__ __align__(8) uint64_t bars[32];
     if (threadIdx.x == 0) {
@@ -319,7 +322,7 @@ __global__ void k_bulk_many(const int8_t* src, int bytes, int k, int separate, l
                 if (separate)
                     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes));
                 asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                                 su32(sm + i * 4096)), "l"(src + static_cast<size_t>(i) * bytes), "r"(bytes), "r"(su32(b)) : "memory");
+                                 su32(sm + i * 4096)), "l"(src + static_cast<size_t>((i * stride) % 56) * bytes), "r"(bytes), "r"(su32(b)) : "memory");
             }
             for (int i = 0; i < (separate ? k : 1); ++i) {
                 uint32_t done = 0;
@@ -332,20 +335,20 @@ __global__ void k_bulk_many(const int8_t* src, int bytes, int k, int separate, l
     }
 }
 
-static void bulk_many(int k, int separate) {
+static void bulk_many(int k, int separate, int stride = 1) {
     const int bytes = 3328;
     int8_t* d;
     long long* dc;
-    CK(cudaMalloc(&d, bytes * k));
-    CK(cudaMemset(d, 3, bytes * k));
+    CK(cudaMalloc(&d, bytes * 56));
+    CK(cudaMemset(d, 3, bytes * 56));
     CK(cudaMalloc(&dc, 16));
     CK(cudaFuncSetAttribute(k_bulk_many, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    k_bulk_many<<<1, 32, 200 * 1024>>>(d, bytes, k, separate, dc);
+    k_bulk_many<<<1, 32, 200 * 1024>>>(d, bytes, k, separate, dc, stride);
     CK(cudaDeviceSynchronize());
     long long c[2];
     CK(cudaMemcpy(c, dc, 16, cudaMemcpyDeviceToHost));
-    printf("bulk %2d x %d B, %s: %lld cycles (%.0f per copy)\n", k, bytes, separate ? "separate mbarriers" : "one mbarrier", c[1],
-           double(c[1]) / k);
+    printf("bulk %2d x %d B, %s, stride %d: %lld cycles (%.0f per copy)\n", k, bytes, separate ? "separate mbarriers" : "one mbarrier",
+           stride, c[1], double(c[1]) / k);
     cudaFree(d);
     cudaFree(dc);
 }
@@ -417,6 +420,8 @@ int main() {
     stream<4, 48>(1120, 0, 56, 1);
     for (int b : {3328, 16384, 65536, 196608}) bulk_one(b);
     for (int k : {1, 4, 16, 32}) { bulk_many(k, 0); bulk_many(k, 1); }
+    bulk_many(16, 1, 7);
+    bulk_many(16, 0, 7);
     ldg_bw<512>(186 * 1024, 20);
     ldg_bw<256>(186 * 1024, 20);
     ldg_bw<512>(1024 * 1024, 4);
