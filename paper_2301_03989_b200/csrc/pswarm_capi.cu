@@ -1015,7 +1015,7 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
         a.anc_fold = fold ? reinterpret_cast<const double*>(op.anc_fold.p) : nullptr;
         a.hist_stride = max_it;
         a.traj_ns = d_tns;
-        a.traj_budget_ns = traj_budget ? static_cast<unsigned long long>(cfg->timeout_s * 1e9) : 0ull;
+        a.traj_budget_ns = traj_budget ? static_cast<unsigned long long>(std::min(cfg->timeout_s * 1e9, 1.8e19)) : 0ull;
         auto launch = [&](const SegArgs& x, int grid) {
             if (small_k) return uni ? small::launch_segment_uni(x, grid, st) : small::launch_segment_ws(x, grid, st);
             return uni ? launch_segment_uni(x, grid, st) : use_ws ? launch_segment_ws(x, grid, st) : launch_segment(x, grid, st);
