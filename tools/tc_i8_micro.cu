@@ -307,9 +307,15 @@ static void bulk_one(int bytes) {
 
 // one CTA: k back-to-back 1-D bulk copies of `bytes` each (distinct sources and destinations),
 // either on ONE mbarrier (expect_tx k*bytes) or on k separate mbarriers waited in order
-__global__ void k_bulk_many(const int8_t* src, int bytes, int k, int separate, long long* cyc, int stride) {
+__global__ void k_bulk_many(const int8_t* src, int bytes, int k, int separate, long long* cyc, int stride, int variant) {
     extern __shared__ __align__(1024) unsigned char sm[];
     __shared__ __align__(8) uint64_t bars[32];
+    __shared__ uint32_t tb;
+    // variant 1: TMEM allocated first (as a tcgen05 kernel would); 2: 128-thread CTA, others parked at a barrier
+    if (variant == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tb)), "n"(256));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
     if (threadIdx.x == 0) {
         for (int i = 0; i < 32; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bars[i])));
         asm volatile("fence.mbarrier_init.release.cluster;");
@@ -333,9 +339,13 @@ __global__ void k_bulk_many(const int8_t* src, int bytes, int k, int separate, l
             cyc[rep] = clock64() - t0;
         }
     }
+    if (variant == 2) __syncthreads();
+    if (variant == 1) {
+        __syncwarp();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tb), "n"(256));
+    }
 }
-
-static void bulk_many(int k, int separate, int stride = 1) {
+static void bulk_many(int k, int separate, int stride = 1, int variant = 0) {
     const int bytes = 3328;
     int8_t* d;
     long long* dc;
@@ -343,12 +353,12 @@ static void bulk_many(int k, int separate, int stride = 1) {
     CK(cudaMemset(d, 3, bytes * 56));
     CK(cudaMalloc(&dc, 16));
     CK(cudaFuncSetAttribute(k_bulk_many, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    k_bulk_many<<<1, 32, 200 * 1024>>>(d, bytes, k, separate, dc, stride);
+    k_bulk_many<<<1, variant == 2 ? 128 : 32, 200 * 1024>>>(d, bytes, k, separate, dc, stride, variant);
     CK(cudaDeviceSynchronize());
     long long c[2];
     CK(cudaMemcpy(c, dc, 16, cudaMemcpyDeviceToHost));
-    printf("bulk %2d x %d B, %s, stride %d: %lld cycles (%.0f per copy)\n", k, bytes, separate ? "separate mbarriers" : "one mbarrier",
-           stride, c[1], double(c[1]) / k);
+    printf("bulk %2d x %d B, %s, stride %d, variant %d: %lld cycles (%.0f per copy)\n", k, bytes,
+           separate ? "separate mbarriers" : "one mbarrier", stride, variant, c[1], double(c[1]) / k);
     cudaFree(d);
     cudaFree(dc);
 }
@@ -422,6 +432,8 @@ int main() {
     for (int k : {1, 4, 16, 32}) { bulk_many(k, 0); bulk_many(k, 1); }
     bulk_many(16, 1, 7);
     bulk_many(16, 0, 7);
+    bulk_many(16, 1, 7, 1);
+    bulk_many(16, 1, 7, 2);
     ldg_bw<512>(186 * 1024, 20);
     ldg_bw<256>(186 * 1024, 20);
     ldg_bw<512>(1024 * 1024, 4);
