@@ -180,6 +180,47 @@ def test_timeout(ctx):
         ctx.propagate(states, [4], plan, cfg)
 
 
+@pytest.mark.parametrize("n,kind,mode,opts,kernel", [
+    (64, "n_body", "independent", {}, "k_pc_ws_fold.x2"),        # two CTAs per SM
+    (200, "n_body", "independent", {}, "k_pc_ws_fold"),
+    (200, "n_body", "grouped", {}, "k_pc_ws_fold"),              # in-CTA groups
+    (200, "n_body", "augmented", {}, "k_pc_ws_fold"),            # member-level rounds
+    (57, "n_body", "independent", {}, "k_pc_ws"),                # dense update
+    (33, "n_body", "independent", {}, "k_pc_segment"),
+    (200, "n_body", "independent", {"unified": 1}, "k_pc_uni"),
+    (128, "n_body_1pn", "independent", {}, "k_pc_uni.x2"),       # relativistic
+    (200, "n_body_1pn", "independent", {}, "k_pc_uni"),
+])
+def test_absolute_error_mode_every_kernel(ctx, oracle, n, kind, mode, opts, kernel):
+    """ErrorMode::absolute (augment.hpp:45-47: |dr|, |dv| without the previous iterate's norms)
+    through every solve kernel: a km / km/s tolerance, iterations and states against the oracle."""
+    base = ps.reference_state()
+    states = ps.make_clone_batch(base, 24, 1e-5)
+    period = ps.osculating_period(base, ps.MU_SUN)
+    plan = ps.plan_segments(base, 0.0, 0.6 * period, ps.MU_SUN, "single", n)
+    cfg = ps.reference_force_config(kind, bodies=ps.planets8(), n_nodes=n)
+    cfg.error_mode = "absolute"
+    # km and km/s.  The absolute change of this orbit's iterate saw-tooths (odd iterations
+    # ~1e-3 km, even ones ~1e4 km early on: the position update lags the velocity update), and
+    # |r| ~ 1e8 km puts the FP64 noise of the position update near 1e-7 km, so a tolerance
+    # around 1e-6 decides on noise; 1e-3 stops at iteration ~9, far from both
+    cfg.tolerance = 1e-3
+    cfg.p_groups = 6
+    for k, v in opts.items():
+        ctx.set_option(k, v)
+    try:
+        got = ctx.run_batch(states, cfg, plan, mode)
+        assert ctx.kernel_name() == kernel
+    finally:
+        for k in opts:
+            ctx.set_option(k, 2 if k == "unified" else 1)
+    want = oracle.run_batch(states, cfg, plan, mode, 1)
+    _parity(got, want)
+    assert got.iterations.min() >= 3
+    cfg.error_mode = "relative"  # the mode is in effect: a relative 1e-3 stops far earlier
+    assert ctx.run_batch(states, cfg, plan, mode).iterations.max() < got.iterations.min()
+
+
 def test_independent_timeout_is_per_trajectory(ctx, oracle):
     """run_independent gives every trajectory a propagate call -- and a deadline -- of its own
     (runner.hpp:63-80, propagator.hpp:233-236): a budget shorter than the whole batch but longer
