@@ -371,7 +371,7 @@ __device__ __forceinline__ void gemm_half_fold(const double2* __restrict__ upf, 
 /// the massive bodies of the node table (Sun row first) per slot pair yields both the
 /// Newtonian sum and the EIH 1PN terms from the same d, |d|^-1 (see rel_correction for the
 /// factorisation); the reference's singularity guards run exactly on the slow path.
-template <int NS>
+template <int NS, bool GLOBAL_TAB>
 __device__ __forceinline__ void force_half_rel(const ForceData& fd, const double* rel_base, const double* ybuf,
                                                double* fb, int* sing_key, int act_h, int h, int j, int s_begin) {
     constexpr int PAIR = NS < 2 ? NS : 2;  // slots per fused pass
@@ -412,8 +412,12 @@ __device__ __forceinline__ void force_half_rel(const ForceData& fd, const double
 #pragma unroll(PAIR == 1 ? 3 : 1)
         for (int A = 0; A < nb1; ++A) {
             const double* t = rt + A * REL_W;
-            const double tx = t[0], ty = t[1], tz = t[2], vax = t[3], vay = t[4], vaz = t[5];
-            const double aax = t[6], aay = t[7], aaz = t[8], mu = t[9], K = t[10];
+            // table in global memory (not staged): the single-chain path (3 bodies unrolled) loads
+            // with ld.global.ca, which the compiler does not hoist across the unrolled bodies --
+            // hoisted, its 33 live table values spilled 116 B per thread in the whole kernel
+            auto ld = [t](int i) { return (GLOBAL_TAB && PAIR == 1) ? __ldca(t + i) : t[i]; };
+            const double tx = ld(0), ty = ld(1), tz = ld(2), vax = ld(3), vay = ld(4), vaz = ld(5);
+            const double aax = ld(6), aay = ld(7), aaz = ld(8), mu = ld(9), K = ld(10);
 #pragma unroll
             for (int k = 0; k < PAIR; ++k) {
                 const double dx = tx - rx[k], dy = ty - ry[k], dz = tz - rz[k];
@@ -1403,7 +1407,7 @@ __global__ void __launch_bounds__(WS_THREADS, PSWARM_MIN_BLOCKS) k_pc_ws(const S
                 } else if (N > FP_THREADS / 2) {
                     for (int j = ft; j < N; j += FP_THREADS) {
                         if constexpr (REL)
-                            force_half_rel<4>(a.fd, rel_base, ybuf, fbh, st.sing_key, act_h, h, j, 0);
+                            force_half_rel<4, !STAGE>(a.fd, rel_base, ybuf, fbh, st.sing_key, act_h, h, j, 0);
                         else
                             force_half<4>(a.fd, ybuf, fbh, st.sing_key, pos_base, ind_base, psj, psc, act_h, h, j, 0);
                     }
@@ -1413,7 +1417,7 @@ __global__ void __launch_bounds__(WS_THREADS, PSWARM_MIN_BLOCKS) k_pc_ws(const S
                         // read per node, broadcast)
                         const int j = REL ? w >> 1 : w % N, s0 = REL ? (w & 1) * 2 : (w / N) * 2;
                         if constexpr (REL)
-                            force_half_rel<2>(a.fd, rel_base, ybuf, fbh, st.sing_key, act_h, h, j, s0);
+                            force_half_rel<2, !STAGE>(a.fd, rel_base, ybuf, fbh, st.sing_key, act_h, h, j, s0);
                         else
                             force_half<2>(a.fd, ybuf, fbh, st.sing_key, pos_base, ind_base, psj, psc, act_h, h, j, s0);
                     }
@@ -1421,7 +1425,7 @@ __global__ void __launch_bounds__(WS_THREADS, PSWARM_MIN_BLOCKS) k_pc_ws(const S
                     for (int w = ft; w < 4 * N; w += FP_THREADS) {
                         const int j = REL ? w >> 2 : w % N, s0 = REL ? w & 3 : w / N;
                         if constexpr (REL)
-                            force_half_rel<1>(a.fd, rel_base, ybuf, fbh, st.sing_key, act_h, h, j, s0);
+                            force_half_rel<1, !STAGE>(a.fd, rel_base, ybuf, fbh, st.sing_key, act_h, h, j, s0);
                         else
                             force_half<1>(a.fd, ybuf, fbh, st.sing_key, pos_base, ind_base, psj, psc, act_h, h, j, s0);
                     }
@@ -1848,9 +1852,9 @@ __global__ void __launch_bounds__(WS_THREADS, PSWARM_MIN_BLOCKS) k_pc_uni(const 
                 if (!act_h) continue;
                 double* fbh = fb0 + h * (fb_bytes / sizeof(double));
                 const int s0 = (r % (4 / ns)) * ns;
-                if (ns == 4) force_half_rel<4>(a.fd, rel_base, ybuf, fbh, st.sing_key, act_h, h, j, s0);
-                else if (ns == 2) force_half_rel<2>(a.fd, rel_base, ybuf, fbh, st.sing_key, act_h, h, j, s0);
-                else force_half_rel<1>(a.fd, rel_base, ybuf, fbh, st.sing_key, act_h, h, j, s0);
+                if (ns == 4) force_half_rel<4, !STAGE>(a.fd, rel_base, ybuf, fbh, st.sing_key, act_h, h, j, s0);
+                else if (ns == 2) force_half_rel<2, !STAGE>(a.fd, rel_base, ybuf, fbh, st.sing_key, act_h, h, j, s0);
+                else force_half_rel<1, !STAGE>(a.fd, rel_base, ybuf, fbh, st.sing_key, act_h, h, j, s0);
             }
             __syncthreads();
             UNI_PHASE(3);
