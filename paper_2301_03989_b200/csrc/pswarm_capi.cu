@@ -1012,6 +1012,18 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
         a.b0_mma = ctx->b0_mma;
         a.fast_decide = ctx->fast_decide;
         a.force_ns = ctx->force_ns;
+        if (a.force_ns == 0 && uni && rel) {
+            // relativistic k_pc_uni force items: 1 slot (one chain) or 2 (two fused chains) per item,
+            // whichever needs fewer rounds of the block's threads weighted by the item cost (a
+            // 2-chain item ~1.8x a 1-chain one) -- fits every 1PN N measured from 64 to 256
+            // (tools/probe_ab_opt.py force_ns): e.g. N = 160, 640 two-chain items = 2 rounds of 512
+            // threads vs 1280 one-chain items = 3 rounds -> one chain, -4.5 % kernel time.  Chosen
+            // here, not in the kernel: ptxas' register allocation of the whole kernel moved (+1 %
+            // elsewhere) when the kernel computed it.
+            const int T = small_k ? 256 : 512;
+            const int r1 = (8 * Ni + T - 1) / T, r2 = (4 * Ni + T - 1) / T;
+            a.force_ns = 10 * r1 <= 18 * r2 ? 1 : 2;
+        }
         a.anc_fold = fold ? reinterpret_cast<const double*>(op.anc_fold.p) : nullptr;
         a.hist_stride = max_it;
         a.traj_ns = d_tns;
