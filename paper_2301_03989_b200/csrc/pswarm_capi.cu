@@ -1023,6 +1023,11 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
             const int T = small_k ? 256 : 512;
             const int r1 = (8 * Ni + T - 1) / T, r2 = (4 * Ni + T - 1) / T;
             a.force_ns = 10 * r1 <= 18 * r2 ? 1 : 2;
+        } else if (a.force_ns == 0 && small_k && !uni) {
+            // k_pc_ws_fold.x2 (128 FP threads): single-slot items up to N = 80 (the kernel's own
+            // threshold is N = 64): -6.6 % / -9.7 % kernel time at N = 72 / 80, two-slot items
+            // from N = 88 (tools/probe_ab_opt.py force_ns)
+            a.force_ns = Ni / 2 > 40 ? 2 : 1;
         }
         a.anc_fold = fold ? reinterpret_cast<const double*>(op.anc_fold.p) : nullptr;
         a.hist_stride = max_it;
