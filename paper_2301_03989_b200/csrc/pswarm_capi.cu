@@ -832,9 +832,9 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
     constexpr size_t SMEM_PAIR = 228 * 1024 / 2 - 2 * 1024;
     bool small_k = false;
     int small_stage = 0, small_xrows = 0;
-    // measured (tools/probe_ab_opt.py small_ctas): Newtonian -32 % kernel time at N = 64, -10 % at 96,
-    // +14 % at 128; 1PN -16 % at 64, +1 % at 96, -6 % at 128
-    const int small_max = ctx->small_max_n > 0 ? ctx->small_max_n : (rel ? 128 : 96);
+    // measured (tools/probe_ab_opt.py small_ctas / small_max_n): Newtonian -32 % kernel time at N = 64,
+    // -10 % at 96, -13 / -6 / -4 % at 104 / 112 / 120, +1 % at 128; 1PN -16 % at 64, +1 % at 96, -6 % at 128
+    const int small_max = ctx->small_max_n > 0 ? ctx->small_max_n : (rel ? 128 : 120);
     if (ctx->small_ctas && fold && Ni <= small_max && small::ws_supported(Ni, true) &&
         (!uni || small::uni_supported(Ni))) {
         small_xrows = uni ? 0 : small::ws_extra_rows(Ni, true);
