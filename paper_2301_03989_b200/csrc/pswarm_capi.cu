@@ -824,8 +824,11 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
     const int xrows = use_ws ? ws_extra_rows(Ni, fold) : extra_rows(Ni, op.gp);
     // auto: the unified kernel for the force-bound 1PN model (node-major force items: 1PN kernel
     // time 15.0 vs 19.2 ms at N = 200, 17.8 vs 27.0 ms at N = 256 against k_pc_ws_fold,
-    // profiles/sanitizer_r02.json run); Newtonian forces stay on the warp-specialised kernel
-    const bool uni = fold && (ctx->unified == 1 || (ctx->unified == 2 && rel)) && uni_supported(Ni);
+    // profiles/sanitizer_r02.json run); Newtonian forces stay on the warp-specialised kernel, except
+    // N = 80...96: the unified kernel's two-CTA variant beats k_pc_ws_fold.x2 by 2 / 10 / 12 %
+    // at N = 80 / 88 / 96 (ties or loses elsewhere: +7 % at 72, +1 % at 104 / 112; tools/probe_ab_opt.py unified)
+    const bool uni_newton = ctx->small_ctas && Ni >= 80 && Ni <= 96;
+    const bool uni = fold && (ctx->unified == 1 || (ctx->unified == 2 && (rel || uni_newton))) && uni_supported(Ni);
     // small N: the 256-thread variants of the same kernels (4 + 4 warps, pswarm_dev::small) run two
     // CTAs per SM, so one CTA's barrier / decision / claim latencies overlap the other's work;
     // each CTA's shared memory must leave room for the second

@@ -373,8 +373,12 @@ def test_folded_tile_plans(ctx, oracle, n):
     leftover tiles as single-n-tile units (staged rows), with and without the anchor row in
     a spare pair row (b0 from the DMMA stream), Sun + 8 planets, 0.5 period."""
     states, plan, cfg = _setup(12, n, 0.5, "planets8")
-    got = ctx.run_batch(states, cfg, plan, "independent")
-    assert ctx.kernel_name().split(".")[0] == "k_pc_ws_fold"
+    ctx.set_option("unified", 0)  # (auto runs k_pc_uni.x2 at N = 80...96)
+    try:
+        got = ctx.run_batch(states, cfg, plan, "independent")
+        assert ctx.kernel_name().split(".")[0] == "k_pc_ws_fold"
+    finally:
+        ctx.set_option("unified", 2)
     want = oracle.run_batch(states, cfg, plan, "independent", 8)
     _parity(got, want)
 
