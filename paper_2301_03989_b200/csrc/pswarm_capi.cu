@@ -218,7 +218,7 @@ struct pswarm_ctx {
     int stage = 1;           // stage the per-segment node table in shared memory when it fits (0: never)
     int eph_nc = 1;          // unstaged ephemeris read node-contiguous from global (eph_t): coalesced
                              // (-14 % kernel time at N = 256, tools/probe_ab_opt.py eph_nc)
-    int b0_mma = 1;          // folded: b0 from the anchor pair row (spare row, N/2 % 8 != 0)
+    int b0_mma = 2;          // folded: b0 from the anchor pair row (spare row, N/2 % 8 != 0): 1 on, 0 off, 2 auto
     int unified = 2;         // folded solves: 1 k_pc_uni (all warps per phase), 0 k_pc_ws_fold, 2 auto =
                              // k_pc_uni for the force-bound 1PN model (N <= 200), else k_pc_ws_fold
                              // (measured, tools/probe_uni.py)
@@ -1012,7 +1012,11 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
         a.phase_cycles = d_phase;
         a.upack_fold = fold ? reinterpret_cast<const double2*>(op.fold.p) : nullptr;
         a.nkp_fold = op.nkp_fold;
-        a.b0_mma = ctx->b0_mma;
+        // auto: the FP group forms b0 itself at N = 168...200 -- k_pc_ws_fold kernel time -1.3 % on C4
+        // (1M ICs, N = 200), -1.8 % on C2, -1.1 / -1.5 % at N = 168 / 184; the anchor pair row of the
+        // DMMA stream everywhere else (+4...7 % without it at N = 120...152 and 216...248;
+        // tools/probe_ab_c4.py, tools/probe_ab_opt.py b0_mma)
+        a.b0_mma = ctx->b0_mma == 2 ? !(Ni >= 168 && Ni <= 200) : ctx->b0_mma;
         a.fast_decide = ctx->fast_decide;
         a.force_ns = ctx->force_ns;
         if (a.force_ns == 0 && uni && rel) {
@@ -1411,7 +1415,7 @@ pswarm_status pswarm_set_option(pswarm_ctx* ctx, const char* key, int64_t value)
         else if (k == "slot_kernel") ctx->slot_kernel = static_cast<int>(value);
         else if (k == "poison_outputs") ctx->poison_outputs = value != 0;
         else if (k == "fold") ctx->fold = value != 0;
-        else if (k == "b0_mma") ctx->b0_mma = value != 0;
+        else if (k == "b0_mma") ctx->b0_mma = static_cast<int>(std::clamp<int64_t>(value, 0, 2));
         else if (k == "fast_decide") ctx->fast_decide = value != 0;
         else if (k == "force_ns") ctx->force_ns = static_cast<int>(value);
         else if (k == "small_ctas") ctx->small_ctas = value != 0;
