@@ -825,9 +825,10 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
     // auto: the unified kernel for the force-bound 1PN model (node-major force items: 1PN kernel
     // time 15.0 vs 19.2 ms at N = 200, 17.8 vs 27.0 ms at N = 256 against k_pc_ws_fold,
     // profiles/sanitizer_r02.json run); Newtonian forces stay on the warp-specialised kernel, except
-    // N = 80...96: the unified kernel's two-CTA variant beats k_pc_ws_fold.x2 by 2 / 10 / 12 %
-    // at N = 80 / 88 / 96 (ties or loses elsewhere: +7 % at 72, +1 % at 104 / 112; tools/probe_ab_opt.py unified)
-    const bool uni_newton = ctx->small_ctas && Ni >= 80 && Ni <= 96;
+    // N = 80...96 and 112...128: the unified kernel's two-CTA variant beats k_pc_ws_fold.x2 by 2 / 10 / 12 %
+    // at N = 80 / 88 / 96, 1 / 0.4 % at 112 / 120, and the 512-thread k_pc_ws_fold by 3.7 % at 128 (+7 % at
+    // 72, +1 % at 104; tools/probe_ab_opt.py unified, tools/probe_ab_uni_small.py)
+    const bool uni_newton = ctx->small_ctas && ((Ni >= 80 && Ni <= 96) || (Ni >= 112 && Ni <= 128));
     const bool uni = fold && (ctx->unified == 1 || (ctx->unified == 2 && (rel || uni_newton))) && uni_supported(Ni);
     // small N: the 256-thread variants of the same kernels (4 + 4 warps, pswarm_dev::small) run two
     // CTAs per SM, so one CTA's barrier / decision / claim latencies overlap the other's work;
@@ -837,7 +838,7 @@ void propagate_impl(pswarm_ctx* ctx, int64_t M, const double* states, int64_t P,
     int small_stage = 0, small_xrows = 0;
     // measured (tools/probe_ab_opt.py small_ctas / small_max_n): Newtonian -32 % kernel time at N = 64,
     // -10 % at 96, -13 / -6 / -4 % at 104 / 112 / 120, +1 % at 128; 1PN -16 % at 64, +1 % at 96, -6 % at 128
-    const int small_max = ctx->small_max_n > 0 ? ctx->small_max_n : (rel ? 128 : 120);
+    const int small_max = ctx->small_max_n > 0 ? ctx->small_max_n : (rel || uni ? 128 : 120);
     if (ctx->small_ctas && fold && Ni <= small_max && small::ws_supported(Ni, true) &&
         (!uni || small::uni_supported(Ni))) {
         small_xrows = uni ? 0 : small::ws_extra_rows(Ni, true);

@@ -284,7 +284,7 @@ def test_singularity_in_solve_names_body(ctx, oracle):
 @pytest.mark.parametrize("n", [64, 72, 80, 88, 96, 104, 112, 120, 128, 160, 168, 184, 200, 232, 256])
 def test_c5_node_sweep(ctx, oracle, n):
     """C5 node-count sweep (64-256 nodes per segment): every warp plan of the slot
-    kernels and every per-N choice (two-CTA variants up to 120, the unified kernel at 80-96,
+    kernels and every per-N choice (two-CTA variants up to 128, the unified kernel at 80-96 and 112-128,
     single-slot force items up to 80, b0 from the FP group at 168-200) against the oracle,
     Sun + 8 planets, 0.6 period."""
     states, plan, cfg = _setup(24, n, 0.6, "planets8")
