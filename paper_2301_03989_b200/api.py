@@ -337,7 +337,7 @@ class _Outputs:
             times=self.times, trajectories=self.samples,
             terminal_states=self.terminal if complete else None, reports=reports,
             group_sizes=np.asarray(group_sizes, dtype=np.int64), segments=plan, warnings=warnings,
-            iterations=self.iters[:S_rep].copy(), converged=self.conv[:S_rep].copy(),
+            iterations=self.iters[:S_rep], converged=self.conv[:S_rep],  # views of this call's buffer
             device_ms=o.device_ms, kernel_ms=o.kernel_ms, trajectory_iterations=int(o.trajectory_iterations),
             gpu_launches=int(o.gpu_launches), wall_s=o.wall_s)
 
