@@ -12,6 +12,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import sys
 import threading
 from dataclasses import dataclass, field
 from typing import List, Optional, Sequence
@@ -279,8 +280,29 @@ def pinned_terminal_buffer(n_states: int) -> np.ndarray:
     return torch.zeros((n_states, 7), dtype=torch.float64, pin_memory=True).numpy()
 
 
+def _pooled_bytes(pool, n):
+    """A zeroed uint8 buffer of n bytes from `pool` (a list kept by the context): a buffer whose
+    only reference is the pool's is reused -- memset instead of the first-touch page faults of a
+    fresh allocation (14 MB of reports per 1M-trajectory call) -- else a new one joins the pool
+    (at most two: a caller that keeps every result keeps getting fresh buffers)."""
+    if pool is not None:
+        for buf in pool:
+            # references: the pool list, the loop variable, getrefcount's argument -- no live
+            # result, view or report of an earlier call still points into it
+            if buf.nbytes >= n and sys.getrefcount(buf) <= 3:
+                view = buf[:n]
+                view.fill(0)
+                return view
+    buf = np.zeros(n, dtype=np.uint8)
+    if pool is not None and n >= (1 << 20):
+        if len(pool) >= 2:
+            pool.pop(0)
+        pool.append(buf)
+    return buf
+
+
 class _Outputs:
-    def __init__(self, M, P, S, N, max_it, samples=True, history=True, terminal=True):
+    def __init__(self, M, P, S, N, max_it, samples=True, history=True, terminal=True, pool=None):
         R = 1 + S * (N - 1)
         self.M, self.P, self.S, self.R, self.max_it = M, P, S, R, max(max_it, 0)
         if isinstance(terminal, np.ndarray):  # caller-owned (e.g. pinned_terminal_buffer) output
@@ -304,7 +326,7 @@ class _Outputs:
         o_i = o_e + al(8 * S * P)
         o_c = o_i + al(4 * S * P)
         o_f = o_c + al(S * P)
-        small = np.zeros(o_f + al(S * M), dtype=np.uint8)  # zeroed: not every writer fills every entry
+        small = _pooled_bytes(pool, o_f + al(S * M))  # zeroed: not every writer fills every entry
         base = small.__array_interface__["data"][0]
         self.times = np.ndarray((R,), np.float64, small, o_t)
         self.ferr = np.ndarray((S, P), np.float64, small, o_e)
@@ -362,6 +384,7 @@ class Context:
     """One device context (pswarm_ctx) bound to a CUDA device."""
 
     def __init__(self, device: int = -1):
+        self._report_pool = []  # reusable report buffers of large calls (_pooled_bytes)
         self.lib = _abi.load()
         self.ptr = C.c_void_p()
         err = _abi.PswarmError()
@@ -449,7 +472,8 @@ class Context:
         cm = self._marshal(config)
         b = np.ascontiguousarray(np.asarray(plan.boundaries, dtype=np.float64))
         S = max(len(b) - 1, 0)
-        outs = _Outputs(st.shape[0], len(gs), S, plan.n_nodes, config.max_iterations, samples, history, terminal)
+        outs = _Outputs(st.shape[0], len(gs), S, plan.n_nodes, config.max_iterations, samples, history, terminal,
+                        pool=self._report_pool)
         err = _abi.PswarmError()
         if mode is None:
             status = self.lib.pswarm_propagate(self.ptr, st.shape[0], _abi.dptr(st), len(gs),

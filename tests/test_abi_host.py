@@ -135,3 +135,24 @@ def test_split_groups_matches_reference_rules():
     assert g.sum() == 13509 and g.max() - g.min() <= 1 and g[0] >= g[-1]
     with pytest.raises(ps.InvalidPlanError):
         ps.split_groups(5, 6)
+
+
+def test_report_buffer_pool_reuses_only_unreferenced_buffers():
+    """Large-call report buffers are recycled only when no result, view or report of an
+    earlier call points into them, and come back zeroed."""
+    from paper_2301_03989_b200.api import _pooled_bytes
+    pool = []
+    a = _pooled_bytes(pool, 2 << 20)
+    a[:] = 7
+    view = a[:16]
+    del a
+    b = _pooled_bytes(pool, 2 << 20)  # the first buffer is still referenced by `view`
+    assert len(pool) == 2 and not np.shares_memory(b, view)
+    del view
+    b[:] = 5
+    del b
+    c = _pooled_bytes(pool, 1 << 20)  # both free now: the first one is reused, zeroed
+    assert c.nbytes == 1 << 20 and not c.any()
+    assert any(np.shares_memory(c, p) for p in pool)
+    small = _pooled_bytes(pool, 100)  # small calls never enter the pool
+    assert small.nbytes == 100 and len(pool) == 2
