@@ -280,6 +280,21 @@ def pinned_terminal_buffer(n_states: int) -> np.ndarray:
     return torch.zeros((n_states, 7), dtype=torch.float64, pin_memory=True).numpy()
 
 
+_SINGLETONS: dict = {}
+
+
+def _singletons(m: int) -> np.ndarray:
+    """Independent mode's group sizes (all 1) as a cached read-only array: a 1M-trajectory call
+    does not allocate and fill 8 MB per call for it."""
+    a = _SINGLETONS.get(m)
+    if a is None:
+        a = np.ones(m, dtype=np.int64)
+        a.setflags(write=False)
+        _SINGLETONS.clear()
+        _SINGLETONS[m] = a
+    return a
+
+
 def _pooled_bytes(pool, n):
     """A zeroed uint8 buffer of n bytes from `pool` (a list kept by the context): a buffer whose
     only reference is the pool's is reused -- memset instead of the first-touch page faults of a
@@ -444,7 +459,7 @@ class Context:
         mode = parse_run_mode(mode)
         M = st.shape[0]
         if mode == "independent":
-            gs = np.ones(M, dtype=np.int64)
+            gs = _singletons(M)
         elif mode.startswith("augmented"):
             gs = np.array([M], dtype=np.int64)
         else:
@@ -753,6 +768,7 @@ class MultiContext:
     Results have the single-device layout and batch order."""
 
     def __init__(self, devices):
+        self._report_pool = []  # reusable report buffers of large calls (_pooled_bytes)
         self.lib = _abi.load()
         self.ptr = C.c_void_p()
         devs = (C.c_int32 * len(devices))(*[int(d) for d in devices])
@@ -783,7 +799,7 @@ class MultiContext:
         mode = parse_run_mode(mode)
         M = st.shape[0]
         if mode == "independent":
-            gs = np.ones(M, dtype=np.int64)
+            gs = _singletons(M)
         elif mode.startswith("augmented"):
             gs = np.array([M], dtype=np.int64)
         else:
@@ -791,7 +807,7 @@ class MultiContext:
         cm = self._marshal(config)
         b = np.ascontiguousarray(np.asarray(plan.boundaries, dtype=np.float64))
         outs = _Outputs(M, len(gs), max(len(b) - 1, 0), plan.n_nodes, config.max_iterations, samples, history,
-                        terminal)
+                        terminal, pool=self._report_pool)
         err = _abi.PswarmError()
         status = self.lib.pswarm_run_batch_multi(self.ptr, M, _abi.dptr(st), len(b), _abi.dptr(b), plan.n_nodes,
                                                  C.byref(cm.cfg), RUN_MODES[mode], workers, C.byref(outs.out),
