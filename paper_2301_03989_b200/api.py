@@ -309,7 +309,7 @@ def _pooled_bytes(pool, n):
                 view.fill(0)
                 return view
     buf = np.zeros(n, dtype=np.uint8)
-    if pool is not None and n >= (1 << 20):
+    if pool is not None and (1 << 20) <= n <= (256 << 20):  # retained memory stays bounded
         if len(pool) >= 2:
             pool.pop(0)
         pool.append(buf)
