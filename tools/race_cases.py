@@ -10,7 +10,7 @@ states = ps.make_clone_batch(base, 24, 1e-5)
 other = ps.elements_to_state([1.15e8, 0.2, 0.05, 0.4, 0.9, 0.0, 0.0], ps.MU_SUN, 0.0)
 states[1::3, 1:] = other[1:]  # mixed members: wide groups need resume rounds
 # (N, mode, p_groups, force kind, start, options)
-CASES = [(200, "independent", 1, "n_body", "warm", {}),                      # k_pc_ws_fold, extra units
+CASES = [(200, "independent", 1, "n_body", "warm", {}),                      # k_pc_ws_fold, extra units, b0 by the FP group
          (160, "independent", 1, "n_body", "warm", {}),                      # k_pc_ws_fold, 6 extra units
          (256, "independent", 1, "n_body", "warm", {}),                      # k_pc_ws_fold, no extras
          (200, "independent", 1, "n_body", "warm", {"fold": 0}),             # dense k_pc_ws
@@ -25,7 +25,11 @@ CASES = [(200, "independent", 1, "n_body", "warm", {}),                      # k
          (64, "augmented", 1, "n_body", "warm", {}),                         # wide rounds on k_pc_ws_fold (resume)
          (64, "independent", 1, "n_body_1pn", "warm", {}),                   # k_pc_uni, 1PN table bulk-staged
          (64, "independent", 1, "n_body", "hot", {}),                        # hot start, multi-segment
-         (96, "grouped", 4, "n_body", "warm", {}),                           # k_pc_ws_fold.x2 (two CTAs per SM)
+         (96, "grouped", 4, "n_body", "warm", {}),                           # k_pc_uni.x2 Newtonian (two CTAs per SM)
+         (104, "independent", 1, "n_body", "warm", {}),                      # k_pc_ws_fold.x2, two-slot items
+         (72, "independent", 1, "n_body", "warm", {}),                       # k_pc_ws_fold.x2, single-slot items
+         (128, "independent", 1, "n_body", "warm", {}),                      # k_pc_uni.x2 Newtonian
+         (160, "independent", 1, "n_body_1pn", "warm", {}),                  # k_pc_uni 1PN, single-slot items
          (128, "augmented", 1, "n_body_1pn", "warm", {})]                    # k_pc_uni.x2, wide rounds
 for n, mode, p, kind, start, opts in CASES:
     plan = ps.plan_segments(base, 0.0, (2.2 if start == "hot" else 0.4) * period, ps.MU_SUN,
